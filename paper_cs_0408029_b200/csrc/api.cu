@@ -1,0 +1,791 @@
+// api.cu -- the C ABI (include/nnls.h) and the host-side driver of the solve.
+//
+// The driver only orders kernels on the caller's stream and reads back one
+// small status block per pivot iteration (the loop test "while (x_F, y_G) is
+// infeasible"); every arithmetic step of the method runs in the sm_100a
+// kernels of this directory.  There is no CPU fallback.
+#include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+
+#include "../../include/nnls.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace nnls;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+cudaError_t ensure(Buf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e == cudaSuccess) b.cap = bytes;
+  return e;
+}
+
+template <class T>
+T* P(Buf& b) {
+  return static_cast<T*>(b.p);
+}
+
+nnls_status map_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return NNLS_OK;
+  if (e == cudaErrorMemoryAllocation) return NNLS_ERR_OOM;
+  return NNLS_ERR_CUDA;
+}
+
+#define CK(expr)                                  \
+  do {                                            \
+    cudaError_t e_ = (expr);                      \
+    if (e_ != cudaSuccess) return map_cuda(e_);   \
+  } while (0)
+
+int round_up(int v, int q) { return (v + q - 1) / q * q; }
+
+}  // namespace
+
+struct HostState {
+  DevState st;
+  int err;
+  int pad[3];
+};
+
+struct nnls_handle {
+  cudaStream_t stream = nullptr;
+  int device = 0, sms = 148;
+  nnls_params prm{};
+  // problem
+  int m = 0, n = 0, ldg = 0;
+  int64_t nnz = 0;
+  bool loaded = false, gram_ready = false;
+  Buf rowptr, colind, vals, b;           // CSR + rhs
+  Buf colptr, rowind, cvals, cursor, tmp_row, tmp_val;  // CSC
+  Buf Gc;                                 // G (n x ldg) followed by c (n)
+  Buf mask, x, y, xF, Fidx, Gidx;         // pivot state
+  Buf Lt, flags;                          // Cholesky tiles + DAG flags
+  Buf U, V, W, X, R, partials, xfin;      // LSQR / report
+  Buf st, err, trace;
+  size_t ntile = 0;
+  int trace_cap = 0;
+  HostState* h = nullptr;                 // pinned readback
+  // batched
+  bool batched = false;
+  int batch = 0;
+  Buf b_nnz_off, b_info_i, b_info_d, b_x, b_mask;
+};
+
+namespace {
+
+nnls_status set_stream_device(nnls_handle* h, void* stream) {
+  h->stream = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  h->device = dev;
+  CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev));
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major < 10) return NNLS_ERR_CUDA;  // sm_100a code only
+  return NNLS_OK;
+}
+
+nnls_status check_params(const nnls_params* p) {
+  if (!(p->zero_tol >= 0.0) || p->p_max < 0 || p->max_iter < 0 || p->lsqr_mode < 0 ||
+      p->lsqr_mode > 2)
+    return NNLS_ERR_INVALID_ARG;
+  return NNLS_OK;
+}
+
+nnls_status map_err_bits(int e) {
+  if (e & 1) return NNLS_ERR_DIMENSION;
+  if (e & 2) return NNLS_ERR_INDEX;
+  if (e & 4) return NNLS_ERR_NONFINITE;
+  return NNLS_OK;
+}
+
+// upload + validate + CSC + Gram over rows [r0, r1)
+nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colind, const double* vals, const double* b, int r0, int r1) {
+  if (!h || m < 1 || n < 1 || m < n || nnz < 0 || !rowptr || !b) return NNLS_ERR_INVALID_ARG;
+  if (nnz > 0 && (!colind || !vals)) return NNLS_ERR_INVALID_ARG;
+  if (nnz > 0x7fffffffLL) return NNLS_ERR_INVALID_ARG;
+  if ((int64_t)n * 8 > 200 * 1024) return NNLS_ERR_INVALID_ARG;  // Gram row accumulator in smem
+  if (r0 < 0 || r1 > m || r0 > r1) return NNLS_ERR_INVALID_ARG;
+  cudaStream_t s = h->stream;
+  h->m = m;
+  h->n = n;
+  h->nnz = nnz;
+  h->ldg = round_up(n, 4);
+  h->gram_ready = false;
+  h->loaded = false;
+  CK(ensure(h->rowptr, sizeof(int32_t) * (size_t)(m + 1)));
+  CK(ensure(h->colind, sizeof(int32_t) * (size_t)nnz));
+  CK(ensure(h->vals, sizeof(double) * (size_t)nnz));
+  CK(ensure(h->b, sizeof(double) * (size_t)m));
+  CK(ensure(h->colptr, sizeof(int32_t) * (size_t)(n + 1)));
+  CK(ensure(h->cursor, sizeof(int32_t) * (size_t)(n + 1)));
+  CK(ensure(h->rowind, sizeof(int32_t) * (size_t)nnz));
+  CK(ensure(h->cvals, sizeof(double) * (size_t)nnz));
+  CK(ensure(h->tmp_row, sizeof(int32_t) * (size_t)nnz));
+  CK(ensure(h->tmp_val, sizeof(double) * (size_t)nnz));
+  CK(ensure(h->Gc, sizeof(double) * ((size_t)n * h->ldg + n)));
+  CK(ensure(h->mask, (size_t)n));
+  CK(ensure(h->x, sizeof(double) * (size_t)n));
+  CK(ensure(h->y, sizeof(double) * (size_t)n));
+  CK(ensure(h->xF, sizeof(double) * (size_t)(n + kTile)));
+  CK(ensure(h->Fidx, sizeof(int32_t) * (size_t)n));
+  CK(ensure(h->Gidx, sizeof(int32_t) * (size_t)n));
+  const size_t ntile = chol_tile_count(n);
+  const size_t nflags = ntile + (size_t)(n + 1 + kTile) / kTile + 1;
+  if (h->flags.cap < sizeof(int) * nflags) {
+    CK(ensure(h->flags, sizeof(int) * nflags));
+    CK(cudaMemsetAsync(h->flags.p, 0, h->flags.cap, s));
+    // a fresh flag array must not alias a reused epoch: reset the epoch too
+    CK(ensure(h->st, sizeof(DevState)));
+    CK(cudaMemsetAsync(h->st.p, 0, sizeof(DevState), s));
+  }
+  h->ntile = ntile;
+  CK(ensure(h->Lt, sizeof(double) * ntile * kTile * kTile));
+  CK(ensure(h->U, sizeof(double) * (size_t)m));
+  CK(ensure(h->R, sizeof(double) * (size_t)m));
+  CK(ensure(h->V, sizeof(double) * (size_t)n));
+  CK(ensure(h->W, sizeof(double) * (size_t)n));
+  CK(ensure(h->X, sizeof(double) * (size_t)n));
+  CK(ensure(h->xfin, sizeof(double) * (size_t)n));
+  CK(ensure(h->partials, sizeof(double) * 8 * (size_t)(h->sms * 4)));
+  CK(ensure(h->st, sizeof(DevState)));
+  CK(ensure(h->err, sizeof(int) * 4));
+  const int cap = h->prm.trace ? (h->prm.max_iter > 0 ? h->prm.max_iter : 10 * n) + 1 : 0;
+  h->trace_cap = cap;
+  if (cap > 0) CK(ensure(h->trace, sizeof(TraceRec) * (size_t)cap));
+
+  CK(cudaMemcpyAsync(h->rowptr.p, rowptr, sizeof(int32_t) * (size_t)(m + 1), cudaMemcpyDefault, s));
+  if (nnz > 0) {
+    CK(cudaMemcpyAsync(h->colind.p, colind, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDefault, s));
+    CK(cudaMemcpyAsync(h->vals.p, vals, sizeof(double) * (size_t)nnz, cudaMemcpyDefault, s));
+  }
+  CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)m, cudaMemcpyDefault, s));
+  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int), s));
+  CK(launch_validate(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                     P<double>(h->b), P<int>(h->err), s));
+  // validation must pass before structure-dependent kernels touch the data
+  int herr = 0;
+  CK(cudaMemcpyAsync(&h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  herr = h->h->err;
+  if (herr) return map_err_bits(herr);
+  CK(launch_csr_to_csc(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                       P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
+                       P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s));
+  double* G = P<double>(h->Gc);
+  double* c = G + (size_t)n * h->ldg;
+  CK(launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                 P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals), P<double>(h->b),
+                 r0, r1, G, h->ldg, c, h->sms, s));
+  h->loaded = true;
+  return NNLS_OK;
+}
+
+nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
+  if (!out) return NNLS_ERR_INVALID_ARG;
+  *out = nullptr;
+  nnls_handle* h = new (std::nothrow) nnls_handle();
+  if (!h) return NNLS_ERR_OOM;
+  nnls_params_default(&h->prm);
+  if (p) {
+    nnls_status ps = check_params(p);
+    if (ps != NNLS_OK) {
+      delete h;
+      return ps;
+    }
+    h->prm = *p;
+  }
+  nnls_status s = set_stream_device(h, stream);
+  if (s == NNLS_OK && cudaMallocHost(&h->h, sizeof(HostState)) != cudaSuccess) s = NNLS_ERR_OOM;
+  if (s != NNLS_OK) {
+    if (h->h) cudaFreeHost(h->h);
+    delete h;
+    return s;
+  }
+  memset(h->h, 0, sizeof(HostState));
+  *out = h;
+  return NNLS_OK;
+}
+
+void free_buf(Buf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+nnls_status read_state(nnls_handle* h) {
+  CK(cudaMemcpyAsync(&h->h->st, h->st.p, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return NNLS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nnls_status_string(nnls_status s) {
+  switch (s) {
+    case NNLS_OK: return "ok";
+    case NNLS_ERR_INVALID_ARG: return "invalid argument";
+    case NNLS_ERR_DIMENSION: return "CSR dimension error";
+    case NNLS_ERR_INDEX: return "CSR column index error";
+    case NNLS_ERR_NONFINITE: return "non-finite value";
+    case NNLS_ERR_CUDA: return "CUDA error";
+    case NNLS_ERR_OOM: return "out of device memory";
+    case NNLS_ERR_NOT_PD: return "Cholesky pivot not positive (A_F rank deficient or kappa^2 eps >= 1)";
+    case NNLS_ITERATION_LIMIT: return "iteration limit";
+    case NNLS_ERR_STATE: return "call out of order";
+  }
+  return "unknown";
+}
+
+nnls_status nnls_params_default(nnls_params* p) {
+  if (!p) return NNLS_ERR_INVALID_ARG;
+  memset(p, 0, sizeof(*p));
+  p->zero_tol = 1e-12;
+  p->p_max = 3;
+  p->max_iter = 0;
+  p->lsqr_mode = 1;
+  p->lsqr_itn_limit = 0;
+  p->lsqr_atol = 1e-15;
+  p->lsqr_btol = 1e-15;
+  p->lsqr_conlim = 1e8;
+  p->trace = 0;
+  p->kkt = 1;
+  return NNLS_OK;
+}
+
+nnls_status nnls_device_info(int32_t* sm_count, int32_t* cc, int32_t* device) {
+  int dev = 0, ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return NNLS_ERR_CUDA;
+  CK(cudaGetDevice(&dev));
+  int sms = 0, ma = 0, mi = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&ma, cudaDevAttrComputeCapabilityMajor, dev));
+  CK(cudaDeviceGetAttribute(&mi, cudaDevAttrComputeCapabilityMinor, dev));
+  if (sm_count) *sm_count = sms;
+  if (cc) *cc = ma * 10 + mi;
+  if (device) *device = dev;
+  return NNLS_OK;
+}
+
+nnls_status nnls_create(nnls_handle** h, const nnls_params* p, void* cuda_stream) {
+  return create_impl(h, p, cuda_stream);
+}
+
+nnls_status nnls_load(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colind, const double* vals, const double* b) {
+  if (!h || h->batched) return NNLS_ERR_INVALID_ARG;
+  nnls_status s = load_impl(h, m, n, nnz, rowptr, colind, vals, b, 0, m);
+  if (s == NNLS_OK) h->gram_ready = true;
+  return s;
+}
+
+nnls_status nnls_setup(nnls_handle** h, int32_t m, int32_t n, int64_t nnz, const int32_t* rowptr,
+                       const int32_t* colind, const double* vals, const double* b,
+                       const nnls_params* p, void* cuda_stream) {
+  nnls_status s = create_impl(h, p, cuda_stream);
+  if (s != NNLS_OK) return s;
+  s = nnls_load(*h, m, n, nnz, rowptr, colind, vals, b);
+  if (s != NNLS_OK) {
+    nnls_destroy(*h);
+    *h = nullptr;
+  }
+  return s;
+}
+
+nnls_status nnls_setup_shard(nnls_handle** h, int32_t m, int32_t n, int64_t nnz,
+                             const int32_t* rowptr, const int32_t* colind, const double* vals,
+                             const double* b, int32_t row_begin, int32_t row_end,
+                             const nnls_params* p, void* cuda_stream) {
+  nnls_status s = create_impl(h, p, cuda_stream);
+  if (s != NNLS_OK) return s;
+  s = load_impl(*h, m, n, nnz, rowptr, colind, vals, b, row_begin, row_end);
+  if (s != NNLS_OK) {
+    nnls_destroy(*h);
+    *h = nullptr;
+  }
+  return s;
+}
+
+nnls_status nnls_gram_buffer(nnls_handle* h, double** dev_ptr, size_t* count, int32_t* ld) {
+  if (!h || !h->loaded || h->batched) return NNLS_ERR_STATE;
+  if (dev_ptr) *dev_ptr = P<double>(h->Gc);
+  if (count) *count = (size_t)h->n * h->ldg + h->n;
+  if (ld) *ld = h->ldg;
+  return NNLS_OK;
+}
+
+nnls_status nnls_gram_finalize(nnls_handle* h) {
+  if (!h || !h->loaded || h->batched) return NNLS_ERR_STATE;
+  h->gram_ready = true;
+  return NNLS_OK;
+}
+
+nnls_status nnls_set_params(nnls_handle* h, const nnls_params* p) {
+  if (!h || !p) return NNLS_ERR_INVALID_ARG;
+  nnls_status s = check_params(p);
+  if (s != NNLS_OK) return s;
+  h->prm = *p;
+  if (h->loaded && !h->batched) {
+    const int cap = p->trace ? (p->max_iter > 0 ? p->max_iter : 10 * h->n) + 1 : 0;
+    h->trace_cap = cap;
+    if (cap > 0) CK(ensure(h->trace, sizeof(TraceRec) * (size_t)cap));
+  }
+  return NNLS_OK;
+}
+
+nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
+  if (!h || h->batched) return NNLS_ERR_INVALID_ARG;
+  if (!h->loaded || !h->gram_ready) return NNLS_ERR_STATE;
+  cudaStream_t s = h->stream;
+  const int n = h->n;
+  const nnls_params& p = h->prm;
+  const int max_iter = p.max_iter > 0 ? p.max_iter : 10 * n;
+  double* G = P<double>(h->Gc);
+  double* c = G + (size_t)n * h->ldg;
+  DevState* st = P<DevState>(h->st);
+  TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
+  CK(launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
+                 p.p_max, max_iter, s));
+  for (;;) {
+    CK(launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), P<int32_t>(h->Fidx),
+                     P<int32_t>(h->Gidx), st, trace, h->trace_cap, s));
+    nnls_status rs = read_state(h);
+    if (rs != NNLS_OK) return rs;
+    const DevState& hs = h->h->st;
+    if (hs.done || hs.status != 0) break;
+    if (hs.f > 0)
+      CK(launch_cholesky_solve(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt),
+                               P<int>(h->flags), P<double>(h->xF), st, h->sms, s));
+    CK(launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
+                   P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st, h->sms,
+                   s));
+  }
+  LsqrArgs a{};
+  a.m = h->m;
+  a.n = n;
+  a.rowptr = P<int32_t>(h->rowptr);
+  a.colind = P<int32_t>(h->colind);
+  a.vals = P<double>(h->vals);
+  a.colptr = P<int32_t>(h->colptr);
+  a.rowind = P<int32_t>(h->rowind);
+  a.cvals = P<double>(h->cvals);
+  a.b = P<double>(h->b);
+  a.mask = P<uint8_t>(h->mask);
+  a.x_ne = P<double>(h->x);
+  a.x_out = P<double>(h->xfin);
+  a.U = P<double>(h->U);
+  a.V = P<double>(h->V);
+  a.W = P<double>(h->W);
+  a.X = P<double>(h->X);
+  a.R = P<double>(h->R);
+  a.partials = P<double>(h->partials);
+  a.st = st;
+  a.mode = p.lsqr_mode;
+  a.itn_limit = p.lsqr_itn_limit;
+  a.atol = p.lsqr_atol;
+  a.btol = p.lsqr_btol;
+  a.conlim = p.lsqr_conlim;
+  a.tol = p.zero_tol;
+  a.kkt = p.kkt;
+  a.G = G;
+  a.ldg = h->ldg;
+  a.c = c;
+  CK(launch_lsqr_final(a, h->sms, s));
+  if (x_out) CK(cudaMemcpyAsync(x_out, h->xfin.p, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
+  nnls_status rs = read_state(h);
+  if (rs != NNLS_OK) return rs;
+  const DevState& hs = h->h->st;
+  nnls_status status = NNLS_OK;
+  if (hs.status == 7) status = NNLS_ERR_NOT_PD;
+  else if (hs.status == 8) status = NNLS_ITERATION_LIMIT;
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->status = status;
+    info->iterations = hs.iter;
+    info->single_exchanges = hs.singles;
+    info->free_count = hs.free_count;
+    info->lsqr_iterations = hs.lsqr_iterations;
+    info->lsqr_stop = hs.lsqr_stop;
+    info->infeasible_after_lsqr = hs.infeasible_after_lsqr;
+    info->not_pd_column = hs.status == 7 ? hs.not_pd_col : -1;
+    info->objective = hs.objective;
+    info->kkt_min_x = hs.kkt_min_x;
+    info->kkt_min_y = hs.kkt_min_y;
+    info->kkt_max_comp = hs.kkt_max_comp;
+    info->kkt_dot = hs.kkt_dot;
+  }
+  return status;
+}
+
+nnls_status nnls_get_free_set(nnls_handle* h, uint8_t* mask_out) {
+  if (!h || !mask_out) return NNLS_ERR_INVALID_ARG;
+  if (!h->loaded || h->batched) return NNLS_ERR_STATE;
+  CK(cudaMemcpyAsync(mask_out, h->mask.p, (size_t)h->n, cudaMemcpyDefault, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return NNLS_OK;
+}
+
+nnls_status nnls_get_x_ne(nnls_handle* h, double* x_out) {
+  if (!h || !x_out) return NNLS_ERR_INVALID_ARG;
+  if (!h->loaded || h->batched) return NNLS_ERR_STATE;
+  CK(cudaMemcpyAsync(x_out, h->x.p, sizeof(double) * (size_t)h->n, cudaMemcpyDefault, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return NNLS_OK;
+}
+
+nnls_status nnls_get_trace(nnls_handle* h, nnls_iter_rec* recs, int32_t cap, int32_t* count) {
+  if (!h || (cap > 0 && !recs)) return NNLS_ERR_INVALID_ARG;
+  if (!h->loaded || h->batched) return NNLS_ERR_STATE;
+  nnls_status rs = read_state(h);
+  if (rs != NNLS_OK) return rs;
+  int it = h->h->st.iter;
+  int cnt = it < h->trace_cap ? it : h->trace_cap;
+  if (cnt > cap) cnt = cap;
+  if (count) *count = cnt;
+  if (cnt > 0) {
+    static_assert(sizeof(nnls_iter_rec) == sizeof(TraceRec), "trace layout");
+    CK(cudaMemcpyAsync(recs, h->trace.p, sizeof(TraceRec) * (size_t)cnt, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  return NNLS_OK;
+}
+
+nnls_status nnls_get_gram(nnls_handle* h, double* G_out, double* c_out) {
+  if (!h) return NNLS_ERR_INVALID_ARG;
+  if (!h->loaded || h->batched) return NNLS_ERR_STATE;
+  const int n = h->n;
+  double* G = P<double>(h->Gc);
+  if (G_out)
+    CK(cudaMemcpy2DAsync(G_out, sizeof(double) * n, G, sizeof(double) * h->ldg, sizeof(double) * n,
+                         n, cudaMemcpyDefault, h->stream));
+  if (c_out)
+    CK(cudaMemcpyAsync(c_out, G + (size_t)n * h->ldg, sizeof(double) * n, cudaMemcpyDefault,
+                       h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return NNLS_OK;
+}
+
+nnls_status nnls_destroy(nnls_handle* h) {
+  if (!h) return NNLS_OK;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  Buf* bufs[] = {&h->rowptr, &h->colind, &h->vals, &h->b, &h->colptr, &h->rowind, &h->cvals,
+                 &h->cursor, &h->tmp_row, &h->tmp_val, &h->Gc, &h->mask, &h->x, &h->y, &h->xF,
+                 &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
+                 &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
+                 &h->b_info_d, &h->b_x, &h->b_mask};
+  for (Buf* b : bufs) free_buf(*b);
+  if (h->h) cudaFreeHost(h->h);
+  delete h;
+  return NNLS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Step-level entry points (device buffers) for kernel unit tests.
+namespace {
+struct TmpBufs {
+  Buf bufs[12];
+  ~TmpBufs() {
+    for (Buf& b : bufs) free_buf(b);
+  }
+};
+nnls_status upload_state(DevState* d, const DevState& hs, cudaStream_t s) {
+  CK(cudaMemcpyAsync(d, &hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  return NNLS_OK;
+}
+nnls_status download_state(DevState& hs, const DevState* d, cudaStream_t s) {
+  CK(cudaMemcpyAsync(&hs, d, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return NNLS_OK;
+}
+int sm_count_now() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+}  // namespace
+
+extern "C" {
+
+nnls_status nnls_step_gram(int32_t m, int32_t n, int64_t nnz, const int32_t* rowptr,
+                           const int32_t* colind, const double* vals, const double* b, double* G,
+                           int32_t ldg, double* c, void* stream) {
+  if (m < 1 || n < 1 || nnz < 0 || !rowptr || !b || !G || !c || ldg < n) return NNLS_ERR_INVALID_ARG;
+  if ((int64_t)n * 8 > 200 * 1024) return NNLS_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TmpBufs t;
+  CK(ensure(t.bufs[0], sizeof(int32_t) * (size_t)(n + 1)));
+  CK(ensure(t.bufs[1], sizeof(int32_t) * (size_t)(n + 1)));
+  CK(ensure(t.bufs[2], sizeof(int32_t) * (size_t)nnz));
+  CK(ensure(t.bufs[3], sizeof(double) * (size_t)nnz));
+  CK(ensure(t.bufs[4], sizeof(int32_t) * (size_t)nnz));
+  CK(ensure(t.bufs[5], sizeof(double) * (size_t)nnz));
+  CK(launch_csr_to_csc(m, n, nnz, rowptr, colind, vals, P<int32_t>(t.bufs[0]), P<int32_t>(t.bufs[2]),
+                       P<double>(t.bufs[3]), P<int32_t>(t.bufs[1]), P<int32_t>(t.bufs[4]),
+                       P<double>(t.bufs[5]), s));
+  CK(launch_gram(m, n, rowptr, colind, vals, P<int32_t>(t.bufs[0]), P<int32_t>(t.bufs[2]),
+                 P<double>(t.bufs[3]), b, 0, m, G, ldg, c, sm_count_now(), s));
+  CK(cudaStreamSynchronize(s));
+  return NNLS_OK;
+}
+
+nnls_status nnls_step_normal_solve(int32_t n, const double* G, int32_t ldg, const double* c,
+                                   int32_t f, const int32_t* Fidx, double* xF, int32_t* not_pd_col,
+                                   void* stream) {
+  if (n < 1 || f < 0 || f > n || !G || !c || ldg < n || (f > 0 && (!Fidx || !xF)))
+    return NNLS_ERR_INVALID_ARG;
+  if (f == 0) return NNLS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TmpBufs t;
+  const size_t ntile = chol_tile_count(n);
+  CK(ensure(t.bufs[0], sizeof(double) * ntile * kTile * kTile));
+  CK(ensure(t.bufs[1], sizeof(int) * (ntile + (size_t)(n + 1 + kTile) / kTile + 1)));
+  CK(ensure(t.bufs[2], sizeof(DevState)));
+  CK(ensure(t.bufs[3], sizeof(double) * (size_t)(f + kTile)));
+  CK(cudaMemsetAsync(t.bufs[1].p, 0, t.bufs[1].cap, s));
+  DevState hs;
+  memset(&hs, 0, sizeof(hs));
+  hs.f = f;
+  hs.g = n - f;
+  hs.epoch = 1;
+  hs.not_pd_col = -1;
+  nnls_status r = upload_state(P<DevState>(t.bufs[2]), hs, s);
+  if (r != NNLS_OK) return r;
+  CK(launch_cholesky_solve(n, G, ldg, c, Fidx, P<double>(t.bufs[0]), P<int>(t.bufs[1]),
+                           P<double>(t.bufs[3]), P<DevState>(t.bufs[2]), sm_count_now(), s));
+  CK(cudaMemcpyAsync(xF, t.bufs[3].p, sizeof(double) * (size_t)f, cudaMemcpyDeviceToDevice, s));
+  r = download_state(hs, P<DevState>(t.bufs[2]), s);
+  if (r != NNLS_OK) return r;
+  if (not_pd_col) *not_pd_col = hs.status == 7 ? hs.not_pd_col : -1;
+  return hs.status == 7 ? NNLS_ERR_NOT_PD : NNLS_OK;
+}
+
+nnls_status nnls_step_exchange(int32_t n, uint8_t* mask, const double* x, const double* y,
+                               int32_t p_max, int32_t* state, int32_t* k_out, int32_t* branch_out,
+                               void* stream) {
+  if (n < 1 || !mask || !x || !y || !state) return NNLS_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TmpBufs t;
+  CK(ensure(t.bufs[0], sizeof(DevState)));
+  CK(ensure(t.bufs[1], sizeof(int32_t) * (size_t)n));
+  CK(ensure(t.bufs[2], sizeof(int32_t) * (size_t)n));
+  DevState hs;
+  memset(&hs, 0, sizeof(hs));
+  hs.N = state[0];
+  hs.p = state[1];
+  hs.iter = state[2];
+  hs.singles = state[3];
+  hs.max_iter = 0x7fffffff;
+  hs.p_max = p_max;
+  nnls_status r = upload_state(P<DevState>(t.bufs[0]), hs, s);
+  if (r != NNLS_OK) return r;
+  CK(launch_decide(n, mask, x, y, P<int32_t>(t.bufs[1]), P<int32_t>(t.bufs[2]),
+                   P<DevState>(t.bufs[0]), nullptr, 0, s));
+  r = download_state(hs, P<DevState>(t.bufs[0]), s);
+  if (r != NNLS_OK) return r;
+  state[0] = hs.N;
+  state[1] = hs.p;
+  state[2] = hs.iter;
+  state[3] = hs.singles;
+  if (k_out) *k_out = hs.k;
+  if (branch_out) *branch_out = hs.done ? -1 : hs.branch;
+  return NNLS_OK;
+}
+
+nnls_status nnls_step_dual(int32_t n, const double* G, int32_t ldg, const double* c,
+                           const uint8_t* mask, double* x, double* y, double tol, void* stream) {
+  if (n < 1 || !G || !c || !mask || !x || !y || ldg < n) return NNLS_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TmpBufs t;
+  CK(ensure(t.bufs[0], sizeof(DevState)));
+  CK(ensure(t.bufs[1], sizeof(int32_t) * (size_t)n));
+  CK(ensure(t.bufs[2], sizeof(int32_t) * (size_t)n));
+  CK(ensure(t.bufs[3], sizeof(double) * (size_t)n));
+  CK(cudaMemsetAsync(t.bufs[0].p, 0, sizeof(DevState), s));
+  CK(launch_compact(n, mask, x, P<int32_t>(t.bufs[1]), P<int32_t>(t.bufs[2]), P<double>(t.bufs[3]),
+                    P<DevState>(t.bufs[0]), s));
+  CK(launch_dual(n, G, ldg, c, P<int32_t>(t.bufs[1]), P<int32_t>(t.bufs[2]), P<double>(t.bufs[3]),
+                 const_cast<uint8_t*>(mask), x, y, tol, P<DevState>(t.bufs[0]), sm_count_now(), s));
+  CK(cudaStreamSynchronize(s));
+  return NNLS_OK;
+}
+
+nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n,
+                              const int64_t* nnz_off, const int32_t* rowptr, const int32_t* colind,
+                              const double* vals, const double* b) {
+  if (!h || !h->batched) return NNLS_ERR_INVALID_ARG;
+  if (batch < 1 || n < 1 || m < n || n > 64 || m > 256 || !nnz_off || !rowptr || !b)
+    return NNLS_ERR_INVALID_ARG;
+  cudaStream_t s = h->stream;
+  h->loaded = false;
+  // nnz offsets are needed on the host to size shared memory (nnz_max)
+  int64_t* hoff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(batch + 1));
+  if (!hoff) return NNLS_ERR_OOM;
+  if (cudaMemcpy(hoff, nnz_off, sizeof(int64_t) * (size_t)(batch + 1), cudaMemcpyDefault) !=
+      cudaSuccess) {
+    free(hoff);
+    return NNLS_ERR_CUDA;
+  }
+  int64_t nnz_max = 0;
+  bool bad = hoff[0] != 0;
+  for (int q = 0; q < batch && !bad; ++q) {
+    const int64_t d = hoff[q + 1] - hoff[q];
+    if (d < 0 || d > (int64_t)m * n) bad = true;
+    if (d > nnz_max) nnz_max = d;
+  }
+  const int64_t total = hoff[batch];
+  free(hoff);
+  if (bad) return NNLS_ERR_DIMENSION;
+  if (total > 0 && (!colind || !vals)) return NNLS_ERR_INVALID_ARG;
+  if (batched_smem_bytes(m, n, (int)nnz_max) > 220 * 1024) return NNLS_ERR_INVALID_ARG;
+  h->m = m;
+  h->n = n;
+  h->batch = batch;
+  h->nnz = total;
+  h->ldg = (int)nnz_max;  // batched: ldg holds nnz_max
+  CK(ensure(h->b_nnz_off, sizeof(int64_t) * (size_t)(batch + 1)));
+  CK(ensure(h->rowptr, sizeof(int32_t) * (size_t)batch * (m + 1)));
+  CK(ensure(h->colind, sizeof(int32_t) * (size_t)total));
+  CK(ensure(h->vals, sizeof(double) * (size_t)total));
+  CK(ensure(h->b, sizeof(double) * (size_t)batch * m));
+  CK(ensure(h->b_x, sizeof(double) * (size_t)batch * n));
+  CK(ensure(h->b_mask, (size_t)batch * n));
+  CK(ensure(h->b_info_i, sizeof(int32_t) * 8 * (size_t)batch));
+  CK(ensure(h->b_info_d, sizeof(double) * 5 * (size_t)batch));
+  CK(ensure(h->err, sizeof(int) * 4));
+  CK(cudaMemcpyAsync(h->b_nnz_off.p, nnz_off, sizeof(int64_t) * (size_t)(batch + 1), cudaMemcpyDefault, s));
+  CK(cudaMemcpyAsync(h->rowptr.p, rowptr, sizeof(int32_t) * (size_t)batch * (m + 1), cudaMemcpyDefault, s));
+  if (total > 0) {
+    CK(cudaMemcpyAsync(h->colind.p, colind, sizeof(int32_t) * (size_t)total, cudaMemcpyDefault, s));
+    CK(cudaMemcpyAsync(h->vals.p, vals, sizeof(double) * (size_t)total, cudaMemcpyDefault, s));
+  }
+  CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)batch * m, cudaMemcpyDefault, s));
+  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int), s));
+  CK(launch_validate_batched(batch, m, n, P<int64_t>(h->b_nnz_off), P<int32_t>(h->rowptr),
+                             P<int32_t>(h->colind), P<double>(h->vals), P<double>(h->b),
+                             P<int>(h->err), s));
+  CK(cudaMemcpyAsync(&h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h->h->err) return map_err_bits(h->h->err);
+  h->loaded = true;
+  return NNLS_OK;
+}
+
+nnls_status nnls_setup_batched(nnls_handle** h, int32_t batch, int32_t m, int32_t n,
+                               const int64_t* nnz_off, const int32_t* rowptr, const int32_t* colind,
+                               const double* vals, const double* b, const nnls_params* p,
+                               void* cuda_stream) {
+  nnls_status s = create_impl(h, p, cuda_stream);
+  if (s != NNLS_OK) return s;
+  (*h)->batched = true;
+  s = nnls_load_batched(*h, batch, m, n, nnz_off, rowptr, colind, vals, b);
+  if (s != NNLS_OK) {
+    nnls_destroy(*h);
+    *h = nullptr;
+  }
+  return s;
+}
+
+nnls_status nnls_create_batched(nnls_handle** h, const nnls_params* p, void* cuda_stream) {
+  nnls_status s = create_impl(h, p, cuda_stream);
+  if (s == NNLS_OK) (*h)->batched = true;
+  return s;
+}
+
+nnls_status nnls_solve_batched(nnls_handle* h, double* x_out, nnls_info* info_out,
+                               uint8_t* mask_out) {
+  if (!h || !h->batched) return NNLS_ERR_INVALID_ARG;
+  if (!h->loaded) return NNLS_ERR_STATE;
+  cudaStream_t s = h->stream;
+  const nnls_params& p = h->prm;
+  BatchArgs a{};
+  a.batch = h->batch;
+  a.m = h->m;
+  a.n = h->n;
+  a.nnz_off = P<int64_t>(h->b_nnz_off);
+  a.rowptr = P<int32_t>(h->rowptr);
+  a.colind = P<int32_t>(h->colind);
+  a.vals = P<double>(h->vals);
+  a.b = P<double>(h->b);
+  a.x_out = P<double>(h->b_x);
+  a.mask_out = P<uint8_t>(h->b_mask);
+  a.info_i = P<int32_t>(h->b_info_i);
+  a.info_d = P<double>(h->b_info_d);
+  a.tol = p.zero_tol;
+  a.atol = p.lsqr_atol;
+  a.btol = p.lsqr_btol;
+  a.conlim = p.lsqr_conlim;
+  a.p_max = p.p_max;
+  a.max_iter = p.max_iter > 0 ? p.max_iter : 10 * h->n;
+  a.lsqr_mode = p.lsqr_mode;
+  a.itn_limit = p.lsqr_itn_limit;
+  a.kkt = p.kkt;
+  CK(launch_batched_nnz(a, h->ldg, h->sms, s));
+  const size_t nb = (size_t)h->batch;
+  if (x_out) CK(cudaMemcpyAsync(x_out, h->b_x.p, sizeof(double) * nb * h->n, cudaMemcpyDefault, s));
+  if (mask_out) CK(cudaMemcpyAsync(mask_out, h->b_mask.p, nb * h->n, cudaMemcpyDefault, s));
+  nnls_status worst = NNLS_OK;
+  if (info_out) {
+    int32_t* ii = (int32_t*)malloc(sizeof(int32_t) * 8 * nb);
+    double* dd = (double*)malloc(sizeof(double) * 5 * nb);
+    if (!ii || !dd) {
+      free(ii);
+      free(dd);
+      return NNLS_ERR_OOM;
+    }
+    cudaError_t e1 = cudaMemcpyAsync(ii, h->b_info_i.p, sizeof(int32_t) * 8 * nb, cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaMemcpyAsync(dd, h->b_info_d.p, sizeof(double) * 5 * nb, cudaMemcpyDeviceToHost, s);
+    cudaError_t e3 = cudaStreamSynchronize(s);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+      free(ii);
+      free(dd);
+      return NNLS_ERR_CUDA;
+    }
+    for (size_t q = 0; q < nb; ++q) {
+      nnls_info& o = info_out[q];
+      memset(&o, 0, sizeof(o));
+      const int st = ii[q * 8 + 0];
+      o.status = st == 7 ? NNLS_ERR_NOT_PD : (st == 8 ? NNLS_ITERATION_LIMIT : NNLS_OK);
+      if (o.status != NNLS_OK && worst == NNLS_OK) worst = (nnls_status)o.status;
+      o.iterations = ii[q * 8 + 1];
+      o.single_exchanges = ii[q * 8 + 2];
+      o.free_count = ii[q * 8 + 3];
+      o.lsqr_iterations = ii[q * 8 + 4];
+      o.lsqr_stop = ii[q * 8 + 5];
+      o.infeasible_after_lsqr = ii[q * 8 + 6];
+      o.not_pd_column = ii[q * 8 + 7];
+      o.objective = dd[q * 5 + 0];
+      o.kkt_min_x = dd[q * 5 + 1];
+      o.kkt_min_y = dd[q * 5 + 2];
+      o.kkt_max_comp = dd[q * 5 + 3];
+      o.kkt_dot = dd[q * 5 + 4];
+    }
+    free(ii);
+    free(dd);
+  } else {
+    CK(cudaStreamSynchronize(s));
+  }
+  return worst;
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// common.cuh -- device helpers shared by the sm_100a kernels of libnnls_b200.
+// (Not shared with the CPU oracle: oracle/ and csrc/ have no code in common.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define NNLS_DEV __device__ __forceinline__
+
+namespace nnls {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Device-resident solver state of one problem (one 128-byte line).
+struct DevState {
+  int32_t k;            // infeasible count of the last decide
+  int32_t N;            // best infeasible count so far (N = inf -> n+1)
+  int32_t p;            // no-progress counter
+  int32_t iter;         // completed normal-equation solves (reading c11)
+  int32_t singles;      // single exchanges taken
+  int32_t f, g;         // |F|, |G| after the last exchange
+  int32_t branch;       // -1 feasible, 0, 1, 2
+  int32_t done;         // 1: feasible (k == 0), stop
+  int32_t status;       // 0 ok, 7 NOT_PD, 8 ITERATION_LIMIT
+  int32_t not_pd_col;   // failing pivot position in F
+  int32_t epoch;        // Cholesky DAG epoch (flags == epoch mean "ready")
+  int32_t tile_counter; // DAG work counter of the factorization
+  int32_t solve_counter;// DAG work counter of the back substitution
+  int32_t max_iter;
+  int32_t p_max;
+  unsigned long long below_bits;  // trace: max |v| < tol (as ordered bits)
+  unsigned long long above_bits;  // trace: min |v| >= tol
+  // final-step report
+  int32_t lsqr_iterations, lsqr_stop, infeasible_after_lsqr, free_count;
+  double objective, kkt_min_x, kkt_min_y, kkt_max_comp, kkt_dot;
+  int32_t pad[2];
+};
+
+struct TraceRec {
+  int32_t iter, k, branch, f;
+  double below_tol, above_tol;
+};
+
+NNLS_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+NNLS_DEV int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+NNLS_DEV int warp_max_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+NNLS_DEV double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+NNLS_DEV double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// D(8x8) += A(8x4) * B(4x8) in FP64 on the tensor pipe (SASS DMMA.8x8x4).
+// Fragments (lane = l): a = A[l>>2][l&3]; b = B[k=l&3][n=l>>2];
+// c0,c1 = C[l>>2][2*(l&3) + {0,1}].
+NNLS_DEV void dmma8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+NNLS_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+NNLS_DEV void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+NNLS_DEV int ld_volatile(const int* p) { return *(volatile const int*)p; }
+
+// spin (one thread) until *flag == want
+NNLS_DEV void wait_flag(const int* flag, int want) {
+  if (ld_acquire(flag) == want) return;
+  unsigned ns = 32;
+  while (ld_acquire(flag) != want) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+// non-negative doubles compare like their bit patterns
+NNLS_DEV unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
+
+}  // namespace nnls

@@ -1,0 +1,243 @@
+// ingest_gram.cu -- a0 (CSR validation, CSC build) and a1 (Gram + A^T b).
+//
+// a1 follows PAPER.md P:126: "A^T A_ij is just the dot product of the i-th and
+// j-th columns of A ... we can precompute the full A^T A" -- formed once per
+// problem and cached.  B200 design: one warp owns one row i of G and
+// accumulates  G[i,:] = sum_{r in col i} a_ri * A[r,:]  (Gustavson row-by-row
+// SpGEMM of A^T A) into a dense FP64 accumulator in shared memory; lanes
+// scatter the entries of sparse row r (distinct columns, no conflicts), rows r
+// are taken in increasing order, products and sums are rounded separately
+// (no FMA).  Every G_ij is therefore the sum of the same terms in the same
+// order as the dense definition -> bit-identical to the CPU oracle, exactly
+// symmetric, deterministic.  The finished row is streamed to HBM once
+// (coalesced), so HBM traffic is the n^2 output write plus L2-resident CSR
+// reads.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace nnls {
+
+// ---------------------------------------------------------------- validate
+__global__ void validate_kernel(int m, int n, int64_t nnz, const int32_t* __restrict__ rowptr,
+                                const int32_t* __restrict__ colind,
+                                const double* __restrict__ vals, const double* __restrict__ b,
+                                int* err) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  int e_local = 0;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
+    int64_t lo = rowptr[r], hi = rowptr[r + 1];
+    if (lane == 0) {
+      if (r == 0 && lo != 0) e_local |= 1;
+      if (r == m - 1 && hi != nnz) e_local |= 1;
+      if (!isfinite(b[r])) e_local |= 4;
+    }
+    if (hi < lo || lo < 0 || hi > nnz) {
+      e_local |= 1;
+      continue;
+    }
+    for (int64_t t = lo + lane; t < hi; t += 32) {
+      int cidx = colind[t];
+      if (cidx < 0 || cidx >= n) e_local |= 2;
+      if (t > lo && colind[t - 1] >= cidx) e_local |= 2;
+      if (!isfinite(vals[t])) e_local |= 4;
+    }
+  }
+  if (e_local) atomicOr(err, e_local);
+}
+
+cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                            const double* vals, const double* b, int* err, cudaStream_t s) {
+  int blocks = (int)((((int64_t)m * 32) + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  validate_kernel<<<blocks, 256, 0, s>>>(m, n, nnz, rowptr, colind, vals, b, err);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- CSR->CSC
+__global__ void colcount_kernel(int64_t nnz, const int32_t* __restrict__ colind, int32_t* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[colind[e] + 1], 1);
+}
+
+// In-place inclusive scan of cnt[0..len) (cnt[0] = 0 on entry) -> colptr; one CTA.
+__global__ void scan_kernel(int len, int32_t* cnt, int32_t* cursor) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < len; base += blockDim.x) {
+    int i = base + tid;
+    int v = i < len ? cnt[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(kFull, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    int incl = x + (wid > 0 ? wsum[wid - 1] : 0) + carry;
+    if (i < len) {
+      cnt[i] = incl;
+      cursor[i] = incl;
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry = incl;
+    __syncthreads();
+  }
+}
+
+__global__ void csc_scatter_kernel(int m, const int32_t* __restrict__ rowptr,
+                                   const int32_t* __restrict__ colind,
+                                   const double* __restrict__ vals, int32_t* cursor,
+                                   int32_t* tmp_row, double* tmp_val) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
+    for (int t = rowptr[r] + lane; t < rowptr[r + 1]; t += 32) {
+      int pos = atomicAdd(&cursor[colind[t]], 1);
+      tmp_row[pos] = r;
+      tmp_val[pos] = vals[t];
+    }
+  }
+}
+
+// Rows within a column arrive in arbitrary order; place each entry at its rank
+// (number of smaller row indices in the column) -> sorted, deterministic.
+__global__ void csc_sort_kernel(int n, const int32_t* __restrict__ colptr,
+                                const int32_t* __restrict__ tmp_row,
+                                const double* __restrict__ tmp_val, int32_t* rowind,
+                                double* cvals) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n; c += warps) {
+    const int lo = colptr[c], len = colptr[c + 1] - lo;
+    for (int i = lane; i < len; i += 32) {
+      const int ri = tmp_row[lo + i];
+      int rank = 0;
+      for (int j = 0; j < len; ++j) rank += tmp_row[lo + j] < ri;
+      rowind[lo + rank] = ri;
+      cvals[lo + rank] = tmp_val[lo + i];
+    }
+  }
+}
+
+cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
+                              const int32_t* colind, const double* vals, int32_t* colptr,
+                              int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,
+                              double* tmp_val, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(colptr, 0, sizeof(int32_t) * (size_t)(n + 1), s);
+  if (e != cudaSuccess) return e;
+  if (nnz > 0) {
+    int blocks = (int)((nnz + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    colcount_kernel<<<blocks, 256, 0, s>>>(nnz, colind, colptr);
+  }
+  scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor);
+  int rb = (int)(((int64_t)m * 32 + 255) / 256);
+  if (rb > 4096) rb = 4096;
+  if (rb < 1) rb = 1;
+  csc_scatter_kernel<<<rb, 256, 0, s>>>(m, rowptr, colind, vals, cursor, tmp_row, tmp_val);
+  int cb = (int)(((int64_t)n * 32 + 255) / 256);
+  if (cb > 4096) cb = 4096;
+  csc_sort_kernel<<<cb, 256, 0, s>>>(n, colptr, tmp_row, tmp_val, rowind, cvals);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- Gram
+__global__ void __launch_bounds__(256) gram_kernel(
+    int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+    const double* __restrict__ vals, const int32_t* __restrict__ colptr,
+    const int32_t* __restrict__ rowind, const double* __restrict__ cvals,
+    const double* __restrict__ b, int row_begin, int row_end, double* __restrict__ G, int ldg,
+    double* __restrict__ c) {
+  extern __shared__ double acc_all[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  double* acc = acc_all + (size_t)wid * n;
+  for (int j = lane; j < n; j += 32) acc[j] = 0.0;
+  __syncwarp();
+  const int total_warps = gridDim.x * wpb;
+  for (int i = blockIdx.x * wpb + wid; i < n; i += total_warps) {
+    const int e0 = colptr[i], e1 = colptr[i + 1];
+    double ci = 0.0;
+    for (int eb = e0; eb < e1; eb += 32) {
+      // prefetch 32 (row, value, row extent) tuples of column i
+      int my_r = 0, my_lo = 0, my_hi = 0;
+      double my_a = 0.0;
+      if (eb + lane < e1) {
+        my_r = rowind[eb + lane];
+        my_a = cvals[eb + lane];
+        if (my_r >= row_begin && my_r < row_end) {
+          my_lo = rowptr[my_r];
+          my_hi = rowptr[my_r + 1];
+        }
+      }
+      const int cnt = min(32, e1 - eb);
+      for (int q = 0; q < cnt; ++q) {
+        const int r = __shfl_sync(kFull, my_r, q);
+        const double a = __shfl_sync(kFull, my_a, q);
+        const int lo = __shfl_sync(kFull, my_lo, q);
+        const int hi = __shfl_sync(kFull, my_hi, q);
+        if (lo == hi) continue;  // row outside [row_begin,row_end) or empty
+        if (lane == 0) ci = __dadd_rn(ci, __dmul_rn(a, b[r]));
+        for (int t = lo + lane; t < hi; t += 32) {
+          const int j = colind[t];
+          acc[j] = __dadd_rn(acc[j], __dmul_rn(a, vals[t]));
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) c[i] = ci;
+    double* Gi = G + (size_t)i * ldg;
+    for (int j = lane; j < n; j += 32) {
+      Gi[j] = acc[j];
+      acc[j] = 0.0;
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
+                        const double* vals, const int32_t* colptr, const int32_t* rowind,
+                        const double* cvals, const double* b, int row_begin, int row_end,
+                        double* G, int ldg, double* c, int sm_count, cudaStream_t s) {
+  (void)m;
+  const size_t per_warp = sizeof(double) * (size_t)n;
+  const size_t smem_cap = 200 * 1024;
+  if (per_warp > smem_cap) return cudaErrorInvalidValue;
+  int wpb = (int)(smem_cap / per_warp);
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1) wpb = 1;
+  const size_t smem = per_warp * wpb;
+  cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = (int)(220 * 1024 / (smem + 1024));
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 8) per_sm = 8;
+  int blocks = (n + wpb - 1) / wpb;
+  if (blocks > sm_count * per_sm) blocks = sm_count * per_sm;
+  if (blocks < 1) blocks = 1;
+  gram_kernel<<<blocks, wpb * 32, smem, s>>>(n, rowptr, colind, vals, colptr, rowind, cvals, b,
+                                            row_begin, row_end, G, ldg, c);
+  return cudaGetLastError();
+}
+
+}  // namespace nnls

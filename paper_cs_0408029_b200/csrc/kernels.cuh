@@ -1,0 +1,97 @@
+// kernels.cuh -- host-side launchers of the sm_100a kernels (one .cu per step).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace nnls {
+
+constexpr int kTile = 64;  // Cholesky tile edge (T x T FP64 tiles, DMMA 8x8x4 updates)
+
+// ---- a0 ingest (ingest_gram.cu) ------------------------------------------
+// Validation error bits written to *err (device int): 1 dimension, 2 index,
+// 4 non-finite.
+cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                            const double* vals, const double* b, int* err, cudaStream_t s);
+// CSR -> CSC (rows sorted within each column).  colcnt: int32[n+1] scratch,
+// tmp_row/tmp_val: nnz scratch.
+cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
+                              const int32_t* colind, const double* vals, int32_t* colptr,
+                              int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,
+                              double* tmp_val, cudaStream_t s);
+// ---- a1 Gram + c (ingest_gram.cu) ---------------------------------------
+// G (n rows of stride ldg) = A_R^T A_R and c = A_R^T b_R over rows R =
+// [row_begin, row_end) (all rows: 0, m).
+cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
+                        const double* vals, const int32_t* colptr, const int32_t* rowind,
+                        const double* cvals, const double* b, int row_begin, int row_end,
+                        double* G, int ldg, double* c, int sm_count, cudaStream_t s);
+
+// ---- a2/a3/a4/a7/a8 pivot steps (pivot.cu) -----------------------------
+cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double* y, double tol,
+                        DevState* st, int p_max, int max_iter, cudaStream_t s);
+// count + decide + exchange + compaction (one CTA); records trace[iter] head.
+cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
+                          int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
+                          cudaStream_t s);
+cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t* Fidx,
+                           int32_t* Gidx, double* xF, DevState* st, cudaStream_t s);
+// y_G = G_GF x_F - c_G (Gram form of Eq. 5), zeroing, scatter x_F into x.
+cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
+                        const int32_t* Gidx, const double* xF, uint8_t* mask, double* x,
+                        double* y, double tol, DevState* st, int sm_count, cudaStream_t s);
+
+// ---- a5/a6 Cholesky + solves (cholesky.cu) -------------------------------
+size_t chol_tile_count(int n);  // tiles needed for |F| <= n (bordered, lower)
+// Factor the bordered matrix [[G_FF, .], [c_F^T, .]] (gathered from G via
+// Fidx) into tiles Lt, then back-substitute L^T x_F = z.  f read from st.
+cudaError_t launch_cholesky_solve(int n, const double* G, int ldg, const double* c,
+                                  const int32_t* Fidx, double* Lt, int* flags, double* xF,
+                                  DevState* st, int sm_count, cudaStream_t s);
+
+// ---- a10 LSQR + final report (lsqr.cu) ----------------------------------
+struct LsqrArgs {
+  int m, n;
+  const int32_t *rowptr, *colind;
+  const double* vals;
+  const int32_t *colptr, *rowind;
+  const double* cvals;
+  const double* b;
+  const uint8_t* mask;
+  const double* x_ne;   // normal-equations x (length n, zero on G)
+  double* x_out;        // final x (length n)
+  double *U, *V, *W, *X;   // work: U[m], V/W/X[n]
+  double* R;            // work[m] (residual for the report)
+  double* partials;     // work[gridDim * 8]
+  DevState* st;
+  int mode;             // 0 none, 1 cold, 2 warm
+  int itn_limit;        // <= 0 -> 4 f
+  double atol, btol, conlim, tol;
+  int kkt;
+  const double* G; int ldg; const double* c;   // for y (report)
+};
+cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s);
+
+// ---- batched whole solve (batched.cu) ------------------------------------
+struct BatchArgs {
+  int batch, m, n;
+  const int64_t* nnz_off;
+  const int32_t* rowptr;
+  const int32_t* colind;
+  const double* vals;
+  const double* b;
+  double* x_out;
+  uint8_t* mask_out;
+  int32_t* info_i;   // batch * 8 ints: status, iter, singles, f, lsqr_itn, lsqr_stop, infeas, notpd
+  double* info_d;    // batch * 5 doubles: objective, min_x, min_y, max_comp, dot
+  double tol, atol, btol, conlim;
+  int p_max, max_iter, lsqr_mode, itn_limit, kkt;
+};
+size_t batched_smem_bytes(int m, int n, int nnz_max);
+cudaError_t launch_validate_batched(int batch, int m, int n, const int64_t* nnz_off,
+                                    const int32_t* rowptr, const int32_t* colind,
+                                    const double* vals, const double* b, int* err, cudaStream_t s);
+cudaError_t launch_batched_nnz(const BatchArgs& a, int nnz_max, int sm_count, cudaStream_t s);
+
+}  // namespace nnls

@@ -1,0 +1,324 @@
+// pivot.cu -- the pivoting steps of the block principal pivoting algorithm
+// that surround the normal-equations solve:
+//   a2 init      F = {}, x = 0, y = -A^T b (zeroed), p = p_max, N = n+1
+//   a3 decide    count infeasibles, choose the branch, exchange
+//   a4 compact   Fidx / Gidx by warp ballot + block prefix scan
+//   a7/a8 dual   y_G = (A^T A)_GF x_F - (A^T b)_G (Eq. 5, Gram form), then
+//                |x_F|, |y_G| < tol -> 0 (reading c1)
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace nnls {
+
+// ---------------------------------------------------------------- init (a2)
+__global__ void init_kernel(int n, const double* __restrict__ c, uint8_t* mask, double* x,
+                            double* y, double tol, DevState* st, int p_max, int max_iter) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    mask[i] = 0;
+    x[i] = 0.0;
+    const double v = -c[i];
+    y[i] = fabs(v) < tol ? 0.0 : v;  // reading c2: the initial y is zeroed too
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->k = 0;
+    st->N = n + 1;  // reading c8: N = infinity
+    st->p = p_max;
+    st->iter = 0;
+    st->singles = 0;
+    st->f = 0;
+    st->g = n;
+    st->branch = -1;
+    st->done = 0;
+    st->status = 0;
+    st->not_pd_col = -1;
+    st->max_iter = max_iter;
+    st->p_max = p_max;
+    st->below_bits = 0ull;
+    st->above_bits = dbits(INFINITY);
+    st->lsqr_iterations = 0;
+    st->lsqr_stop = 0;
+    st->infeasible_after_lsqr = 0;
+  }
+}
+
+cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double* y, double tol,
+                        DevState* st, int p_max, int max_iter, cudaStream_t s) {
+  int blocks = (n + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  if (blocks < 1) blocks = 1;
+  init_kernel<<<blocks, 256, 0, s>>>(n, c, mask, x, y, tol, st, p_max, max_iter);
+  return cudaGetLastError();
+}
+
+// Fidx = sorted F, Gidx = sorted G (warp ballot + block prefix scan over
+// chunks of blockDim.x).  Called by all threads of one CTA; *carryF/*carryG
+// (shared, zero on entry) end as |F| and |G|.
+__device__ void block_compact(int n, const uint8_t* __restrict__ mask, int32_t* __restrict__ Fidx,
+                              int32_t* __restrict__ Gidx, int* s_wF, int* s_wG, int* s_cnt,
+                              int* carryF, int* carryG) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + tid;
+    const bool valid = i < n;
+    const bool inF = valid && mask[i];
+    const bool inG = valid && !mask[i];
+    const unsigned bF = __ballot_sync(kFull, inF), bG = __ballot_sync(kFull, inG);
+    if (lane == 0) {
+      s_wF[wid] = __popc(bF);
+      s_wG[wid] = __popc(bG);
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const int nw = blockDim.x >> 5;
+      int a = lane < nw ? s_wF[lane] : 0, bb = lane < nw ? s_wG[lane] : 0;
+      int ia = a, ib = bb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int ya = __shfl_up_sync(kFull, ia, o), yb = __shfl_up_sync(kFull, ib, o);
+        if (lane >= o) {
+          ia += ya;
+          ib += yb;
+        }
+      }
+      s_wF[lane] = ia - a;  // exclusive
+      s_wG[lane] = ib - bb;
+      if (lane == 31) {
+        s_cnt[0] = ia;  // chunk totals
+        s_cnt[1] = ib;
+      }
+    }
+    __syncthreads();
+    if (inF) Fidx[*carryF + s_wF[wid] + __popc(bF & lt)] = i;
+    if (inG) Gidx[*carryG + s_wG[wid] + __popc(bG & lt)] = i;
+    __syncthreads();
+    if (tid == 0) {
+      *carryF += s_cnt[0];
+      *carryG += s_cnt[1];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------- decide + exchange (a3, a4)
+// One CTA of 1024 threads.  Each thread owns the indices i = tid + 1024 q, so
+// the "snapshot before any flip" of reading c10 is automatic: a thread reads
+// its own (mask, x, y) and flips only its own entries after the block-wide
+// decision.
+constexpr int kDecideThreads = 1024;
+
+__global__ void __launch_bounds__(kDecideThreads) decide_kernel(
+    int n, uint8_t* __restrict__ mask, const double* __restrict__ x,
+    const double* __restrict__ y, int32_t* __restrict__ Fidx, int32_t* __restrict__ Gidx,
+    DevState* st, TraceRec* trace, int trace_cap) {
+  __shared__ int s_cnt[32], s_max[32];
+  __shared__ int s_wF[32], s_wG[32];
+  __shared__ int s_branch, s_last, s_carryF, s_carryG;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  // close the previous iteration's trace record (extremes from the dual kernel)
+  if (tid == 0 && trace != nullptr) {
+    const int it = st->iter;
+    if (it > 0 && it - 1 < trace_cap) {
+      trace[it - 1].below_tol = __longlong_as_double((long long)st->below_bits);
+      trace[it - 1].above_tol = __longlong_as_double((long long)st->above_bits);
+    }
+  }
+  if (st->status != 0 || st->done) return;
+
+  // pass 1: k = #{i in F: x_i < 0} + #{j in G: y_j < 0} (reading c5);
+  // largest infeasible original index (reading c6)
+  int k = 0, last = -1;
+  for (int i = tid; i < n; i += kDecideThreads) {
+    const bool inf = mask[i] ? (x[i] < 0.0) : (y[i] < 0.0);
+    if (inf) {
+      ++k;
+      last = i;
+    }
+  }
+  k = warp_sum_i(k);
+  last = warp_max_i(last);
+  if (lane == 0) {
+    s_cnt[wid] = k;
+    s_max[wid] = last;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    int kk = s_cnt[lane], ll = s_max[lane];
+    kk = warp_sum_i(kk);
+    ll = warp_max_i(ll);
+    if (lane == 0) {
+      int branch;
+      st->k = kk;
+      if (kk == 0) {
+        st->done = 1;  // feasible: the while-loop of P:89 ends
+        branch = -1;
+      } else if (st->iter >= st->max_iter) {
+        st->status = 8;  // ITERATION_LIMIT (reading c12)
+        branch = -1;
+      } else if (kk < st->N) {
+        st->N = kk;
+        st->p = st->p_max;
+        branch = 0;
+      } else if (st->p > 0) {
+        st->p -= 1;
+        branch = 1;
+      } else {
+        st->singles += 1;
+        branch = 2;
+      }
+      st->branch = branch;
+      s_branch = branch;
+      s_last = ll;
+      s_carryF = 0;
+      s_carryG = 0;
+    }
+  }
+  __syncthreads();
+  const int branch = s_branch;
+  if (branch < 0) return;
+  const int lastidx = s_last;
+
+  // pass 2: exchange (from the snapshot: each thread re-reads its own entries)
+  for (int i = tid; i < n; i += kDecideThreads) {
+    const uint8_t mi = mask[i];
+    const bool inf = mi ? (x[i] < 0.0) : (y[i] < 0.0);
+    const bool flip = (branch == 2) ? (i == lastidx) : inf;
+    if (flip) mask[i] = mi ? 0 : 1;
+  }
+  __syncthreads();
+
+  block_compact(n, mask, Fidx, Gidx, s_wF, s_wG, s_cnt, &s_carryF, &s_carryG);
+  if (tid == 0) {
+    const int f = s_carryF;
+    st->f = f;
+    st->g = s_carryG;
+    st->epoch += 1;
+    st->tile_counter = 0;
+    st->solve_counter = 0;
+    st->below_bits = 0ull;
+    st->above_bits = dbits(INFINITY);
+    const int it = st->iter;
+    if (trace != nullptr && it < trace_cap) {
+      trace[it].iter = it + 1;
+      trace[it].k = st->k;
+      trace[it].branch = branch;
+      trace[it].f = f;
+      trace[it].below_tol = 0.0;
+      trace[it].above_tol = INFINITY;
+    }
+  }
+}
+
+// Step-API helper: Fidx/Gidx/f/g from a given mask, and x_F = x[Fidx].
+__global__ void __launch_bounds__(kDecideThreads) compact_kernel(int n, const uint8_t* mask,
+                                                                 const double* x, int32_t* Fidx,
+                                                                 int32_t* Gidx, double* xF,
+                                                                 DevState* st) {
+  __shared__ int s_cnt[32], s_wF[32], s_wG[32];
+  __shared__ int s_carryF, s_carryG;
+  if (threadIdx.x == 0) {
+    s_carryF = 0;
+    s_carryG = 0;
+  }
+  __syncthreads();
+  block_compact(n, mask, Fidx, Gidx, s_wF, s_wG, s_cnt, &s_carryF, &s_carryG);
+  const int f = s_carryF;
+  for (int a = threadIdx.x; a < f; a += blockDim.x) xF[a] = x[Fidx[a]];
+  if (threadIdx.x == 0) {
+    st->f = f;
+    st->g = s_carryG;
+  }
+}
+
+cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t* Fidx,
+                           int32_t* Gidx, double* xF, DevState* st, cudaStream_t s) {
+  compact_kernel<<<1, kDecideThreads, 0, s>>>(n, mask, x, Fidx, Gidx, xF, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
+                          int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
+                          cudaStream_t s) {
+  decide_kernel<<<1, kDecideThreads, 0, s>>>(n, mask, x, y, Fidx, Gidx, st, trace, trace_cap);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------- dual (a7, a8)
+// Warps over G: y_j = sum_a G[j, Fidx[a]] x_F[a] - c_j, from the UNCLAMPED
+// x_F (reading c3), then zeroing.  Threads over F: scatter the zeroed x_F.
+__global__ void __launch_bounds__(256) dual_kernel(
+    int n, const double* __restrict__ G, int ldg, const double* __restrict__ c,
+    const int32_t* __restrict__ Fidx, const int32_t* __restrict__ Gidx,
+    const double* __restrict__ xF, uint8_t* __restrict__ mask, double* __restrict__ x,
+    double* __restrict__ y, double tol, DevState* st) {
+  const int status = st->status;
+  if (status != 0) {
+    if (status == 7) {  // NOT_PD: the solve failed, x = 0 (as the oracle)
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        x[i] = 0.0;
+    }
+    return;
+  }
+  if (st->done) return;
+  const int f = st->f, g = st->g;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  double below = 0.0, above = INFINITY;
+  for (int jj = gwarp; jj < g; jj += nwarps) {
+    const int j = Gidx[jj];
+    const double* Gj = G + (size_t)j * ldg;
+    double s = 0.0;
+    for (int a = lane; a < f; a += 32) s = fma(Gj[Fidx[a]], xF[a], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      const double v = s - c[j];
+      const double av = fabs(v);
+      if (av < tol) {
+        below = fmax(below, av);
+        y[j] = 0.0;
+      } else {
+        above = fmin(above, av);
+        y[j] = v;
+      }
+      x[j] = 0.0;
+    }
+  }
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < f; a += gridDim.x * blockDim.x) {
+    const int i = Fidx[a];
+    const double v = xF[a];
+    const double av = fabs(v);
+    if (av < tol) {
+      below = fmax(below, av);
+      x[i] = 0.0;
+    } else {
+      above = fmin(above, av);
+      x[i] = v;
+    }
+    y[i] = 0.0;
+  }
+  below = warp_max(below);
+  above = warp_min(above);
+  if (lane == 0) {
+    if (below > 0.0) atomicMax(&st->below_bits, dbits(below));
+    if (above < INFINITY) atomicMin(&st->above_bits, dbits(above));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->iter += 1;
+  (void)mask;
+}
+
+cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
+                        const int32_t* Gidx, const double* xF, uint8_t* mask, double* x,
+                        double* y, double tol, DevState* st, int sm_count, cudaStream_t s) {
+  int blocks = (n + 7) / 8;  // one warp per G index upper bound
+  if (blocks > sm_count * 8) blocks = sm_count * 8;
+  if (blocks < 1) blocks = 1;
+  dual_kernel<<<blocks, 256, 0, s>>>(n, G, ldg, c, Fidx, Gidx, xF, mask, x, y, tol, st);
+  return cudaGetLastError();
+}
+
+}  // namespace nnls

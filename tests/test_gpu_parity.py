@@ -1,0 +1,368 @@
+"""GPU parity tests (-m gpu): the CUDA path, called through the C ABI, against
+the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): final free set F and pivot-iteration count
+identical, x within relative inf-norm 1e-9 (FP64).  The Gram matrix and A^T b
+are compared BITWISE (exact for the quantized inputs, and the kernel also
+keeps the oracle's summation order).  Integer decisions (branch per
+iteration, infeasible counts, |F|) are compared exactly via the trace.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import nnls_gen as g  # noqa: E402
+import oracle as O  # noqa: E402
+
+TOL_X = 1e-9
+HERE = os.path.dirname(os.path.abspath(__file__))
+SINGLES = json.load(open(os.path.join(HERE, "golden", "single_exchange_seeds.json")))
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_cs_0408029_b200 as pkg
+    assert pkg.device_info()["cc"] >= 100
+    return pkg
+
+
+def rel(a, b):
+    d = np.abs(b).max() if np.size(b) else 0.0
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / (d if d > 0 else 1.0) if np.size(b) else 0.0
+
+
+def run_gpu(P, prob, **kw):
+    S = P.setup(prob, trace=1, **kw)
+    x, info = S.solve()
+    return dict(x=x, info=info, mask=S.free_set(), x_ne=S.x_ne(), trace=S.trace(), S=S)
+
+
+def assert_parity(P, prob, check_trace=True, **kw):
+    r = O.solve(prob, trace_cap=10 * prob.n + 2, **kw)
+    gpu = run_gpu(P, prob, **kw)
+    info = gpu["info"]
+    assert info["status"] == r["status"], (info["status"], r["status"])
+    assert np.array_equal(gpu["mask"], r["mask"]), "final free set differs"
+    assert info["iterations"] == r["iterations"]
+    assert info["single_exchanges"] == r["single_exchanges"]
+    assert info["free_count"] == r["free_count"]
+    if check_trace:
+        tg, to = gpu["trace"], r["trace"]
+        assert [(t["k"], t["branch"], t["f"]) for t in tg] == [(t["k"], t["branch"], t["f"]) for t in to]
+    assert rel(gpu["x_ne"], r["x_ne"]) <= TOL_X
+    assert rel(gpu["x"], r["x"]) <= TOL_X
+    if r["status"] == 0:
+        assert gpu["x"].min() >= 0.0
+    if r["status"] == 0 and info["free_count"] > 0 and kw.get("lsqr_mode", 1) == 1:
+        assert info["lsqr_iterations"] > 0
+    return gpu, r
+
+
+# ------------------------------------------------------------------- Gram
+@pytest.mark.parametrize("cfg", [0, 1, 3, dict(m=333, n=129, density=0.07), dict(m=50, n=50, density=1.0)])
+def test_gram_bitwise(P, cfg):
+    prob = g.make_problem(cfg, seed=1)
+    S = P.setup(prob)
+    G, c = S.gram()
+    Go, co = O.gram(prob)
+    assert np.array_equal(G, Go) and np.array_equal(c, co)
+
+
+def test_gram_bitwise_raw_inputs(P):
+    """Unquantized values: the kernel keeps the oracle's term order and rounding."""
+    prob = g.make_problem(dict(m=400, n=150, density=0.05), seed=2, raw=True)
+    G, c = P.setup(prob).gram()
+    Go, co = O.gram(prob)
+    assert np.array_equal(G, Go) and np.array_equal(c, co)
+
+
+def test_step_gram_device_buffers(P):
+    prob = g.make_problem(dict(m=300, n=97, density=0.1), seed=3)
+    dev = "cuda"
+    rp = torch.tensor(prob.rowptr, device=dev)
+    ci = torch.tensor(prob.colind, device=dev)
+    v = torch.tensor(prob.vals, device=dev)
+    b = torch.tensor(prob.b, device=dev)
+    ldg = 100
+    G = torch.full((prob.n, ldg), -7.0, dtype=torch.float64, device=dev)
+    c = torch.empty(prob.n, dtype=torch.float64, device=dev)
+    P.step_gram(prob.m, prob.n, rp, ci, v, b, G, c, ldg=ldg)
+    Go, co = O.gram(prob)
+    assert np.array_equal(G[:, :prob.n].cpu().numpy(), Go)
+    assert np.array_equal(c.cpu().numpy(), co)
+
+
+# --------------------------------------------------- normal solve (a5, a6)
+@pytest.mark.parametrize("f", [1, 2, 63, 64, 65, 127, 128, 129, 191, 257])
+def test_normal_solve_tile_edges(P, f):
+    prob = g.make_problem(dict(m=900, n=300, density=0.06), seed=f)
+    Go, co = O.gram(prob)
+    rng = np.random.default_rng(f)
+    F = np.sort(rng.choice(prob.n, f, replace=False)).astype(np.int32)
+    L, rc = O.cholesky(O.gather(Go, F))
+    assert rc == 0
+    want = O.chol_solve(L, co[F])
+    G = torch.tensor(Go, device="cuda")
+    c = torch.tensor(co, device="cuda")
+    xF = torch.empty(f, dtype=torch.float64, device="cuda")
+    st, col = P.step_normal_solve(prob.n, G, c, torch.tensor(F, device="cuda"), xF)
+    assert st == P.OK and col == -1
+    assert rel(xF.cpu().numpy(), want) <= 1e-12
+
+
+def test_normal_solve_not_pd(P):
+    A = np.random.default_rng(0).standard_normal((40, 6))
+    A[:, 4] = A[:, 1]
+    prob = g.from_dense(np.round(A * 64) / 64, np.ones(40))
+    Go, co = O.gram(prob)
+    F = np.array([0, 1, 2, 4], dtype=np.int32)
+    _, rc = O.cholesky(O.gather(Go, F))
+    xF = torch.empty(4, dtype=torch.float64, device="cuda")
+    st, col = P.step_normal_solve(6, torch.tensor(Go, device="cuda"), torch.tensor(co, device="cuda"),
+                                  torch.tensor(F, device="cuda"), xF)
+    assert st == P.ERR_NOT_PD and col == -rc - 1 == 3
+
+
+# ---------------------------------------------------- exchange (a3, a4)
+def _exchange_gpu(P, mask, x, y, N, p, p_max=3):
+    m = torch.tensor(mask, dtype=torch.uint8, device="cuda")
+    state = [N, p, 0, 0]
+    k, br = P.step_exchange(len(mask), m, torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"),
+                            state, p_max=p_max)
+    return k, m.cpu().numpy(), state[0], state[1], br
+
+
+def test_exchange_hand_states(P):
+    mask = np.array([1, 1, 0, 0, 1, 0], dtype=np.uint8)
+    x = np.array([-1.0, 2.0, 0.0, 0.0, -3.0, 0.0])
+    y = np.array([0.0, 0.0, -1.0, 4.0, 0.0, -2.0])
+    for N, p in [(5, 1), (4, 2), (3, 0), (1, 0), (4, 0)]:
+        kg, mg, Ng, pg, bg = _exchange_gpu(P, mask, x, y, N, p)
+        ko, mo, No, po, bo = O.exchange(mask, x, y, N, p)
+        assert (kg, Ng, pg, bg) == (ko, No, po, bo) and np.array_equal(mg, mo)
+    kg, mg, _, _, bg = _exchange_gpu(P, mask, np.abs(x), np.abs(y), 2, 1)
+    assert kg == 0 and bg == -1 and np.array_equal(mg, mask)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1023, 1024, 1025, 5000])
+def test_exchange_random_states(P, n):
+    rng = np.random.default_rng(n)
+    for trial in range(4):
+        mask = (rng.random(n) < 0.5).astype(np.uint8)
+        x = np.where(mask == 1, rng.standard_normal(n), 0.0)
+        y = np.where(mask == 0, rng.standard_normal(n), 0.0)
+        N = int(rng.integers(0, n + 2))
+        p = int(rng.integers(0, 4))
+        kg, mg, Ng, pg, bg = _exchange_gpu(P, mask, x, y, N, p)
+        ko, mo, No, po, bo = O.exchange(mask, x, y, N, p)
+        assert (kg, Ng, pg, bg) == (ko, No, po, bo) and np.array_equal(mg, mo)
+
+
+# ------------------------------------------------------- dual (a7, a8)
+@pytest.mark.parametrize("seed", range(3))
+def test_dual_matches_oracle(P, seed):
+    prob = g.make_problem(dict(m=500, n=200, density=0.05), seed=seed)
+    Go, co = O.gram(prob)
+    rng = np.random.default_rng(seed)
+    mask = (rng.random(prob.n) < 0.5).astype(np.uint8)
+    x = np.where(mask == 1, rng.standard_normal(prob.n), 0.0)
+    x[np.nonzero(mask)[0][:3]] = [3e-13, -5e-13, 1e-12]          # zeroing boundary cases
+    yo = O.dual_gram(Go, co, mask, x)
+    xo = x.copy()
+    for i in range(prob.n):
+        if mask[i] and abs(xo[i]) < 1e-12:
+            xo[i] = 0.0
+        if not mask[i] and abs(yo[i]) < 1e-12:
+            yo[i] = 0.0
+    xd = torch.tensor(x, device="cuda")
+    yd = torch.full((prob.n,), 9.0, dtype=torch.float64, device="cuda")
+    P.step_dual(prob.n, torch.tensor(Go, device="cuda"), torch.tensor(co, device="cuda"),
+                torch.tensor(mask, device="cuda"), xd, yd)
+    assert np.array_equal(xd.cpu().numpy(), xo)
+    yg = yd.cpu().numpy()
+    assert np.all(yg[mask == 1] == 0)
+    scale = np.abs(Go).max() * np.abs(x).sum() + np.abs(co).max()
+    assert np.abs(yg - yo).max() <= 1e-14 * scale
+
+
+# ----------------------------------------------------- whole solve parity
+@pytest.mark.parametrize("cfg,seed", [(0, s) for s in range(5)] + [(1, s) for s in range(3)] +
+                         [(3, s) for s in range(3)])
+def test_solve_parity_configs(P, cfg, seed):
+    gpu, r = assert_parity(P, g.make_problem(cfg, seed))
+    i = gpu["info"]
+    assert abs(i["objective"] - r["objective"]) <= 1e-9 * max(1.0, r["objective"])
+    assert i["kkt_min_x"] >= 0.0
+
+
+@pytest.mark.parametrize("n", [63, 64, 65, 127, 128, 129, 192])
+def test_solve_all_free_tile_edges(P, n):
+    """b = A x* with x* > 0: every column ends in F, so |F| = n hits each ragged tile edge."""
+    prob = g.make_problem(dict(m=3 * n, n=n, density=0.08, rhs="degenerate"), seed=n)
+    x = prob.x_gen.copy()
+    x[x == 0] = 0.75                       # all strictly positive
+    A = prob.dense()
+    b = np.round(A @ x * (1 << 24)) / (1 << 24)
+    q = g.from_dense(A, b)
+    gpu, r = assert_parity(P, q)
+    assert r["free_count"] == n
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_solve_parity_random_shapes(P, seed):
+    rng = np.random.default_rng([seed, 9])
+    n = int(rng.integers(2, 300))
+    m = n + int(rng.integers(1, 3 * n))
+    d = float(rng.choice([0.02, 0.1, 0.5]))
+    assert_parity(P, g.make_problem(dict(m=m, n=n, density=max(d, 2.0 / n)), seed=seed))
+
+
+@pytest.mark.parametrize("case", SINGLES["cases"][:20], ids=lambda c: f"seed{c['seed']}")
+def test_single_exchange_parity(P, case):
+    gpu, r = assert_parity(P, g.make_correlated(case["seed"], 0.05), lsqr_mode=0)
+    assert gpu["info"]["single_exchanges"] >= 1
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_lsqr_modes(P, mode):
+    assert_parity(P, g.make_problem(0, 7), lsqr_mode=mode)
+
+
+def test_edge_cases(P):
+    # A^T b <= 0: zero iterations, x = 0
+    A = np.array([[1.0, 2.0], [0.5, 1.0], [0.0, 3.0]])
+    b = -A @ np.array([1.0, 0.5])
+    gpu, r = assert_parity(P, g.from_dense(A, b))
+    assert gpu["info"]["iterations"] == 0 and np.all(gpu["x"] == 0)
+    # n = 1, m = 1
+    assert_parity(P, g.from_dense(np.array([[2.0]]), np.array([3.0])))
+    assert_parity(P, g.from_dense(np.array([[2.0], [1.0]]), np.array([-3.0, 1.0])))
+    # identity: x = max(b, 0) exactly, one iteration
+    bb = np.round(np.random.default_rng(1).standard_normal(70) * 64) / 64
+    gpu, _ = assert_parity(P, g.from_dense(np.eye(70), bb), lsqr_mode=0)
+    assert np.array_equal(gpu["x"], np.maximum(bb, 0)) and gpu["info"]["iterations"] == 1
+    # iteration limit (reading c12)
+    gpu, r = assert_parity(P, g.make_problem(0, 0), max_iter=1)
+    assert gpu["info"]["status"] == 8
+
+
+def test_not_pd_status(P):
+    p = g.make_problem(0, 0)
+    A = p.dense()
+    A = np.concatenate([A, A[:, :1]], axis=1)
+    q = g.from_dense(A, p.b)
+    r = O.solve(q)
+    gpu = run_gpu(P, q)
+    assert gpu["info"]["status"] == r["status"]
+    assert gpu["info"]["iterations"] == r["iterations"]
+    if r["status"] == 7:
+        assert gpu["info"]["not_pd_column"] >= 0
+
+
+def test_invalid_inputs(P):
+    p = g.make_problem(dict(m=20, n=10, density=0.3), seed=0)
+    S = P.Solver()
+    bad = p.colind.copy()
+    bad[3] = 10
+    with pytest.raises(P.NNLSError) as e:
+        S.load(p.m, p.n, p.rowptr, bad, p.vals, p.b)
+    assert e.value.status == P.ERR_INDEX
+    rp = p.rowptr.copy()
+    rp[-1] -= 1
+    with pytest.raises(P.NNLSError) as e:
+        S.load(p.m, p.n, rp, p.colind, p.vals, p.b)
+    assert e.value.status == P.ERR_DIMENSION
+    v = p.vals.copy()
+    v[0] = np.nan
+    with pytest.raises(P.NNLSError) as e:
+        S.load(p.m, p.n, p.rowptr, p.colind, v, p.b)
+    assert e.value.status == P.ERR_NONFINITE
+    with pytest.raises(P.NNLSError) as e:
+        S.solve()
+    assert e.value.status == P.ERR_STATE
+    # a valid load afterwards works on the same handle
+    S.load_problem(p)
+    x, info = S.solve()
+    assert info["status"] == 0
+
+
+def test_repeated_solves_and_reload(P):
+    """Handles are reusable: reload different problems into one handle (buffer reuse)."""
+    S = P.Solver(trace=1)
+    for cfg, seed in [(0, 1), (dict(m=700, n=300, density=0.05), 2), (0, 3)]:
+        prob = g.make_problem(cfg, seed)
+        S.load_problem(prob)
+        for _ in range(2):
+            x, info = S.solve()
+            r = O.solve(prob)
+            assert np.array_equal(S.free_set(), r["mask"]) and info["iterations"] == r["iterations"]
+            assert rel(x, r["x"]) <= TOL_X
+
+
+def test_device_resident_inputs_and_outputs(P):
+    prob = g.make_problem(1, 4)
+    t = {k: torch.tensor(getattr(prob, k), device="cuda") for k in ("rowptr", "colind", "vals", "b")}
+    S = P.Solver().load(prob.m, prob.n, t["rowptr"], t["colind"], t["vals"], t["b"])
+    xd = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    S.solve(x_out=xd)
+    r = O.solve(prob)
+    assert rel(xd.cpu().numpy(), r["x"]) <= TOL_X
+
+
+# ---------------------------------------------------------------- batched
+def _batched_parity(P, B, **kw):
+    out = P.BatchedSolver(**kw).load_batch(B).solve()
+    ref = O.solve_batched(B, O.default_params(**kw), threads=0)
+    x = out["x"].reshape(B.count, B.n)
+    mask = out["mask"].reshape(B.count, B.n)
+    info = out["info"]
+    assert np.array_equal(info["status"], ref["status"])
+    assert np.array_equal(mask, ref["mask"])
+    assert np.array_equal(info["iterations"], ref["iterations"])
+    assert np.array_equal(info["single_exchanges"], ref["single_exchanges"])
+    scale = np.maximum(np.abs(ref["x"]).max(axis=1), 1e-300)
+    err = np.abs(x - ref["x"]).max(axis=1) / np.where(np.abs(ref["x"]).max(axis=1) > 0, scale, 1.0)
+    assert err.max() <= TOL_X
+    return out, ref
+
+
+def test_batched_config4_slice(P):
+    B = g.make_batch(seed=0, start=0, count=2048)
+    out, ref = _batched_parity(P, B)
+    assert out["info"]["kkt_min_x"].min() >= 0
+
+
+def test_batched_slices_independent_of_position(P):
+    """A problem's result does not depend on its batch neighbours (sharding invariance)."""
+    B = g.make_batch(seed=1, start=0, count=300)
+    full = P.BatchedSolver().load_batch(B).solve()
+    C = g.make_batch(seed=1, start=100, count=57)
+    part = P.BatchedSolver().load_batch(C).solve()
+    assert np.array_equal(full["x"].reshape(300, 64)[100:157], part["x"].reshape(57, 64))
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_batched_lsqr_modes(P, mode):
+    _batched_parity(P, g.make_batch(seed=2, start=0, count=256), lsqr_mode=mode)
+
+
+def test_batched_x_ne_bitwise(P):
+    """NE path of the batched kernel keeps the oracle's operation order: x (mode 0) is bit-identical."""
+    B = g.make_batch(seed=3, start=0, count=512)
+    out = P.BatchedSolver(lsqr_mode=0).load_batch(B).solve()
+    ref = O.solve_batched(B, O.default_params(lsqr_mode=0), threads=0)
+    assert np.array_equal(out["x"].reshape(512, 64), ref["x"])
+
+
+def test_batched_single_exchange_cases(P):
+    for case in SINGLES["cases"][:10]:
+        p = g.make_correlated(case["seed"], 0.05)
+        B = g.Batch(p.m, p.n, 1, np.array([0, p.nnz], dtype=np.int64), p.rowptr, p.colind, p.vals, p.b,
+                    np.zeros(p.n), 0, 0)
+        _batched_parity(P, B, lsqr_mode=0)
