@@ -222,6 +222,32 @@ NNLS_API nnls_status nnls_step_exchange(int32_t n, uint8_t* mask, const double* 
 NNLS_API nnls_status nnls_step_dual(int32_t n, const double* G, int32_t ldg, const double* c,
                            const uint8_t* mask, double* x, double* y, double tol, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Instrumentation: per-phase CUDA-event timing on the handle's stream and
+ * kernel-launch counts (the bench's roofline and gpu_launches evidence).
+ * nnls_timing_enable(h, 1) resets the accumulators and records an event pair
+ * around every phase; nnls_timing_read syncs the stream and returns the
+ * accumulated milliseconds and launch counts per phase (cap entries).
+ * Launch counts are kept even when timing is off.
+ */
+#define NNLS_NPHASES 16
+enum {
+  NNLS_PH_UPLOAD = 0,      /* input copies into the handle (H2D or D2D)          */
+  NNLS_PH_VALIDATE = 1,    /* a0 CSR validation                                  */
+  NNLS_PH_CSC = 2,         /* a0 CSR -> CSC (4 kernels)                          */
+  NNLS_PH_GRAM = 3,        /* a1 A^T A, A^T b                                    */
+  NNLS_PH_INIT = 4,        /* a2                                                 */
+  NNLS_PH_DECIDE = 5,      /* a3 + a4 count/decide/exchange/compaction           */
+  NNLS_PH_CHOL_FACTOR = 6, /* a5 (+ forward solve via the bordered row)          */
+  NNLS_PH_CHOL_SOLVE = 7,  /* a6 back substitution                               */
+  NNLS_PH_DUAL = 8,        /* a7 + a8                                            */
+  NNLS_PH_LSQR = 9,        /* a10 + a11 report                                   */
+  NNLS_PH_DOWNLOAD = 10,   /* x_out copy                                         */
+  NNLS_PH_BATCHED = 11     /* batched whole-solve kernel                         */
+};
+NNLS_API nnls_status nnls_timing_enable(nnls_handle* h, int32_t on);
+NNLS_API nnls_status nnls_timing_read(nnls_handle* h, double* ms, int64_t* launches, int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

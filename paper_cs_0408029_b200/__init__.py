@@ -25,6 +25,11 @@ STATUS_NAMES = ["OK", "ERR_INVALID_ARG", "ERR_DIMENSION", "ERR_INDEX", "ERR_NONF
                 "ERR_OOM", "ERR_NOT_PD", "ITERATION_LIMIT", "ERR_STATE"]
 
 
+NPHASES = 16
+PHASES = ["upload", "validate", "csc", "gram", "init", "decide", "chol_factor", "chol_solve", "dual",
+          "lsqr", "download", "batched"]
+
+
 class NNLSError(RuntimeError):
     def __init__(self, status, where=""):
         self.status = int(status)
@@ -86,6 +91,8 @@ def _load():
         "nnls_step_normal_solve": ([i32, P, i32, P, i32, P, P, P, P], i32),
         "nnls_step_exchange": ([i32, P, P, P, i32, P, P, P, P], i32),
         "nnls_step_dual": ([i32, P, i32, P, P, P, P, d, P], i32),
+        "nnls_timing_enable": ([P, i32], i32),
+        "nnls_timing_read": ([P, P, P, i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -220,6 +227,18 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def timing_enable(handle, on=True):
+    _check(lib.nnls_timing_enable(handle, 1 if on else 0), "nnls_timing_enable")
+
+
+def timing_read(handle):
+    """{phase: (ms, launches)} accumulated since timing_enable."""
+    ms = (C.c_double * NPHASES)()
+    nl = (C.c_int64 * NPHASES)()
+    _check(lib.nnls_timing_read(handle, ms, nl, NPHASES), "nnls_timing_read")
+    return {name: (ms[i], nl[i]) for i, name in enumerate(PHASES)}
 
 
 def setup(prob, params: Params | None = None, stream=None, **kw) -> Solver:

@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <new>
+#include <vector>
 
 #include "../../include/nnls.h"
 #include "common.cuh"
@@ -61,7 +62,20 @@ struct HostState {
   int pad[3];
 };
 
+struct Timing {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Pend {
+    int phase, b, e;
+  };
+  std::vector<Pend> pending;
+  double ms[NNLS_NPHASES] = {0};
+  long long launches[NNLS_NPHASES] = {0};
+};
+
 struct nnls_handle {
+  Timing tm;
   cudaStream_t stream = nullptr;
   int device = 0, sms = 148;
   nnls_params prm{};
@@ -86,6 +100,52 @@ struct nnls_handle {
 };
 
 namespace {
+
+int tm_event(nnls_handle* h) {
+  Timing& t = h->tm;
+  if (t.used == t.pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    t.pool.push_back(e);
+  }
+  return (int)t.used++;
+}
+int tm_begin(nnls_handle* h) {
+  if (!h->tm.on) return -1;
+  const int i = tm_event(h);
+  if (i >= 0) cudaEventRecord(h->tm.pool[i], h->stream);
+  return i;
+}
+void tm_end(nnls_handle* h, int phase, int ib, int nlaunch) {
+  h->tm.launches[phase] += nlaunch;
+  if (ib < 0) return;
+  const int ie = tm_event(h);
+  if (ie < 0) return;
+  cudaEventRecord(h->tm.pool[ie], h->stream);
+  h->tm.pending.push_back({phase, ib, ie});
+}
+// resolve recorded pairs (after a stream sync) to free the event pool
+void tm_flush(nnls_handle* h) {
+  Timing& t = h->tm;
+  if (t.pending.empty()) {
+    t.used = 0;
+    return;
+  }
+  cudaStreamSynchronize(h->stream);
+  for (const auto& p : t.pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, t.pool[p.b], t.pool[p.e]) == cudaSuccess) t.ms[p.phase] += ms;
+  }
+  t.pending.clear();
+  t.used = 0;
+}
+
+#define TIMED(phase, nl, expr)            \
+  do {                                    \
+    const int ib_ = tm_begin(h);          \
+    CK(expr);                             \
+    tm_end(h, (phase), ib_, (nl));        \
+  } while (0)
 
 nnls_status set_stream_device(nnls_handle* h, void* stream) {
   h->stream = static_cast<cudaStream_t>(stream);
@@ -169,6 +229,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   h->trace_cap = cap;
   if (cap > 0) CK(ensure(h->trace, sizeof(TraceRec) * (size_t)cap));
 
+  int ib = tm_begin(h);
   CK(cudaMemcpyAsync(h->rowptr.p, rowptr, sizeof(int32_t) * (size_t)(m + 1), cudaMemcpyDefault, s));
   if (nnz > 0) {
     CK(cudaMemcpyAsync(h->colind.p, colind, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDefault, s));
@@ -176,22 +237,26 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   }
   CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)m, cudaMemcpyDefault, s));
   CK(cudaMemsetAsync(h->err.p, 0, sizeof(int), s));
-  CK(launch_validate(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
-                     P<double>(h->b), P<int>(h->err), s));
+  tm_end(h, NNLS_PH_UPLOAD, ib, 0);
+  TIMED(NNLS_PH_VALIDATE, 1,
+        launch_validate(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                        P<double>(h->b), P<int>(h->err), s));
   // validation must pass before structure-dependent kernels touch the data
   int herr = 0;
   CK(cudaMemcpyAsync(&h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   herr = h->h->err;
   if (herr) return map_err_bits(herr);
-  CK(launch_csr_to_csc(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
-                       P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                       P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s));
+  TIMED(NNLS_PH_CSC, nnz > 0 ? 4 : 3,
+        launch_csr_to_csc(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                          P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
+                          P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s));
   double* G = P<double>(h->Gc);
   double* c = G + (size_t)n * h->ldg;
-  CK(launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
-                 P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals), P<double>(h->b),
-                 r0, r1, G, h->ldg, c, h->sms, s));
+  TIMED(NNLS_PH_GRAM, 1,
+        launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                    P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
+                    P<double>(h->b), r0, r1, G, h->ldg, c, h->sms, s));
   h->loaded = true;
   return NNLS_OK;
 }
@@ -231,8 +296,10 @@ void free_buf(Buf& b) {
 nnls_status read_state(nnls_handle* h) {
   CK(cudaMemcpyAsync(&h->h->st, h->st.p, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  if (h->tm.pending.size() > 256) tm_flush(h);
   return NNLS_OK;
 }
+
 
 }  // namespace
 
@@ -361,21 +428,29 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   double* c = G + (size_t)n * h->ldg;
   DevState* st = P<DevState>(h->st);
   TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
-  CK(launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
-                 p.p_max, max_iter, s));
+  TIMED(NNLS_PH_INIT, 1,
+        launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
+                    p.p_max, max_iter, s));
   for (;;) {
-    CK(launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), P<int32_t>(h->Fidx),
-                     P<int32_t>(h->Gidx), st, trace, h->trace_cap, s));
+    TIMED(NNLS_PH_DECIDE, 1,
+          launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
+                        P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s));
     nnls_status rs = read_state(h);
     if (rs != NNLS_OK) return rs;
     const DevState& hs = h->h->st;
     if (hs.done || hs.status != 0) break;
-    if (hs.f > 0)
-      CK(launch_cholesky_solve(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt),
-                               P<int>(h->flags), P<double>(h->xF), st, h->sms, s));
-    CK(launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
-                   P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st, h->sms,
-                   s));
+    if (hs.f > 0) {
+      TIMED(NNLS_PH_CHOL_FACTOR, 1,
+            launch_chol_factor(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt),
+                               P<int>(h->flags), st, h->sms, s));
+      TIMED(NNLS_PH_CHOL_SOLVE, 1,
+            launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st,
+                                  h->sms, s));
+    }
+    TIMED(NNLS_PH_DUAL, 1,
+          launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
+                      P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
+                      h->sms, s));
   }
   LsqrArgs a{};
   a.m = h->m;
@@ -407,8 +482,12 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   a.G = G;
   a.ldg = h->ldg;
   a.c = c;
-  CK(launch_lsqr_final(a, h->sms, s));
-  if (x_out) CK(cudaMemcpyAsync(x_out, h->xfin.p, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
+  TIMED(NNLS_PH_LSQR, 1, launch_lsqr_final(a, h->sms, s));
+  if (x_out) {
+    const int ib = tm_begin(h);
+    CK(cudaMemcpyAsync(x_out, h->xfin.p, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
+    tm_end(h, NNLS_PH_DOWNLOAD, ib, 0);
+  }
   nnls_status rs = read_state(h);
   if (rs != NNLS_OK) return rs;
   const DevState& hs = h->h->st;
@@ -483,6 +562,27 @@ nnls_status nnls_get_gram(nnls_handle* h, double* G_out, double* c_out) {
   return NNLS_OK;
 }
 
+nnls_status nnls_timing_enable(nnls_handle* h, int32_t on) {
+  if (!h) return NNLS_ERR_INVALID_ARG;
+  tm_flush(h);
+  for (int i = 0; i < NNLS_NPHASES; ++i) {
+    h->tm.ms[i] = 0.0;
+    h->tm.launches[i] = 0;
+  }
+  h->tm.on = on != 0;
+  return NNLS_OK;
+}
+
+nnls_status nnls_timing_read(nnls_handle* h, double* ms, int64_t* launches, int32_t cap) {
+  if (!h) return NNLS_ERR_INVALID_ARG;
+  tm_flush(h);
+  for (int i = 0; i < NNLS_NPHASES && i < cap; ++i) {
+    if (ms) ms[i] = h->tm.ms[i];
+    if (launches) launches[i] = h->tm.launches[i];
+  }
+  return NNLS_OK;
+}
+
 nnls_status nnls_destroy(nnls_handle* h) {
   if (!h) return NNLS_OK;
   if (h->stream) cudaStreamSynchronize(h->stream);
@@ -492,6 +592,7 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
                  &h->b_info_d, &h->b_x, &h->b_mask};
   for (Buf* b : bufs) free_buf(*b);
+  for (cudaEvent_t e : h->tm.pool) cudaEventDestroy(e);
   if (h->h) cudaFreeHost(h->h);
   delete h;
   return NNLS_OK;
@@ -681,9 +782,10 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
   }
   CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)batch * m, cudaMemcpyDefault, s));
   CK(cudaMemsetAsync(h->err.p, 0, sizeof(int), s));
-  CK(launch_validate_batched(batch, m, n, P<int64_t>(h->b_nnz_off), P<int32_t>(h->rowptr),
-                             P<int32_t>(h->colind), P<double>(h->vals), P<double>(h->b),
-                             P<int>(h->err), s));
+  TIMED(NNLS_PH_VALIDATE, 1,
+        launch_validate_batched(batch, m, n, P<int64_t>(h->b_nnz_off), P<int32_t>(h->rowptr),
+                                P<int32_t>(h->colind), P<double>(h->vals), P<double>(h->b),
+                                P<int>(h->err), s));
   CK(cudaMemcpyAsync(&h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (h->h->err) return map_err_bits(h->h->err);
@@ -740,10 +842,12 @@ nnls_status nnls_solve_batched(nnls_handle* h, double* x_out, nnls_info* info_ou
   a.lsqr_mode = p.lsqr_mode;
   a.itn_limit = p.lsqr_itn_limit;
   a.kkt = p.kkt;
-  CK(launch_batched_nnz(a, h->ldg, h->sms, s));
+  TIMED(NNLS_PH_BATCHED, 1, launch_batched_nnz(a, h->ldg, h->sms, s));
   const size_t nb = (size_t)h->batch;
+  const int ibd = tm_begin(h);
   if (x_out) CK(cudaMemcpyAsync(x_out, h->b_x.p, sizeof(double) * nb * h->n, cudaMemcpyDefault, s));
   if (mask_out) CK(cudaMemcpyAsync(mask_out, h->b_mask.p, nb * h->n, cudaMemcpyDefault, s));
+  tm_end(h, NNLS_PH_DOWNLOAD, ibd, 0);
   nnls_status worst = NNLS_OK;
   if (info_out) {
     int32_t* ii = (int32_t*)malloc(sizeof(int32_t) * 8 * nb);

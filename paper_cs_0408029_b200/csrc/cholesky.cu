@@ -275,32 +275,49 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
   }
 }
 
+static cudaError_t set_attrs() {
+  static bool attr_set = false;
+  if (attr_set) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * kSmemDoubles));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(double) * (T * LDS + 4 * T)));
+  if (e != cudaSuccess) return e;
+  attr_set = true;
+  return cudaSuccess;
+}
+
+cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
+                               double* Lt, int* flags, DevState* st, int sm_count, cudaStream_t s) {
+  cudaError_t e = set_attrs();
+  if (e != cudaSuccess) return e;
+  // grid sized for the largest possible DAG; tasks are claimed dynamically
+  const int ntr = (n + 1 + T - 1) / T;
+  const int tasks = ntr * (ntr + 1) / 2;
+  int grid = sm_count * 2;
+  if (grid > tasks) grid = tasks;
+  chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, flags, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
+                                  int sm_count, cudaStream_t s) {
+  cudaError_t e = set_attrs();
+  if (e != cudaSuccess) return e;
+  const int ntr = (n + 1 + T - 1) / T;
+  int* xflags = flags + chol_tile_count(n);
+  const int g2 = ntr < sm_count ? ntr : sm_count;
+  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * (T * LDS + 4 * T), s>>>(Lt, xflags, xF, st);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cholesky_solve(int n, const double* G, int ldg, const double* c,
                                   const int32_t* Fidx, double* Lt, int* flags, double* xF,
                                   DevState* st, int sm_count, cudaStream_t s) {
-  const size_t smem = sizeof(double) * kSmemDoubles;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * (T * LDS + 4 * T)));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const size_t ntile = chol_tile_count(n);
-  int* xflags = flags + ntile;
-  // grid sized for the largest possible DAG; tasks are claimed dynamically
-  const int ntr = (n + 1 + T - 1) / T;
-  int tasks = ntr * (ntr + 1) / 2;
-  int grid = sm_count * 2;
-  if (grid > tasks) grid = tasks;
-  chol_factor_kernel<<<grid, kThreads, smem, s>>>(G, ldg, c, Fidx, Lt, flags, st);
-  int g2 = ntr < sm_count ? ntr : sm_count;
-  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * (T * LDS + 4 * T), s>>>(Lt, xflags, xF,
-                                                                               st);
-  return cudaGetLastError();
+  cudaError_t e = launch_chol_factor(n, G, ldg, c, Fidx, Lt, flags, st, sm_count, s);
+  if (e != cudaSuccess) return e;
+  return launch_chol_backsolve(n, Lt, flags, xF, st, sm_count, s);
 }
 
 }  // namespace nnls

@@ -49,6 +49,10 @@ size_t chol_tile_count(int n);  // tiles needed for |F| <= n (bordered, lower)
 cudaError_t launch_cholesky_solve(int n, const double* G, int ldg, const double* c,
                                   const int32_t* Fidx, double* Lt, int* flags, double* xF,
                                   DevState* st, int sm_count, cudaStream_t s);
+cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
+                               double* Lt, int* flags, DevState* st, int sm_count, cudaStream_t s);
+cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
+                                  int sm_count, cudaStream_t s);
 
 // ---- a10 LSQR + final report (lsqr.cu) ----------------------------------
 struct LsqrArgs {
