@@ -58,8 +58,8 @@ int round_up(int v, int q) { return (v + q - 1) / q * q; }
 
 struct HostState {
   DevState st;
-  int err;
-  int pad[3];
+  int err[4];   // validation bits, longest row, longest column
+  int plan[4];  // cluster LSQR slice maxima (rows, CSR nnz, cols, CSC nnz)
 };
 
 struct Timing {
@@ -93,6 +93,7 @@ struct nnls_handle {
   size_t ntile = 0;
   int trace_cap = 0;
   HostState* h = nullptr;                 // pinned readback
+  bool no_cluster = false;  // force the full-grid LSQR (tests / env NNLS_NO_CLUSTER)
   // batched
   bool batched = false;
   int batch = 0;
@@ -224,7 +225,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->xfin, sizeof(double) * (size_t)n));
   CK(ensure(h->partials, sizeof(double) * 8 * (size_t)(h->sms * 4)));
   CK(ensure(h->st, sizeof(DevState)));
-  CK(ensure(h->err, sizeof(int) * 4));
+  CK(ensure(h->err, sizeof(int) * 8));
   const int cap = h->prm.trace ? (h->prm.max_iter > 0 ? h->prm.max_iter : 10 * n) + 1 : 0;
   h->trace_cap = cap;
   if (cap > 0) CK(ensure(h->trace, sizeof(TraceRec) * (size_t)cap));
@@ -236,21 +237,25 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
     CK(cudaMemcpyAsync(h->vals.p, vals, sizeof(double) * (size_t)nnz, cudaMemcpyDefault, s));
   }
   CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)m, cudaMemcpyDefault, s));
-  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int), s));
+  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int) * 8, s));
   tm_end(h, NNLS_PH_UPLOAD, ib, 0);
   TIMED(NNLS_PH_VALIDATE, 1,
         launch_validate(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                         P<double>(h->b), P<int>(h->err), s));
   // validation must pass before structure-dependent kernels touch the data
   int herr = 0;
-  CK(cudaMemcpyAsync(&h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  herr = h->h->err;
+  herr = h->h->err[0];
   if (herr) return map_err_bits(herr);
   TIMED(NNLS_PH_CSC, nnz > 0 ? 4 : 3,
         launch_csr_to_csc(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                           P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                          P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s));
+                          P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s,
+                          P<int>(h->err) + 2));
+  // cluster-LSQR slice plan; read back with the first status sync of nnls_solve
+  CK(launch_lsqr_plan(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colptr), P<int>(h->err) + 4, s));
+  CK(cudaMemcpyAsync(h->h->plan, P<int>(h->err) + 4, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
   double* G = P<double>(h->Gc);
   double* c = G + (size_t)n * h->ldg;
   TIMED(NNLS_PH_GRAM, 1,
@@ -283,6 +288,7 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
     return s;
   }
   memset(h->h, 0, sizeof(HostState));
+  h->no_cluster = getenv("NNLS_NO_CLUSTER") != nullptr;
   *out = h;
   return NNLS_OK;
 }
@@ -482,7 +488,19 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   a.G = G;
   a.ldg = h->ldg;
   a.c = c;
-  TIMED(NNLS_PH_LSQR, 1, launch_lsqr_final(a, h->sms, s));
+  // cluster-resident LSQR when A's slices fit in one 16-CTA cluster's shared
+  // memory (configs 0, 1, 3); the full-grid cooperative kernel otherwise
+  {
+    const int ib = tm_begin(h);
+    cudaError_t e = h->no_cluster ? cudaErrorNotSupported
+                                  : launch_lsqr_cluster_planned(a, h->h->plan, s);
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      e = launch_lsqr_final(a, h->sms, s);
+    }
+    CK(e);
+    tm_end(h, NNLS_PH_LSQR, ib, 1);
+  }
   if (x_out) {
     const int ib = tm_begin(h);
     CK(cudaMemcpyAsync(x_out, h->xfin.p, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
@@ -559,6 +577,17 @@ nnls_status nnls_get_gram(nnls_handle* h, double* G_out, double* c_out) {
     CK(cudaMemcpyAsync(c_out, G + (size_t)n * h->ldg, sizeof(double) * n, cudaMemcpyDefault,
                        h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  return NNLS_OK;
+}
+
+// debug hook (not in nnls.h): per-task timestamps of the Cholesky DAG
+NNLS_API nnls_status nnls_debug_chol_profile(unsigned long long* dev_buf) {
+  CK(chol_debug_set_profile(dev_buf));
+  return NNLS_OK;
+}
+
+NNLS_API nnls_status nnls_debug_lsqr_profile(unsigned long long* dev_buf) {
+  CK(lsqr_debug_set_profile(dev_buf));
   return NNLS_OK;
 }
 
@@ -786,9 +815,9 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
         launch_validate_batched(batch, m, n, P<int64_t>(h->b_nnz_off), P<int32_t>(h->rowptr),
                                 P<int32_t>(h->colind), P<double>(h->vals), P<double>(h->b),
                                 P<int>(h->err), s));
-  CK(cudaMemcpyAsync(&h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (h->h->err) return map_err_bits(h->h->err);
+  if (h->h->err[0]) return map_err_bits(h->h->err[0]);
   h->loaded = true;
   return NNLS_OK;
 }

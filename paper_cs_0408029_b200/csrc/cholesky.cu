@@ -16,14 +16,19 @@
 //     so there is no grid-wide barrier; a task only waits for the tiles it
 //     reads.  Since tasks are claimed in topological order by running CTAs,
 //     the DAG cannot deadlock.
-//   * The tile update  C_ij -= L_ik L_jk^T  (the O(f^3) work) runs on the FP64
-//     tensor pipe: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), the only FP64 tensor
-//     path on sm_100a (tcgen05 has no f64 kind).  8 warps, each a 16 x 32
-//     register accumulator; operands staged in shared memory.
-//   * Diagonal tiles are factored (POTRF) and off-diagonal tiles triangular-
-//     solved (TRSM) in shared memory, column by column.  Pivot <= 0,
-//     < 1e-300 or non-finite -> NOT_PD (reading c13).
-//   * L^T x = z by a second DAG kernel over column tiles (last to first).
+//   * Every O(T^3) step runs on the FP64 tensor pipe, mma.sync.m8n8k4.f64
+//     (SASS DMMA.8x8x4 -- the only FP64 tensor path on sm_100a, tcgen05 has no
+//     f64 kind): the left-looking update C_ij -= L_ik L_jk^T, and the
+//     triangular solve of the off-diagonal tiles, done as a product with the
+//     explicit inverse of the diagonal tile, X = C_ij L_jj^-T.
+//   * The diagonal task factors its tile (2 x 2 blocks of 32: POTRF, TRSM,
+//     SYRK, POTRF in one warp) and inverts it (TRTRI of the two 32-blocks by
+//     two warps, off-diagonal block by products).  Column-sequential work is
+//     thereby confined to the diagonal tile; the off-diagonal tiles never run
+//     a column-sequential loop.  Pivot <= 0, < 1e-300 or non-finite -> NOT_PD
+//     (reading c13).
+//   * L^T x = z by a second DAG kernel over column tiles (last to first), each
+//     step a GEMV with the published inverse diagonal tile.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -36,14 +41,32 @@ namespace {
 constexpr int T = kTile;
 constexpr int LDS = T + 4;  // smem row stride (doubles): conflict-free 8x4 fragment reads
 constexpr int kThreads = 256;
-constexpr int kSmemDoubles = 3 * T * LDS;
+constexpr int kSmemDoubles = 4 * T * LDS;
 
 __host__ __device__ inline int tidx(int i, int j) { return i * (i + 1) / 2 + j; }
+inline int tri_tiles(int n) {
+  const int ntr = (n + 1 + T - 1) / T;
+  return ntr * (ntr + 1) / 2;
+}
 }  // namespace
 
+// Debug hook (not part of the ABI): per-task %globaltimer stamps of the
+// factorization DAG, enabled by nnls_debug_chol_profile(ptr).
+__device__ unsigned long long* g_chol_prof = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROF_STAMP(task, slot)                                                                  \
+  do {                                                                                          \
+    if (g_chol_prof != nullptr && threadIdx.x == 0) g_chol_prof[(task) * 8 + (slot)] = gtimer(); \
+  } while (0)
+
+// Lower tiles L(i,j) followed by one inverse tile per tile column.
 size_t chol_tile_count(int n) {
   const int ntr = (n + 1 + T - 1) / T;
-  return (size_t)ntr * (ntr + 1) / 2;
+  return (size_t)tri_tiles(n) + ntr;
 }
 
 // load a T x T tile (row-major, contiguous) from global into smem (stride LDS)
@@ -65,15 +88,141 @@ __device__ __forceinline__ void store_tile(double* __restrict__ dst, const doubl
   }
 }
 
-__global__ void __launch_bounds__(kThreads) chol_factor_kernel(
+// asynchronous 16-byte copies global -> shared (cp.async.cg: L2 only)
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void tile_async(double* __restrict__ dst, const double* __restrict__ src) {
+  for (int e = threadIdx.x; e < T * T / 2; e += kThreads) {
+    const int r = (2 * e) / T, c = (2 * e) % T;
+    cp_async16(dst + r * LDS + c, src + 2 * e);
+  }
+}
+
+// acc (16 x 32 per warp) += sign * A B^T for 64 x 64 tiles in smem (B given
+// by rows: C[m][n] += sum_k A[m][k] B[n][k]), on DMMA 8x8x4.
+template <bool kNegate>
+__device__ __forceinline__ void dmma_tile(double (&acc)[2][4][2], const double* __restrict__ A,
+                                          const double* __restrict__ B, int lane, int rb0, int cb0) {
+#pragma unroll 4
+  for (int kk = 0; kk < T; kk += 4) {
+    double av[2], bv[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const double v = A[(rb0 + 8 * a + (lane >> 2)) * LDS + kk + (lane & 3)];
+      av[a] = kNegate ? -v : v;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bv[q] = B[(cb0 + 8 * q + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
+  }
+}
+__device__ __forceinline__ void acc_load(double (&acc)[2][4][2], const double* S, int lane, int rb0,
+                                         int cb0) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        acc[a][q][v] = S[(rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v];
+}
+__device__ __forceinline__ void acc_store(const double (&acc)[2][4][2], double* S, int lane, int rb0,
+                                          int cb0) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        S[(rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v] = acc[a][q][v];
+}
+
+// POTRF of a 32-row block held by one warp, lane = row, a[t] = A[lane][t].
+// Columns c < ncols are pivots; rows >= ncols (e.g. the bordered row c_F^T)
+// are eliminated as off-diagonal rows.  Right-looking, updates applied in
+// increasing c.  The finished column is broadcast through shared memory
+// (colbuf: broadcast loads at immediate offsets); updates are predicated,
+// never divergent.  The column loop is rolled 4 columns at a time with a
+// register shift (register arrays are indexed by compile-time constants only;
+// a fully unrolled loop is instruction-bound, not cheaper).  Writes L[lane][c]
+// to out[lane*LDS + c] (0 above the diagonal and in non-pivot columns),
+// 1/l_cc to rinv[c].  Returns the first bad pivot or -1.
+__device__ __forceinline__ int warp_potrf32(double (&a)[32], int ncols, int lane, double* rinv,
+                                            double* out, double* colbuf) {
+  int bad = -1;
+#pragma unroll 1
+  for (int c0 = 0; c0 < ncols; c0 += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u;
+      if (c < ncols) {
+        const double d = __shfl_sync(kFull, a[u], c);
+        if ((!(d > 0.0) || d < 1e-300 || !isfinite(d)) && bad < 0) bad = c;
+        const double inv = rsqrt(d);
+        const double lic = (lane == c) ? d * inv : ((lane > c) ? a[u] * inv : 0.0);
+        colbuf[lane] = lic;
+        if (lane == 0) rinv[c] = inv;
+        out[lane * LDS + c] = lic;
+        __syncwarp();
+        const double* cb = colbuf + c;             // cb[t] = l_{c+t, c}
+        const int lim = min(lane, ncols - 1) - c;  // update columns c+t, 1 <= t <= lim
+#pragma unroll
+        for (int t = 1; u + t < 32; ++t) {
+          const double v = cb[t];
+          if (t <= lim) a[u + t] = fma(-lic, v, a[u + t]);
+        }
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 28; ++t) a[t] = a[t + 4];
+    a[28] = a[29] = a[30] = a[31] = 0.0;
+  }
+  for (int col = ncols; col < 32; ++col) out[lane * LDS + col] = 0.0;
+  return bad;
+}
+
+// Inverse of a 32 x 32 lower-triangular block (smem, stride LDS) with
+// reciprocal diagonal rinvb: lane = column c computes X[:, c] by forward
+// substitution, x_i = (delta_ic - sum_{k<i} L_ik x_k) / L_ii.  ncols pivots;
+// rows/columns >= ncols are zero.  Writes X (lower) to out (stride LDS).
+__device__ __forceinline__ void warp_trtri32(const double* __restrict__ Lb,
+                                             const double* __restrict__ rinvb, int ncols, int lane,
+                                             double* __restrict__ out) {
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) s = fma(-Lb[i * LDS + k], x[k], s);
+    x[i] = (i < ncols && lane < ncols) ? s * rinvb[i] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) out[i * LDS + lane] = x[i];
+}
+
+__global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     const double* __restrict__ G, int ldg, const double* __restrict__ cvec,
-    const int32_t* __restrict__ Fidx, double* __restrict__ Lt, int* __restrict__ flags,
-    DevState* st) {
+    const int32_t* __restrict__ Fidx, double* __restrict__ Lt, double* __restrict__ Linv,
+    int* __restrict__ flags, DevState* st) {
   extern __shared__ double smem[];
-  double* S = smem;               // task tile (accumulator / result)
-  double* LA = smem + T * LDS;    // L(i,k)
-  double* LB = smem + 2 * T * LDS;  // L(j,k) or L(j,j)
-  __shared__ int s_task;
+  // four T x LDS buffers: BUF(0) = S (task tile) and, during the update loop,
+  // the second (i,k)/(j,k) operand pair with BUF(1); BUF(2)/BUF(3) = first pair.
+#define BUF(q) (smem + (q) * (T * LDS))
+  double* S = BUF(0);
+  __shared__ double rinv[T];
+  __shared__ double colbuf[64];
+  __shared__ int s_task, s_ready, s_bad;
 
   const int f = st->f;
   const int epoch = st->epoch;
@@ -82,8 +231,8 @@ __global__ void __launch_bounds__(kThreads) chol_factor_kernel(
   const int ntr = (f + 1 + T - 1) / T;  // tile rows (incl. the rhs row f)
   const int total = ntc * ntr - ntc * (ntc - 1) / 2;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int rb0 = (w >> 1) * 16;  // warp tile: rows rb0..rb0+15
-  const int cb0 = (w & 1) * 32;   //            cols cb0..cb0+31
+  const int rb0 = (w >> 1) * 16;  // warp tile of the DMMA products: rows rb0..rb0+15
+  const int cb0 = (w & 1) * 32;   //                                 cols cb0..cb0+31
 
   for (;;) {
     if (tid == 0) s_task = atomicAdd(&st->tile_counter, 1);
@@ -98,6 +247,13 @@ __global__ void __launch_bounds__(kThreads) chol_factor_kernel(
     const int i = j + t;
     const int rv = min(T, f + 1 - i * T);  // valid rows in this tile (incl. rhs row)
     const int cv = min(T, f - j * T);      // valid (factored) columns
+    const int task = s_task;
+    PROF_STAMP(task, 0);
+    if (g_chol_prof != nullptr && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_chol_prof[task * 8 + 7] = ((unsigned long long)i << 40) | ((unsigned long long)j << 20) | smid;
+    }
 
     // 1) gather A(i,j) = [G_FF; c_F^T] block straight from the cached Gram
     for (int e = tid; e < T * T; e += kThreads) {
@@ -110,112 +266,194 @@ __global__ void __launch_bounds__(kThreads) chol_factor_kernel(
       S[r * LDS + cc] = v;
     }
     __syncthreads();
+    PROF_STAMP(task, 1);
 
-    // 2) left-looking update S -= sum_{k<j} L(i,k) L(j,k)^T on the DMMA pipe
+    // 2) left-looking update S -= sum_{k<j} L(i,k) L(j,k)^T on the DMMA pipe,
+    //    operand tiles double-buffered with cp.async
     if (j > 0) {
       double acc[2][4][2];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int v = 0; v < 2; ++v)
-            acc[a][q][v] = S[(rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v];
+      acc_load(acc, S, lane, rb0, cb0);
+      __syncthreads();  // BUF(0) is reused as an operand buffer below
+      bool have_next = false;
       for (int k = 0; k < j; ++k) {
-        if (tid == 0) {
-          wait_flag(&flags[tidx(i, k)], epoch);
-          wait_flag(&flags[tidx(j, k)], epoch);
+        double* LA = BUF((k & 1) ? 0 : 2);
+        double* LB = BUF((k & 1) ? 1 : 3);
+        if (!have_next) {
+          if (tid == 0) {
+            wait_flag(&flags[tidx(i, k)], epoch);
+            wait_flag(&flags[tidx(j, k)], epoch);
+          }
+          __syncthreads();
+          tile_async(LA, Lt + (size_t)tidx(i, k) * T * T);
+          tile_async(LB, Lt + (size_t)tidx(j, k) * T * T);
+          cp_async_commit();
         }
-        __syncthreads();
-        load_tile(LA, Lt + (size_t)tidx(i, k) * T * T);
-        load_tile(LB, Lt + (size_t)tidx(j, k) * T * T);
-        __syncthreads();
-#pragma unroll 4
-        for (int kk = 0; kk < T; kk += 4) {
-          double av[2], bv[4];
-#pragma unroll
-          for (int a = 0; a < 2; ++a) av[a] = -LA[(rb0 + 8 * a + (lane >> 2)) * LDS + kk + (lane & 3)];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) bv[q] = LB[(cb0 + 8 * q + (lane >> 2)) * LDS + kk + (lane & 3)];
-#pragma unroll
-          for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
+        // try to prefetch k+1 into the other pair if its tiles are ready
+        have_next = false;
+        if (k + 1 < j) {
+          if (tid == 0)
+            s_ready = (ld_acquire(&flags[tidx(i, k + 1)]) == epoch) &&
+                      (ld_acquire(&flags[tidx(j, k + 1)]) == epoch);
+          __syncthreads();
+          if (s_ready) {
+            tile_async(BUF((k & 1) ? 2 : 0), Lt + (size_t)tidx(i, k + 1) * T * T);
+            tile_async(BUF((k & 1) ? 3 : 1), Lt + (size_t)tidx(j, k + 1) * T * T);
+            cp_async_commit();
+            have_next = true;
+          }
         }
+        if (have_next) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncthreads();
+        dmma_tile<true>(acc, LA, LB, lane, rb0, cb0);
         __syncthreads();
       }
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int v = 0; v < 2; ++v)
-            S[(rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v] = acc[a][q][v];
+      acc_store(acc, S, lane, rb0, cb0);
       __syncthreads();
     }
+    PROF_STAMP(task, 2);
 
     if (i == j) {
-      // 3a) POTRF of the diagonal tile (rows may include the rhs row f)
-      for (int c = 0; c < cv; ++c) {
-        const double d = S[c * LDS + c];
-        const bool bad = !(d > 0.0) || d < 1e-300 || !isfinite(d);
-        if (bad && tid == 0) {
-          if (atomicCAS(&st->status, 0, 7) == 0) st->not_pd_col = j * T + c;
-        }
-        const double l = sqrt(d);
-        __syncthreads();
-        if (tid > c && tid < rv) S[tid * LDS + c] = S[tid * LDS + c] / l;
-        if (tid == 0) S[c * LDS + c] = l;
-        __syncthreads();
-        // trailing update of the tile: S[r][q] -= S[r][c] S[q][c], c < q <= r
-        const int nr = rv - c - 1;
-        for (int e = tid; e < nr * (cv - c - 1); e += kThreads) {
-          const int r = c + 1 + e / (cv - c - 1);
-          const int q = c + 1 + e % (cv - c - 1);
-          if (q <= r) S[r * LDS + q] -= S[r * LDS + c] * S[q * LDS + c];
-        }
-        __syncthreads();
+      // 3a) diagonal tile: L_jj = chol(A_jj) as 2 x 2 blocks of 32, and
+      //     Linv_jj = L_jj^-1 (published for the TRSM tasks and the solve).
+      double* X = BUF(1);   // inverse
+      double* Tm = BUF(2);  // scratch: L21 Linv11
+      const int n1 = min(32, cv), n2 = cv - 32;
+      if (tid == 0) s_bad = -1;
+      if (w == 0) {
+        double a[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) a[k] = S[lane * LDS + k];
+        const int b1 = warp_potrf32(a, n1, lane, rinv, S, colbuf);
+        if (b1 >= 0 && lane == 0) s_bad = b1;
       }
-      for (int e = tid; e < T * T; e += kThreads) {  // clear the strict upper part
+      __syncthreads();
+      if (w == 1) {
+        warp_trtri32(S, rinv, n1, lane, X);  // Linv11, concurrently with block 2
+      } else if (w == 0 && rv > 32) {
+        // TRSM of rows 32..63 against L11 (lane = row, shifted registers)
+        double bq[32];
+        double* R2 = S + 32 * LDS;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) bq[k] = R2[lane * LDS + k];
+#pragma unroll 1
+        for (int c0 = 0; c0 < n1; c0 += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u;
+            if (c < n1) {
+              const double x = bq[u] * rinv[c];
+              bq[u] = x;
+              R2[lane * LDS + c] = x;
+              const double* Lc = S + c * LDS + c;  // Lc[tt*LDS] = L11[c+tt][c]
+#pragma unroll
+              for (int tt = 1; u + tt < 32; ++tt) {
+                const double v = Lc[tt * LDS];
+                if (c + tt < n1) bq[u + tt] = fma(-x, v, bq[u + tt]);
+              }
+            }
+          }
+#pragma unroll
+          for (int tt = 0; tt < 28; ++tt) bq[tt] = bq[tt + 4];
+          bq[28] = bq[29] = bq[30] = bq[31] = 0.0;
+        }
+        __syncwarp();
+        // SYRK: A22[lane][k] -= L21[lane][:] . L21[k][:]
+        double a[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) a[k] = R2[lane * LDS + 32 + k];
+        if (n2 > 0) {
+#pragma unroll 1
+          for (int c = 0; c < n1; ++c) {
+            const double lrc = R2[lane * LDS + c];
+            const double* Lk = R2 + c;  // Lk[k*LDS] = L21[k][c]
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const double v = Lk[k * LDS];
+              if (k < n2 && k <= lane) a[k] = fma(-lrc, v, a[k]);
+            }
+          }
+          const int b2 = warp_potrf32(a, n2, lane, rinv + 32, S + 32 * LDS + 32, colbuf);
+          if (b2 >= 0 && lane == 0 && s_bad < 0) s_bad = 32 + b2;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) R2[lane * LDS + 32 + k] = 0.0;
+        }
+      }
+      __syncthreads();
+      // Linv22 (warp 0) || Tm = L21 Linv11 over the pivot rows (other warps)
+      if (w == 0) {
+        if (n2 > 0) {
+          warp_trtri32(S + 32 * LDS + 32, rinv + 32, n2, lane, X + 32 * LDS + 32);
+        } else {
+          for (int r = 0; r < 32; ++r) X[(32 + r) * LDS + 32 + lane] = 0.0;
+        }
+      } else {
+        for (int e = tid - 32; e < 32 * 32; e += kThreads - 32) {
+          const int r = e >> 5, c = e & 31;  // Tm[r][c] = sum_k L21[r][k] Linv11[k][c]
+          double s = 0.0;
+          if (r < n2)
+            for (int k = c; k < n1; ++k) s = fma(S[(32 + r) * LDS + k], X[k * LDS + c], s);
+          Tm[r * LDS + c] = s;
+        }
+      }
+      __syncthreads();
+      // Linv21 = -Linv22 Tm; clear the strict upper parts of X and S
+      for (int e = tid; e < 32 * 32; e += kThreads) {
+        const int r = e >> 5, c = e & 31;
+        double s = 0.0;
+        for (int k = 0; k <= r; ++k) s = fma(X[(32 + r) * LDS + 32 + k], Tm[k * LDS + c], s);
+        X[(32 + r) * LDS + c] = -s;
+        X[r * LDS + 32 + c] = 0.0;  // upper-right block
+      }
+      for (int e = tid; e < T * T; e += kThreads) {
         const int r = e / T, q = e % T;
         if (q > r) S[r * LDS + q] = 0.0;
       }
       __syncthreads();
+      if (tid == 0 && s_bad >= 0) {
+        if (atomicCAS(&st->status, 0, 7) == 0) st->not_pd_col = j * T + s_bad;
+      }
+      store_tile(Linv + (size_t)j * T * T, X);
     } else {
-      // 3b) TRSM: S <- S L(j,j)^-T, column by column
+      // 3b) TRSM as a product with the inverse diagonal tile: S <- S Linv_jj^T
+      double* LB = BUF(1);
       if (tid == 0) wait_flag(&flags[tidx(j, j)], epoch);
       __syncthreads();
-      load_tile(LB, Lt + (size_t)tidx(j, j) * T * T);
+      PROF_STAMP(task, 3);
+      load_tile(LB, Linv + (size_t)j * T * T);
       __syncthreads();
-      for (int c = 0; c < cv; ++c) {
-        if (tid < rv) S[tid * LDS + c] = S[tid * LDS + c] / LB[c * LDS + c];
-        __syncthreads();
-        const int nq = cv - c - 1;
-        for (int e = tid; e < rv * nq; e += kThreads) {
-          const int r = e / nq, q = c + 1 + e % nq;
-          S[r * LDS + q] -= S[r * LDS + c] * LB[q * LDS + c];
-        }
-        __syncthreads();
-      }
+      double acc[2][4][2] = {};
+      dmma_tile<false>(acc, S, LB, lane, rb0, cb0);
+      __syncthreads();
+      acc_store(acc, S, lane, rb0, cb0);
+      __syncthreads();
     }
+    PROF_STAMP(task, 4);
     // 4) publish
     store_tile(Lt + (size_t)tidx(i, j) * T * T, S);
     __threadfence();
     __syncthreads();
     if (tid == 0) st_release(&flags[tidx(i, j)], epoch);
+    PROF_STAMP(task, 5);
   }
+#undef BUF
+}
+
+cudaError_t chol_debug_set_profile(unsigned long long* p) {
+  return cudaMemcpyToSymbol(g_chol_prof, &p, sizeof(p));
 }
 
 // L^T x = z, z = row f of the bordered factor.  Column tiles J from the last
 // to the first; task J waits for x_I (I > J), subtracts L_IJ^T x_I, then
-// solves with L_JJ^T.  xflags[J] == epoch: x_J published.
+// x_J = Linv_JJ^T s (a GEMV, no sequential substitution).  xflags[J] == epoch:
+// x_J published.
 __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* __restrict__ Lt,
+                                                                   const double* __restrict__ Linv,
                                                                    int* __restrict__ xflags,
                                                                    double* __restrict__ xF,
                                                                    DevState* st) {
-  extern __shared__ double smem[];
-  double* Ls = smem;             // tile L(J,J) or L(I,J), stride LDS
-  double* part = smem + T * LDS;  // 4 x T partial sums
+  __shared__ double part[4 * T];
   __shared__ double s_rhs[T];
   __shared__ double s_x[T];
   __shared__ int s_task;
@@ -225,6 +463,7 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
   const int ntc = (f + T - 1) / T;
   const int Rf = f / T, rf = f % T;  // tile row / local row of the rhs row
   const int tid = threadIdx.x;
+  const int c = tid & (T - 1), rg = tid >> 6;  // column, 4 row groups
   for (;;) {
     if (tid == 0) s_task = atomicAdd(&st->solve_counter, 1);
     __syncthreads();
@@ -232,7 +471,6 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
     if (t >= ntc) break;
     const int J = ntc - 1 - t;
     const int cv = min(T, f - J * T);
-    // z_J
     if (tid < T) s_rhs[tid] = (tid < cv) ? __ldcg(&Lt[(size_t)tidx(Rf, J) * T * T + rf * T + tid]) : 0.0;
     __syncthreads();
     // subtract L_IJ^T x_I for I = ntc-1 .. J+1 (the latest-ready block last)
@@ -243,7 +481,6 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
       if (tid < T) s_x[tid] = (tid < rvI) ? __ldcg(&xF[I * T + tid]) : 0.0;
       __syncthreads();
       const double* L = Lt + (size_t)tidx(I, J) * T * T;
-      const int c = tid & (T - 1), rg = tid >> 6;  // 4 row groups
       double p = 0.0;
       for (int r = rg; r < rvI; r += 4) p = fma(__ldcg(&L[r * T + c]), s_x[r], p);
       part[rg * T + c] = p;
@@ -251,24 +488,13 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
       if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
       __syncthreads();
     }
-    // diagonal: L_JJ^T x_J = s_rhs (backward substitution), one warp
-    load_tile(Ls, Lt + (size_t)tidx(J, J) * T * T);
+    // x_J = Linv_JJ^T s : x[c] = sum_{r >= c} Linv[r][c] s[r]
+    const double* X = Linv + (size_t)J * T * T;
+    double p = 0.0;
+    for (int r = rg; r < cv; r += 4) p = fma(__ldcg(&X[r * T + c]), s_rhs[r], p);
+    part[rg * T + c] = p;
     __syncthreads();
-    if (tid < 32) {
-      const int l = tid;
-      double s0 = s_rhs[l], s1 = s_rhs[l + 32];
-      for (int c = cv - 1; c >= 0; --c) {
-        const double own = (c < 32) ? s0 : s1;
-        const double sc = __shfl_sync(kFull, own, c & 31);
-        const double xc = sc / Ls[c * LDS + c];
-        if (l == 0) s_x[c] = xc;
-        // s_t -= L[c][t] x_c for t < c
-        if (l < c) s0 = fma(-Ls[c * LDS + l], xc, s0);
-        if (l + 32 < c) s1 = fma(-Ls[c * LDS + l + 32], xc, s1);
-      }
-    }
-    __syncthreads();
-    if (tid < cv) xF[J * T + tid] = s_x[tid];
+    if (tid < cv) xF[J * T + tid] = (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
     __threadfence();
     __syncthreads();
     if (tid == 0) st_release(&xflags[J], epoch);
@@ -281,9 +507,6 @@ static cudaError_t set_attrs() {
   cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * kSmemDoubles));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(double) * (T * LDS + 4 * T)));
-  if (e != cudaSuccess) return e;
   attr_set = true;
   return cudaSuccess;
 }
@@ -293,22 +516,22 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
   // grid sized for the largest possible DAG; tasks are claimed dynamically
-  const int ntr = (n + 1 + T - 1) / T;
-  const int tasks = ntr * (ntr + 1) / 2;
-  int grid = sm_count * 2;
+  const int tasks = tri_tiles(n);
+  int grid = sm_count;  // 136 KB smem per CTA: one persistent CTA per SM
   if (grid > tasks) grid = tasks;
-  chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, flags, st);
+  double* Linv = Lt + (size_t)tri_tiles(n) * T * T;
+  chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, Linv,
+                                                                          flags, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
                                   int sm_count, cudaStream_t s) {
-  cudaError_t e = set_attrs();
-  if (e != cudaSuccess) return e;
   const int ntr = (n + 1 + T - 1) / T;
-  int* xflags = flags + chol_tile_count(n);
+  int* xflags = flags + tri_tiles(n);
+  const double* Linv = Lt + (size_t)tri_tiles(n) * T * T;
   const int g2 = ntr < sm_count ? ntr : sm_count;
-  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * (T * LDS + 4 * T), s>>>(Lt, xflags, xF, st);
+  chol_backsolve_kernel<<<g2, kThreads, 0, s>>>(Lt, Linv, xflags, xF, st);
   return cudaGetLastError();
 }
 

@@ -87,11 +87,9 @@ NNLS_DEV int ld_volatile(const int* p) { return *(volatile const int*)p; }
 
 // spin (one thread) until *flag == want
 NNLS_DEV void wait_flag(const int* flag, int want) {
-  if (ld_acquire(flag) == want) return;
-  unsigned ns = 32;
+  int spins = 0;
   while (ld_acquire(flag) != want) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+    if (++spins > 64) __nanosleep(40);
   }
 }
 

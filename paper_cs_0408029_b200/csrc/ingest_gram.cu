@@ -26,9 +26,10 @@ __global__ void validate_kernel(int m, int n, int64_t nnz, const int32_t* __rest
                                 int* err) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  int e_local = 0;
+  int e_local = 0, maxlen = 0;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
     int64_t lo = rowptr[r], hi = rowptr[r + 1];
+    if (hi - lo > maxlen) maxlen = (int)min((int64_t)0x7fffffff, hi - lo);
     if (lane == 0) {
       if (r == 0 && lo != 0) e_local |= 1;
       if (r == m - 1 && hi != nnz) e_local |= 1;
@@ -46,6 +47,7 @@ __global__ void validate_kernel(int m, int n, int64_t nnz, const int32_t* __rest
     }
   }
   if (e_local) atomicOr(err, e_local);
+  if (lane == 0 && maxlen > 0) atomicMax(err + 1, maxlen);  // longest row (LSQR planning)
 }
 
 cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
@@ -65,15 +67,17 @@ __global__ void colcount_kernel(int64_t nnz, const int32_t* __restrict__ colind,
 }
 
 // In-place inclusive scan of cnt[0..len) (cnt[0] = 0 on entry) -> colptr; one CTA.
-__global__ void scan_kernel(int len, int32_t* cnt, int32_t* cursor) {
+__global__ void scan_kernel(int len, int32_t* cnt, int32_t* cursor, int* maxcnt) {
   __shared__ int32_t wsum[32];
   __shared__ int32_t carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) carry = 0;
   __syncthreads();
+  int vmax = 0;
   for (int base = 0; base < len; base += blockDim.x) {
     int i = base + tid;
     int v = i < len ? cnt[i] : 0;
+    vmax = max(vmax, v);
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -101,6 +105,8 @@ __global__ void scan_kernel(int len, int32_t* cnt, int32_t* cursor) {
     if (tid == blockDim.x - 1) carry = incl;
     __syncthreads();
   }
+  vmax = warp_max_i(vmax);
+  if (lane == 0 && maxcnt != nullptr) atomicMax(maxcnt, vmax);  // longest column
 }
 
 __global__ void csc_scatter_kernel(int m, const int32_t* __restrict__ rowptr,
@@ -141,7 +147,7 @@ __global__ void csc_sort_kernel(int n, const int32_t* __restrict__ colptr,
 cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
                               const int32_t* colind, const double* vals, int32_t* colptr,
                               int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,
-                              double* tmp_val, cudaStream_t s) {
+                              double* tmp_val, cudaStream_t s, int* maxcnt) {
   cudaError_t e = cudaMemsetAsync(colptr, 0, sizeof(int32_t) * (size_t)(n + 1), s);
   if (e != cudaSuccess) return e;
   if (nnz > 0) {
@@ -149,7 +155,7 @@ cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
     if (blocks > 4096) blocks = 4096;
     colcount_kernel<<<blocks, 256, 0, s>>>(nnz, colind, colptr);
   }
-  scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor);
+  scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor, maxcnt);
   int rb = (int)(((int64_t)m * 32 + 255) / 256);
   if (rb > 4096) rb = 4096;
   if (rb < 1) rb = 1;

@@ -19,7 +19,7 @@ cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, co
 cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
                               const int32_t* colind, const double* vals, int32_t* colptr,
                               int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,
-                              double* tmp_val, cudaStream_t s);
+                              double* tmp_val, cudaStream_t s, int* maxcnt = nullptr);
 // ---- a1 Gram + c (ingest_gram.cu) ---------------------------------------
 // G (n rows of stride ldg) = A_R^T A_R and c = A_R^T b_R over rows R =
 // [row_begin, row_end) (all rows: 0, m).
@@ -43,7 +43,8 @@ cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const 
                         double* y, double tol, DevState* st, int sm_count, cudaStream_t s);
 
 // ---- a5/a6 Cholesky + solves (cholesky.cu) -------------------------------
-size_t chol_tile_count(int n);  // tiles needed for |F| <= n (bordered, lower)
+size_t chol_tile_count(int n);
+cudaError_t chol_debug_set_profile(unsigned long long* p);  // tiles needed for |F| <= n (bordered, lower)
 // Factor the bordered matrix [[G_FF, .], [c_F^T, .]] (gathered from G via
 // Fidx) into tiles Lt, then back-substitute L^T x_F = z.  f read from st.
 cudaError_t launch_cholesky_solve(int n, const double* G, int ldg, const double* c,
@@ -76,6 +77,14 @@ struct LsqrArgs {
   const double* G; int ldg; const double* c;   // for y (report)
 };
 cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s);
+// Cluster-resident variant for problems whose CSR + CSC slices fit in the
+// shared memory of one thread-block cluster (max_row / max_col: longest
+// row / column).  Returns cudaErrorNotSupported when it does not fit.
+cudaError_t lsqr_debug_set_profile(unsigned long long* p);
+cudaError_t launch_lsqr_plan(int m, int n, const int32_t* rowptr, const int32_t* colptr, int* out,
+                             cudaStream_t s);
+size_t lsqr_cluster_smem(int m, int n, const int* plan);
+cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host, cudaStream_t s);
 
 // ---- batched whole solve (batched.cu) ------------------------------------
 struct BatchArgs {

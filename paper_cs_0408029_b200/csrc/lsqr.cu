@@ -330,4 +330,499 @@ cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s) {
   return cudaLaunchCooperativeKernel((void*)lsqr_final_kernel, dim3(grid), dim3(kThreads), params, 0, s);
 }
 
+// ===========================================================================
+// Cluster-resident LSQR (configs 0, 1, 3: A fits in the shared memory of one
+// 16-CTA thread-block cluster).  Each CTA keeps its CSR row slice and CSC
+// column slice (balanced by nonzeros) in shared memory for the whole solve,
+// plus full replicas of u (m) and v (n).  Vector pieces are exchanged by
+// pushing them into every CTA's replica through distributed shared memory
+// (st.shared::cluster), norms by reading the 16 partials from each CTA's
+// shared memory in a fixed order (deterministic, identical in every CTA).
+// Two cluster barriers per iteration (the stopping test of iteration i is
+// evaluated after the first barrier of iteration i+1; no extra state is
+// touched before it, so the result is the standard LSQR iterate).
+// ===========================================================================
+namespace {
+constexpr int kCT = 512;
+constexpr int kMaxC = 16;
+
+struct ClSlices {
+  int r0, r1, e0, e1;   // rows [r0,r1), CSR entries [e0,e1)
+  int j0, j1, f0, f1;   // cols [j0,j1), CSC entries [f0,f1)
+};
+
+__device__ __forceinline__ int lower_bound_i(const int32_t* __restrict__ p, int len, int key) {
+  int lo = 0, hi = len;  // first index with p[idx] >= key
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (p[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ ClSlices cl_slices(int k, int C, int m, int n, const int32_t* rowptr,
+                                              const int32_t* colptr) {
+  ClSlices s;
+  const long long nnz = rowptr[m];
+  s.r0 = (k == 0) ? 0 : lower_bound_i(rowptr, m + 1, (int)(nnz * k / C));
+  s.r1 = (k == C - 1) ? m : lower_bound_i(rowptr, m + 1, (int)(nnz * (k + 1) / C));
+  s.r0 = min(s.r0, m);
+  s.r1 = min(max(s.r1, s.r0), m);
+  s.e0 = rowptr[s.r0];
+  s.e1 = rowptr[s.r1];
+  s.j0 = (k == 0) ? 0 : lower_bound_i(colptr, n + 1, (int)(nnz * k / C));
+  s.j1 = (k == C - 1) ? n : lower_bound_i(colptr, n + 1, (int)(nnz * (k + 1) / C));
+  s.j0 = min(s.j0, n);
+  s.j1 = min(max(s.j1, s.j0), n);
+  s.f0 = colptr[s.j0];
+  s.f1 = colptr[s.j1];
+  return s;
+}
+
+struct ClLayout {
+  int rows_max, cols_max, nzr_max, nzc_max;
+  size_t bytes;
+};
+
+__host__ __device__ inline ClLayout cl_layout(int m, int n, const int* mx) {
+  ClLayout L;
+  L.rows_max = mx[0];
+  L.nzr_max = mx[1];
+  L.cols_max = mx[2];
+  L.nzc_max = mx[3];
+  size_t d = (size_t)m + n + L.nzr_max + L.nzc_max + 4 * (size_t)L.cols_max + 3 * 32;
+  size_t i = (size_t)L.nzr_max + L.nzc_max + L.rows_max + 1 + L.cols_max + 1 + L.cols_max;
+  L.bytes = 8 * d + 4 * i + 64;
+  return L;
+}
+}  // namespace
+
+// plan: per-CTA slice maxima for cluster size C -> out[0..3] = rows, nzr, cols, nzc
+__global__ void lsqr_plan_kernel(int m, int n, const int32_t* rowptr, const int32_t* colptr, int C,
+                                 int* out) {
+  const int k = threadIdx.x;
+  int v[4] = {0, 0, 0, 0};
+  if (k < C) {
+    const ClSlices s = cl_slices(k, C, m, n, rowptr, colptr);
+    v[0] = s.r1 - s.r0;
+    v[1] = s.e1 - s.e0;
+    v[2] = s.j1 - s.j0;
+    v[3] = s.f1 - s.f0;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int x = warp_max_i(v[q]);
+    if (k == 0) out[q] = x;
+  }
+}
+
+// debug hook: per-phase %globaltimer stamps of CTA 0 (nnls_debug_lsqr_profile)
+__device__ unsigned long long* g_lsqr_prof = nullptr;
+#define LQ_STAMP(slot)                                                                     \
+  do {                                                                                     \
+    if (g_lsqr_prof != nullptr && kr == 0 && threadIdx.x == 0 && itn < 64) {               \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_lsqr_prof[itn * 16 + (slot)] = t_;                                                 \
+    }                                                                                      \
+  } while (0)
+cudaError_t lsqr_debug_set_profile(unsigned long long* p) {
+  return cudaMemcpyToSymbol(g_lsqr_prof, &p, sizeof(p));
+}
+
+// Sub-warp segmented dot products: segment q (a row of the CSR slice or a
+// column of the CSC slice) is handled by a group of g lanes (g = power of two
+// sized so that all segments of the slice are processed in ONE pass by the
+// 512 threads), each lane striding over the segment; the group reduces with
+// xor-shuffles.  emit(q, s) is called by the group's first lane.
+template <class Emit>
+__device__ __forceinline__ void seg_dots(int nseg, int g, const int* __restrict__ sp,
+                                         const double* __restrict__ val, const int* __restrict__ idx,
+                                         const double* __restrict__ vec, const int* __restrict__ skip,
+                                         Emit emit) {
+  const int tid = threadIdx.x, sl = tid & (g - 1);
+  const int per = kCT / g;
+  for (int base = 0; base < nseg; base += per) {
+    const int q = base + tid / g;
+    double s = 0.0;
+    if (q < nseg && (skip == nullptr || skip[q])) {
+      const int t1 = sp[q + 1];
+#pragma unroll 4
+      for (int t = sp[q] + sl; t < t1; t += g) s = fma(val[t], vec[idx[t]], s);
+    }
+    for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (sl == 0 && q < nseg) emit(q, s);
+  }
+}
+__device__ __forceinline__ int seg_group(int nseg) {
+  int g = 32;
+  while (g > 1 && (long long)nseg * g > kCT) g >>= 1;
+  return g;
+}
+
+__global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayout Ly) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks(), kr = (int)cl.block_rank();
+  extern __shared__ double smem[];
+  __shared__ double red[4][32];
+  __shared__ double parts[8][kMaxC];  // [slot][source CTA] partials, pushed by every CTA
+  const int m = a.m, n = a.n;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = kCT / 32;
+  const ClSlices S = cl_slices(kr, C, m, n, a.rowptr, a.colptr);
+  const int nrows = S.r1 - S.r0, ncols = S.j1 - S.j0;
+  const int gR = seg_group(nrows), gC = seg_group(ncols);
+  // ---- shared memory carve-up
+  double* Urep = smem;                 // m  (u replica, unnormalised)
+  double* Vrep = Urep + m;             // n  (v replica, unnormalised)
+  double* sv = Vrep + n;               // nzr (CSR values of own rows)
+  double* scv = sv + Ly.nzr_max;       // nzc (CSC values of own columns)
+  double* vo = scv + Ly.nzc_max;       // own columns: v (normalised)
+  double* wo = vo + Ly.cols_max;       //              w
+  double* xo = wo + Ly.cols_max;       //              x
+  double* scr = xo + Ly.cols_max;      //              scratch
+  int* sci = reinterpret_cast<int*>(scr + Ly.cols_max + 3 * 32);
+  int* sri = sci + Ly.nzr_max;         // CSC row indices
+  int* srp = sri + Ly.nzc_max;         // local rowptr (nrows + 1)
+  int* scp = srp + Ly.rows_max + 1;    // local colptr (ncols + 1)
+  int* smk = scp + Ly.cols_max + 1;    // own column mask
+  const uint8_t* __restrict__ mask = a.mask;
+
+  // ---- stage the slices (once per solve)
+  for (int t = tid; t < S.e1 - S.e0; t += kCT) {
+    sv[t] = a.vals[S.e0 + t];
+    sci[t] = a.colind[S.e0 + t];
+  }
+  for (int t = tid; t < S.f1 - S.f0; t += kCT) {
+    scv[t] = a.cvals[S.f0 + t];
+    sri[t] = a.rowind[S.f0 + t];
+  }
+  for (int r = tid; r <= nrows; r += kCT) srp[r] = a.rowptr[S.r0 + r] - S.e0;
+  for (int j = tid; j <= ncols; j += kCT) scp[j] = a.colptr[S.j0 + j] - S.f0;
+  for (int j = tid; j < ncols; j += kCT) smk[j] = mask[S.j0 + j];
+  __syncthreads();
+
+  // Cluster reductions without remote loads: every CTA reduces its values
+  // block-wide and warp 0 PUSHES the block totals into slot [slot+q][kr] of
+  // every CTA's parts[][] array; after the cluster barrier each thread sums
+  // its local copy in rank order (deterministic, identical everywhere).
+  auto publish = [&](int nv, const double* v, const int* kind, int slot) {
+    __syncthreads();  // red[][] reuse
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q < nv) {
+        double x = v[q];
+        x = kind[q] == 0 ? warp_sum(x) : (kind[q] == 1 ? warp_min(x) : warp_max(x));
+        if (lane == 0) red[q][wid] = x;
+      }
+    }
+    __syncthreads();
+    if (wid < nv) {
+      const int k = kind[wid];
+      double x = lane < NW ? red[wid][lane] : (k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY));
+      x = k == 0 ? warp_sum(x) : (k == 1 ? warp_min(x) : warp_max(x));
+      if (lane < C) *cl.map_shared_rank(&parts[slot + wid][kr], lane) = x;
+    }
+  };
+  auto ctotal = [&](int nv, const int* kind, int slot, double* out) {
+    for (int q = 0; q < nv; ++q) {
+      const int k = kind[q];
+      double x = k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY);
+      for (int r = 0; r < C; ++r) {
+        const double y = parts[slot + q][r];
+        x = k == 0 ? x + y : (k == 1 ? fmin(x, y) : fmax(x, y));
+      }
+      out[q] = x;
+    }
+  };
+  const int K_SUM[3] = {0, 0, 0};
+  // push own rows/cols of a replica to every CTA's copy
+  auto push = [&](double* rep, int base, int cnt) {
+    for (int q = 0; q < C; ++q) {
+      double* dst = cl.map_shared_rank(rep, q);
+      if (q == kr) continue;
+      for (int i = tid; i < cnt; i += kCT) dst[base + i] = rep[base + i];
+    }
+  };
+
+  const int f = a.st->f;
+  const int status = a.st->status;
+  const int mode = (status == 0 && a.st->done && f > 0) ? a.mode : 0;
+  int itn = 0, istop = 0;
+
+  if (mode != 0) {
+    const int itn_limit = a.itn_limit > 0 ? a.itn_limit : 4 * f;
+    // U' = rhs on own rows (mode 2: b - A_F x_ne)
+    if (mode == 2) {
+      for (int j = tid; j < n; j += kCT) Vrep[j] = mask[j] ? __ldcg(&a.x_ne[j]) : 0.0;
+      __syncthreads();
+    }
+    seg_dots(nrows, gR, srp, sv, sci, Vrep, nullptr, [&](int r, double s) {
+      Urep[S.r0 + r] = a.b[S.r0 + r] - (mode == 2 ? s : 0.0);
+    });
+    __syncthreads();
+    double p = 0.0;
+    for (int r = tid; r < nrows; r += kCT) p += Urep[S.r0 + r] * Urep[S.r0 + r];
+    push(Urep, S.r0, nrows);
+    publish(1, &p, K_SUM, 0);
+    cl.sync();
+    double tot[3];
+    ctotal(1, K_SUM, 0, tot);
+    double beta = sqrt(tot[0]);
+    const double bnorm = beta;
+    // V' = A_F^T u on own columns
+    const double ib0 = beta > 0.0 ? 1.0 / beta : 0.0;
+    seg_dots(ncols, gC, scp, scv, sri, Urep, smk, [&](int j, double s) { Vrep[S.j0 + j] = s * ib0; });
+    __syncthreads();
+    p = 0.0;
+    for (int j = tid; j < ncols; j += kCT) {
+      if (!smk[j]) Vrep[S.j0 + j] = 0.0;
+      p += Vrep[S.j0 + j] * Vrep[S.j0 + j];
+    }
+    __syncthreads();
+    push(Vrep, S.j0, ncols);
+    publish(1, &p, K_SUM, 4);
+    cl.sync();
+    ctotal(1, K_SUM, 4, tot);
+    double alpha = beta > 0.0 ? sqrt(tot[0]) : 0.0;
+    const double ia0 = alpha > 0.0 ? 1.0 / alpha : 0.0;
+    for (int j = tid; j < ncols; j += kCT) {
+      const double v = Vrep[S.j0 + j] * ia0;
+      vo[j] = v;
+      wo[j] = v;
+      xo[j] = 0.0;
+    }
+    double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
+    double vscale = ia0;  // Vrep * vscale = v
+    const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
+    double last_phi = 0.0, last_sn = 0.0;  // for the deferred stopping test
+    bool pending = false;
+    double pd = 0.0, px = 0.0;
+    __syncthreads();
+    if (alpha * beta != 0.0) {
+      for (;;) {
+        // ---- phase A (iteration itn+1): U' = A v - alpha u on own rows
+        LQ_STAMP(0);
+        const bool more = itn < itn_limit;
+        if (more) {
+          const double au = beta > 0.0 ? alpha / beta : 0.0;
+          const double vs = vscale;
+          seg_dots(nrows, gR, srp, sv, sci, Vrep, nullptr, [&](int r, double s) {
+            Urep[S.r0 + r] = s * vs - au * Urep[S.r0 + r];  // own slot
+          });
+        }
+        __syncthreads();
+        LQ_STAMP(1);
+        double pu = 0.0;
+        if (more) {
+          for (int r = tid; r < nrows; r += kCT) pu += Urep[S.r0 + r] * Urep[S.r0 + r];
+          push(Urep, S.r0, nrows);
+        }
+        {
+          const double v3[3] = {pu, pd, px};
+          publish(3, v3, K_SUM, 0);  // parts 0 (|U'|^2), 1 (|d|^2), 2 (|x|^2)
+        }
+        LQ_STAMP(2);
+        cl.sync();
+        LQ_STAMP(3);
+        double t3[3];
+        ctotal(3, K_SUM, 0, t3);
+        // ---- deferred stopping test of the previous iteration
+        if (pending) {
+          ddnorm += t3[1];
+          const double xnorm = sqrt(t3[2]);
+          const double acond = anorm * sqrt(ddnorm);
+          const double rnorm = phibar;
+          const double arnorm = alpha * fabs(last_sn * last_phi);
+          const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+          const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
+          const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
+          const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
+          const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
+          if (itn >= itn_limit) istop = 7;
+          if (1.0 + test3 <= 1.0) istop = 6;
+          if (1.0 + test2 <= 1.0) istop = 5;
+          if (1.0 + tt1 <= 1.0) istop = 4;
+          if (test3 <= ctol) istop = 3;
+          if (test2 <= a.atol) istop = 2;
+          if (test1 <= rtol) istop = 1;
+          if (istop != 0) break;
+        }
+        LQ_STAMP(4);
+        ++itn;
+        const double beta_new = sqrt(t3[0]);
+        // ---- phase B: V' = A_F^T u - beta v on own columns (u = U'/beta_new)
+        double alpha_new = alpha;
+        if (beta_new > 0.0) {
+          anorm = sqrt(anorm * anorm + alpha * alpha + beta_new * beta_new);
+          const double ib = 1.0 / beta_new;
+          seg_dots(ncols, gC, scp, scv, sri, Urep, smk, [&](int j, double s) {
+            Vrep[S.j0 + j] = s * ib - beta_new * vo[j];
+          });
+          __syncthreads();
+          LQ_STAMP(5);
+          double pv = 0.0;
+          for (int j = tid; j < ncols; j += kCT)
+            if (smk[j]) pv += Vrep[S.j0 + j] * Vrep[S.j0 + j];
+          push(Vrep, S.j0, ncols);
+          publish(1, &pv, K_SUM, 3);
+          LQ_STAMP(6);
+          cl.sync();
+          LQ_STAMP(7);
+          double t1v[3];
+          ctotal(1, K_SUM, 3, t1v);
+          alpha_new = sqrt(t1v[0]);
+          LQ_STAMP(8);
+        } else {
+          cl.sync();  // keep the two-barrier rhythm (partials are reused)
+        }
+        beta = beta_new;
+        // ---- rotation (replicated scalars)
+        const double rho = sqrt(rhobar * rhobar + beta * beta);
+        const double cs = rhobar / rho, sn = beta / rho;
+        const double theta = sn * alpha_new;
+        rhobar = -cs * alpha_new;
+        const double phi = cs * phibar;
+        phibar = sn * phibar;
+        const double t1 = phi / rho, t2 = -theta / rho;
+        // ---- phase C: v, x, w on own columns (partials ride on the next barrier)
+        const bool newv = beta_new > 0.0;
+        const double ia = (newv && alpha_new > 0.0) ? 1.0 / alpha_new : 1.0;
+        pd = 0.0;
+        px = 0.0;
+        for (int j = tid; j < ncols; j += kCT) {
+          if (!smk[j]) continue;
+          double v = vo[j];
+          if (newv) {
+            v = Vrep[S.j0 + j] * ia;
+            vo[j] = v;
+          }
+          const double w = wo[j];
+          const double d = w / rho;
+          pd += d * d;
+          const double x = xo[j] + t1 * w;
+          xo[j] = x;
+          wo[j] = v + t2 * w;
+          px += x * x;
+        }
+        if (newv) vscale = ia;
+        alpha = alpha_new;
+        last_phi = phi;
+        last_sn = sn;
+        pending = true;
+        LQ_STAMP(9);
+        LQ_STAMP(10);
+      }
+    }
+  }
+
+  // ---- x on own columns, zeroing (c16), write out, replicate into Vrep
+  cl.sync();  // every CTA is done reading the replicas
+  double pinf = 0.0;
+  for (int j = tid; j < ncols; j += kCT) {
+    const int g = S.j0 + j;
+    double v;
+    if (!mask[g]) v = 0.0;
+    else if (mode == 1) v = xo[j];
+    else if (mode == 2) v = __ldcg(&a.x_ne[g]) + xo[j];
+    else v = __ldcg(&a.x_ne[g]);
+    if (fabs(v) < a.tol) v = 0.0;
+    if (v < 0.0) pinf = 1.0;
+    a.x_out[g] = v;
+    Vrep[g] = v;
+  }
+  __syncthreads();
+  push(Vrep, S.j0, ncols);
+  {
+    const int K_MAX[1] = {2};
+    publish(1, &pinf, K_MAX, 6);
+    cl.sync();
+    double t[3];
+    ctotal(1, K_MAX, 6, t);
+    if (kr == 0 && tid == 0) {
+      a.st->lsqr_iterations = itn;
+      a.st->lsqr_stop = istop;
+      a.st->infeasible_after_lsqr = (mode != 0 && t[0] > 0.0) ? 1 : 0;
+      a.st->free_count = f;
+    }
+  }
+  if (a.kkt) {
+    // ---- report: R = A x - b on own rows -> Urep; y' = A^T R on own columns
+    seg_dots(nrows, gR, srp, sv, sci, Vrep, nullptr, [&](int r, double s) {
+      Urep[S.r0 + r] = s - a.b[S.r0 + r];
+    });
+    __syncthreads();
+    double po = 0.0;
+    for (int r = tid; r < nrows; r += kCT) po += Urep[S.r0 + r] * Urep[S.r0 + r];
+    push(Urep, S.r0, nrows);
+    publish(1, &po, K_SUM, 0);
+    cl.sync();
+    seg_dots(ncols, gC, scp, scv, sri, Urep, nullptr, [&](int j, double s) { scr[j] = s; });
+    __syncthreads();
+    double mx = INFINITY, my = INFINITY, mc = 0.0, dot = 0.0;
+    for (int j = tid; j < ncols; j += kCT) {
+      const double xj = Vrep[S.j0 + j], yj = scr[j];
+      mx = fmin(mx, xj);
+      my = fmin(my, yj);
+      mc = fmax(mc, fabs(xj * yj));
+      dot += xj * yj;
+    }
+    const int K3[3] = {1, 1, 2};
+    const double v3[3] = {mx, my, mc};
+    publish(3, v3, K3, 1);
+    publish(1, &dot, K_SUM, 5);
+    cl.sync();
+    double o1[3], o3[3], o5[3];
+    ctotal(1, K_SUM, 0, o1);
+    ctotal(3, K3, 1, o3);
+    ctotal(1, K_SUM, 5, o5);
+    if (kr == 0 && tid == 0) {
+      a.st->objective = 0.5 * o1[0];
+      a.st->kkt_min_x = o3[0];
+      a.st->kkt_min_y = o3[1];
+      a.st->kkt_max_comp = o3[2];
+      a.st->kkt_dot = o5[0];
+    }
+  }
+  cl.sync();  // keep every CTA's shared memory alive until remote reads finish
+}
+
+cudaError_t launch_lsqr_plan(int m, int n, const int32_t* rowptr, const int32_t* colptr, int* out,
+                             cudaStream_t s) {
+  lsqr_plan_kernel<<<1, 32, 0, s>>>(m, n, rowptr, colptr, kMaxC, out);
+  return cudaGetLastError();
+}
+
+size_t lsqr_cluster_smem(int m, int n, const int* plan) { return cl_layout(m, n, plan).bytes; }
+
+cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host, cudaStream_t s) {
+  const ClLayout Ly = cl_layout(a.m, a.n, plan_host);
+  if (Ly.bytes > 220 * 1024) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Ly.bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kMaxC);
+  cfg.blockDim = dim3(kCT);
+  cfg.dynamicSmemBytes = Ly.bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kMaxC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&nclusters, lsqr_cluster_kernel, &cfg);
+  if (e != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    return cudaErrorNotSupported;
+  }
+  return cudaLaunchKernelEx(&cfg, lsqr_cluster_kernel, a, Ly);
+}
+
 }  // namespace nnls

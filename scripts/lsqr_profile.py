@@ -1,0 +1,40 @@
+"""Per-phase timeline of the cluster LSQR (debug hook nnls_debug_lsqr_profile):
+average ns per phase over iterations (CTA 0's view)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import nnls_gen as g  # noqa: E402
+import paper_cs_0408029_b200 as P  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+prob = g.make_problem(cfg, 0)
+S = P.setup(prob)
+prof = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
+P.lib.nnls_debug_lsqr_profile.argtypes = [C.c_void_p]
+for rep in range(2):
+    prof.zero_()
+    P.lib.nnls_debug_lsqr_profile(C.c_void_p(prof.data_ptr()))
+    x, info = S.solve()
+    P.lib.nnls_debug_lsqr_profile(C.c_void_p(0))
+p = prof.cpu().numpy().reshape(64, 16).astype(np.float64)
+names = ["A.compute", "A.push+bsum", "A.clsync", "test", "B.compute(+ctotal)", "B.push+bsum", "B.clsync",
+         "ctotal(alpha)", "C.compute", "C.bsum x2"]
+rows = [r for r in range(1, 63) if p[r, 0] > 0 and p[r, 10] > 0 and p[r + 1, 0] > 0]
+d = {n: [] for n in names}
+d["C->nextA"] = []
+for r in rows:
+    for k in range(10):
+        d[names[k]].append(p[r, k + 1] - p[r, k])
+    d["C->nextA"].append(p[r + 1, 0] - p[r, 10])
+print("iterations profiled:", len(rows), "lsqr_iterations:", info["lsqr_iterations"])
+tot = 0
+for k, v in d.items():
+    if v:
+        print(f"{k:22s} {np.mean(v):9.0f} ns")
+        tot += np.mean(v)
+print(f"{'per iteration':22s} {tot:9.0f} ns")

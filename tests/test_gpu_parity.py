@@ -366,3 +366,11 @@ def test_batched_single_exchange_cases(P):
         B = g.Batch(p.m, p.n, 1, np.array([0, p.nnz], dtype=np.int64), p.rowptr, p.colind, p.vals, p.b,
                     np.zeros(p.n), 0, 0)
         _batched_parity(P, B, lsqr_mode=0)
+
+
+@pytest.mark.parametrize("cfg,seed", [(0, 3), (1, 1), (3, 1)])
+def test_lsqr_full_grid_path(P, cfg, seed, monkeypatch):
+    """The cluster-resident LSQR is used when A fits in one cluster's shared
+    memory; force the full-grid cooperative kernel and check it too."""
+    monkeypatch.setenv("NNLS_NO_CLUSTER", "1")
+    assert_parity(P, g.make_problem(cfg, seed))
