@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256, 1) tile_bench(double* out, long long* cyc
   }
   long long t1 = clock64();
   for (int rep = 0; rep < reps; ++rep) {
-    if (w == 0) warp_trtri32(S, rinv, 32, lane, L + 32);
+    if (w == 0) warp_trtri32(S, rinv, 32, lane, L + 32, nullptr);
     __syncthreads();
   }
   long long t2 = clock64();
@@ -56,11 +56,17 @@ __global__ void __launch_bounds__(256, 1) tile_bench(double* out, long long* cyc
     __syncthreads();
   }
   long long t3 = clock64();
+  __shared__ int sbad;
   for (int rep = 0; rep < reps; ++rep) {
-    load_tile(L, out + 8192);
+    potrf64_panel8(L, 64, 64, rinv, &sbad);
     __syncthreads();
   }
   long long t4 = clock64();
+  for (int rep = 0; rep < reps * 64; ++rep) {
+    __syncthreads();
+  }
+  long long t5 = clock64();
+  if (tid == 0) cyc[4] = (t5 - t4) / (reps * 64);
   if (tid == 0) {
     cyc[0] = (t1 - t0) / reps;
     cyc[1] = (t2 - t1) / reps;
@@ -81,8 +87,9 @@ int main() {
   tile_bench<<<1, 256, smem>>>(out, cyc, 2);
   tile_bench<<<1, 256, smem>>>(out, cyc, 20);
   cudaDeviceSynchronize();
-  long long h[4];
+  long long h[5];
   cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("{\"syncthreads256_cycles\": %lld}\n", h[4]);
   printf("{\"potrf32_cycles\": %lld, \"trsm_rows64_cycles\": %lld, \"dmma_64x64x64_cycles\": %lld, "
          "\"load_tile_cycles\": %lld, \"err\": \"%s\"}\n",
          h[0], h[1], h[2], h[3], cudaGetErrorString(cudaGetLastError()));

@@ -198,7 +198,7 @@ __device__ __forceinline__ int warp_potrf32(double (&a)[32], int ncols, int lane
 // rows/columns >= ncols are zero.  Writes X (lower) to out (stride LDS).
 __device__ __forceinline__ void warp_trtri32(const double* __restrict__ Lb,
                                              const double* __restrict__ rinvb, int ncols, int lane,
-                                             double* __restrict__ out) {
+                                             double* __restrict__ out, double* __restrict__ outT) {
   double x[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
@@ -209,6 +209,161 @@ __device__ __forceinline__ void warp_trtri32(const double* __restrict__ Lb,
   }
 #pragma unroll
   for (int i = 0; i < 32; ++i) out[i * LDS + lane] = x[i];
+  if (outT != nullptr) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) outT[lane * LDS + i] = x[i];
+  }
+}
+
+// Cholesky of the diagonal 64 x 64 tile S (smem, rows < rv, pivot columns
+// < cv; a row >= cv is the bordered row c_F^T and is only eliminated) by all
+// 256 threads.  Thread t owns the lower-triangle entries e = t + 256 s of the
+// tile in registers.  Column c: the owners of column c publish it into a
+// ping-pong buffer, ONE barrier, then every thread updates its own entries
+// with l_rc l_kc = b_r b_k / d (and finalises column c).  Writes L back into S
+// (zero above the diagonal / beyond cv), 1/l_cc into rinv.  Returns the first
+// bad pivot column or -1.
+__device__ __forceinline__ int block_potrf64(double* __restrict__ S, int rv, int cv,
+                                             double* __restrict__ rinv, double (*colbuf)[T]) {
+  constexpr int NS = (T * (T + 1) / 2 + kThreads - 1) / kThreads;  // 9 slots
+  const int tid = threadIdx.x;
+  double a[NS];
+  int rs[NS], ks[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int e = tid + kThreads * s;
+    int r = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+    while (r * (r + 1) / 2 > e) --r;
+    while ((r + 1) * (r + 2) / 2 <= e) ++r;
+    const int k = e - r * (r + 1) / 2;
+    const bool valid = e < T * (T + 1) / 2 && r < rv && k < cv;
+    rs[s] = valid ? r : 0;
+    ks[s] = valid ? k : T;  // k = T: never updated (and never published)
+    a[s] = valid ? S[r * LDS + k] : 0.0;
+  }
+  int bad = -1;
+  // branch-free column loop: every slot computes both candidates and selects
+  // (divergent if/else per slot cost ~1.7K cycles per column)
+#pragma unroll 1
+  for (int c = 0; c < cv; ++c) {
+    double* buf = colbuf[c & 1];
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (ks[s] == c) buf[rs[s]] = a[s];
+    __syncthreads();
+    const double d = buf[c];
+    if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) bad = (bad < 0) ? c : bad;
+    const double inv = rsqrt(d);
+    if (tid == 0) rinv[c] = inv;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int k = ks[s];
+      const double br = buf[rs[s]], bk = buf[min(k, T - 1)];
+      const double upd = fma(-(br * inv), bk * inv, a[s]);
+      const double fin = (rs[s] == c) ? d * inv : a[s] * inv;
+      a[s] = (k == c) ? fin : ((k > c && k < T) ? upd : a[s]);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < T * T; e += kThreads) S[(e / T) * LDS + (e % T)] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (ks[s] < T) S[rs[s] * LDS + ks[s]] = a[s];
+  return bad;
+}
+
+// Cholesky of the diagonal 64 x 64 tile S (smem; rows < rv, pivot columns
+// < cv; a row >= cv is the bordered row c_F^T and is only eliminated), by
+// panels of 8 columns: warp 0 factors the 8-wide panel in registers (lane l
+// holds rows 8p+l and 8p+l+32; 8 shuffle-broadcast columns), then all 8
+// warps apply the rank-8 trailing update with DMMA.  Column-sequential work
+// per lane is 8 wide instead of 32/64 (the column chain is latency-bound).
+// Writes L into S (lower; the strict upper part is cleared by the caller),
+// 1/l_cc into rinv; returns the first bad pivot column or -1.
+__device__ __forceinline__ int potrf64_panel8(double* __restrict__ S, int rv, int cv,
+                                              double* __restrict__ rinv, int* s_bad) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) *s_bad = -1;
+  const int np = (cv + 7) >> 3;
+#pragma unroll 1
+  for (int p = 0; p < np; ++p) {
+    const int c0 = 8 * p;
+    if (w == 0) {
+      const int R0 = c0 + lane, R1 = c0 + 32 + lane;
+      const bool v0 = R0 < rv, v1 = R1 < rv;
+      double a0[8], a1[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        a0[c] = v0 ? S[R0 * LDS + c0 + c] : 0.0;
+        a1[c] = v1 ? S[R1 * LDS + c0 + c] : 0.0;
+      }
+      int bad = -1;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c0 + c < cv) {
+          const double d = __shfl_sync(kFull, a0[c], c);
+          if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) bad = (bad < 0) ? c0 + c : bad;
+          const double inv = rsqrt(d);
+          if (lane == 0) rinv[c0 + c] = inv;
+          a0[c] = (lane == c) ? d * inv : ((lane > c) ? a0[c] * inv : 0.0);
+          a1[c] *= inv;
+#pragma unroll
+          for (int c2 = c + 1; c2 < 8; ++c2) {
+            const double x = __shfl_sync(kFull, a0[c], c2);  // l_{c0+c2, c0+c}
+            if (c0 + c2 < cv) {
+              if (lane >= c2) a0[c2] = fma(-a0[c], x, a0[c2]);
+              a1[c2] = fma(-a1[c], x, a1[c2]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (v0) S[R0 * LDS + c0 + c] = (c0 + c < cv) ? a0[c] : 0.0;
+        if (v1) S[R1 * LDS + c0 + c] = (c0 + c < cv) ? a1[c] : 0.0;
+      }
+      if (lane == 0 && bad >= 0 && *s_bad < 0) *s_bad = bad;
+    }
+    __syncthreads();
+    // rank-8 trailing update of the lower 8x8 blocks (I >= J > p) with DMMA
+    const int nb = 8 - (p + 1);  // trailing block rows/cols
+    const int nblk = nb * (nb + 1) / 2;
+    for (int b = w; b < nblk; b += 8) {
+      int I = (int)((sqrtf(8.0f * b + 1.0f) - 1.0f) * 0.5f);
+      while (I * (I + 1) / 2 > b) --I;
+      while ((I + 1) * (I + 2) / 2 <= b) ++I;
+      const int J = b - I * (I + 1) / 2;
+      const int r0 = 8 * (p + 1 + I), k0 = 8 * (p + 1 + J);
+      double* Cp = S + (r0 + (lane >> 2)) * LDS + k0 + 2 * (lane & 3);
+      double cacc0 = Cp[0], cacc1 = Cp[1];
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 4) {
+        const double av = -S[(r0 + (lane >> 2)) * LDS + c0 + kk + (lane & 3)];
+        const double bv = S[(k0 + (lane >> 2)) * LDS + c0 + kk + (lane & 3)];
+        dmma8x8x4(cacc0, cacc1, av, bv);
+      }
+      Cp[0] = cacc0;
+      Cp[1] = cacc1;
+    }
+    __syncthreads();
+  }
+  return *s_bad;
+}
+
+// acc[q] (rows 8w.. of a 32 x 32 product, cols 8q..) += A B^T, A and B
+// 32 x 32 row-major (B by rows n: C[m][n] += sum_k A[m][k] B[n][k]).
+__device__ __forceinline__ void dmma32(double (&acc)[4][2], const double* __restrict__ A,
+                                       const double* __restrict__ B, int lane, int w) {
+#pragma unroll
+  for (int kk = 0; kk < 32; kk += 4) {
+    const double av = A[(8 * w + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double bv = B[(8 * q + (lane >> 2)) * LDS + kk + (lane & 3)];
+      dmma8x8x4(acc[q][0], acc[q][1], av, bv);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
@@ -221,7 +376,6 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
 #define BUF(q) (smem + (q) * (T * LDS))
   double* S = BUF(0);
   __shared__ double rinv[T];
-  __shared__ double colbuf[64];
   __shared__ int s_task, s_ready, s_bad;
 
   const int f = st->f;
@@ -314,105 +468,52 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     PROF_STAMP(task, 2);
 
     if (i == j) {
-      // 3a) diagonal tile: L_jj = chol(A_jj) as 2 x 2 blocks of 32, and
-      //     Linv_jj = L_jj^-1 (published for the TRSM tasks and the solve).
-      double* X = BUF(1);   // inverse
-      double* Tm = BUF(2);  // scratch: L21 Linv11
+      // 3a) diagonal tile: L_jj = chol(A_jj) by all 256 threads (block_potrf64,
+      //     one barrier per column), then Linv_jj = L_jj^-1 (published for the
+      //     TRSM tasks and the solve): TRTRI of the two 32-blocks by two warps,
+      //     the off-diagonal block -X22 L21 X11 by two 32^3 DMMA products.
+      double* X = BUF(1);    // inverse
+      double* X11t = BUF(2); // X11^T
+      double* Tmt = BUF(3);  // (L21 X11)^T
       const int n1 = min(32, cv), n2 = cv - 32;
-      if (tid == 0) s_bad = -1;
-      if (w == 0) {
-        double a[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) a[k] = S[lane * LDS + k];
-        const int b1 = warp_potrf32(a, n1, lane, rinv, S, colbuf);
-        if (b1 >= 0 && lane == 0) s_bad = b1;
-      }
+      const int bad = potrf64_panel8(S, rv, cv, rinv, &s_bad);
+      for (int e = tid; e < T * T; e += kThreads)  // strict upper part
+        if ((e % T) > (e / T)) S[(e / T) * LDS + (e % T)] = 0.0;
       __syncthreads();
-      if (w == 1) {
-        warp_trtri32(S, rinv, n1, lane, X);  // Linv11, concurrently with block 2
-      } else if (w == 0 && rv > 32) {
-        // TRSM of rows 32..63 against L11 (lane = row, shifted registers)
-        double bq[32];
-        double* R2 = S + 32 * LDS;
-#pragma unroll
-        for (int k = 0; k < 32; ++k) bq[k] = R2[lane * LDS + k];
-#pragma unroll 1
-        for (int c0 = 0; c0 < n1; c0 += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c = c0 + u;
-            if (c < n1) {
-              const double x = bq[u] * rinv[c];
-              bq[u] = x;
-              R2[lane * LDS + c] = x;
-              const double* Lc = S + c * LDS + c;  // Lc[tt*LDS] = L11[c+tt][c]
-#pragma unroll
-              for (int tt = 1; u + tt < 32; ++tt) {
-                const double v = Lc[tt * LDS];
-                if (c + tt < n1) bq[u + tt] = fma(-x, v, bq[u + tt]);
-              }
-            }
-          }
-#pragma unroll
-          for (int tt = 0; tt < 28; ++tt) bq[tt] = bq[tt + 4];
-          bq[28] = bq[29] = bq[30] = bq[31] = 0.0;
-        }
-        __syncwarp();
-        // SYRK: A22[lane][k] -= L21[lane][:] . L21[k][:]
-        double a[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) a[k] = R2[lane * LDS + 32 + k];
-        if (n2 > 0) {
-#pragma unroll 1
-          for (int c = 0; c < n1; ++c) {
-            const double lrc = R2[lane * LDS + c];
-            const double* Lk = R2 + c;  // Lk[k*LDS] = L21[k][c]
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const double v = Lk[k * LDS];
-              if (k < n2 && k <= lane) a[k] = fma(-lrc, v, a[k]);
-            }
-          }
-          const int b2 = warp_potrf32(a, n2, lane, rinv + 32, S + 32 * LDS + 32, colbuf);
-          if (b2 >= 0 && lane == 0 && s_bad < 0) s_bad = 32 + b2;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) R2[lane * LDS + 32 + k] = 0.0;
-        }
-      }
-      __syncthreads();
-      // Linv22 (warp 0) || Tm = L21 Linv11 over the pivot rows (other warps)
       if (w == 0) {
+        warp_trtri32(S, rinv, n1, lane, X, X11t);
+      } else if (w == 1) {
         if (n2 > 0) {
-          warp_trtri32(S + 32 * LDS + 32, rinv + 32, n2, lane, X + 32 * LDS + 32);
+          warp_trtri32(S + 32 * LDS + 32, rinv + 32, n2, lane, X + 32 * LDS + 32, nullptr);
         } else {
           for (int r = 0; r < 32; ++r) X[(32 + r) * LDS + 32 + lane] = 0.0;
         }
+      }
+      __syncthreads();
+      if (w < 4) {  // Tm = L21 X11 (rows 32.., stored transposed)
+        double acc[4][2] = {};
+        dmma32(acc, S + 32 * LDS, X11t, lane, w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            Tmt[(8 * q + 2 * (lane & 3) + v) * LDS + 8 * w + (lane >> 2)] = acc[q][v];
+      }
+      __syncthreads();
+      if (w < 4) {  // Linv21 = -X22 Tm
+        double acc[4][2] = {};
+        dmma32(acc, X + 32 * LDS + 32, Tmt, lane, w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            X[(32 + 8 * w + (lane >> 2)) * LDS + 8 * q + 2 * (lane & 3) + v] = -acc[q][v];
       } else {
-        for (int e = tid - 32; e < 32 * 32; e += kThreads - 32) {
-          const int r = e >> 5, c = e & 31;  // Tm[r][c] = sum_k L21[r][k] Linv11[k][c]
-          double s = 0.0;
-          if (r < n2)
-            for (int k = c; k < n1; ++k) s = fma(S[(32 + r) * LDS + k], X[k * LDS + c], s);
-          Tm[r * LDS + c] = s;
-        }
+        for (int e = tid - 128; e < 32 * 32; e += 128) X[(e >> 5) * LDS + 32 + (e & 31)] = 0.0;
       }
       __syncthreads();
-      // Linv21 = -Linv22 Tm; clear the strict upper parts of X and S
-      for (int e = tid; e < 32 * 32; e += kThreads) {
-        const int r = e >> 5, c = e & 31;
-        double s = 0.0;
-        for (int k = 0; k <= r; ++k) s = fma(X[(32 + r) * LDS + 32 + k], Tm[k * LDS + c], s);
-        X[(32 + r) * LDS + c] = -s;
-        X[r * LDS + 32 + c] = 0.0;  // upper-right block
-      }
-      for (int e = tid; e < T * T; e += kThreads) {
-        const int r = e / T, q = e % T;
-        if (q > r) S[r * LDS + q] = 0.0;
-      }
-      __syncthreads();
-      if (tid == 0 && s_bad >= 0) {
-        if (atomicCAS(&st->status, 0, 7) == 0) st->not_pd_col = j * T + s_bad;
+      if (tid == 0 && bad >= 0) {
+        if (atomicCAS(&st->status, 0, 7) == 0) st->not_pd_col = j * T + bad;
       }
       store_tile(Linv + (size_t)j * T * T, X);
     } else {
