@@ -32,8 +32,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
+    # static CUDA runtime: the headers we compile against (12.9) and the
+    # runtime must match; a dynamic libcudart.so.12 would resolve to whatever
+    # the process loaded first (e.g. torch's 12.8 wheel)
     subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
-                           *objs, "-lcudart"])
+                           *objs, "-cudart", "static", "-Xcompiler", "-fvisibility=hidden"])
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

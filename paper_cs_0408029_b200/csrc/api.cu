@@ -5,6 +5,7 @@
 // infeasible"); every arithmetic step of the method runs in the sm_100a
 // kernels of this directory.  There is no CPU fallback.
 #include <cuda_runtime.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -94,6 +95,11 @@ struct nnls_handle {
   int trace_cap = 0;
   HostState* h = nullptr;                 // pinned readback
   bool no_cluster = false;  // force the full-grid LSQR (tests / env NNLS_NO_CLUSTER)
+  bool no_graph = false;    // host-driven pivot loop (env NNLS_NO_GRAPH, or capture failed)
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<double> gkey;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev[2] = {nullptr, nullptr};
   // batched
   bool batched = false;
   int batch = 0;
@@ -242,20 +248,22 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   TIMED(NNLS_PH_VALIDATE, 1,
         launch_validate(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                         P<double>(h->b), P<int>(h->err), s));
-  // validation must pass before structure-dependent kernels touch the data
-  int herr = 0;
-  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  herr = h->h->err[0];
-  if (herr) return map_err_bits(herr);
-  TIMED(NNLS_PH_CSC, nnz > 0 ? 4 : 3,
-        launch_csr_to_csc(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
-                          P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                          P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s,
-                          P<int>(h->err) + 2));
-  // cluster-LSQR slice plan; read back with the first status sync of nnls_solve
+  // column counts (guarded against invalid indices) and the cluster-LSQR
+  // slice plan are computed before the validation readback, so ONE host sync
+  // returns the error bits, the longest row/column and the plan together
+  TIMED(NNLS_PH_CSC, nnz > 0 ? 2 : 1,
+        launch_csc_count(m, n, nnz, P<int32_t>(h->colind), P<int32_t>(h->colptr),
+                         P<int32_t>(h->cursor), s, P<int>(h->err) + 2));
   CK(launch_lsqr_plan(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colptr), P<int>(h->err) + 4, s));
-  CK(cudaMemcpyAsync(h->h->plan, P<int>(h->err) + 4, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+  tm_end(h, NNLS_PH_CSC, -1, 1);
+  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int herr = h->h->err[0];
+  if (herr) return map_err_bits(herr);
+  TIMED(NNLS_PH_CSC, 2,
+        launch_csc_fill(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                        P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
+                        P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s));
   double* G = P<double>(h->Gc);
   double* c = G + (size_t)n * h->ldg;
   TIMED(NNLS_PH_GRAM, 1,
@@ -289,6 +297,7 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
   }
   memset(h->h, 0, sizeof(HostState));
   h->no_cluster = getenv("NNLS_NO_CLUSTER") != nullptr;
+  h->no_graph = getenv("NNLS_NO_GRAPH") != nullptr;
   *out = h;
   return NNLS_OK;
 }
@@ -423,41 +432,13 @@ nnls_status nnls_set_params(nnls_handle* h, const nnls_params* p) {
   return NNLS_OK;
 }
 
-nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
-  if (!h || h->batched) return NNLS_ERR_INVALID_ARG;
-  if (!h->loaded || !h->gram_ready) return NNLS_ERR_STATE;
-  cudaStream_t s = h->stream;
+}  // extern "C"
+
+namespace {
+LsqrArgs lsqr_args(nnls_handle* h) {
   const int n = h->n;
   const nnls_params& p = h->prm;
-  const int max_iter = p.max_iter > 0 ? p.max_iter : 10 * n;
   double* G = P<double>(h->Gc);
-  double* c = G + (size_t)n * h->ldg;
-  DevState* st = P<DevState>(h->st);
-  TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
-  TIMED(NNLS_PH_INIT, 1,
-        launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
-                    p.p_max, max_iter, s));
-  for (;;) {
-    TIMED(NNLS_PH_DECIDE, 1,
-          launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
-                        P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s));
-    nnls_status rs = read_state(h);
-    if (rs != NNLS_OK) return rs;
-    const DevState& hs = h->h->st;
-    if (hs.done || hs.status != 0) break;
-    if (hs.f > 0) {
-      TIMED(NNLS_PH_CHOL_FACTOR, 1,
-            launch_chol_factor(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt),
-                               P<int>(h->flags), st, h->sms, s));
-      TIMED(NNLS_PH_CHOL_SOLVE, 1,
-            launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st,
-                                  h->sms, s));
-    }
-    TIMED(NNLS_PH_DUAL, 1,
-          launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
-                      P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
-                      h->sms, s));
-  }
   LsqrArgs a{};
   a.m = h->m;
   a.n = n;
@@ -477,7 +458,7 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   a.X = P<double>(h->X);
   a.R = P<double>(h->R);
   a.partials = P<double>(h->partials);
-  a.st = st;
+  a.st = P<DevState>(h->st);
   a.mode = p.lsqr_mode;
   a.itn_limit = p.lsqr_itn_limit;
   a.atol = p.lsqr_atol;
@@ -487,19 +468,213 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   a.kkt = p.kkt;
   a.G = G;
   a.ldg = h->ldg;
-  a.c = c;
-  // cluster-resident LSQR when A's slices fit in one 16-CTA cluster's shared
-  // memory (configs 0, 1, 3); the full-grid cooperative kernel otherwise
-  {
-    const int ib = tm_begin(h);
-    cudaError_t e = h->no_cluster ? cudaErrorNotSupported
-                                  : launch_lsqr_cluster_planned(a, h->h->plan, s);
-    if (e == cudaErrorNotSupported) {
-      cudaGetLastError();
-      e = launch_lsqr_final(a, h->sms, s);
+  a.c = G + (size_t)n * h->ldg;
+  return a;
+}
+
+// cluster-resident LSQR when A's slices fit in one 16-CTA cluster's shared
+// memory (configs 0, 1, 3); the full-grid cooperative kernel otherwise
+cudaError_t launch_lsqr(nnls_handle* h, cudaStream_t s) {
+  const LsqrArgs a = lsqr_args(h);
+  cudaError_t e = h->no_cluster ? cudaErrorNotSupported : launch_lsqr_cluster_planned(a, h->h->plan, s);
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    e = launch_lsqr_final(a, h->sms, s);
+  }
+  return e;
+}
+
+// one pivot iteration: decide -> (gather + Cholesky + forward) -> back solve -> dual
+cudaError_t launch_iteration(nnls_handle* h, cudaStream_t s, const cudaGraphConditionalHandle* loop) {
+  const int n = h->n;
+  double* G = P<double>(h->Gc);
+  double* c = G + (size_t)n * h->ldg;
+  DevState* st = P<DevState>(h->st);
+  TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
+  cudaError_t e = launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
+                                P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s, loop);
+  if (e == cudaSuccess)
+    e = launch_chol_factor(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt), P<int>(h->flags), st,
+                           h->sms, s);
+  if (e == cudaSuccess)
+    e = launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st, h->sms, s);
+  if (e == cudaSuccess)
+    e = launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
+                    P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), h->prm.zero_tol, st, h->sms, s);
+  return e;
+}
+
+// Everything a captured solve graph depends on.
+std::vector<double> graph_key(nnls_handle* h) {
+  const nnls_params& p = h->prm;
+  std::vector<double> k = {(double)h->m, (double)h->n, (double)h->nnz, (double)h->ldg,
+                           (double)h->h->plan[0], (double)h->h->plan[1], (double)h->h->plan[2],
+                           (double)h->h->plan[3], p.zero_tol, (double)p.p_max, (double)p.max_iter,
+                           (double)p.lsqr_mode, (double)p.lsqr_itn_limit, p.lsqr_atol, p.lsqr_btol,
+                           p.lsqr_conlim, (double)p.kkt, (double)h->trace_cap, (double)h->no_cluster};
+  const Buf* bufs[] = {&h->rowptr, &h->colind, &h->vals, &h->b, &h->colptr, &h->rowind, &h->cvals,
+                       &h->Gc, &h->mask, &h->x, &h->y, &h->xF, &h->Fidx, &h->Gidx, &h->Lt, &h->flags,
+                       &h->U, &h->V, &h->W, &h->X, &h->R, &h->partials, &h->xfin, &h->st, &h->trace};
+  for (const Buf* b : bufs) k.push_back((double)(uintptr_t)b->p);
+  return k;
+}
+
+void drop_graph(nnls_handle* h) {
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  h->gexec = nullptr;
+  h->gkey.clear();
+}
+
+// Device-resident solve: init -> WHILE(decide clears the condition) { one
+// pivot iteration } -> LSQR, captured once per problem shape / buffer set and
+// replayed with one graph launch (no host round trip per pivot iteration).
+#define GDBG(msg)                                                                         \
+  do {                                                                                    \
+    if (getenv("NNLS_DEBUG")) fprintf(stderr, "[nnls graph] %s: %s\n", msg, cudaGetErrorString(e)); \
+  } while (0)
+cudaError_t build_graph(nnls_handle* h, cudaStream_t s) {
+  drop_graph(h);
+  const int n = h->n;
+  const nnls_params& p = h->prm;
+  const int max_iter = p.max_iter > 0 ? p.max_iter : 10 * n;
+  double* G = P<double>(h->Gc);
+  double* c = G + (size_t)n * h->ldg;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaGraphCreate(&g, 0);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle cond;
+  cudaGraphNode_t init_node = nullptr, cond_node = nullptr;
+  e = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
+  GDBG("handle");
+  if (getenv("NNLS_DEBUG")) {
+    fprintf(stderr, "[nnls graph] stream %p graph %p query %d\n", (void*)s, (void*)g, (int)cudaStreamQuery(s));
+    fflush(stderr);
+  }
+  if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+  GDBG("begin1");
+  if (e == cudaSuccess) {
+    cudaError_t el = launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol,
+                                 P<DevState>(h->st), p.p_max, max_iter, s);
+    cudaGraph_t gg = g;
+    e = cudaStreamEndCapture(s, &gg);
+    if (e == cudaSuccess) e = el;
+  }
+  GDBG("init");
+  if (e == cudaSuccess) {
+    size_t nn = 0;
+    e = cudaGraphGetRootNodes(g, nullptr, &nn);
+    if (e == cudaSuccess && nn != 1) e = cudaErrorNotSupported;
+    if (e == cudaSuccess) e = cudaGraphGetRootNodes(g, &init_node, &nn);
+  }
+  GDBG("roots");
+  cudaGraph_t body = nullptr;
+  if (e == cudaSuccess) {
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&cond_node, g, &init_node, 1, &cp);
+    if (e == cudaSuccess) body = cp.conditional.phGraph_out[0];
+  }
+  GDBG("cond");
+  if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+  if (e == cudaSuccess) {
+    cudaError_t el = launch_iteration(h, s, &cond);
+    cudaGraph_t bb = body;
+    e = cudaStreamEndCapture(s, &bb);
+    if (e == cudaSuccess) e = el;
+  }
+  GDBG("body");
+  if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(s, g, &cond_node, nullptr, 1, cudaStreamCaptureModeRelaxed);
+  if (e == cudaSuccess) {
+    cudaError_t el = launch_lsqr(h, s);
+    cudaGraph_t gg = g;
+    e = cudaStreamEndCapture(s, &gg);
+    if (e == cudaSuccess) e = el;
+  }
+  GDBG("lsqr");
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&h->gexec, g, 0);
+  GDBG("instantiate");
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    h->gexec = nullptr;
+    return e;
+  }
+  h->gkey = graph_key(h);
+  return cudaSuccess;
+}
+}  // namespace
+
+extern "C" {
+
+nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
+  if (!h || h->batched) return NNLS_ERR_INVALID_ARG;
+  if (!h->loaded || !h->gram_ready) return NNLS_ERR_STATE;
+  cudaStream_t s = h->stream;
+  const int n = h->n;
+  const nnls_params& p = h->prm;
+  const int max_iter = p.max_iter > 0 ? p.max_iter : 10 * n;
+  double* G = P<double>(h->Gc);
+  double* c = G + (size_t)n * h->ldg;
+  DevState* st = P<DevState>(h->st);
+  bool done_graph = false;
+  if (!h->tm.on && !h->no_graph) {
+    // device-resident loop (one graph launch); per-phase timing uses the host loop
+    // graphs are captured and launched on a private stream fenced to the
+    // caller's stream with events (capture is not allowed on the legacy stream)
+    if (!h->gstream) {
+      if (cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->gev[0], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->gev[1], cudaEventDisableTiming) != cudaSuccess)
+        h->no_graph = true;
     }
-    CK(e);
-    tm_end(h, NNLS_PH_LSQR, ib, 1);
+    if (!h->no_graph && (!h->gexec || h->gkey != graph_key(h))) {
+      CK(cudaStreamSynchronize(s));
+      if (build_graph(h, h->gstream) != cudaSuccess) h->no_graph = true;  // fall back for this handle
+    }
+    if (!h->no_graph && h->gexec) {
+      CK(cudaEventRecord(h->gev[0], s));
+      CK(cudaStreamWaitEvent(h->gstream, h->gev[0], 0));
+      CK(cudaGraphLaunch(h->gexec, h->gstream));
+      CK(cudaEventRecord(h->gev[1], h->gstream));
+      CK(cudaStreamWaitEvent(s, h->gev[1], 0));
+      h->tm.launches[NNLS_PH_INIT] += 1;
+      done_graph = true;
+    }
+  }
+  if (!done_graph) {
+    TIMED(NNLS_PH_INIT, 1,
+          launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
+                      p.p_max, max_iter, s));
+    TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
+    for (;;) {
+      TIMED(NNLS_PH_DECIDE, 1,
+            launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
+                          P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s));
+      nnls_status rs = read_state(h);
+      if (rs != NNLS_OK) return rs;
+      const DevState& hs = h->h->st;
+      if (hs.done || hs.status != 0) break;
+      if (hs.f > 0) {
+        TIMED(NNLS_PH_CHOL_FACTOR, 1,
+              launch_chol_factor(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt),
+                                 P<int>(h->flags), st, h->sms, s));
+        TIMED(NNLS_PH_CHOL_SOLVE, 1,
+              launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st,
+                                    h->sms, s));
+      }
+      TIMED(NNLS_PH_DUAL, 1,
+            launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
+                        P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
+                        h->sms, s));
+    }
+    {
+      const int ib = tm_begin(h);
+      CK(launch_lsqr(h, s));
+      tm_end(h, NNLS_PH_LSQR, ib, 1);
+    }
   }
   if (x_out) {
     const int ib = tm_begin(h);
@@ -509,6 +684,14 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   nnls_status rs = read_state(h);
   if (rs != NNLS_OK) return rs;
   const DevState& hs = h->h->st;
+  if (done_graph) {  // kernels the graph ran (the WHILE body runs iterations + 1 times)
+    const int body = hs.iter + 1;
+    h->tm.launches[NNLS_PH_DECIDE] += body;
+    h->tm.launches[NNLS_PH_CHOL_FACTOR] += body;
+    h->tm.launches[NNLS_PH_CHOL_SOLVE] += body;
+    h->tm.launches[NNLS_PH_DUAL] += body;
+    h->tm.launches[NNLS_PH_LSQR] += 1;
+  }
   nnls_status status = NNLS_OK;
   if (hs.status == 7) status = NNLS_ERR_NOT_PD;
   else if (hs.status == 8) status = NNLS_ITERATION_LIMIT;
@@ -622,6 +805,10 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->b_info_d, &h->b_x, &h->b_mask};
   for (Buf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : h->tm.pool) cudaEventDestroy(e);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
+  for (cudaEvent_t e : h->gev)
+    if (e) cudaEventDestroy(e);
   if (h->h) cudaFreeHost(h->h);
   delete h;
   return NNLS_OK;

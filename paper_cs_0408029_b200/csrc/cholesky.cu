@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
 
   const int f = st->f;
   const int epoch = st->epoch;
-  if (f <= 0) return;
+  if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
   const int ntc = (f + T - 1) / T;      // tile columns to factor
   const int ntr = (f + 1 + T - 1) / T;  // tile rows (incl. the rhs row f)
   const int total = ntc * ntr - ntc * (ntc - 1) / 2;
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
   __shared__ int s_task;
   const int f = st->f;
   const int epoch = st->epoch;
-  if (f <= 0) return;
+  if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
   const int ntc = (f + T - 1) / T;
   const int Rf = f / T, rf = f % T;  // tile row / local row of the rhs row
   const int tid = threadIdx.x;

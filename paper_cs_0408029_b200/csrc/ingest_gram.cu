@@ -60,10 +60,12 @@ cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, co
 }
 
 // ---------------------------------------------------------------- CSR->CSC
-__global__ void colcount_kernel(int64_t nnz, const int32_t* __restrict__ colind, int32_t* cnt) {
+__global__ void colcount_kernel(int64_t nnz, int n, const int32_t* __restrict__ colind, int32_t* cnt) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&cnt[colind[e] + 1], 1);
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = colind[e];
+    if (c >= 0 && c < n) atomicAdd(&cnt[c + 1], 1);  // runs before validation completes
+  }
 }
 
 // In-place inclusive scan of cnt[0..len) (cnt[0] = 0 on entry) -> colptr; one CTA.
@@ -153,7 +155,7 @@ cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
   if (nnz > 0) {
     int blocks = (int)((nnz + 255) / 256);
     if (blocks > 4096) blocks = 4096;
-    colcount_kernel<<<blocks, 256, 0, s>>>(nnz, colind, colptr);
+    colcount_kernel<<<blocks, 256, 0, s>>>(nnz, n, colind, colptr);
   }
   scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor, maxcnt);
   int rb = (int)(((int64_t)m * 32 + 255) / 256);
@@ -162,6 +164,35 @@ cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
   csc_scatter_kernel<<<rb, 256, 0, s>>>(m, rowptr, colind, vals, cursor, tmp_row, tmp_val);
   int cb = (int)(((int64_t)n * 32 + 255) / 256);
   if (cb > 4096) cb = 4096;
+  csc_sort_kernel<<<cb, 256, 0, s>>>(n, colptr, tmp_row, tmp_val, rowind, cvals);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csc_count(int m, int n, int64_t nnz, const int32_t* colind, int32_t* colptr,
+                             int32_t* cursor, cudaStream_t s, int* maxcnt) {
+  (void)m;
+  cudaError_t e = cudaMemsetAsync(colptr, 0, sizeof(int32_t) * (size_t)(n + 1), s);
+  if (e != cudaSuccess) return e;
+  if (nnz > 0) {
+    int blocks = (int)((nnz + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    colcount_kernel<<<blocks, 256, 0, s>>>(nnz, n, colind, colptr);
+  }
+  scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor, maxcnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* colind,
+                            const double* vals, const int32_t* colptr, int32_t* rowind,
+                            double* cvals, int32_t* cursor, int32_t* tmp_row, double* tmp_val,
+                            cudaStream_t s) {
+  int rb = (int)(((int64_t)m * 32 + 255) / 256);
+  if (rb > 4096) rb = 4096;
+  if (rb < 1) rb = 1;
+  csc_scatter_kernel<<<rb, 256, 0, s>>>(m, rowptr, colind, vals, cursor, tmp_row, tmp_val);
+  int cb = (int)(((int64_t)n * 32 + 255) / 256);
+  if (cb > 4096) cb = 4096;
+  if (cb < 1) cb = 1;
   csc_sort_kernel<<<cb, 256, 0, s>>>(n, colptr, tmp_row, tmp_val, rowind, cvals);
   return cudaGetLastError();
 }
@@ -232,9 +263,13 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
   const size_t smem = per_warp * wpb;
-  cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+  static bool attr = false;  // once, at the maximum (a driver round trip per call otherwise)
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_cap);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   int per_sm = (int)(220 * 1024 / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 8) per_sm = 8;

@@ -16,6 +16,14 @@ cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, co
                             const double* vals, const double* b, int* err, cudaStream_t s);
 // CSR -> CSC (rows sorted within each column).  colcnt: int32[n+1] scratch,
 // tmp_row/tmp_val: nnz scratch.
+// colcount + scan only (safe on unvalidated CSR: out-of-range columns are
+// skipped), then the rest of the CSC build after validation.
+cudaError_t launch_csc_count(int m, int n, int64_t nnz, const int32_t* colind, int32_t* colptr,
+                             int32_t* cursor, cudaStream_t s, int* maxcnt);
+cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* colind,
+                            const double* vals, const int32_t* colptr, int32_t* rowind,
+                            double* cvals, int32_t* cursor, int32_t* tmp_row, double* tmp_val,
+                            cudaStream_t s);
 cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
                               const int32_t* colind, const double* vals, int32_t* colptr,
                               int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,
@@ -32,9 +40,11 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
 cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double* y, double tol,
                         DevState* st, int p_max, int max_iter, cudaStream_t s);
 // count + decide + exchange + compaction (one CTA); records trace[iter] head.
+// loop != nullptr: the kernel runs inside a CUDA-graph WHILE node and clears
+// its condition when the pivot loop ends (feasible, limit, or failure).
 cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
                           int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
-                          cudaStream_t s);
+                          cudaStream_t s, const cudaGraphConditionalHandle* loop = nullptr);
 cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t* Fidx,
                            int32_t* Gidx, double* xF, DevState* st, cudaStream_t s);
 // y_G = G_GF x_F - c_G (Gram form of Eq. 5), zeroing, scatter x_F into x.

@@ -525,15 +525,20 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
       if (lane < C) *cl.map_shared_rank(&parts[slot + wid][kr], lane) = x;
     }
   };
+  // fixed pairwise tree over the kMaxC slots (independent loads, short chain)
   auto ctotal = [&](int nv, const int* kind, int slot, double* out) {
     for (int q = 0; q < nv; ++q) {
       const int k = kind[q];
-      double x = k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY);
-      for (int r = 0; r < C; ++r) {
-        const double y = parts[slot + q][r];
-        x = k == 0 ? x + y : (k == 1 ? fmin(x, y) : fmax(x, y));
-      }
-      out[q] = x;
+      const double id = k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY);
+      double y[kMaxC];
+#pragma unroll
+      for (int r = 0; r < kMaxC; ++r) y[r] = r < C ? parts[slot + q][r] : id;
+#pragma unroll
+      for (int h = kMaxC / 2; h > 0; h >>= 1)
+#pragma unroll
+        for (int r = 0; r < h; ++r)
+          y[r] = k == 0 ? y[r] + y[r + h] : (k == 1 ? fmin(y[r], y[r + h]) : fmax(y[r], y[r + h]));
+      out[q] = y[0];
     }
   };
   const int K_SUM[3] = {0, 0, 0};
@@ -799,11 +804,35 @@ size_t lsqr_cluster_smem(int m, int n, const int* plan) { return cl_layout(m, n,
 cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host, cudaStream_t s) {
   const ClLayout Ly = cl_layout(a.m, a.n, plan_host);
   if (Ly.bytes > 220 * 1024) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)Ly.bytes);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e != cudaSuccess) return e;
+  // attributes and the co-residency check are host round trips: do them once
+  // at the maximum shared-memory size (valid for every smaller launch)
+  static int checked = 0;  // 0 unknown, 1 supported, -1 not supported
+  constexpr size_t kMaxSmem = 220 * 1024;
+  cudaError_t e;
+  if (checked == 0) {
+    e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kMaxSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    int nclusters = 0;
+    if (e == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(kMaxC);
+      q.blockDim = dim3(kCT);
+      q.dynamicSmemBytes = kMaxSmem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kMaxC;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      e = cudaOccupancyMaxActiveClusters(&nclusters, lsqr_cluster_kernel, &q);
+    }
+    checked = (e == cudaSuccess && nclusters >= 1) ? 1 : -1;
+    cudaGetLastError();
+  }
+  if (checked < 0) return cudaErrorNotSupported;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kMaxC);
   cfg.blockDim = dim3(kCT);
@@ -816,12 +845,6 @@ cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  int nclusters = 0;
-  e = cudaOccupancyMaxActiveClusters(&nclusters, lsqr_cluster_kernel, &cfg);
-  if (e != cudaSuccess || nclusters < 1) {
-    cudaGetLastError();
-    return cudaErrorNotSupported;
-  }
   return cudaLaunchKernelEx(&cfg, lsqr_cluster_kernel, a, Ly);
 }
 

@@ -113,7 +113,7 @@ constexpr int kDecideThreads = 1024;
 __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
     int n, uint8_t* __restrict__ mask, const double* __restrict__ x,
     const double* __restrict__ y, int32_t* __restrict__ Fidx, int32_t* __restrict__ Gidx,
-    DevState* st, TraceRec* trace, int trace_cap) {
+    DevState* st, TraceRec* trace, int trace_cap, cudaGraphConditionalHandle loop, int use_loop) {
   __shared__ int s_cnt[32], s_max[32];
   __shared__ int s_wF[32], s_wG[32];
   __shared__ int s_branch, s_last, s_carryF, s_carryG;
@@ -127,7 +127,10 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
       trace[it - 1].above_tol = __longlong_as_double((long long)st->above_bits);
     }
   }
-  if (st->status != 0 || st->done) return;
+  if (st->status != 0 || st->done) {
+    if (use_loop && tid == 0) cudaGraphSetConditional(loop, 0);  // leave the device-side loop
+    return;
+  }
 
   // pass 1: k = #{i in F: x_i < 0} + #{j in G: y_j < 0} (reading c5);
   // largest infeasible original index (reading c6)
@@ -179,7 +182,10 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
   }
   __syncthreads();
   const int branch = s_branch;
-  if (branch < 0) return;
+  if (branch < 0) {
+    if (use_loop && tid == 0) cudaGraphSetConditional(loop, 0);  // feasible / iteration limit
+    return;
+  }
   const int lastidx = s_last;
 
   // pass 2: exchange (from the snapshot: each thread re-reads its own entries)
@@ -242,8 +248,10 @@ cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t*
 
 cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
                           int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
-                          cudaStream_t s) {
-  decide_kernel<<<1, kDecideThreads, 0, s>>>(n, mask, x, y, Fidx, Gidx, st, trace, trace_cap);
+                          cudaStream_t s, const cudaGraphConditionalHandle* loop) {
+  decide_kernel<<<1, kDecideThreads, 0, s>>>(n, mask, x, y, Fidx, Gidx, st, trace, trace_cap,
+                                             loop ? *loop : cudaGraphConditionalHandle{},
+                                             loop ? 1 : 0);
   return cudaGetLastError();
 }
 

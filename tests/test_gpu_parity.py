@@ -374,3 +374,24 @@ def test_lsqr_full_grid_path(P, cfg, seed, monkeypatch):
     memory; force the full-grid cooperative kernel and check it too."""
     monkeypatch.setenv("NNLS_NO_CLUSTER", "1")
     assert_parity(P, g.make_problem(cfg, seed))
+
+
+@pytest.mark.parametrize("cfg,seed", [(0, 4), (1, 2), (3, 2)])
+def test_host_driven_loop_path(P, cfg, seed, monkeypatch):
+    """The pivot loop normally runs device-resident (CUDA-graph WHILE node);
+    the host-driven loop (used for per-phase timing) must agree."""
+    monkeypatch.setenv("NNLS_NO_GRAPH", "1")
+    assert_parity(P, g.make_problem(cfg, seed))
+
+
+def test_graph_replay_across_loads(P):
+    """One handle, the captured solve graph is reused / rebuilt across loads."""
+    S = P.Solver(trace=1)
+    for cfg, seed in [(1, 0), (1, 0), (0, 2), (1, 1), (3, 0)]:
+        prob = g.make_problem(cfg, seed)
+        S.load_problem(prob)
+        x, info = S.solve()
+        r = O.solve(prob, trace_cap=10 * prob.n + 2)
+        assert np.array_equal(S.free_set(), r["mask"]) and info["iterations"] == r["iterations"]
+        assert [t["branch"] for t in S.trace()] == [t["branch"] for t in r["trace"]]
+        assert rel(x, r["x"]) <= TOL_X
