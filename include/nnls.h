@@ -172,6 +172,12 @@ NNLS_API nnls_status nnls_setup_shard(nnls_handle** h, int32_t m, int32_t n, int
                              const int32_t* rowptr, const int32_t* colind, const double* vals,
                              const double* b, int32_t row_begin, int32_t row_end,
                              const nnls_params* p, void* cuda_stream);
+/* Reload a (new) problem into a handle as a row shard (as nnls_load, Gram
+ * over rows [row_begin, row_end) only; finalize required again). */
+NNLS_API nnls_status nnls_load_shard(nnls_handle* h, int32_t m, int32_t n, int64_t nnz,
+                                     const int32_t* rowptr, const int32_t* colind,
+                                     const double* vals, const double* b, int32_t row_begin,
+                                     int32_t row_end);
 NNLS_API nnls_status nnls_gram_buffer(nnls_handle* h, double** dev_ptr, size_t* count, int32_t* ld);
 NNLS_API nnls_status nnls_gram_finalize(nnls_handle* h);
 

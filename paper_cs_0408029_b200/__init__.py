@@ -82,6 +82,7 @@ def _load():
         "nnls_destroy": ([P], i32),
         "nnls_setup_shard": ([P, i32, i32, i64, P, P, P, P, i32, i32, P, P], i32),
         "nnls_gram_buffer": ([P, P, P, P], i32),
+        "nnls_load_shard": ([P, i32, i32, i64, P, P, P, P, i32, i32], i32),
         "nnls_gram_finalize": ([P], i32),
         "nnls_setup_batched": ([P, i32, i32, i32, P, P, P, P, P, P, P], i32),
         "nnls_create_batched": ([P, P, P], i32),
@@ -257,6 +258,13 @@ class ShardSolver(Solver):
                                     _ptr(v), _ptr(bb), int(row_begin), int(row_end),
                                     C.byref(self.params), _stream_ptr(stream)), "nnls_setup_shard")
         self.m, self.n = int(m), int(n)
+
+    def load_shard(self, m, n, rowptr, colind, vals, b, row_begin, row_end):
+        rp, ci, v, bb = _as(rowptr, np.int32), _as(colind, np.int32), _as(vals, np.float64), _as(b, np.float64)
+        _check(lib.nnls_load_shard(self.h, int(m), int(n), int(ci.shape[0]), _ptr(rp), _ptr(ci), _ptr(v),
+                                   _ptr(bb), int(row_begin), int(row_end)), "nnls_load_shard")
+        self.m, self.n = int(m), int(n)
+        return self
 
     def gram_buffer(self):
         """(device pointer, element count, row stride) of [G | c]."""

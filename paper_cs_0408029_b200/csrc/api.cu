@@ -405,6 +405,13 @@ nnls_status nnls_setup_shard(nnls_handle** h, int32_t m, int32_t n, int64_t nnz,
   return s;
 }
 
+nnls_status nnls_load_shard(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const int32_t* rowptr,
+                            const int32_t* colind, const double* vals, const double* b,
+                            int32_t row_begin, int32_t row_end) {
+  if (!h || h->batched) return NNLS_ERR_INVALID_ARG;
+  return load_impl(h, m, n, nnz, rowptr, colind, vals, b, row_begin, row_end);
+}
+
 nnls_status nnls_gram_buffer(nnls_handle* h, double** dev_ptr, size_t* count, int32_t* ld) {
   if (!h || !h->loaded || h->batched) return NNLS_ERR_STATE;
   if (dev_ptr) *dev_ptr = P<double>(h->Gc);

@@ -395,3 +395,29 @@ def test_graph_replay_across_loads(P):
         assert np.array_equal(S.free_set(), r["mask"]) and info["iterations"] == r["iterations"]
         assert [t["branch"] for t in S.trace()] == [t["branch"] for t in r["trace"]]
         assert rel(x, r["x"]) <= TOL_X
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_gram_path(P, world):
+    """nnls_setup_shard on each row block + summed [G | c] buffers (the
+    all-reduce, done here by torch on one GPU) + nnls_gram_finalize: the Gram
+    is bitwise the full one and the solve matches the oracle."""
+    from paper_cs_0408029_b200.dist import gram_tensor, row_shards
+    prob = g.make_problem(1, 5)
+    shards = [P.ShardSolver(prob.m, prob.n, prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1)
+              for r0, r1 in row_shards(prob.m, world)]
+    torch.cuda.synchronize()
+    with pytest.raises(P.NNLSError):
+        shards[0].solve()                                  # not finalized yet
+    acc = gram_tensor(shards[0])
+    for s in shards[1:]:
+        acc += gram_tensor(s)
+    torch.cuda.synchronize()
+    shards[0].finalize()
+    G, c = shards[0].gram()
+    Go, co = O.gram(prob)
+    assert np.array_equal(G, Go) and np.array_equal(c, co)
+    x, info = shards[0].solve()
+    r = O.solve(prob)
+    assert np.array_equal(shards[0].free_set(), r["mask"]) and info["iterations"] == r["iterations"]
+    assert rel(x, r["x"]) <= TOL_X
