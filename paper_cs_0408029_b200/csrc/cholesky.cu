@@ -281,15 +281,38 @@ __device__ __forceinline__ int block_potrf64(double* __restrict__ S, int rv, int
 // per lane is 8 wide instead of 32/64 (the column chain is latency-bound).
 // Writes L into S (lower; the strict upper part is cleared by the caller),
 // 1/l_cc into rinv; returns the first bad pivot column or -1.
+__device__ __forceinline__ void panel8_update_block(double* __restrict__ S, int c0, int r0, int k0,
+                                                    int lane) {
+  // S[r0..r0+8)[k0..k0+8) -= S[r0..][c0..c0+8) S[k0..][c0..c0+8)^T  (one DMMA block, K = 8)
+  double* Cp = S + (r0 + (lane >> 2)) * LDS + k0 + 2 * (lane & 3);
+  double c0v = Cp[0], c1v = Cp[1];
+#pragma unroll
+  for (int kk = 0; kk < 8; kk += 4) {
+    const double av = -S[(r0 + (lane >> 2)) * LDS + c0 + kk + (lane & 3)];
+    const double bv = S[(k0 + (lane >> 2)) * LDS + c0 + kk + (lane & 3)];
+    dmma8x8x4(c0v, c1v, av, bv);
+  }
+  Cp[0] = c0v;
+  Cp[1] = c1v;
+}
+
 __device__ __forceinline__ int potrf64_panel8(double* __restrict__ S, int rv, int cv,
                                               double* __restrict__ rinv, int* s_bad) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_bad = -1;
   const int np = (cv + 7) >> 3;
+  const int nbr = (rv + 7) >> 3;  // 8-row blocks holding valid rows
+  __syncthreads();
 #pragma unroll 1
   for (int p = 0; p < np; ++p) {
     const int c0 = 8 * p;
+    // (a) critical: apply panel p-1's update to column block p (blocks (I, p))
+    if (p > 0) {
+      for (int I = p + w; I < nbr; I += 8) panel8_update_block(S, c0 - 8, 8 * I, c0, lane);
+      __syncthreads();
+    }
     if (w == 0) {
+      // (b) warp 0 factors panel p in registers: lane l holds rows c0+l, c0+32+l
       const int R0 = c0 + lane, R1 = c0 + 32 + lane;
       const bool v0 = R0 < rv, v1 = R1 < rv;
       double a0[8], a1[8];
@@ -324,27 +347,18 @@ __device__ __forceinline__ int potrf64_panel8(double* __restrict__ S, int rv, in
         if (v1) S[R1 * LDS + c0 + c] = (c0 + c < cv) ? a1[c] : 0.0;
       }
       if (lane == 0 && bad >= 0 && *s_bad < 0) *s_bad = bad;
-    }
-    __syncthreads();
-    // rank-8 trailing update of the lower 8x8 blocks (I >= J > p) with DMMA
-    const int nb = 8 - (p + 1);  // trailing block rows/cols
-    const int nblk = nb * (nb + 1) / 2;
-    for (int b = w; b < nblk; b += 8) {
-      int I = (int)((sqrtf(8.0f * b + 1.0f) - 1.0f) * 0.5f);
-      while (I * (I + 1) / 2 > b) --I;
-      while ((I + 1) * (I + 2) / 2 <= b) ++I;
-      const int J = b - I * (I + 1) / 2;
-      const int r0 = 8 * (p + 1 + I), k0 = 8 * (p + 1 + J);
-      double* Cp = S + (r0 + (lane >> 2)) * LDS + k0 + 2 * (lane & 3);
-      double cacc0 = Cp[0], cacc1 = Cp[1];
-#pragma unroll
-      for (int kk = 0; kk < 8; kk += 4) {
-        const double av = -S[(r0 + (lane >> 2)) * LDS + c0 + kk + (lane & 3)];
-        const double bv = S[(k0 + (lane >> 2)) * LDS + c0 + kk + (lane & 3)];
-        dmma8x8x4(cacc0, cacc1, av, bv);
+    } else if (p > 0) {
+      // (c) meanwhile warps 1..7: the rest of panel p-1's trailing update
+      //     (blocks (I, J) with I >= J >= p+1), disjoint from panel p
+      const int nb = nbr - (p + 1);
+      const int nblk = nb > 0 ? nb * (nb + 1) / 2 : 0;
+      for (int bq = w - 1; bq < nblk; bq += 7) {
+        int I = (int)((sqrtf(8.0f * bq + 1.0f) - 1.0f) * 0.5f);
+        while (I * (I + 1) / 2 > bq) --I;
+        while ((I + 1) * (I + 2) / 2 <= bq) ++I;
+        const int J = bq - I * (I + 1) / 2;
+        if (8 * (p + 1 + J) < cv) panel8_update_block(S, c0 - 8, 8 * (p + 1 + I), 8 * (p + 1 + J), lane);
       }
-      Cp[0] = cacc0;
-      Cp[1] = cacc1;
     }
     __syncthreads();
   }
@@ -554,6 +568,9 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
                                                                    int* __restrict__ xflags,
                                                                    double* __restrict__ xF,
                                                                    DevState* st) {
+  extern __shared__ double bsm[];
+  double* Lnext = bsm;        // L(J+1, J): the only tile on the critical path
+  double* Xinv = bsm + T * T; // Linv(J, J)
   __shared__ double part[4 * T];
   __shared__ double s_rhs[T];
   __shared__ double s_x[T];
@@ -572,10 +589,16 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
     if (t >= ntc) break;
     const int J = ntc - 1 - t;
     const int cv = min(T, f - J * T);
+    // prefetch the critical-path tiles (the factorization is complete)
+    for (int e = tid; e < T * T / 2; e += kThreads) {
+      cp_async16(Xinv + 2 * e, Linv + (size_t)J * T * T + 2 * e);
+      if (J + 1 < ntc) cp_async16(Lnext + 2 * e, Lt + (size_t)tidx(J + 1, J) * T * T + 2 * e);
+    }
+    cp_async_commit();
     if (tid < T) s_rhs[tid] = (tid < cv) ? __ldcg(&Lt[(size_t)tidx(Rf, J) * T * T + rf * T + tid]) : 0.0;
     __syncthreads();
-    // subtract L_IJ^T x_I for I = ntc-1 .. J+1 (the latest-ready block last)
-    for (int I = ntc - 1; I > J; --I) {
+    // subtract L_IJ^T x_I for I = ntc-1 .. J+2 straight from L2 (off the critical path)
+    for (int I = ntc - 1; I > J + 1; --I) {
       if (tid == 0) wait_flag(&xflags[I], epoch);
       __syncthreads();
       const int rvI = min(T, f - I * T);  // rows of L_IJ that are < f
@@ -589,10 +612,26 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
       if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
       __syncthreads();
     }
-    // x_J = Linv_JJ^T s : x[c] = sum_{r >= c} Linv[r][c] s[r]
-    const double* X = Linv + (size_t)J * T * T;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (J + 1 < ntc) {  // the critical step: x_{J+1} from the previous task
+      if (tid == 0) wait_flag(&xflags[J + 1], epoch);
+      __syncthreads();
+      const int rvI = min(T, f - (J + 1) * T);
+      if (tid < T) s_x[tid] = (tid < rvI) ? __ldcg(&xF[(J + 1) * T + tid]) : 0.0;
+      __syncthreads();
+      double p = 0.0;
+#pragma unroll 4
+      for (int r = rg; r < T; r += 4) p = fma(Lnext[r * T + c], s_x[r], p);
+      part[rg * T + c] = p;
+      __syncthreads();
+      if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
+      __syncthreads();
+    }
+    // x_J = Linv_JJ^T s : x[c] = sum_{r >= c} Linv[r][c] s[r]  (Linv is zero beyond cv)
     double p = 0.0;
-    for (int r = rg; r < cv; r += 4) p = fma(__ldcg(&X[r * T + c]), s_rhs[r], p);
+#pragma unroll 4
+    for (int r = rg; r < T; r += 4) p = fma(Xinv[r * T + c], s_rhs[r], p);
     part[rg * T + c] = p;
     __syncthreads();
     if (tid < cv) xF[J * T + tid] = (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
@@ -607,6 +646,9 @@ static cudaError_t set_attrs() {
   if (attr_set) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * kSmemDoubles));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(double) * 2 * T * T));
   if (e != cudaSuccess) return e;
   attr_set = true;
   return cudaSuccess;
@@ -632,7 +674,9 @@ cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* x
   int* xflags = flags + tri_tiles(n);
   const double* Linv = Lt + (size_t)tri_tiles(n) * T * T;
   const int g2 = ntr < sm_count ? ntr : sm_count;
-  chol_backsolve_kernel<<<g2, kThreads, 0, s>>>(Lt, Linv, xflags, xF, st);
+  cudaError_t e = set_attrs();
+  if (e != cudaSuccess) return e;
+  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * 2 * T * T, s>>>(Lt, Linv, xflags, xF, st);
   return cudaGetLastError();
 }
 

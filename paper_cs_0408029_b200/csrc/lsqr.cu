@@ -440,9 +440,10 @@ template <class Emit>
 __device__ __forceinline__ void seg_dots(int nseg, int g, const int* __restrict__ sp,
                                          const double* __restrict__ val, const int* __restrict__ idx,
                                          const double* __restrict__ vec, const int* __restrict__ skip,
-                                         Emit emit) {
-  const int tid = threadIdx.x, sl = tid & (g - 1);
-  const int per = kCT / g;
+                                         Emit emit, int t0 = 0) {
+  if ((int)threadIdx.x < t0) return;  // (whole warps: t0 is a multiple of 32)
+  const int tid = threadIdx.x - t0, sl = tid & (g - 1);
+  const int per = (kCT - t0) / g;
   for (int base = 0; base < nseg; base += per) {
     const int q = base + tid / g;
     double s = 0.0;
@@ -455,9 +456,9 @@ __device__ __forceinline__ void seg_dots(int nseg, int g, const int* __restrict_
     if (sl == 0 && q < nseg) emit(q, s);
   }
 }
-__device__ __forceinline__ int seg_group(int nseg) {
+__device__ __forceinline__ int seg_group(int nseg, int nthreads = kCT) {
   int g = 32;
-  while (g > 1 && (long long)nseg * g > kCT) g >>= 1;
+  while (g > 1 && (long long)nseg * g > nthreads) g >>= 1;
   return g;
 }
 
@@ -489,18 +490,48 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   int* smk = scp + Ly.cols_max + 1;    // own column mask
   const uint8_t* __restrict__ mask = a.mask;
 
-  // ---- stage the slices (once per solve)
-  for (int t = tid; t < S.e1 - S.e0; t += kCT) {
-    sv[t] = a.vals[S.e0 + t];
-    sci[t] = a.colind[S.e0 + t];
-  }
+  // ---- stage the slices (once per solve).  Every CSR product of the path
+  //      multiplies a vector that is zero outside F (v, x_ne, x), so the row
+  //      slice keeps only the F columns; the CSC slice (A^T u, y') is kept whole.
   for (int t = tid; t < S.f1 - S.f0; t += kCT) {
     scv[t] = a.cvals[S.f0 + t];
     sri[t] = a.rowind[S.f0 + t];
   }
-  for (int r = tid; r <= nrows; r += kCT) srp[r] = a.rowptr[S.r0 + r] - S.e0;
   for (int j = tid; j <= ncols; j += kCT) scp[j] = a.colptr[S.j0 + j] - S.f0;
   for (int j = tid; j < ncols; j += kCT) smk[j] = mask[S.j0 + j];
+  for (int r = tid; r < nrows; r += kCT) {  // F-entries per row
+    int cnt = 0;
+    for (int t = a.rowptr[S.r0 + r]; t < a.rowptr[S.r0 + r + 1]; ++t) cnt += mask[a.colind[t]];
+    srp[r + 1] = cnt;
+  }
+  if (tid == 0) srp[0] = 0;
+  __syncthreads();
+  if (wid == 0) {  // inclusive scan of the row counts (one warp)
+    int carry = 0;
+    for (int b0 = 0; b0 < nrows; b0 += 32) {
+      int v = (b0 + lane < nrows) ? srp[b0 + lane + 1] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += y;
+      }
+      if (b0 + lane < nrows) srp[b0 + lane + 1] = v + carry;
+      carry += __shfl_sync(kFull, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < nrows; r += kCT) {
+    int pos = srp[r];
+    for (int t = a.rowptr[S.r0 + r]; t < a.rowptr[S.r0 + r + 1]; ++t) {
+      const int j = a.colind[t];
+      if (mask[j]) {
+        sv[pos] = a.vals[t];
+        sci[pos] = j;
+        ++pos;
+      }
+    }
+  }
+  __shared__ double sc[16];  // scalars computed by warp 0, broadcast after a barrier
   __syncthreads();
 
   // Cluster reductions without remote loads: every CTA reduces its values
@@ -525,29 +556,33 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
       if (lane < C) *cl.map_shared_rank(&parts[slot + wid][kr], lane) = x;
     }
   };
-  // fixed pairwise tree over the kMaxC slots (independent loads, short chain)
+  // cluster totals of parts[slot..slot+nv): lane r < C loads source r's
+  // partial, one xor-butterfly per value (fixed order: identical in every CTA
+  // and every warp).  Called by whole warps.
   auto ctotal = [&](int nv, const int* kind, int slot, double* out) {
-    for (int q = 0; q < nv; ++q) {
-      const int k = kind[q];
-      const double id = k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY);
-      double y[kMaxC];
 #pragma unroll
-      for (int r = 0; r < kMaxC; ++r) y[r] = r < C ? parts[slot + q][r] : id;
-#pragma unroll
-      for (int h = kMaxC / 2; h > 0; h >>= 1)
-#pragma unroll
-        for (int r = 0; r < h; ++r)
-          y[r] = k == 0 ? y[r] + y[r + h] : (k == 1 ? fmin(y[r], y[r + h]) : fmax(y[r], y[r + h]));
-      out[q] = y[0];
+    for (int q = 0; q < 3; ++q) {
+      if (q < nv) {
+        const int k = kind[q];
+        double x = (lane < C) ? parts[slot + q][lane] : (k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY));
+        if (k == 0) x = warp_sum(x);
+        else if (k == 1) x = warp_min(x);
+        else x = warp_max(x);
+        out[q] = x;
+      }
     }
   };
   const int K_SUM[3] = {0, 0, 0};
   // push own rows/cols of a replica to every CTA's copy
+  // (all 512 threads share the (destination, element) space: a loop over
+  //  destinations with only `cnt` active threads was 4x slower)
   auto push = [&](double* rep, int base, int cnt) {
-    for (int q = 0; q < C; ++q) {
+    const int tot = cnt * (C - 1);
+    for (int e = tid; e < tot; e += kCT) {
+      const int qq = e / cnt, i = e - qq * cnt;
+      const int q = qq + (qq >= kr);  // skip self
       double* dst = cl.map_shared_rank(rep, q);
-      if (q == kr) continue;
-      for (int i = tid; i < cnt; i += kCT) dst[base + i] = rep[base + i];
+      dst[base + i] = rep[base + i];
     }
   };
 
@@ -604,10 +639,11 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
     double last_phi = 0.0, last_sn = 0.0;  // for the deferred stopping test
     bool pending = false;
     double pd = 0.0, px = 0.0;
+    const int gCw = seg_group(ncols, kCT - 32);  // phase B runs on warps 1.. (warp 0: scalars)
     __syncthreads();
     if (alpha * beta != 0.0) {
       for (;;) {
-        // ---- phase A (iteration itn+1): U' = A v - alpha u on own rows
+        // ---- phase A (iteration itn+1): U' = A_F v - alpha u on own rows
         LQ_STAMP(0);
         const bool more = itn < itn_limit;
         if (more) {
@@ -624,6 +660,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
           for (int r = tid; r < nrows; r += kCT) pu += Urep[S.r0 + r] * Urep[S.r0 + r];
           push(Urep, S.r0, nrows);
         }
+        LQ_STAMP(11);
         {
           const double v3[3] = {pu, pd, px};
           publish(3, v3, K_SUM, 0);  // parts 0 (|U'|^2), 1 (|d|^2), 2 (|x|^2)
@@ -631,53 +668,79 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
         LQ_STAMP(2);
         cl.sync();
         LQ_STAMP(3);
-        double t3[3];
-        ctotal(3, K_SUM, 0, t3);
-        // ---- deferred stopping test of the previous iteration
-        if (pending) {
-          ddnorm += t3[1];
-          const double xnorm = sqrt(t3[2]);
-          const double acond = anorm * sqrt(ddnorm);
-          const double rnorm = phibar;
-          const double arnorm = alpha * fabs(last_sn * last_phi);
-          const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
-          const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
-          const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
-          const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
-          const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
-          if (itn >= itn_limit) istop = 7;
-          if (1.0 + test3 <= 1.0) istop = 6;
-          if (1.0 + test2 <= 1.0) istop = 5;
-          if (1.0 + tt1 <= 1.0) istop = 4;
-          if (test3 <= ctol) istop = 3;
-          if (test2 <= a.atol) istop = 2;
-          if (test1 <= rtol) istop = 1;
-          if (istop != 0) break;
+        // ---- warp 0: deferred stopping test of the previous iteration, beta;
+        //      warps 1..: the A_F^T U' dots of phase B (no scalar dependency)
+        if (wid == 0) {
+          double t3[3];
+          ctotal(3, K_SUM, 0, t3);
+          int stop = 0;
+          if (pending) {
+            ddnorm += t3[1];
+            const double xnorm = sqrt(t3[2]);
+            const double acond = anorm * sqrt(ddnorm);
+            const double rnorm = phibar;
+            const double arnorm = alpha * fabs(last_sn * last_phi);
+            const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+            const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
+            const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
+            const double axb = bnorm > 0.0 ? anorm * xnorm / bnorm : 0.0;
+            const double tt1 = bnorm > 0.0 ? test1 / (1.0 + axb) : 0.0;
+            const double rtol = a.btol + a.atol * axb;
+            if (itn >= itn_limit) stop = 7;
+            if (1.0 + test3 <= 1.0) stop = 6;
+            if (1.0 + test2 <= 1.0) stop = 5;
+            if (1.0 + tt1 <= 1.0) stop = 4;
+            if (test3 <= ctol) stop = 3;
+            if (test2 <= a.atol) stop = 2;
+            if (test1 <= rtol) stop = 1;
+          }
+          if (lane == 0) {
+            sc[0] = sqrt(t3[0]);   // beta_new
+            sc[1] = (double)stop;
+            sc[2] = ddnorm;
+          }
+          LQ_STAMP(12);
+        } else if (more) {
+          seg_dots(ncols, gCw, scp, scv, sri, Urep, smk, [&](int j, double s) { scr[j] = s; }, 32);
+          if (g_lsqr_prof != nullptr && kr == 0 && threadIdx.x == 32 && itn < 64) {
+            unsigned long long t_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+            g_lsqr_prof[itn * 16 + 13] = t_;
+          }
         }
+        __syncthreads();
         LQ_STAMP(4);
+        istop = (int)sc[1];
+        ddnorm = sc[2];
+        if (istop != 0) break;
         ++itn;
-        const double beta_new = sqrt(t3[0]);
+        const double beta_new = sc[0];
         // ---- phase B: V' = A_F^T u - beta v on own columns (u = U'/beta_new)
         double alpha_new = alpha;
         if (beta_new > 0.0) {
           anorm = sqrt(anorm * anorm + alpha * alpha + beta_new * beta_new);
           const double ib = 1.0 / beta_new;
-          seg_dots(ncols, gC, scp, scv, sri, Urep, smk, [&](int j, double s) {
-            Vrep[S.j0 + j] = s * ib - beta_new * vo[j];
-          });
+          double pv = 0.0;
+          for (int j = tid; j < ncols; j += kCT) {
+            if (!smk[j]) continue;
+            const double v = scr[j] * ib - beta_new * vo[j];
+            Vrep[S.j0 + j] = v;
+            pv += v * v;
+          }
           __syncthreads();
           LQ_STAMP(5);
-          double pv = 0.0;
-          for (int j = tid; j < ncols; j += kCT)
-            if (smk[j]) pv += Vrep[S.j0 + j] * Vrep[S.j0 + j];
           push(Vrep, S.j0, ncols);
           publish(1, &pv, K_SUM, 3);
           LQ_STAMP(6);
           cl.sync();
           LQ_STAMP(7);
-          double t1v[3];
-          ctotal(1, K_SUM, 3, t1v);
-          alpha_new = sqrt(t1v[0]);
+          if (wid == 0) {
+            double t1v[3];
+            ctotal(1, K_SUM, 3, t1v);
+            if (lane == 0) sc[3] = sqrt(t1v[0]);
+          }
+          __syncthreads();
+          alpha_new = sc[3];
           LQ_STAMP(8);
         } else {
           cl.sync();  // keep the two-barrier rhythm (partials are reused)
@@ -694,6 +757,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
         // ---- phase C: v, x, w on own columns (partials ride on the next barrier)
         const bool newv = beta_new > 0.0;
         const double ia = (newv && alpha_new > 0.0) ? 1.0 / alpha_new : 1.0;
+        const double irho = 1.0 / rho;
         pd = 0.0;
         px = 0.0;
         for (int j = tid; j < ncols; j += kCT) {
@@ -704,7 +768,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
             vo[j] = v;
           }
           const double w = wo[j];
-          const double d = w / rho;
+          const double d = w * irho;
           pd += d * d;
           const double x = xo[j] + t1 * w;
           xo[j] = x;

@@ -32,6 +32,15 @@ for r in rows:
         d[names[k]].append(p[r, k + 1] - p[r, k])
     d["C->nextA"].append(p[r + 1, 0] - p[r, 10])
 print("iterations profiled:", len(rows), "lsqr_iterations:", info["lsqr_iterations"])
+bd = [p[r, 13] - p[r, 3] for r in rows if p[r, 13] > 0]
+if bd:
+    print(f"{'  B dots (warp 1)':22s} {np.mean(bd):9.0f} ns")
+ws = [p[r, 12] - p[r, 3] for r in rows if p[r, 12] > 0]
+if ws:
+    print(f"{'  warp0 scalars':22s} {np.mean(ws):9.0f} ns")
+pp = [p[r, 11] - p[r, 1] for r in rows if p[r, 11] > 0]
+if pp:
+    print(f"{'  of which push':22s} {np.mean(pp):9.0f} ns")
 tot = 0
 for k, v in d.items():
     if v:
