@@ -213,7 +213,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->Fidx, sizeof(int32_t) * (size_t)n));
   CK(ensure(h->Gidx, sizeof(int32_t) * (size_t)n));
   const size_t ntile = chol_tile_count(n);
-  const size_t nflags = ntile + (size_t)(n + 1 + kTile) / kTile + 1;
+  const size_t nflags = chol_flag_count(n);
   if (h->flags.cap < sizeof(int) * nflags) {
     CK(ensure(h->flags, sizeof(int) * nflags));
     CK(cudaMemsetAsync(h->flags.p, 0, h->flags.cap, s));
@@ -883,7 +883,7 @@ nnls_status nnls_step_normal_solve(int32_t n, const double* G, int32_t ldg, cons
   TmpBufs t;
   const size_t ntile = chol_tile_count(n);
   CK(ensure(t.bufs[0], sizeof(double) * ntile * kTile * kTile));
-  CK(ensure(t.bufs[1], sizeof(int) * (ntile + (size_t)(n + 1 + kTile) / kTile + 1)));
+  CK(ensure(t.bufs[1], sizeof(int) * chol_flag_count(n)));
   CK(ensure(t.bufs[2], sizeof(DevState)));
   CK(ensure(t.bufs[3], sizeof(double) * (size_t)(f + kTile)));
   CK(cudaMemsetAsync(t.bufs[1].p, 0, t.bufs[1].cap, s));

@@ -41,9 +41,12 @@ namespace {
 constexpr int T = kTile;
 constexpr int LDS = T + 4;  // smem row stride (doubles): conflict-free 8x4 fragment reads
 constexpr int kThreads = 256;
-constexpr int kSmemDoubles = 4 * T * LDS;
+constexpr int kSmemDoubles = 6 * T * LDS;
 
 __host__ __device__ inline int tidx(int i, int j) { return i * (i + 1) / 2 + j; }
+// Barrier of the CTA's 8 warps as named barrier 1 (barrier 2 is the 7-warp
+// barrier of the chain's POTRF, see wsync).
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 inline int tri_tiles(int n) {
   const int ntr = (n + 1 + T - 1) / T;
   return ntr * (ntr + 1) / 2;
@@ -62,6 +65,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                                                                                          \
     if (g_chol_prof != nullptr && threadIdx.x == 0) g_chol_prof[(task) * 8 + (slot)] = gtimer(); \
   } while (0)
+
+// DAG flags: full[tri], part[tri], inv[ntr], back-solve x[ntr].
+size_t chol_flag_count(int n) {
+  const int ntr = (n + 1 + T - 1) / T;
+  return 2 * (size_t)tri_tiles(n) + 2 * (size_t)ntr + 4;
+}
 
 // Lower tiles L(i,j) followed by one inverse tile per tile column.
 size_t chol_tile_count(int n) {
@@ -147,51 +156,6 @@ __device__ __forceinline__ void acc_store(const double (&acc)[2][4][2], double* 
         S[(rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v] = acc[a][q][v];
 }
 
-// POTRF of a 32-row block held by one warp, lane = row, a[t] = A[lane][t].
-// Columns c < ncols are pivots; rows >= ncols (e.g. the bordered row c_F^T)
-// are eliminated as off-diagonal rows.  Right-looking, updates applied in
-// increasing c.  The finished column is broadcast through shared memory
-// (colbuf: broadcast loads at immediate offsets); updates are predicated,
-// never divergent.  The column loop is rolled 4 columns at a time with a
-// register shift (register arrays are indexed by compile-time constants only;
-// a fully unrolled loop is instruction-bound, not cheaper).  Writes L[lane][c]
-// to out[lane*LDS + c] (0 above the diagonal and in non-pivot columns),
-// 1/l_cc to rinv[c].  Returns the first bad pivot or -1.
-__device__ __forceinline__ int warp_potrf32(double (&a)[32], int ncols, int lane, double* rinv,
-                                            double* out, double* colbuf) {
-  int bad = -1;
-#pragma unroll 1
-  for (int c0 = 0; c0 < ncols; c0 += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u;
-      if (c < ncols) {
-        const double d = __shfl_sync(kFull, a[u], c);
-        if ((!(d > 0.0) || d < 1e-300 || !isfinite(d)) && bad < 0) bad = c;
-        const double inv = rsqrt(d);
-        const double lic = (lane == c) ? d * inv : ((lane > c) ? a[u] * inv : 0.0);
-        colbuf[lane] = lic;
-        if (lane == 0) rinv[c] = inv;
-        out[lane * LDS + c] = lic;
-        __syncwarp();
-        const double* cb = colbuf + c;             // cb[t] = l_{c+t, c}
-        const int lim = min(lane, ncols - 1) - c;  // update columns c+t, 1 <= t <= lim
-#pragma unroll
-        for (int t = 1; u + t < 32; ++t) {
-          const double v = cb[t];
-          if (t <= lim) a[u + t] = fma(-lic, v, a[u + t]);
-        }
-        __syncwarp();
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < 28; ++t) a[t] = a[t + 4];
-    a[28] = a[29] = a[30] = a[31] = 0.0;
-  }
-  for (int col = ncols; col < 32; ++col) out[lane * LDS + col] = 0.0;
-  return bad;
-}
-
 // Inverse of a 32 x 32 lower-triangular block (smem, stride LDS) with
 // reciprocal diagonal rinvb: lane = column c computes X[:, c] by forward
 // substitution, x_i = (delta_ic - sum_{k<i} L_ik x_k) / L_ii.  ncols pivots;
@@ -213,64 +177,6 @@ __device__ __forceinline__ void warp_trtri32(const double* __restrict__ Lb,
 #pragma unroll
     for (int i = 0; i < 32; ++i) outT[lane * LDS + i] = x[i];
   }
-}
-
-// Cholesky of the diagonal 64 x 64 tile S (smem, rows < rv, pivot columns
-// < cv; a row >= cv is the bordered row c_F^T and is only eliminated) by all
-// 256 threads.  Thread t owns the lower-triangle entries e = t + 256 s of the
-// tile in registers.  Column c: the owners of column c publish it into a
-// ping-pong buffer, ONE barrier, then every thread updates its own entries
-// with l_rc l_kc = b_r b_k / d (and finalises column c).  Writes L back into S
-// (zero above the diagonal / beyond cv), 1/l_cc into rinv.  Returns the first
-// bad pivot column or -1.
-__device__ __forceinline__ int block_potrf64(double* __restrict__ S, int rv, int cv,
-                                             double* __restrict__ rinv, double (*colbuf)[T]) {
-  constexpr int NS = (T * (T + 1) / 2 + kThreads - 1) / kThreads;  // 9 slots
-  const int tid = threadIdx.x;
-  double a[NS];
-  int rs[NS], ks[NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    const int e = tid + kThreads * s;
-    int r = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-    while (r * (r + 1) / 2 > e) --r;
-    while ((r + 1) * (r + 2) / 2 <= e) ++r;
-    const int k = e - r * (r + 1) / 2;
-    const bool valid = e < T * (T + 1) / 2 && r < rv && k < cv;
-    rs[s] = valid ? r : 0;
-    ks[s] = valid ? k : T;  // k = T: never updated (and never published)
-    a[s] = valid ? S[r * LDS + k] : 0.0;
-  }
-  int bad = -1;
-  // branch-free column loop: every slot computes both candidates and selects
-  // (divergent if/else per slot cost ~1.7K cycles per column)
-#pragma unroll 1
-  for (int c = 0; c < cv; ++c) {
-    double* buf = colbuf[c & 1];
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-      if (ks[s] == c) buf[rs[s]] = a[s];
-    __syncthreads();
-    const double d = buf[c];
-    if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) bad = (bad < 0) ? c : bad;
-    const double inv = rsqrt(d);
-    if (tid == 0) rinv[c] = inv;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const int k = ks[s];
-      const double br = buf[rs[s]], bk = buf[min(k, T - 1)];
-      const double upd = fma(-(br * inv), bk * inv, a[s]);
-      const double fin = (rs[s] == c) ? d * inv : a[s] * inv;
-      a[s] = (k == c) ? fin : ((k > c && k < T) ? upd : a[s]);
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < T * T; e += kThreads) S[(e / T) * LDS + (e % T)] = 0.0;
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < NS; ++s)
-    if (ks[s] < T) S[rs[s] * LDS + ks[s]] = a[s];
-  return bad;
 }
 
 // Cholesky of the diagonal 64 x 64 tile S (smem; rows < rv, pivot columns
@@ -296,73 +202,245 @@ __device__ __forceinline__ void panel8_update_block(double* __restrict__ S, int 
   Cp[1] = c1v;
 }
 
-__device__ __forceinline__ int potrf64_panel8(double* __restrict__ S, int rv, int cv,
-                                              double* __restrict__ rinv, int* s_bad) {
+// C(rows r0..r0+7, column blocks J in [j0, j1)) -= A(r0.., panel c0) B(8J.., panel c0)^T
+// (rank-8 DMMA strip, j1 > j0).  Blocks go in groups of 4; inside a group
+// the DMMAs are unconditional (a block index past j1 is clamped to j1 - 1
+// and its result dropped) so the compiler emits no branch + warp-sync per
+// block around the mma.sync.
+__device__ __forceinline__ void strip8_gemm(double* __restrict__ C, const double* __restrict__ A,
+                                           const double* __restrict__ B, int c0, int r0, int j0, int j1,
+                                           int lane) {
+  const int rr = r0 + (lane >> 2), kq = lane & 3, rq = lane >> 2;
+  const double a0 = -A[rr * LDS + c0 + kq], a1 = -A[rr * LDS + c0 + 4 + kq];
+#pragma unroll
+  for (int h = 0; h < 8; h += 4) {
+    if (j0 + h < j1) {
+      double cv0[4], cv1[4];
+      int Jq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Jq[q] = min(j0 + h + q, j1 - 1);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double* Cp = C + rr * LDS + 8 * Jq[q] + 2 * kq;
+        cv0[q] = Cp[0];
+        cv1[q] = Cp[1];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double b0 = B[(8 * Jq[q] + rq) * LDS + c0 + kq];
+        const double b1 = B[(8 * Jq[q] + rq) * LDS + c0 + 4 + kq];
+        dmma8x8x4(cv0[q], cv1[q], a0, b0);
+        dmma8x8x4(cv0[q], cv1[q], a1, b1);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (j0 + h + q < j1) {
+          double* Cp = C + rr * LDS + 8 * Jq[q] + 2 * kq;
+          Cp[0] = cv0[q];
+          Cp[1] = cv1[q];
+        }
+      }
+    }
+  }
+}
+
+// Warp 0's share of one potrf_r8 panel [c0, c0+8): see potrf_r8.  FULL: all
+// 8 columns valid (no per-column bound checks, so the column chain is one
+// straight-line block).  Returns the first bad pivot column or -1.
+template <int NR, bool FULL>
+__device__ __forceinline__ int panel_factor8(double* __restrict__ S, int c0, int rv, int cv,
+                                             double* __restrict__ rinv, int lane) {
+  double D[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) D[r][c] = S[(c0 + r) * LDS + c0 + c];
+  double a[NR][8];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const int R = c0 + lane + 32 * k;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[k][c] = (R < rv) ? S[R * LDS + c0 + c] : 0.0;
+  }
+  int bad = -1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (FULL || c0 + c < cv) {
+      double d = D[c][c];
+      const bool ok = (d >= 1e-300) && (d <= 1.7976931348623157e308);  // false for NaN
+      bad = (!ok && bad < 0) ? c0 + c : bad;
+      d = ok ? d : 1.0;  // keep the chain finite; the status reports the failure
+      const double inv = rsqrt(d);
+      if (lane == 0) rinv[c0 + c] = inv;
+#pragma unroll
+      for (int c2 = c + 1; c2 < 8; ++c2) D[c2][c] *= inv;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) a[k][c] *= inv;
+#pragma unroll
+      for (int c2 = c + 1; c2 < 8; ++c2) {
+        if (FULL || c0 + c2 < cv) {
+#pragma unroll
+          for (int c3 = c + 1; c3 <= c2; ++c3) D[c2][c3] = fma(-D[c2][c], D[c3][c], D[c2][c3]);
+#pragma unroll
+          for (int k = 0; k < NR; ++k) a[k][c2] = fma(-a[k][c], D[c2][c], a[k][c2]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NR; ++k) a[k][c] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const int R = c0 + lane + 32 * k;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (R < rv && R - c0 >= c) S[R * LDS + c0 + c] = a[k][c];
+  }
+  return bad;
+}
+
+// Cholesky of the leading cv columns of an rv-row smem tile (rv <= 32*NR+c,
+// NR = 2 covers 64 rows), in 8-column panels.  Per panel p:
+//  (a) all warps apply panel p-1 to column block p (the lookahead block);
+//  (b) warp 0 factors panel p: every lane factors the 8x8 diagonal block
+//      REDUNDANTLY in registers (no shuffles on the rsqrt -> scale -> FMA
+//      column chain) and carries the rows c0+lane+32k, k < NR, of the
+//      panel (lanes 0..7, k = 0 are the diagonal-block rows themselves, with
+//      the same arithmetic, so their stored values equal the redundant copy);
+//  (c) meanwhile warps 1..7 apply panel p-1 to the column blocks > p.
+// Returns the first non-positive pivot column or -1; 1/l_cc goes to rinv.
+// Barrier of the first NW warps: NW = 8 -> csync (barrier 1); NW = 7 ->
+// barrier 2 over warps 0..6 (the chain's POTRF, while warp 7 runs its
+// prefetch / publish loop).
+template <int NW>
+__device__ __forceinline__ void wsync() {
+  if (NW == 8) csync();
+  else asm volatile("bar.sync 2, %0;\n" ::"n"(NW * 32) : "memory");
+}
+
+template <int NR, int NW = 8>
+__device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
+                                        double* __restrict__ rinv, int* s_bad) {
+  static_assert(NW == 7 || NW == 8, "potrf_r8 runs on 7 or 8 warps");
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_bad = -1;
   const int np = (cv + 7) >> 3;
-  const int nbr = (rv + 7) >> 3;  // 8-row blocks holding valid rows
-  __syncthreads();
+  const int nbr = (rv + 7) >> 3;
+  wsync<NW>();
 #pragma unroll 1
   for (int p = 0; p < np; ++p) {
     const int c0 = 8 * p;
-    // (a) critical: apply panel p-1's update to column block p (blocks (I, p))
-    if (p > 0) {
-      for (int I = p + w; I < nbr; I += 8) panel8_update_block(S, c0 - 8, 8 * I, c0, lane);
-      __syncthreads();
+    if (p > 0) {  // (a) the lookahead column block: at most 7 row blocks for p >= 1
+      for (int I = p + w; I < nbr; I += NW) panel8_update_block(S, c0 - 8, 8 * I, c0, lane);
+      wsync<NW>();
     }
     if (w == 0) {
-      // (b) warp 0 factors panel p in registers: lane l holds rows c0+l, c0+32+l
-      const int R0 = c0 + lane, R1 = c0 + 32 + lane;
-      const bool v0 = R0 < rv, v1 = R1 < rv;
-      double a0[8], a1[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        a0[c] = v0 ? S[R0 * LDS + c0 + c] : 0.0;
-        a1[c] = v1 ? S[R1 * LDS + c0 + c] : 0.0;
-      }
-      int bad = -1;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (c0 + c < cv) {
-          const double d = __shfl_sync(kFull, a0[c], c);
-          if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) bad = (bad < 0) ? c0 + c : bad;
-          const double inv = rsqrt(d);
-          if (lane == 0) rinv[c0 + c] = inv;
-          a0[c] = (lane == c) ? d * inv : ((lane > c) ? a0[c] * inv : 0.0);
-          a1[c] *= inv;
-#pragma unroll
-          for (int c2 = c + 1; c2 < 8; ++c2) {
-            const double x = __shfl_sync(kFull, a0[c], c2);  // l_{c0+c2, c0+c}
-            if (c0 + c2 < cv) {
-              if (lane >= c2) a0[c2] = fma(-a0[c], x, a0[c2]);
-              a1[c2] = fma(-a1[c], x, a1[c2]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (v0) S[R0 * LDS + c0 + c] = (c0 + c < cv) ? a0[c] : 0.0;
-        if (v1) S[R1 * LDS + c0 + c] = (c0 + c < cv) ? a1[c] : 0.0;
-      }
+      const int bad = (c0 + 8 <= cv) ? panel_factor8<NR, true>(S, c0, rv, cv, rinv, lane)
+                                     : panel_factor8<NR, false>(S, c0, rv, cv, rinv, lane);
       if (lane == 0 && bad >= 0 && *s_bad < 0) *s_bad = bad;
     } else if (p > 0) {
-      // (c) meanwhile warps 1..7: the rest of panel p-1's trailing update
-      //     (blocks (I, J) with I >= J >= p+1), disjoint from panel p
-      const int nb = nbr - (p + 1);
-      const int nblk = nb > 0 ? nb * (nb + 1) / 2 : 0;
-      for (int bq = w - 1; bq < nblk; bq += 7) {
-        int I = (int)((sqrtf(8.0f * bq + 1.0f) - 1.0f) * 0.5f);
-        while (I * (I + 1) / 2 > bq) --I;
-        while ((I + 1) * (I + 2) / 2 <= bq) ++I;
-        const int J = bq - I * (I + 1) / 2;
-        if (8 * (p + 1 + J) < cv) panel8_update_block(S, c0 - 8, 8 * (p + 1 + I), 8 * (p + 1 + J), lane);
+      // (c) row strips I in [p+1, nbr) x column blocks [p+1, min(I, ncb-1)]
+      const int ncb = (cv + 7) >> 3;
+      for (int I = p + w; I < nbr; I += NW - 1) {
+        const int j1 = min(I + 1, ncb);
+        if (p + 1 < j1) strip8_gemm(S, S, S, c0 - 8, 8 * I, p + 1, j1, lane);
       }
     }
-    __syncthreads();
+    wsync<NW>();
   }
   return *s_bad;
+}
+
+struct NoHook {
+  __device__ __forceinline__ void operator()(int, int) const {}
+};
+
+// X := X L^-T for a 64x64 smem tile X and lower L (cv valid columns), in
+// 8-column panels: warps 0-1 solve the panel row by row (thread per row,
+// the 8x8 diagonal block of L in registers), then every warp folds the
+// panel into the later column blocks with DMMA (warp w: rows 8w..8w+7).
+// hook(p, lane) runs on warp 7 during the solve phase of panel p.
+template <class Hook = NoHook>
+__device__ __forceinline__ void trsm_blocked(double* __restrict__ X, const double* __restrict__ L,
+                                             const double* __restrict__ rinv, int cv,
+                                             const Hook& hook = Hook()) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int np = (cv + 7) >> 3;
+#pragma unroll 1
+  for (int p = 0; p < np; ++p) {
+    const int c0 = 8 * p;
+    if (tid < 64) {
+      double Ld[8][8], ri[8], x[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        ri[c] = (c0 + c < cv) ? rinv[c0 + c] : 0.0;
+#pragma unroll
+        for (int c2 = c + 1; c2 < 8; ++c2) Ld[c2][c] = L[(c0 + c2) * LDS + c0 + c];
+        x[c] = X[tid * LDS + c0 + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        x[c] *= ri[c];
+#pragma unroll
+        for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], Ld[c2][c], x[c2]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) X[tid * LDS + c0 + c] = x[c];
+    } else if (w == 7) {
+      hook(p, lane);  // warp 7 is idle in the solve phase
+    }
+    csync();
+    if (p + 1 < np) {  // X(rows of warp w, J) -= X(., panel) L(J, panel)^T for J in (p, np)
+      strip8_gemm(X, X, L, c0, 8 * w, p + 1, np, lane);
+    }
+    csync();
+  }
+}
+
+// Y (lower 8x8 blocks of a 64x64 tile) -= X X^T, K = 64, on warps 0..6:
+// block b = I(I+1)/2 + J goes to warp b % 7 (slot b / 7); warps with 5
+// blocks repeat one as a dummy 6th (result dropped), so the 6 independent
+// 16-step DMMA chains of a warp are unconditional.
+__device__ __forceinline__ void syrk64_lower7(double* __restrict__ Y, const double* __restrict__ X, int w,
+                                             int lane) {
+  if (w >= 7) return;
+  const int kq = lane & 3, rq = lane >> 2;
+  int ra[6], rb[6], ci[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    int b = w + 7 * q;
+    if (b > 35) b = w + 7 * (q - 1);  // dummy slot
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= b) ++I;
+    const int J = b - I * (I + 1) / 2;
+    ra[q] = (8 * I + rq) * LDS + kq;
+    rb[q] = (8 * J + rq) * LDS + kq;
+    ci[q] = (8 * I + rq) * LDS + 8 * J + 2 * kq;
+  }
+  double cv0[6], cv1[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    cv0[q] = Y[ci[q]];
+    cv1[q] = Y[ci[q] + 1];
+  }
+#pragma unroll 4
+  for (int kk = 0; kk < T; kk += 4) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const double av = -X[ra[q] + kk];
+      const double bv = X[rb[q] + kk];
+      dmma8x8x4(cv0[q], cv1[q], av, bv);
+    }
+  }
+  const int nq = (w == 0) ? 6 : 5;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    if (q < nq) {
+      Y[ci[q]] = cv0[q];
+      Y[ci[q] + 1] = cv1[q];
+    }
+  }
 }
 
 // acc[q] (rows 8w.. of a 32 x 32 product, cols 8q..) += A B^T, A and B
@@ -380,140 +458,321 @@ __device__ __forceinline__ void dmma32(double (&acc)[4][2], const double* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// Factorization DAG with a diagonal CHAIN.  CTA 0 walks the diagonal:
+//   for column j:  L_jj = chol(A_jj);  store;
+//                  L(j+1,j) = A(j+1,j) L_jj^-T, and in the same pass
+//                  A_(j+1)(j+1) -= L(j+1,j) L(j+1,j)^T (its last update);  store
+// so the per-column critical path is one POTRF and one TRSM with no tile
+// hand-off between CTAs; warp 7 hides the flag fences and the prefetches of
+// the helpers' partial tiles in its idle phases.  CTAs 1.. claim helper
+// tasks from a queue ordered by column:
+//   P(j+1,j+1): tile (j+1,j+1) with its updates k < j      -> "partial" flag
+//   P(j+1,j)  : tile (j+1,j)   with its updates k < j      -> "partial" flag
+//   T(i,j), i >= j+2: updates k < j, wait L_jj, TRSM       -> "full" flag
+//   I(j)      : Linv_jj = L_jj^-1 (for the back substitution)
+// Every wait is on a task queued earlier or on the chain, and the chain only
+// waits on queued tasks, so the DAG cannot deadlock.
+namespace {
+struct FlagSet {
+  int* full;   // [tri]   L(i,j) final
+  int* part;   // [tri]   partial tile (helper -> chain)
+  int* inv;    // [ntr]   Linv_jj
+};
+// all threads' stores -> barrier -> one st.release (cumulative over what the
+// barrier ordered before it) makes the tile visible with the flag
+__device__ __forceinline__ void publish_flag(int* f, int epoch) {
+  csync();
+  if (threadIdx.x == 0) st_release(f, epoch);
+}
+}  // namespace
+
+// gather tile (i,jj) of [G_FF; c_F^T] into S (lower part only on the diagonal)
+__device__ __forceinline__ void gather_tile(double* __restrict__ S, const double* __restrict__ G,
+                                            int ldg, const double* __restrict__ cvec,
+                                            const int32_t* __restrict__ Fidx, int f, int i, int jj) {
+  const int rv = min(T, f + 1 - i * T), cv = min(T, f - jj * T);
+  for (int e = threadIdx.x; e < T * T; e += kThreads) {
+    const int r = e / T, cc = e % T;
+    const int gi = i * T + r, gj = jj * T + cc;
+    double v = 0.0;
+    if (r < rv && cc < cv && (i != jj || cc <= r))
+      v = (gi < f) ? G[(size_t)Fidx[gi] * ldg + Fidx[gj]] : cvec[Fidx[gj]];
+    S[r * LDS + cc] = v;
+  }
+}
+
+// S (smem tile i,jj) -= sum_{k < kmax} L(i,k) L(jj,k)^T, operands double-
+// buffered through BUF(1..4) with cp.async (waits on the "full" flags).
+__device__ __forceinline__ void left_update(double* __restrict__ smem, double* __restrict__ S,
+                                            const double* __restrict__ Lt, const int* __restrict__ full,
+                                            int epoch, int i, int jj, int kmax, int* s_ready) {
+  if (kmax <= 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
+  double acc[2][4][2];
+  acc_load(acc, S, lane, rb0, cb0);
+  bool have_next = false;
+  for (int k = 0; k < kmax; ++k) {
+    double* LA = smem + ((k & 1) ? 3 : 1) * (T * LDS);
+    double* LB = smem + ((k & 1) ? 4 : 2) * (T * LDS);
+    if (!have_next) {
+      if (tid == 0) {
+        wait_flag(&full[tidx(i, k)], epoch);
+        wait_flag(&full[tidx(jj, k)], epoch);
+      }
+      csync();
+      tile_async(LA, Lt + (size_t)tidx(i, k) * T * T);
+      tile_async(LB, Lt + (size_t)tidx(jj, k) * T * T);
+      cp_async_commit();
+    }
+    have_next = false;
+    if (k + 1 < kmax) {
+      if (tid == 0)
+        *s_ready = (ld_acquire(&full[tidx(i, k + 1)]) == epoch) && (ld_acquire(&full[tidx(jj, k + 1)]) == epoch);
+      csync();
+      if (*s_ready) {
+        tile_async(smem + ((k & 1) ? 1 : 3) * (T * LDS), Lt + (size_t)tidx(i, k + 1) * T * T);
+        tile_async(smem + ((k & 1) ? 2 : 4) * (T * LDS), Lt + (size_t)tidx(jj, k + 1) * T * T);
+        cp_async_commit();
+        have_next = true;
+      }
+    }
+    if (have_next) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    csync();
+    dmma_tile<true>(acc, LA, LB, lane, rb0, cb0);
+    csync();
+  }
+  acc_store(acc, S, lane, rb0, cb0);
+  csync();
+}
+
+// L (smem) -> 1/L[c][c] for c < cv
+__device__ __forceinline__ void diag_recip(const double* __restrict__ L, double* __restrict__ rinv, int cv) {
+  if (threadIdx.x < T) rinv[threadIdx.x] = (threadIdx.x < cv) ? 1.0 / L[threadIdx.x * LDS + threadIdx.x] : 0.0;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     const double* __restrict__ G, int ldg, const double* __restrict__ cvec,
     const int32_t* __restrict__ Fidx, double* __restrict__ Lt, double* __restrict__ Linv,
-    int* __restrict__ flags, DevState* st) {
+    int* __restrict__ flags, int tri, DevState* st) {
   extern __shared__ double smem[];
-  // four T x LDS buffers: BUF(0) = S (task tile) and, during the update loop,
-  // the second (i,k)/(j,k) operand pair with BUF(1); BUF(2)/BUF(3) = first pair.
-#define BUF(q) (smem + (q) * (T * LDS))
-  double* S = BUF(0);
+  // helpers: BUF(0) = S, BUF(1..4) = operand double-buffers.
+  // chain: BUF(0)/BUF(1) = diagonal tile of column j (alternating), BUF(5) = A/L(j+1,j)
   __shared__ double rinv[T];
   __shared__ int s_task, s_ready, s_bad;
-
   const int f = st->f;
   const int epoch = st->epoch;
   if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
   const int ntc = (f + T - 1) / T;      // tile columns to factor
   const int ntr = (f + 1 + T - 1) / T;  // tile rows (incl. the rhs row f)
-  const int total = ntc * ntr - ntc * (ntc - 1) / 2;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int rb0 = (w >> 1) * 16;  // warp tile of the DMMA products: rows rb0..rb0+15
-  const int cb0 = (w & 1) * 32;   //                                 cols cb0..cb0+31
+  FlagSet F{flags, flags + tri, flags + 2 * tri};
+  const int tid = threadIdx.x;
+  double* S = smem;
 
+  if (blockIdx.x == 0) {
+    // ============================== the diagonal chain
+    // BUF(0)/BUF(1): diagonal tile of column j (alternating), BUF(5): A/L(j+1,j).
+    // Per column: POTRF on warps 0-6 while warp 7 raises the release flag of
+    // the previous sub-diagonal tile and prefetches (cp.async) the helpers'
+    // partials A(j+1,j) and A(j+1,j+1); TRSM on all warps (warp 7 raises
+    // L_jj's flag in a solve phase); last update of A(j+1,j+1) on warps 0-6
+    // while warp 7 raises L(j+1,j)'s flag.
+    double* Lnext = smem + 5 * (T * LDS);
+    int first_bad = -1;
+    int* pending = nullptr;  // (warp 7) flag of a stored tile not yet released
+    for (int j = 0; j < ntc; ++j) {
+      double* Sd = smem + (j & 1) * (T * LDS);
+      double* Snext = smem + ((j + 1) & 1) * (T * LDS);
+      const int cv = min(T, f - j * T), rv = min(T, f + 1 - j * T);
+      const bool has_sub = j + 1 < ntr, has_next = j + 1 < ntc;
+      int* const fl_sub = &F.part[tidx(j + 1, j)];
+      int* const fl_next = &F.part[tidx(j + 1, j + 1)];
+      PROF_STAMP(j, 0);
+      if (j == 0) {
+        gather_tile(Sd, G, ldg, cvec, Fidx, f, 0, 0);
+        csync();
+      }
+      // (j > 0: Sd holds A_jj fully updated at the end of the previous column)
+      if ((tid >> 5) == 7) {
+        // ---- warp 7: release the pending flag, then prefetch both partials
+        const int lane = tid & 31;
+        if (pending != nullptr && lane == 0) {
+          st_release(pending, epoch);
+        }
+        int want = (has_sub ? 1 : 0) | (has_next ? 2 : 0);
+        while (want) {
+          int ok = 0;
+          if (lane == 0) {
+            if ((want & 1) && ld_acquire(fl_sub) == epoch) ok |= 1;
+            if ((want & 2) && ld_acquire(fl_next) == epoch) ok |= 2;
+          }
+          ok = __shfl_sync(kFull, ok, 0);
+          if (ok & 1) {
+            const double* src = Lt + (size_t)tidx(j + 1, j) * T * T;
+            for (int e = lane; e < T * T / 2; e += 32)
+              cp_async16(Lnext + ((2 * e) / T) * LDS + (2 * e) % T, src + 2 * e);
+          }
+          if (ok & 2) {
+            const double* src = Lt + (size_t)tidx(j + 1, j + 1) * T * T;
+            for (int e = lane; e < T * T / 2; e += 32)
+              cp_async16(Snext + ((2 * e) / T) * LDS + (2 * e) % T, src + 2 * e);
+          }
+          if (ok) cp_async_commit();
+          want &= ~ok;
+          if (want) __nanosleep(64);
+        }
+        cp_async_wait<0>();
+      } else {
+        // ---- warps 0..6: L_jj = chol(A_jj), stored
+        const int bad = potrf_r8<2, 7>(Sd, rv, cv, rinv, &s_bad);
+        for (int e = tid; e < T * T; e += kThreads - 32)  // strict upper part
+          if ((e % T) > (e / T)) Sd[(e / T) * LDS + (e % T)] = 0.0;
+        if (bad >= 0 && first_bad < 0) first_bad = j * T + bad;
+        wsync<7>();
+        PROF_STAMP(j, 1);
+        {
+          double2* d2 = reinterpret_cast<double2*>(Lt + (size_t)tidx(j, j) * T * T);
+          for (int e = tid; e < T * T / 2; e += kThreads - 32) {
+            const int r = (2 * e) / T, c = (2 * e) % T;
+            d2[e] = make_double2(Sd[r * LDS + c], Sd[r * LDS + c + 1]);
+          }
+        }
+      }
+      pending = nullptr;
+      csync();  // L_jj stored; partials in smem
+      PROF_STAMP(j, 2);
+      int* const fl_jj = &F.full[tidx(j, j)];
+      if (!has_sub) {  // last column without a sub-diagonal tile
+        if (tid == 0) {
+          st_release(fl_jj, epoch);
+        }
+        break;
+      }
+      PROF_STAMP(j, 3);
+      // L(j+1,j) = A(j+1,j) L_jj^-T; warp 7 releases L_jj's flag in the second
+      // solve phase (its stores have drained by then, the fence is short)
+      const int np = (cv + 7) >> 3;
+      auto trsm_hook = [&](int p, int lane) {
+        if (p == min(1, np - 1) && lane == 0) {
+          st_release(fl_jj, epoch);
+        }
+      };
+      trsm_blocked(Lnext, Sd, rinv, cv, trsm_hook);
+      PROF_STAMP(j, 4);
+      store_tile(Lt + (size_t)tidx(j + 1, j) * T * T, Lnext);
+      csync();
+      if (has_next) {
+        // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T on warps 0-6; warp 7 releases L(j+1,j)
+        if ((tid >> 5) == 7) {
+          if ((tid & 31) == 0) {
+            st_release(&F.full[tidx(j + 1, j)], epoch);
+          }
+        } else {
+          syrk64_lower7(Snext, Lnext, tid >> 5, tid & 31);
+        }
+        csync();
+      } else {
+        pending = &F.full[tidx(j + 1, j)];
+      }
+      PROF_STAMP(j, 5);
+    }
+    if (pending != nullptr && tid == 0) {  // the last sub-diagonal tile
+      st_release(pending, epoch);
+    }
+    // NOT_PD is raised only after the whole chain ran: helpers read the status
+    // at entry, and a helper that left early must not strand the chain
+    if (tid == 0 && first_bad >= 0) {
+      if (atomicCAS(&st->status, 0, 7) == 0) st->not_pd_col = first_bad;
+    }
+    return;
+  }
+
+  // ============================== helpers
+  // queue per column j: [P(j+1,j+1)?, P(j+1,j)?, T(j+2..ntr-1, j), I(j)]
   for (;;) {
     if (tid == 0) s_task = atomicAdd(&st->tile_counter, 1);
-    __syncthreads();
+    csync();
     int t = s_task;
-    if (t >= total) break;
-    int j = 0;
-    while (t >= ntr - j) {
-      t -= ntr - j;
+    csync();
+    int j = 0, kind = -1, i = 0;
+    while (j < ntc) {
+      const int np1 = (j + 1 < ntc) ? 1 : 0;          // P(j+1,j+1)
+      const int np2 = (j + 1 < ntr) ? 1 : 0;          // P(j+1,j)
+      const int nT = max(0, ntr - (j + 2));           // T(i,j)
+      const int cnt = np1 + np2 + nT + 1;             // + I(j)
+      if (t < cnt) {
+        if (t < np1) { kind = 0; i = j + 1; }
+        else if (t < np1 + np2) { kind = 1; i = j + 1; }
+        else if (t < np1 + np2 + nT) { kind = 2; i = j + 2 + (t - np1 - np2); }
+        else { kind = 3; }
+        break;
+      }
+      t -= cnt;
       ++j;
     }
-    const int i = j + t;
-    const int rv = min(T, f + 1 - i * T);  // valid rows in this tile (incl. rhs row)
-    const int cv = min(T, f - j * T);      // valid (factored) columns
-    const int task = s_task;
-    PROF_STAMP(task, 0);
-    if (g_chol_prof != nullptr && tid == 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      g_chol_prof[task * 8 + 7] = ((unsigned long long)i << 40) | ((unsigned long long)j << 20) | smid;
-    }
-
-    // 1) gather A(i,j) = [G_FF; c_F^T] block straight from the cached Gram
-    for (int e = tid; e < T * T; e += kThreads) {
-      const int r = e / T, cc = e % T;
-      const int gi = i * T + r, gj = j * T + cc;
-      double v = 0.0;
-      if (r < rv && cc < cv && (i != j || cc <= r)) {
-        v = (gi < f) ? G[(size_t)Fidx[gi] * ldg + Fidx[gj]] : cvec[Fidx[gj]];
-      }
-      S[r * LDS + cc] = v;
-    }
-    __syncthreads();
-    PROF_STAMP(task, 1);
-
-    // 2) left-looking update S -= sum_{k<j} L(i,k) L(j,k)^T on the DMMA pipe,
-    //    operand tiles double-buffered with cp.async
-    if (j > 0) {
-      double acc[2][4][2];
-      acc_load(acc, S, lane, rb0, cb0);
-      __syncthreads();  // BUF(0) is reused as an operand buffer below
-      bool have_next = false;
-      for (int k = 0; k < j; ++k) {
-        double* LA = BUF((k & 1) ? 0 : 2);
-        double* LB = BUF((k & 1) ? 1 : 3);
-        if (!have_next) {
-          if (tid == 0) {
-            wait_flag(&flags[tidx(i, k)], epoch);
-            wait_flag(&flags[tidx(j, k)], epoch);
-          }
-          __syncthreads();
-          tile_async(LA, Lt + (size_t)tidx(i, k) * T * T);
-          tile_async(LB, Lt + (size_t)tidx(j, k) * T * T);
-          cp_async_commit();
-        }
-        // try to prefetch k+1 into the other pair if its tiles are ready
-        have_next = false;
-        if (k + 1 < j) {
-          if (tid == 0)
-            s_ready = (ld_acquire(&flags[tidx(i, k + 1)]) == epoch) &&
-                      (ld_acquire(&flags[tidx(j, k + 1)]) == epoch);
-          __syncthreads();
-          if (s_ready) {
-            tile_async(BUF((k & 1) ? 2 : 0), Lt + (size_t)tidx(i, k + 1) * T * T);
-            tile_async(BUF((k & 1) ? 3 : 1), Lt + (size_t)tidx(j, k + 1) * T * T);
-            cp_async_commit();
-            have_next = true;
-          }
-        }
-        if (have_next) cp_async_wait<1>();
-        else cp_async_wait<0>();
-        __syncthreads();
-        dmma_tile<true>(acc, LA, LB, lane, rb0, cb0);
-        __syncthreads();
-      }
-      acc_store(acc, S, lane, rb0, cb0);
-      __syncthreads();
-    }
-    PROF_STAMP(task, 2);
-
-    if (i == j) {
-      // 3a) diagonal tile: L_jj = chol(A_jj) by all 256 threads (block_potrf64,
-      //     one barrier per column), then Linv_jj = L_jj^-1 (published for the
-      //     TRSM tasks and the solve): TRTRI of the two 32-blocks by two warps,
-      //     the off-diagonal block -X22 L21 X11 by two 32^3 DMMA products.
-      double* X = BUF(1);    // inverse
-      double* X11t = BUF(2); // X11^T
-      double* Tmt = BUF(3);  // (L21 X11)^T
+    if (kind < 0) break;
+    const int cv = min(T, f - j * T);
+    if (kind == 0) {                 // P(j+1, j+1): diagonal tile, updates k < j
+      gather_tile(S, G, ldg, cvec, Fidx, f, j + 1, j + 1);
+      csync();
+      left_update(smem, S, Lt, F.full, epoch, j + 1, j + 1, j, &s_ready);
+      store_tile(Lt + (size_t)tidx(j + 1, j + 1) * T * T, S);
+      publish_flag(&F.part[tidx(j + 1, j + 1)], epoch);
+      PROF_STAMP(1000 + j + 1, 2);
+    } else if (kind == 1) {          // P(j+1, j): updates k < j (the chain does the TRSM)
+      gather_tile(S, G, ldg, cvec, Fidx, f, j + 1, j);
+      csync();
+      left_update(smem, S, Lt, F.full, epoch, j + 1, j, j, &s_ready);
+      PROF_STAMP(1000 + j, 4);
+      store_tile(Lt + (size_t)tidx(j + 1, j) * T * T, S);
+      publish_flag(&F.part[tidx(j + 1, j)], epoch);
+      PROF_STAMP(1000 + j, 0);
+    } else if (kind == 2) {          // T(i, j): updates k < j, then TRSM with L_jj
+      gather_tile(S, G, ldg, cvec, Fidx, f, i, j);
+      csync();
+      left_update(smem, S, Lt, F.full, epoch, i, j, j, &s_ready);
+      double* LB = smem + T * LDS;
+      if (tid == 0) wait_flag(&F.full[tidx(j, j)], epoch);
+      csync();
+      load_tile(LB, Lt + (size_t)tidx(j, j) * T * T);
+      csync();
+      diag_recip(LB, rinv, cv);
+      csync();
+      trsm_blocked(S, LB, rinv, cv);
+      store_tile(Lt + (size_t)tidx(i, j) * T * T, S);
+      publish_flag(&F.full[tidx(i, j)], epoch);
+      if (i == j + 2) PROF_STAMP(1000 + j + 1, 1);
+    } else {                         // I(j): Linv_jj for the back substitution
+      double* X = smem + T * LDS;
+      double* X11t = smem + 2 * T * LDS;
+      double* Tmt = smem + 3 * T * LDS;
+      const int lane = tid & 31, w = tid >> 5;
+      if (tid == 0) wait_flag(&F.full[tidx(j, j)], epoch);
+      csync();
+      load_tile(S, Lt + (size_t)tidx(j, j) * T * T);
+      csync();
+      diag_recip(S, rinv, cv);
+      csync();
       const int n1 = min(32, cv), n2 = cv - 32;
-      const int bad = potrf64_panel8(S, rv, cv, rinv, &s_bad);
-      for (int e = tid; e < T * T; e += kThreads)  // strict upper part
-        if ((e % T) > (e / T)) S[(e / T) * LDS + (e % T)] = 0.0;
-      __syncthreads();
       if (w == 0) {
         warp_trtri32(S, rinv, n1, lane, X, X11t);
       } else if (w == 1) {
-        if (n2 > 0) {
-          warp_trtri32(S + 32 * LDS + 32, rinv + 32, n2, lane, X + 32 * LDS + 32, nullptr);
-        } else {
+        if (n2 > 0) warp_trtri32(S + 32 * LDS + 32, rinv + 32, n2, lane, X + 32 * LDS + 32, nullptr);
+        else
           for (int r = 0; r < 32; ++r) X[(32 + r) * LDS + 32 + lane] = 0.0;
-        }
       }
-      __syncthreads();
-      if (w < 4) {  // Tm = L21 X11 (rows 32.., stored transposed)
+      csync();
+      if (w < 4) {  // Tm = L21 X11 (stored transposed)
         double acc[4][2] = {};
         dmma32(acc, S + 32 * LDS, X11t, lane, w);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int v = 0; v < 2; ++v)
-            Tmt[(8 * q + 2 * (lane & 3) + v) * LDS + 8 * w + (lane >> 2)] = acc[q][v];
+          for (int v = 0; v < 2; ++v) Tmt[(8 * q + 2 * (lane & 3) + v) * LDS + 8 * w + (lane >> 2)] = acc[q][v];
       }
-      __syncthreads();
+      csync();
       if (w < 4) {  // Linv21 = -X22 Tm
         double acc[4][2] = {};
         dmma32(acc, X + 32 * LDS + 32, Tmt, lane, w);
@@ -525,34 +784,11 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       } else {
         for (int e = tid - 128; e < 32 * 32; e += 128) X[(e >> 5) * LDS + 32 + (e & 31)] = 0.0;
       }
-      __syncthreads();
-      if (tid == 0 && bad >= 0) {
-        if (atomicCAS(&st->status, 0, 7) == 0) st->not_pd_col = j * T + bad;
-      }
+      csync();
       store_tile(Linv + (size_t)j * T * T, X);
-    } else {
-      // 3b) TRSM as a product with the inverse diagonal tile: S <- S Linv_jj^T
-      double* LB = BUF(1);
-      if (tid == 0) wait_flag(&flags[tidx(j, j)], epoch);
-      __syncthreads();
-      PROF_STAMP(task, 3);
-      load_tile(LB, Linv + (size_t)j * T * T);
-      __syncthreads();
-      double acc[2][4][2] = {};
-      dmma_tile<false>(acc, S, LB, lane, rb0, cb0);
-      __syncthreads();
-      acc_store(acc, S, lane, rb0, cb0);
-      __syncthreads();
+      publish_flag(&F.inv[j], epoch);
     }
-    PROF_STAMP(task, 4);
-    // 4) publish
-    store_tile(Lt + (size_t)tidx(i, j) * T * T, S);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(&flags[tidx(i, j)], epoch);
-    PROF_STAMP(task, 5);
   }
-#undef BUF
 }
 
 cudaError_t chol_debug_set_profile(unsigned long long* p) {
@@ -659,19 +895,20 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
   // grid sized for the largest possible DAG; tasks are claimed dynamically
-  const int tasks = tri_tiles(n);
-  int grid = sm_count;  // 136 KB smem per CTA: one persistent CTA per SM
+  const int tasks = tri_tiles(n) + (n + 1 + T - 1) / T + 1;  // helper tasks + the chain
+  int grid = sm_count;  // ~204 KB smem per CTA: one persistent CTA per SM
   if (grid > tasks) grid = tasks;
+  if (grid < 2) grid = 2;
   double* Linv = Lt + (size_t)tri_tiles(n) * T * T;
   chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, Linv,
-                                                                          flags, st);
+                                                                          flags, tri_tiles(n), st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
                                   int sm_count, cudaStream_t s) {
   const int ntr = (n + 1 + T - 1) / T;
-  int* xflags = flags + tri_tiles(n);
+  int* xflags = flags + 2 * tri_tiles(n) + (n + 1 + T - 1) / T;
   const double* Linv = Lt + (size_t)tri_tiles(n) * T * T;
   const int g2 = ntr < sm_count ? ntr : sm_count;
   cudaError_t e = set_attrs();

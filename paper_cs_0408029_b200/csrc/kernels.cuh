@@ -54,6 +54,7 @@ cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const 
 
 // ---- a5/a6 Cholesky + solves (cholesky.cu) -------------------------------
 size_t chol_tile_count(int n);
+size_t chol_flag_count(int n);
 cudaError_t chol_debug_set_profile(unsigned long long* p);  // tiles needed for |F| <= n (bordered, lower)
 // Factor the bordered matrix [[G_FF, .], [c_F^T, .]] (gathered from G via
 // Fidx) into tiles Lt, then back-substitute L^T x_F = z.  f read from st.

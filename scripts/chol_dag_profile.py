@@ -42,15 +42,27 @@ for rep in range(3):
     torch.cuda.synchronize()
     P.lib.nnls_debug_chol_profile(C.c_void_p(0))
 print("step_normal_solve ms", t0.elapsed_time(t1))
-p = prof.cpu().numpy().reshape(-1, 8)
+allp = prof.cpu().numpy().reshape(-1, 8)
+hp = allp[1000:1200]
+p = allp[:1000]
 p = p[p[:, 0] > 0]
 base = p[:, 0].min()
-print(" task   i   j  sm    start gathered  updated  Ljj-rdy factored published (us)")
-for t, r in enumerate(p):
-    meta = int(r[7])
-    i, j, sm = meta >> 40, (meta >> 20) & 0xFFFFF, meta & 0xFFFFF
-
+# chain CTA: one row per tile column j
+print("   j    start  factored  Ljj-stored  sub-ready  trsm-done  end (us)")
+for j, r in enumerate(p):
+    v = [(x - base) / 1e3 if x > 0 else float("nan") for x in r[:6]]
+    print(f"{j:4d} " + " ".join(f"{x:9.1f}" for x in v))
+if len(p) > 1:
+    d = np.diff(p[:, 0]) / 1e3
+    print("per-column period us: mean %.2f  min %.2f  max %.2f" % (d.mean(), d.min(), d.max()))
+    q = p[:-1]
+    print("potrf %.2f  store Ljj %.2f  wait sub %.2f  trsm(+next update) %.2f  store sub %.2f" % (
+        ((q[:, 1] - q[:, 0]) / 1e3).mean(), ((q[:, 2] - q[:, 1]) / 1e3).mean(),
+        ((q[:, 3] - q[:, 2]) / 1e3).mean(), ((q[:, 4] - q[:, 3]) / 1e3).mean(), ((q[:, 5] - q[:, 4]) / 1e3).mean()))
+print("helpers, per column j (us, same base): P(j+1,j) last-update-start / published, T(j+1,j-1) published, P(j+1,j+1)... ")
+for j in range(len(p)):
+    h = hp[j]
     def us(x):
         return (x - base) / 1e3 if x > 0 else float("nan")
-    print(f"{t:5d} {i:3d} {j:3d} {sm:3d} {us(r[0]):8.1f} {us(r[1]):8.1f} {us(r[2]):8.1f} "
-          f"{us(r[3]):8.1f} {us(r[4]):8.1f} {us(r[5]):9.1f}")
+    print(f"{j:4d}  P(j+1,j) upd-done {us(h[4]):8.1f} pub {us(h[0]):8.1f} | T(j+1,j-1) pub {us(h[1]):8.1f} | "
+          f"P(j,j) pub {us(h[2]):8.1f} | chain needs sub at {us(p[j][2]):8.1f}")
