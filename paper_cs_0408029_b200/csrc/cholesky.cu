@@ -393,8 +393,8 @@ __device__ __forceinline__ void trsm_blocked(double* __restrict__ X, const doubl
     csync();
     if (p + 1 < np) {  // X(rows of warp w, J) -= X(., panel) L(J, panel)^T for J in (p, np)
       strip8_gemm(X, X, L, c0, 8 * w, p + 1, np, lane);
+      csync();
     }
-    csync();
   }
 }
 
@@ -456,6 +456,31 @@ __device__ __forceinline__ void dmma32(double (&acc)[4][2], const double* __rest
       dmma8x8x4(acc[q][0], acc[q][1], av, bv);
     }
   }
+}
+
+// Bulk (async-proxy) store of a smem tile (stride LDS) to a dense T x T
+// global tile: 64 row copies of 512 B issued by one thread, completed later
+// by bulk_store_release() of the same thread, so the chain never waits on
+// them.
+// The smem rows must have been made visible to the async proxy
+// (fence_proxy_async_smem() by the writers, then a barrier).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store_tile(double* __restrict__ dst, const double* __restrict__ src) {
+  for (int r = 0; r < T; ++r) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(src + r * LDS);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst + r * T), "r"(sa),
+                 "n"(T * 8)
+                 : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+// wait for this thread's bulk stores, then release the flag (lane 0 calls)
+__device__ __forceinline__ void bulk_store_release(int* flag, int epoch) {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  st_release(flag, epoch);
 }
 
 // ---------------------------------------------------------------------------
@@ -598,9 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       if ((tid >> 5) == 7) {
         // ---- warp 7: release the pending flag, then prefetch both partials
         const int lane = tid & 31;
-        if (pending != nullptr && lane == 0) {
-          st_release(pending, epoch);
-        }
+        if (pending != nullptr && lane == 0) bulk_store_release(pending, epoch);
         int want = (has_sub ? 1 : 0) | (has_next ? 2 : 0);
         while (want) {
           int ok = 0;
@@ -632,22 +655,15 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
         if (bad >= 0 && first_bad < 0) first_bad = j * T + bad;
         wsync<7>();
         PROF_STAMP(j, 1);
-        {
-          double2* d2 = reinterpret_cast<double2*>(Lt + (size_t)tidx(j, j) * T * T);
-          for (int e = tid; e < T * T / 2; e += kThreads - 32) {
-            const int r = (2 * e) / T, c = (2 * e) % T;
-            d2[e] = make_double2(Sd[r * LDS + c], Sd[r * LDS + c + 1]);
-          }
-        }
+        fence_proxy_async_smem();  // L_jj (Sd) -> the bulk store below
       }
       pending = nullptr;
-      csync();  // L_jj stored; partials in smem
+      csync();  // L_jj factored; partials in smem
+      if ((tid >> 5) == 7 && (tid & 31) == 0) bulk_store_tile(Lt + (size_t)tidx(j, j) * T * T, Sd);
       PROF_STAMP(j, 2);
       int* const fl_jj = &F.full[tidx(j, j)];
       if (!has_sub) {  // last column without a sub-diagonal tile
-        if (tid == 0) {
-          st_release(fl_jj, epoch);
-        }
+        if (tid == kThreads - 32) bulk_store_release(fl_jj, epoch);
         break;
       }
       PROF_STAMP(j, 3);
@@ -655,20 +671,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       // solve phase (its stores have drained by then, the fence is short)
       const int np = (cv + 7) >> 3;
       auto trsm_hook = [&](int p, int lane) {
-        if (p == min(1, np - 1) && lane == 0) {
-          st_release(fl_jj, epoch);
-        }
+        if (p == min(1, np - 1) && lane == 0) bulk_store_release(fl_jj, epoch);
       };
       trsm_blocked(Lnext, Sd, rinv, cv, trsm_hook);
       PROF_STAMP(j, 4);
-      store_tile(Lt + (size_t)tidx(j + 1, j) * T * T, Lnext);
+      fence_proxy_async_smem();  // L(j+1,j) (Lnext) -> the bulk store
       csync();
+      if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j + 1, j) * T * T, Lnext);
       if (has_next) {
         // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T on warps 0-6; warp 7 releases L(j+1,j)
         if ((tid >> 5) == 7) {
-          if ((tid & 31) == 0) {
-            st_release(&F.full[tidx(j + 1, j)], epoch);
-          }
+          if ((tid & 31) == 0) bulk_store_release(&F.full[tidx(j + 1, j)], epoch);
         } else {
           syrk64_lower7(Snext, Lnext, tid >> 5, tid & 31);
         }
@@ -678,9 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       }
       PROF_STAMP(j, 5);
     }
-    if (pending != nullptr && tid == 0) {  // the last sub-diagonal tile
-      st_release(pending, epoch);
-    }
+    if (pending != nullptr && tid == kThreads - 32) bulk_store_release(pending, epoch);  // last sub tile
     // NOT_PD is raised only after the whole chain ran: helpers read the status
     // at entry, and a helper that left early must not strand the chain
     if (tid == 0 && first_bad >= 0) {

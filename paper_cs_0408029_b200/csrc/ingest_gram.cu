@@ -203,47 +203,89 @@ __global__ void __launch_bounds__(256) gram_kernel(
     const double* __restrict__ vals, const int32_t* __restrict__ colptr,
     const int32_t* __restrict__ rowind, const double* __restrict__ cvals,
     const double* __restrict__ b, int row_begin, int row_end, double* __restrict__ G, int ldg,
-    double* __restrict__ c) {
+    double* __restrict__ c, int chunk) {
+  // work item = (G row i, column chunk [j0, j0 + chunk)); the chunk width
+  // bounds the per-warp smem accumulator so that many warps per SM hide the
+  // L2 latency of the A-row gathers.  Each entry still sums its products in
+  // increasing row order r.
   extern __shared__ double acc_all[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
-  double* acc = acc_all + (size_t)wid * n;
-  for (int j = lane; j < n; j += 32) acc[j] = 0.0;
+  double* acc = acc_all + (size_t)wid * chunk;
+  for (int j = lane; j < chunk; j += 32) acc[j] = 0.0;
   __syncwarp();
   const int total_warps = gridDim.x * wpb;
-  for (int i = blockIdx.x * wpb + wid; i < n; i += total_warps) {
+  const int nchunk = (n + chunk - 1) / chunk;
+  constexpr int U = 8;  // A rows whose (j, a_rj) are in flight together (hides the L2 latency)
+  for (int item = blockIdx.x * wpb + wid; item < n * nchunk; item += total_warps) {
+    const int i = item / nchunk, j0 = (item % nchunk) * chunk;
+    const int jw = min(chunk, n - j0);
     const int e0 = colptr[i], e1 = colptr[i + 1];
     double ci = 0.0;
     for (int eb = e0; eb < e1; eb += 32) {
-      // prefetch 32 (row, value, row extent) tuples of column i
+      // prefetch 32 (row, value, row extent, b_r) tuples of column i
       int my_r = 0, my_lo = 0, my_hi = 0;
-      double my_a = 0.0;
+      double my_a = 0.0, my_b = 0.0;
       if (eb + lane < e1) {
         my_r = rowind[eb + lane];
         my_a = cvals[eb + lane];
         if (my_r >= row_begin && my_r < row_end) {
           my_lo = rowptr[my_r];
           my_hi = rowptr[my_r + 1];
+          my_b = b[my_r];
         }
       }
       const int cnt = min(32, e1 - eb);
-      for (int q = 0; q < cnt; ++q) {
-        const int r = __shfl_sync(kFull, my_r, q);
-        const double a = __shfl_sync(kFull, my_a, q);
-        const int lo = __shfl_sync(kFull, my_lo, q);
-        const int hi = __shfl_sync(kFull, my_hi, q);
-        if (lo == hi) continue;  // row outside [row_begin,row_end) or empty
-        if (lane == 0) ci = __dadd_rn(ci, __dmul_rn(a, b[r]));
-        for (int t = lo + lane; t < hi; t += 32) {
-          const int j = colind[t];
-          acc[j] = __dadd_rn(acc[j], __dmul_rn(a, vals[t]));
+      for (int q0 = 0; q0 < cnt; q0 += U) {
+        // gather: the first 64 entries of U rows (2 per lane), all loads in flight
+        int jj[U][2];
+        double av[U], vv[U][2];
+        int lo_[U], hi_[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = min(q0 + u, cnt - 1);
+          lo_[u] = __shfl_sync(kFull, my_lo, q);
+          hi_[u] = (q0 + u < cnt) ? __shfl_sync(kFull, my_hi, q) : lo_[u];
+          av[u] = __shfl_sync(kFull, my_a, q);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int t = lo_[u] + lane + 32 * h;
+            jj[u][h] = -1;
+            vv[u][h] = 0.0;
+            if (t < hi_[u]) {
+              jj[u][h] = colind[t];
+              vv[u][h] = vals[t];
+            }
+          }
         }
-        __syncwarp();
+        // apply in increasing row order (bit-identical to the sequential sum)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (q0 + u < cnt) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const unsigned jl = (unsigned)(jj[u][h] - j0);  // -1 (empty) wraps and is skipped
+              if (jl < (unsigned)jw) acc[jl] = __dadd_rn(acc[jl], __dmul_rn(av[u], vv[u][h]));
+            }
+            for (int t = lo_[u] + 64 + lane; t < hi_[u]; t += 32) {  // rows longer than 64
+              const unsigned jl = (unsigned)(colind[t] - j0);
+              if (jl < (unsigned)jw) acc[jl] = __dadd_rn(acc[jl], __dmul_rn(av[u], vals[t]));
+            }
+            __syncwarp();
+          }
+        }
+      }
+      // c_i = sum_r a_ri b_r in increasing r (lane 0, values already in registers)
+      for (int q = 0; q < cnt && j0 == 0; ++q) {
+        const double a = __shfl_sync(kFull, my_a, q);
+        const double bb = __shfl_sync(kFull, my_b, q);
+        const int lo = __shfl_sync(kFull, my_lo, q), hi = __shfl_sync(kFull, my_hi, q);
+        if (lane == 0 && hi > lo) ci = __dadd_rn(ci, __dmul_rn(a, bb));
       }
     }
-    if (lane == 0) c[i] = ci;
-    double* Gi = G + (size_t)i * ldg;
-    for (int j = lane; j < n; j += 32) {
+    if (lane == 0 && j0 == 0) c[i] = ci;
+    double* Gi = G + (size_t)i * ldg + j0;
+    for (int j = lane; j < jw; j += 32) {
       Gi[j] = acc[j];
       acc[j] = 0.0;
     }
@@ -256,28 +298,30 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
                         const double* cvals, const double* b, int row_begin, int row_end,
                         double* G, int ldg, double* c, int sm_count, cudaStream_t s) {
   (void)m;
-  const size_t per_warp = sizeof(double) * (size_t)n;
-  const size_t smem_cap = 200 * 1024;
-  if (per_warp > smem_cap) return cudaErrorInvalidValue;
-  int wpb = (int)(smem_cap / per_warp);
+  // One chunk = the whole row when it fits (measured: splitting a row into
+  // column chunks multiplies the A-row gathers and is slower at config 2).
+  const int chunk = n < 1 ? 1 : (n <= 25600 ? n : 25600);
+  int wpb = (int)((200 * 1024) / (sizeof(double) * (size_t)chunk));
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
-  const size_t smem = per_warp * wpb;
+  const size_t smem = sizeof(double) * (size_t)chunk * wpb;
   static bool attr = false;  // once, at the maximum (a driver round trip per call otherwise)
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_cap);
+                                         (int)(200 * 1024));
     if (e != cudaSuccess) return e;
     attr = true;
   }
   int per_sm = (int)(220 * 1024 / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
-  if (per_sm > 8) per_sm = 8;
-  int blocks = (n + wpb - 1) / wpb;
-  if (blocks > sm_count * per_sm) blocks = sm_count * per_sm;
+  if (per_sm * wpb > 16) per_sm = 16 / wpb;  // ~126 registers: at most 16 warps per SM
+  if (per_sm < 1) per_sm = 1;
+  const long long items = (long long)n * ((n + chunk - 1) / chunk);
+  long long blocks = (items + wpb - 1) / wpb;
+  if (blocks > (long long)sm_count * per_sm) blocks = (long long)sm_count * per_sm;
   if (blocks < 1) blocks = 1;
-  gram_kernel<<<blocks, wpb * 32, smem, s>>>(n, rowptr, colind, vals, colptr, rowind, cvals, b,
-                                            row_begin, row_end, G, ldg, c);
+  gram_kernel<<<(int)blocks, wpb * 32, smem, s>>>(n, rowptr, colind, vals, colptr, rowind, cvals, b,
+                                                 row_begin, row_end, G, ldg, c, chunk);
   return cudaGetLastError();
 }
 
