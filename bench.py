@@ -152,7 +152,8 @@ def load_peaks():
 
 
 def load_traffic():
-    """DRAM bytes per launch from a committed `ncu --set full` capture."""
+    """DRAM bytes per launch from committed `ncu --set full` captures, keyed by
+    config then phase (profiles/ncu_traffic.json); absent -> null."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
         try:
@@ -380,7 +381,7 @@ def run_ours(args):
                        "algorithmic_per_launch": work / launches,
                        "avg_launch_ms": round(phases[dom][0] / launches, 5),
                        "share_of_step": round(phases[dom][0] / max(instr_ms, 1e-9), 4),
-                       "traffic": traffic.get(dom, {}).get("dram_bytes_per_launch")}
+                       "traffic": traffic.get("config%d" % args.config, {}).get(dom, {}).get("dram_bytes_per_launch")}
     if e2e_ms is not None:
         h2d = sum(int(v.nbytes) for v in host.values())
         out["e2e"] = {"value": round(units / (e2e_ms / 1e3), 3), "unit": "solves/s",
