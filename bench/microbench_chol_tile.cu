@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256, 1) tile_bench(double* out, long long* cyc
   t[2] = clock64();
   for (int rep = 0; rep < reps; ++rep) { copy_in(S, B, 2 * T); potrf_r8<2>(S, 64, 64, rinv, &sbad); __syncthreads(); }
   t[3] = clock64();
-  for (int rep = 0; rep < reps; ++rep) { copy_in(S, B, 2 * T); potrf_r8<4>(S, 128, 64, rinv, &sbad); __syncthreads(); }
+  for (int rep = 0; rep < reps; ++rep) { copy_in(S, B, 2 * T); potrf_r8<1, 8, true>(S, 64, 64, rinv, &sbad); __syncthreads(); }
   t[4] = clock64();
   for (int rep = 0; rep < reps; ++rep) { copy_in(S, B, 2 * T); trsm_rows(S, L, rinv, 64); __syncthreads(); }
   t[5] = clock64();
@@ -160,9 +160,7 @@ __global__ void __launch_bounds__(256, 1) tile_bench(double* out, long long* cyc
   t[7] = clock64();
   for (int rep = 0; rep < reps; ++rep) { copy_in(S, B, 2 * T); trsm_blocked(S, L, rinv, 64); __syncthreads(); }
   t[8] = clock64();
-  for (int rep = 0; rep < reps; ++rep) { copy_in(S, B, 2 * T); trsm_blocked(S, L, rinv, 64, S + T * LDS); __syncthreads(); }
-  long long t9 = clock64();
-  if (tid == 0) out[302] = (double)((t9 - t[8]) / reps - (t[1] - t[0]) / reps);
+
   if (tid == 0) {
     const long long cp = (t[1] - t[0]) / reps;
     cyc[0] = cp;
@@ -197,11 +195,11 @@ __global__ void __launch_bounds__(256, 1) stamp_run(double* out) {
   long long t0 = clock64();
   int bad = 0;
   if (tid < 32)
-    for (int p = 0; p < 8; ++p) bad += panel_factor8<2, true>(S, 8 * p, 64, 64, rinv, tid & 31);
+    for (int p = 0; p < 8; ++p) bad += panel_factor8<2, true>(S, 8 * p, 8 * p, 64, 64, rinv, tid & 31, true);
   __syncthreads();
   long long t1 = clock64();
   if (tid < 32)
-    for (int p = 0; p < 8; ++p) bad += panel_factor8<2, false>(S, 8 * p, 64, 61, rinv, tid & 31);
+    for (int p = 0; p < 8; ++p) bad += panel_factor8<2, false>(S, 8 * p, 8 * p, 64, 61, rinv, tid & 31, true);
   __syncthreads();
   long long t2 = clock64();
   if (tid == 0) { out[300] = (t1 - t0) / 8; out[301] = (t2 - t1) / 8; }
@@ -230,8 +228,8 @@ __device__ int potrf_dbg(double* __restrict__ S, int rv, int cv, double* __restr
       __syncthreads();
     }
     if (w == 0) {
-      const int bad = (c0 + 8 <= cv) ? panel_factor8<2, true>(S, c0, rv, cv, rinv, lane)
-                                     : panel_factor8<2, false>(S, c0, rv, cv, rinv, lane);
+      const int bad = (c0 + 8 <= cv) ? panel_factor8<2, true>(S, c0, c0, rv, cv, rinv, lane, true)
+                                     : panel_factor8<2, false>(S, c0, c0, rv, cv, rinv, lane, true);
       if (lane == 0 && bad >= 0 && *s_bad < 0) *s_bad = bad;
     }
     __syncthreads();
@@ -272,7 +270,7 @@ __global__ void __launch_bounds__(256, 1) check(double* err, int cv, int dbg) {
   potrf64_panel8(S1, 64, cv, rinv1, &sbad);
   __syncthreads();
   if (dbg == 0) potrf_r8<2>(S2, 64, cv, rinv2, &sbad);
-  else if (dbg == 1) potrf_dbg<1>(S2, 64, cv, rinv2, &sbad);
+  else if (dbg == 1) potrf_r8<1, 8, true>(S2, 64, cv, rinv2, &sbad);
   else potrf_dbg<2>(S2, 64, cv, rinv2, &sbad);
   __syncthreads();
   if (dbg == 0 && cv == 64 && tid == 0) {
@@ -330,7 +328,7 @@ int main() {
     check<<<1, 256, smem>>>(e2, 64, 1);
     check<<<1, 256, smem>>>(e2 + 3, 64, 2);
     double hh[6]; cudaMemcpy(hh, e2, 48, cudaMemcpyDeviceToHost);
-    printf("dbg1 (serialised c) resid %.2e   dbg2 (left-looking, no c) resid %.2e\n", hh[1], hh[4]);
+    printf("split potrf resid %.2e   dbg2 (left-looking, no c) resid %.2e\n", hh[1], hh[4]);
   }
   tile_bench<<<1, 256, smem>>>(out, cyc, src, 2);
   tile_bench<<<1, 256, smem>>>(out, cyc, src, 20);
@@ -339,15 +337,11 @@ int main() {
   double he[6];
   cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
   cudaMemcpy(he, err, sizeof(he), cudaMemcpyDeviceToHost);
-  printf("{\"copy128_cycles\": %lld, \"potrf64_panel8\": %lld, \"potrf_r8_64\": %lld, \"potrf_r8_128\": %lld, "
+  printf("{\"copy128_cycles\": %lld, \"potrf64_panel8\": %lld, \"potrf_r8_64\": %lld, \"potrf_r8_split64\": %lld, "
          "\"trsm_rows64\": %lld, \"dmma_update_64x64x64\": %lld, \"load_tile_L2\": %lld, \"trsm_blocked64\": %lld, "
          "\"resid_panel8\": [%.2e, %.2e], \"resid_r8\": [%.2e, %.2e], \"trsm_blocked_vs_rows\": [%.2e, %.2e], \"err\": \"%s\"}\n",
          h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], he[0], he[3], he[1], he[4], he[2], he[5],
          cudaGetErrorString(cudaGetLastError()));
-  {
-    double o; cudaMemcpy(&o, out + 302, 8, cudaMemcpyDeviceToHost);
-    printf("trsm_blocked fused with Y update: %.0f cycles\n", o);
-  }
   cudaFuncSetAttribute(stamp_run, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   stamp_run<<<1, 256, smem>>>(out);
   stamp_run<<<1, 256, smem>>>(out);

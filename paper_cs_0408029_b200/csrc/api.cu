@@ -90,6 +90,7 @@ struct nnls_handle {
   Buf mask, x, y, xF, Fidx, Gidx;         // pivot state
   Buf Lt, flags;                          // Cholesky tiles + DAG flags
   Buf U, V, W, X, R, partials, xfin;      // LSQR / report
+  Buf Fval, Fcol, Fcnt;                   // A restricted to the final F (cluster LSQR)
   Buf st, err, trace;
   size_t ntile = 0;
   int trace_cap = 0;
@@ -225,6 +226,9 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->Lt, sizeof(double) * ntile * kTile * kTile));
   CK(ensure(h->U, sizeof(double) * (size_t)m));
   CK(ensure(h->R, sizeof(double) * (size_t)m));
+  CK(ensure(h->Fval, sizeof(double) * (size_t)(nnz > 0 ? nnz : 1)));
+  CK(ensure(h->Fcol, sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1)));
+  CK(ensure(h->Fcnt, sizeof(int32_t) * (size_t)m));
   CK(ensure(h->V, sizeof(double) * (size_t)n));
   CK(ensure(h->W, sizeof(double) * (size_t)n));
   CK(ensure(h->X, sizeof(double) * (size_t)n));
@@ -476,6 +480,9 @@ LsqrArgs lsqr_args(nnls_handle* h) {
   a.G = G;
   a.ldg = h->ldg;
   a.c = G + (size_t)n * h->ldg;
+  a.Fval = P<double>(h->Fval);
+  a.Fcol = P<int32_t>(h->Fcol);
+  a.Fcnt = P<int32_t>(h->Fcnt);
   return a;
 }
 
@@ -483,7 +490,11 @@ LsqrArgs lsqr_args(nnls_handle* h) {
 // memory (configs 0, 1, 3); the full-grid cooperative kernel otherwise
 cudaError_t launch_lsqr(nnls_handle* h, cudaStream_t s) {
   const LsqrArgs a = lsqr_args(h);
-  cudaError_t e = h->no_cluster ? cudaErrorNotSupported : launch_lsqr_cluster_planned(a, h->h->plan, s);
+  cudaError_t e = cudaErrorNotSupported;
+  if (!h->no_cluster) {
+    e = launch_lsqr_compact(a, h->sms, s);
+    if (e == cudaSuccess) e = launch_lsqr_cluster_planned(a, h->h->plan, s);
+  }
   if (e == cudaErrorNotSupported) {
     cudaGetLastError();
     e = launch_lsqr_final(a, h->sms, s);
@@ -521,7 +532,8 @@ std::vector<double> graph_key(nnls_handle* h) {
                            p.lsqr_conlim, (double)p.kkt, (double)h->trace_cap, (double)h->no_cluster};
   const Buf* bufs[] = {&h->rowptr, &h->colind, &h->vals, &h->b, &h->colptr, &h->rowind, &h->cvals,
                        &h->Gc, &h->mask, &h->x, &h->y, &h->xF, &h->Fidx, &h->Gidx, &h->Lt, &h->flags,
-                       &h->U, &h->V, &h->W, &h->X, &h->R, &h->partials, &h->xfin, &h->st, &h->trace};
+                       &h->U, &h->V, &h->W, &h->X, &h->R, &h->partials, &h->xfin, &h->st, &h->trace,
+                       &h->Fval, &h->Fcol, &h->Fcnt};
   for (const Buf* b : bufs) k.push_back((double)(uintptr_t)b->p);
   return k;
 }
@@ -809,7 +821,7 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->cursor, &h->tmp_row, &h->tmp_val, &h->Gc, &h->mask, &h->x, &h->y, &h->xF,
                  &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
-                 &h->b_info_d, &h->b_x, &h->b_mask};
+                 &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt};
   for (Buf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : h->tm.pool) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);

@@ -248,8 +248,8 @@ __device__ __forceinline__ void strip8_gemm(double* __restrict__ C, const double
 // 8 columns valid (no per-column bound checks, so the column chain is one
 // straight-line block).  Returns the first bad pivot column or -1.
 template <int NR, bool FULL>
-__device__ __forceinline__ int panel_factor8(double* __restrict__ S, int c0, int rv, int cv,
-                                             double* __restrict__ rinv, int lane) {
+__device__ __forceinline__ int panel_factor8(double* __restrict__ S, int c0, int r0, int rv, int cv,
+                                             double* __restrict__ rinv, int lane, bool wr_rinv) {
   double D[8][8];
 #pragma unroll
   for (int r = 0; r < 8; ++r)
@@ -258,7 +258,7 @@ __device__ __forceinline__ int panel_factor8(double* __restrict__ S, int c0, int
   double a[NR][8];
 #pragma unroll
   for (int k = 0; k < NR; ++k) {
-    const int R = c0 + lane + 32 * k;
+    const int R = r0 + lane + 32 * k;
 #pragma unroll
     for (int c = 0; c < 8; ++c) a[k][c] = (R < rv) ? S[R * LDS + c0 + c] : 0.0;
   }
@@ -292,7 +292,7 @@ __device__ __forceinline__ int panel_factor8(double* __restrict__ S, int c0, int
   }
 #pragma unroll
   for (int k = 0; k < NR; ++k) {
-    const int R = c0 + lane + 32 * k;
+    const int R = r0 + lane + 32 * k;
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       if (R < rv && R - c0 >= c) S[R * LDS + c0 + c] = a[k][c];
@@ -319,10 +319,15 @@ __device__ __forceinline__ void wsync() {
   else asm volatile("bar.sync 2, %0;\n" ::"n"(NW * 32) : "memory");
 }
 
-template <int NR, int NW = 8>
+template <int NR, int NW = 8, bool SPLIT = false>
 __device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
                                         double* __restrict__ rinv, int* s_bad) {
   static_assert(NW == 7 || NW == 8, "potrf_r8 runs on 7 or 8 warps");
+  static_assert(!SPLIT || NR == 1, "SPLIT: two panel warps with 32 rows each");
+  // SPLIT: the panel rows are shared by warps 0 (rows c0..c0+31) and 1
+  // (c0+32..c0+63), each also factoring the 8x8 block redundantly, which
+  // halves the FP64 instructions on the column chain's warp; warps 2.. do (c).
+  constexpr int NPW = SPLIT ? 2 : 1;  // panel warps
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) *s_bad = -1;
   const int np = (cv + 7) >> 3;
@@ -335,14 +340,15 @@ __device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
       for (int I = p + w; I < nbr; I += NW) panel8_update_block(S, c0 - 8, 8 * I, c0, lane);
       wsync<NW>();
     }
-    if (w == 0) {
-      const int bad = (c0 + 8 <= cv) ? panel_factor8<NR, true>(S, c0, rv, cv, rinv, lane)
-                                     : panel_factor8<NR, false>(S, c0, rv, cv, rinv, lane);
-      if (lane == 0 && bad >= 0 && *s_bad < 0) *s_bad = bad;
+    if (w < NPW) {
+      const int r0 = c0 + 32 * w;
+      const int bad = (c0 + 8 <= cv) ? panel_factor8<NR, true>(S, c0, r0, rv, cv, rinv, lane, w == 0)
+                                     : panel_factor8<NR, false>(S, c0, r0, rv, cv, rinv, lane, w == 0);
+      if (w == 0 && lane == 0 && bad >= 0 && *s_bad < 0) *s_bad = bad;
     } else if (p > 0) {
       // (c) row strips I in [p+1, nbr) x column blocks [p+1, min(I, ncb-1)]
       const int ncb = (cv + 7) >> 3;
-      for (int I = p + w; I < nbr; I += NW - 1) {
+      for (int I = p + 1 + (w - NPW); I < nbr; I += NW - NPW) {
         const int j1 = min(I + 1, ncb);
         if (p + 1 < j1) strip8_gemm(S, S, S, c0 - 8, 8 * I, p + 1, j1, lane);
       }
@@ -649,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
         cp_async_wait<0>();
       } else {
         // ---- warps 0..6: L_jj = chol(A_jj), stored
-        const int bad = potrf_r8<2, 7>(Sd, rv, cv, rinv, &s_bad);
+        const int bad = potrf_r8<1, 7, true>(Sd, rv, cv, rinv, &s_bad);
         for (int e = tid; e < T * T; e += kThreads - 32)  // strict upper part
           if ((e % T) > (e / T)) Sd[(e / T) * LDS + (e % T)] = 0.0;
         if (bad >= 0 && first_bad < 0) first_bad = j * T + bad;

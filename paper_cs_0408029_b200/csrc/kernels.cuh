@@ -86,7 +86,11 @@ struct LsqrArgs {
   double atol, btol, conlim, tol;
   int kkt;
   const double* G; int ldg; const double* c;   // for y (report)
+  // rows of A restricted to the final F, compacted in place of each row
+  // (row r: Fcnt[r] entries from offset rowptr[r]); built by launch_lsqr_compact
+  double* Fval; int32_t* Fcol; int32_t* Fcnt;
 };
+cudaError_t launch_lsqr_compact(const LsqrArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s);
 // Cluster-resident variant for problems whose CSR + CSC slices fit in the
 // shared memory of one thread-block cluster (max_row / max_col: longest

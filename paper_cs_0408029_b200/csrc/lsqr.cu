@@ -419,6 +419,15 @@ __global__ void lsqr_plan_kernel(int m, int n, const int32_t* rowptr, const int3
 
 // debug hook: per-phase %globaltimer stamps of CTA 0 (nnls_debug_lsqr_profile)
 __device__ unsigned long long* g_lsqr_prof = nullptr;
+// setup / epilogue stamps go to row 63 (slots 0..)
+#define LQ_STAMP_SETUP(slot)                                                               \
+  do {                                                                                     \
+    if (g_lsqr_prof != nullptr && kr == 0 && threadIdx.x == 0) {                           \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_lsqr_prof[63 * 16 + (slot)] = t_;                                                  \
+    }                                                                                      \
+  } while (0)
 #define LQ_STAMP(slot)                                                                     \
   do {                                                                                     \
     if (g_lsqr_prof != nullptr && kr == 0 && threadIdx.x == 0 && itn < 64) {               \
@@ -471,8 +480,10 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   const int m = a.m, n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kCT / 32;
+  LQ_STAMP_SETUP(0);
   const ClSlices S = cl_slices(kr, C, m, n, a.rowptr, a.colptr);
   const int nrows = S.r1 - S.r0, ncols = S.j1 - S.j0;
+  LQ_STAMP_SETUP(1);
   const int gR = seg_group(nrows), gC = seg_group(ncols);
   // ---- shared memory carve-up
   double* Urep = smem;                 // m  (u replica, unnormalised)
@@ -499,11 +510,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   }
   for (int j = tid; j <= ncols; j += kCT) scp[j] = a.colptr[S.j0 + j] - S.f0;
   for (int j = tid; j < ncols; j += kCT) smk[j] = mask[S.j0 + j];
-  for (int r = tid; r < nrows; r += kCT) {  // F-entries per row
-    int cnt = 0;
-    for (int t = a.rowptr[S.r0 + r]; t < a.rowptr[S.r0 + r + 1]; ++t) cnt += mask[a.colind[t]];
-    srp[r + 1] = cnt;
-  }
+  for (int r = tid; r < nrows; r += kCT) srp[r + 1] = __ldcg(&a.Fcnt[S.r0 + r]);  // F-entries per row
   if (tid == 0) srp[0] = 0;
   __syncthreads();
   if (wid == 0) {  // inclusive scan of the row counts (one warp)
@@ -520,19 +527,16 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
     }
   }
   __syncthreads();
-  for (int r = tid; r < nrows; r += kCT) {
-    int pos = srp[r];
-    for (int t = a.rowptr[S.r0 + r]; t < a.rowptr[S.r0 + r + 1]; ++t) {
-      const int j = a.colind[t];
-      if (mask[j]) {
-        sv[pos] = a.vals[t];
-        sci[pos] = j;
-        ++pos;
-      }
+  for (int r = wid; r < nrows; r += NW) {  // copy the compacted rows (warp per row, coalesced)
+    const int pos = srp[r], cnt = srp[r + 1] - pos, base = a.rowptr[S.r0 + r];
+    for (int t = lane; t < cnt; t += 32) {
+      sv[pos + t] = __ldcg(&a.Fval[base + t]);
+      sci[pos + t] = __ldcg(&a.Fcol[base + t]);
     }
   }
   __shared__ double sc[16];  // scalars computed by warp 0, broadcast after a barrier
   __syncthreads();
+  LQ_STAMP_SETUP(2);
 
   // Cluster reductions without remote loads: every CTA reduces its values
   // block-wide and warp 0 PUSHES the block totals into slot [slot+q][kr] of
@@ -641,6 +645,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
     double pd = 0.0, px = 0.0;
     const int gCw = seg_group(ncols, kCT - 32);  // phase B runs on warps 1.. (warp 0: scalars)
     __syncthreads();
+    LQ_STAMP_SETUP(3);
     if (alpha * beta != 0.0) {
       for (;;) {
         // ---- phase A (iteration itn+1): U' = A_F v - alpha u on own rows
@@ -787,6 +792,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   }
 
   // ---- x on own columns, zeroing (c16), write out, replicate into Vrep
+  LQ_STAMP_SETUP(4);
   cl.sync();  // every CTA is done reading the replicas
   double pinf = 0.0;
   for (int j = tid; j < ncols; j += kCT) {
@@ -854,7 +860,49 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
       a.st->kkt_dot = o5[0];
     }
   }
+  LQ_STAMP_SETUP(5);
   cl.sync();  // keep every CTA's shared memory alive until remote reads finish
+}
+
+// A restricted to the final F, row by row (warp per row, ballot compaction
+// keeps the entries in column order), written in place of each row.
+__global__ void lsqr_compact_kernel(int m, const int32_t* __restrict__ rowptr,
+                                    const int32_t* __restrict__ colind, const double* __restrict__ vals,
+                                    const uint8_t* __restrict__ mask, double* __restrict__ Fval,
+                                    int32_t* __restrict__ Fcol, int32_t* __restrict__ Fcnt) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
+    const int t0 = rowptr[r], t1 = rowptr[r + 1];
+    int cnt = 0;
+    for (int tb = t0; tb < t1; tb += 32) {
+      const int t = tb + lane;
+      int j = 0;
+      double v = 0.0;
+      bool keep = false;
+      if (t < t1) {
+        j = colind[t];
+        v = vals[t];
+        keep = mask[j] != 0;
+      }
+      const unsigned bal = __ballot_sync(kFull, keep);
+      if (keep) {
+        const int pos = t0 + cnt + __popc(bal & ((1u << lane) - 1u));
+        Fval[pos] = v;
+        Fcol[pos] = j;
+      }
+      cnt += __popc(bal);
+    }
+    if (lane == 0) Fcnt[r] = cnt;
+  }
+}
+
+cudaError_t launch_lsqr_compact(const LsqrArgs& a, int sm_count, cudaStream_t s) {
+  int blocks = (a.m + 7) / 8;
+  if (blocks > sm_count * 8) blocks = sm_count * 8;
+  if (blocks < 1) blocks = 1;
+  lsqr_compact_kernel<<<blocks, 256, 0, s>>>(a.m, a.rowptr, a.colind, a.vals, a.mask, a.Fval, a.Fcol, a.Fcnt);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_lsqr_plan(int m, int n, const int32_t* rowptr, const int32_t* colptr, int* out,

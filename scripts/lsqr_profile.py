@@ -47,3 +47,8 @@ for k, v in d.items():
         print(f"{k:22s} {np.mean(v):9.0f} ns")
         tot += np.mean(v)
 print(f"{'per iteration':22s} {tot:9.0f} ns")
+
+st = p[63]
+if st[0] > 0:
+    lab = ["entry", "slices", "staged", "loop start", "loop end", "report end"]
+    print("setup/epilogue (us from kernel entry):", ", ".join(f"{lab[i]} {(st[i] - st[0]) / 1e3:.2f}" for i in range(6) if st[i] > 0))
