@@ -104,7 +104,7 @@ struct nnls_handle {
   // batched
   bool batched = false;
   int batch = 0;
-  Buf b_nnz_off, b_info_i, b_info_d, b_x, b_mask;
+  Buf b_nnz_off, b_info_i, b_info_d, b_x, b_mask, b_colview, b_gram;
 };
 
 namespace {
@@ -793,6 +793,11 @@ NNLS_API nnls_status nnls_debug_lsqr_profile(unsigned long long* dev_buf) {
   return NNLS_OK;
 }
 
+NNLS_API nnls_status nnls_debug_batched_profile(long long* dev_buf) {
+  CK(batched_debug_set_profile(dev_buf));
+  return NNLS_OK;
+}
+
 nnls_status nnls_timing_enable(nnls_handle* h, int32_t on) {
   if (!h) return NNLS_ERR_INVALID_ARG;
   tm_flush(h);
@@ -821,7 +826,7 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->cursor, &h->tmp_row, &h->tmp_val, &h->Gc, &h->mask, &h->x, &h->y, &h->xF,
                  &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
-                 &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt};
+                 &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt, &h->b_colview, &h->b_gram};
   for (Buf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : h->tm.pool) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
@@ -1006,6 +1011,8 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
   CK(ensure(h->b, sizeof(double) * (size_t)batch * m));
   CK(ensure(h->b_x, sizeof(double) * (size_t)batch * n));
   CK(ensure(h->b_mask, (size_t)batch * n));
+  CK(ensure(h->b_colview, batched_colview_stride(n, (int)nnz_max) * (size_t)batch));
+  CK(ensure(h->b_gram, batched_gram_scratch(n, h->sms)));
   CK(ensure(h->b_info_i, sizeof(int32_t) * 8 * (size_t)batch));
   CK(ensure(h->b_info_d, sizeof(double) * 5 * (size_t)batch));
   CK(ensure(h->err, sizeof(int) * 4));
@@ -1077,7 +1084,10 @@ nnls_status nnls_solve_batched(nnls_handle* h, double* x_out, nnls_info* info_ou
   a.lsqr_mode = p.lsqr_mode;
   a.itn_limit = p.lsqr_itn_limit;
   a.kkt = p.kkt;
-  TIMED(NNLS_PH_BATCHED, 1, launch_batched_nnz(a, h->ldg, h->sms, s));
+  a.colview = P<uint8_t>(h->b_colview);
+  a.cv_stride = batched_colview_stride(h->n, h->ldg);
+  a.gram = P<double>(h->b_gram);
+  TIMED(NNLS_PH_BATCHED, 2, launch_batched_nnz(a, h->ldg, h->sms, s));
   const size_t nb = (size_t)h->batch;
   const int ibd = tm_begin(h);
   if (x_out) CK(cudaMemcpyAsync(x_out, h->b_x.p, sizeof(double) * nb * h->n, cudaMemcpyDefault, s));

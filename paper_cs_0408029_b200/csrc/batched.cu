@@ -2,19 +2,24 @@
 // per CTA, for batches of independent problems (BASELINE config 4: 65536
 // problems of 128 x 64, 20% dense; "one warp-group per problem").
 //
-// Everything for a problem lives in shared memory: CSR rows, a column view
-// (per-column row bitmasks + values in row order), the packed Gram, the
-// packed bordered factor and all vectors.  Steps, following PAPER.md:
+// Everything for a problem lives in shared memory: CSR rows (values, 16-bit
+// column indices), a column view (per-column row bitmasks for the Gram, and
+// row index / CSR position lists for A^T u), the packed Gram, the packed
+// bordered factor and all vectors.  Steps, following PAPER.md:
 //   a1 Gram  G_ij = sum over rows set in mask_i & mask_j, increasing
 //                    row order, separate multiply/add -> same terms, same
 //                    order, same roundings as the CPU oracle (bit-identical).
 //   a2 init, a3 decide/exchange, a4 compaction (ballot)
-//   a5/a6 Cholesky of the bordered [G_FF; c_F^T] (right-looking, updates
-//                    applied in increasing k with separate mul/sub -> the same
-//                    rounding sequence as the oracle's jki loop) and the back
-//                    substitution L^T x = z (sequential, oracle order)
-//   a7/a8 dual y_G = G_GF x_F - c_G (sequential over F, oracle order), zeroing
-//   a10 LSQR on the final F, block reductions for the norms
+//   a5 Cholesky of the bordered [G_FF; c_F^T], right-looking, each entry
+//                    updated in increasing k with separate mul/sub (the
+//                    oracle's jki rounding sequence: bit-identical factor);
+//                    two CTA barriers per column, no index decoding (every
+//                    thread steps through its own packed entries).
+//   a6 back substitution L^T x = z by a column sweep on one warp (lane k
+//                    owns z_k; x_i is broadcast by a shuffle)
+//   a7/a8 dual y_G = G_GF x_F - c_G (oracle order per entry), zeroing
+//   a10 LSQR on the final F on warp 0 alone: warp-shuffle norms, no
+//                    CTA barriers inside the iteration
 //   a11 report (objective, KKT of Eq. 3)
 // Problems are independent: CTAs grid-stride over the batch; no inter-CTA
 // communication.
@@ -33,43 +38,43 @@ __device__ __forceinline__ int pk(int i, int j) {  // packed lower index, any or
   return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i;
 }
 
+// Kernel A's shared memory: the phase-1 region (CSR, column view, b: load,
+// Gram) and the phase-2 region (bordered factor, pivot vectors) overlap --
+// A is not needed after the Gram (which goes to a per-CTA global scratch,
+// L2-resident) -- so ~24 KB per problem at config 4: 9 problems per SM.
 struct Lay {
-  int oG, oL, ocv, orv, ob, ou, oc, ox, oy, oxF, ov, ow, oX, ored;  // double offsets
-  int doubles;
-  int irp, ici, icm, ico, iF, iG, imk;  // int offsets (after doubles)
-  int ints;
+  // byte offsets
+  size_t c;                                         // persistent: c (n)
+  size_t rv, bb, cm, co, rp, ci, crow, cpos;        // phase 1
+  size_t L, colk, xF, x, y, Fidx, Gidx, mk;         // phase 2
   size_t bytes;
 };
-
+__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
 __host__ __device__ inline Lay layout(int m, int n, int nnz_max) {
   Lay L;
-  int o = 0;
-  L.oG = o; o += n * (n + 1) / 2;
-  L.oL = o; o += (n + 1) * (n + 2) / 2;
-  L.ocv = o; o += nnz_max;
-  L.orv = o; o += nnz_max;
-  L.ob = o; o += m;
-  L.ou = o; o += m;
-  L.oc = o; o += n;
-  L.ox = o; o += n;
-  L.oy = o; o += n;
-  L.oxF = o; o += n;
-  L.ov = o; o += n;
-  L.ow = o; o += n;
-  L.oX = o; o += n;
-  L.ored = o; o += 64;
-  L.doubles = o;
   const int W = (m + 31) / 32;
-  int q = 0;
-  L.irp = q; q += m + 1;
-  L.ici = q; q += nnz_max;
-  L.icm = q; q += n * W;
-  L.ico = q; q += n + 1;
-  L.iF = q; q += n;
-  L.iG = q; q += n;
-  L.imk = q; q += (n + 3) / 4;
-  L.ints = q + 8;
-  L.bytes = sizeof(double) * (size_t)L.doubles + sizeof(int) * (size_t)L.ints;
+  size_t o = 0;
+  L.c = o; o = al16(o + 8 * (size_t)n);
+  const size_t base = o;
+  L.rv = o; o = al16(o + 8 * (size_t)nnz_max);
+  L.bb = o; o = al16(o + 8 * (size_t)m);
+  L.cm = o; o = al16(o + 4 * (size_t)n * W);
+  L.co = o; o = al16(o + 4 * (size_t)(n + 1));
+  L.rp = o; o = al16(o + 4 * (size_t)(m + 1));
+  L.ci = o; o = al16(o + (size_t)nnz_max);
+  L.crow = o; o = al16(o + (size_t)nnz_max);
+  L.cpos = o; o = al16(o + 2 * (size_t)nnz_max);
+  const size_t end1 = o;
+  o = base;
+  L.L = o; o = al16(o + 8 * (size_t)(n + 1) * (n + 2) / 2);
+  L.colk = o; o = al16(o + 8 * (size_t)(n + 1));
+  L.xF = o; o = al16(o + 8 * (size_t)(n + 1));
+  L.x = o; o = al16(o + 8 * (size_t)n);
+  L.y = o; o = al16(o + 8 * (size_t)n);
+  L.Fidx = o; o = al16(o + 4 * (size_t)n);
+  L.Gidx = o; o = al16(o + 4 * (size_t)n);
+  L.mk = o; o = al16(o + (size_t)n);
+  L.bytes = end1 > o ? end1 : o;
   return L;
 }
 
@@ -97,36 +102,56 @@ __device__ double block_max(double v, double* red) {
   __syncthreads();
   return fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
 }
+// next packed-lower position (i, j) -> (i, j + step), wrapping rows
+__device__ __forceinline__ void pk_step(int& i, int& j, int step) {
+  j += step;
+  while (j > i) {
+    j -= i + 1;
+    ++i;
+  }
+}
 }  // namespace
 
+// Debug hook (not part of the ABI): accumulated clock64 cycles per phase of
+// CTA 0's problems, enabled by nnls_debug_batched_profile(ptr).
+__device__ long long* g_batch_prof = nullptr;
+#define BP_MARK(slot)                                                      \
+  do {                                                                     \
+    if (g_batch_prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {  \
+      const long long t_ = clock64();                                      \
+      g_batch_prof[slot] += t_ - bp_t;                                     \
+      bp_t = t_;                                                           \
+    }                                                                      \
+  } while (0)
+
 __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
+  long long bp_t = clock64();
   extern __shared__ double sm[];
+  unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
   const int m = a.m, n = a.n, W = (m + 31) / 32;
   const Lay Ly = layout(m, n, nnz_max);
-  double* G = sm + Ly.oG;
-  double* L = sm + Ly.oL;
-  double* cv = sm + Ly.ocv;
-  double* rv = sm + Ly.orv;
-  double* bb = sm + Ly.ob;
-  double* u = sm + Ly.ou;
-  double* c = sm + Ly.oc;
-  double* x = sm + Ly.ox;
-  double* y = sm + Ly.oy;
-  double* xF = sm + Ly.oxF;
-  double* v = sm + Ly.ov;
-  double* w = sm + Ly.ow;
-  double* X = sm + Ly.oX;
-  double* red = sm + Ly.ored;
-  int* ib = reinterpret_cast<int*>(sm + Ly.doubles);
-  int* rp = ib + Ly.irp;
-  int* ci = ib + Ly.ici;
-  unsigned* cm = reinterpret_cast<unsigned*>(ib + Ly.icm);
-  int* co = ib + Ly.ico;
-  int* Fidx = ib + Ly.iF;
-  int* Gidx = ib + Ly.iG;
-  uint8_t* mk = reinterpret_cast<uint8_t*>(ib + Ly.imk);
-  __shared__ int s_last, s_f;
-  __shared__ unsigned s_bF[2], s_bG[2];
+  double* c = reinterpret_cast<double*>(smb + Ly.c);
+  double* rv = reinterpret_cast<double*>(smb + Ly.rv);
+  double* bb = reinterpret_cast<double*>(smb + Ly.bb);
+  unsigned* cm = reinterpret_cast<unsigned*>(smb + Ly.cm);
+  int* co = reinterpret_cast<int*>(smb + Ly.co);
+  int* rp = reinterpret_cast<int*>(smb + Ly.rp);
+  uint8_t* ci = smb + Ly.ci;
+  uint8_t* crow = smb + Ly.crow;
+  uint16_t* cpos = reinterpret_cast<uint16_t*>(smb + Ly.cpos);
+  double* L = reinterpret_cast<double*>(smb + Ly.L);
+  double* colk = reinterpret_cast<double*>(smb + Ly.colk);
+  double* xF = reinterpret_cast<double*>(smb + Ly.xF);
+  double* x = reinterpret_cast<double*>(smb + Ly.x);
+  double* y = reinterpret_cast<double*>(smb + Ly.y);
+  int* Fidx = reinterpret_cast<int*>(smb + Ly.Fidx);
+  int* Gidx = reinterpret_cast<int*>(smb + Ly.Gidx);
+  uint8_t* mk = smb + Ly.mk;
+  // the Gram of the current problem: per-CTA global scratch (L2-resident)
+  double* G = a.gram + (size_t)blockIdx.x * ((size_t)n * (n + 1) / 2);
+  __shared__ int s_last, s_f, s_bad;
+  __shared__ unsigned s_bF[BT / 32], s_bG[BT / 32];
+  __shared__ int s_scan[BT / 32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double tol = a.tol;
 
@@ -136,23 +161,40 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
     const int nz = (int)(a.nnz_off[prob + 1] - e0);
     for (int r = tid; r <= m; r += BT) rp[r] = a.rowptr[(size_t)prob * (m + 1) + r];
     for (int e = tid; e < nz; e += BT) {
-      ci[e] = a.colind[e0 + e];
+      ci[e] = (uint8_t)a.colind[e0 + e];
       rv[e] = a.vals[e0 + e];
     }
     for (int r = tid; r < m; r += BT) bb[r] = a.b[(size_t)prob * m + r];
     for (int q = tid; q < n * W; q += BT) cm[q] = 0u;
     __syncthreads();
-    // column view: row bitmasks, counts, values in row order
+    BP_MARK(0);  // load
+    // column view: row bitmasks, counts (block scan), row lists in row order
     for (int r = tid; r < m; r += BT)
       for (int e = rp[r]; e < rp[r + 1]; ++e) atomicOr(&cm[ci[e] * W + (r >> 5)], 1u << (r & 31));
     __syncthreads();
-    if (tid == 0) {
-      int acc = 0;
-      for (int j = 0; j < n; ++j) {
+    {
+      // each thread owns a contiguous run of columns; block-wide exclusive scan
+      const int per = (n + BT - 1) / BT;
+      const int j0 = tid * per, j1 = min(n, j0 + per);
+      int run = 0;
+      for (int j = j0; j < j1; ++j)
+        for (int q = 0; q < W; ++q) run += __popc(cm[j * W + q]);
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int yv = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += yv;
+      }
+      if (lane == 31) s_scan[wid] = incl;
+      __syncthreads();
+      int base = 0;
+      for (int q = 0; q < wid; ++q) base += s_scan[q];
+      int acc = base + incl - run;
+      for (int j = j0; j < j1; ++j) {
         co[j] = acc;
         for (int q = 0; q < W; ++q) acc += __popc(cm[j * W + q]);
       }
-      co[n] = acc;
+      if (tid == BT - 1) co[n] = base + incl;
     }
     __syncthreads();
     for (int r = tid; r < m; r += BT) {
@@ -163,49 +205,65 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
         int rank = co[j];
         for (int q = 0; q < wr; ++q) rank += __popc(cm[j * W + q]);
         rank += __popc(cm[j * W + wr] & below);
-        cv[rank] = rv[e];
+        crow[rank] = (uint8_t)r;
+        cpos[rank] = (uint16_t)e;
       }
     }
     __syncthreads();
+    BP_MARK(1);  // column view
     // ---------------------------------------------------------- a1 Gram, c
-    const int npair = n * (n + 1) / 2;
-    for (int q = tid; q < npair; q += BT) {
-      int i = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
-      while (i * (i + 1) / 2 > q) --i;
-      while ((i + 1) * (i + 2) / 2 <= q) ++i;
-      const int j = q - i * (i + 1) / 2;
-      double s = 0.0;
-      int ki = co[i], kj = co[j];
-      for (int wq = 0; wq < W; ++wq) {
-        const unsigned mi = cm[i * W + wq], mj = cm[j * W + wq];
-        unsigned both = mi & mj;
-        while (both) {
-          const int bpos = __ffs(both) - 1;
-          const unsigned below = (1u << bpos) - 1u;
-          const double vi = cv[ki + __popc(mi & below)];
-          const double vj = cv[kj + __popc(mj & below)];
-          s = __dadd_rn(s, __dmul_rn(vi, vj));
-          both &= both - 1u;
+    // rows i and n-1-i are folded (i+1 + n-i = n+1 pairs per fold): the work
+    // index decodes without a square root
+    {
+      const int nf = (n + 1) / 2, np1 = n + 1;
+      for (int wk = tid; wk < nf * np1; wk += BT) {
+        const int fo = wk / np1, k = wk - fo * np1;
+        const int i1 = fo, i2 = n - 1 - fo;
+        int i, j;
+        if (k <= i1) {
+          i = i1;
+          j = k;
+        } else {
+          if (i2 == i1) continue;  // odd n: the middle row is alone
+          i = i2;
+          j = k - i1 - 1;
         }
-        ki += __popc(mi);
-        kj += __popc(mj);
+        double sacc = 0.0;
+        int ki = co[i], kj = co[j];
+        for (int wq = 0; wq < W; ++wq) {
+          const unsigned mi = cm[i * W + wq], mj = cm[j * W + wq];
+          unsigned both = mi & mj;
+          while (both) {
+            const int bpos = __ffs(both) - 1;
+            const unsigned bl = (1u << bpos) - 1u;
+            const double vi = rv[cpos[ki + __popc(mi & bl)]];
+            const double vj = rv[cpos[kj + __popc(mj & bl)]];
+            sacc = __dadd_rn(sacc, __dmul_rn(vi, vj));
+            both &= both - 1u;
+          }
+          ki += __popc(mi);
+          kj += __popc(mj);
+        }
+        G[i * (i + 1) / 2 + j] = sacc;
       }
-      G[q] = s;
     }
     for (int j = tid; j < n; j += BT) {
-      double s = 0.0;
-      int k = co[j];
-      for (int wq = 0; wq < W; ++wq) {
-        unsigned bits = cm[j * W + wq];
-        while (bits) {
-          const int r = wq * 32 + __ffs(bits) - 1;
-          s = __dadd_rn(s, __dmul_rn(cv[k++], bb[r]));
-          bits &= bits - 1u;
-        }
+      double sacc = 0.0;
+      for (int t = co[j]; t < co[j + 1]; ++t) sacc = __dadd_rn(sacc, __dmul_rn(rv[cpos[t]], bb[crow[t]]));
+      c[j] = sacc;
+    }
+    // the column view goes to kernel B now (phase 2 overwrites it)
+    {
+      int32_t* cvw = reinterpret_cast<int32_t*>(a.colview + (size_t)prob * a.cv_stride);
+      uint16_t* cvr = reinterpret_cast<uint16_t*>(cvw + (n + 1));
+      for (int j = tid; j <= n; j += BT) cvw[j] = co[j];
+      for (int t = tid; t < nz; t += BT) {
+        cvr[t] = crow[t];
+        cvr[nnz_max + t] = cpos[t];
       }
-      c[j] = s;
     }
     __syncthreads();
+    BP_MARK(2);  // Gram
     // ---------------------------------------------------------- a2 init
     for (int j = tid; j < n; j += BT) {
       mk[j] = 0;
@@ -244,76 +302,118 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
       }
       if (tid < n && ((branch == 2) ? (tid == last) : inf)) mk[tid] ^= 1;
       __syncthreads();
-      // a4 compaction (n <= 64: two warps)
+      // a4 compaction (n <= BT)
       const bool inF = (tid < n) && mk[tid];
       const bool inG = (tid < n) && !mk[tid];
       const unsigned bF = __ballot_sync(kFull, inF);
       const unsigned bG = __ballot_sync(kFull, inG);
-      if (lane == 0 && wid < 2) {
+      if (lane == 0) {
         s_bF[wid] = bF;
         s_bG[wid] = bG;
       }
       __syncthreads();
-      if (wid < 2) {
+      {
         const unsigned lt = (1u << lane) - 1u;
-        const int offF = wid == 1 ? __popc(s_bF[0]) : 0;
-        const int offG = wid == 1 ? __popc(s_bG[0]) : 0;
+        int offF = 0, offG = 0;
+        for (int q = 0; q < wid; ++q) {
+          offF += __popc(s_bF[q]);
+          offG += __popc(s_bG[q]);
+        }
         if (inF) Fidx[offF + __popc(bF & lt)] = tid;
         if (inG) Gidx[offG + __popc(bG & lt)] = tid;
       }
-      if (tid == 0) s_f = __popc(s_bF[0]) + __popc(s_bF[1]);
-      __syncthreads();
-      f = s_f;
-      // a5 Cholesky of the bordered (f+1) x (f+1) matrix, packed lower
-      const int fa = f + 1;
-      for (int q = tid; q < fa * (fa + 1) / 2; q += BT) {
-        int i = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
-        while (i * (i + 1) / 2 > q) --i;
-        while ((i + 1) * (i + 2) / 2 <= q) ++i;
-        const int j = q - i * (i + 1) / 2;
-        double val = 0.0;
-        if (j < f) val = (i < f) ? G[pk(Fidx[i], Fidx[j])] : c[Fidx[j]];
-        L[q] = val;
+      if (tid == 0) {
+        int ff = 0;
+        for (int q = 0; q < BT / 32; ++q) ff += __popc(s_bF[q]);
+        s_f = ff;
       }
       __syncthreads();
-      for (int kk = 0; kk < f; ++kk) {
-        const double d = L[pk(kk, kk)];
-        if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) {
-          if (status == 0) not_pd = kk;
+      f = s_f;
+      BP_MARK(3);  // decide + compaction
+      // a5 Cholesky of the bordered (f+1) x (f+1) matrix [G_FF; c_F^T], packed
+      // lower (no (f, f) entry)
+      const int fa = f + 1;
+      const int ne = fa * (fa + 1) / 2 - 1;  // entries (i, j), j <= i, j < f
+      {
+        int i = 0, jx = 0;
+        pk_step(i, jx, tid);
+        for (int e = tid; e < ne; e += BT) {
+          double val = (i < f) ? G[pk(Fidx[i], Fidx[jx])] : c[Fidx[jx]];
+          L[e] = val;
+          pk_step(i, jx, BT);
+        }
+      }
+      // left-looking by columns (the oracle's jki order per entry, so the
+      // factor is bit-identical): in step j the thread of row i > j finishes
+      // L(i, j) with a sequential dot in increasing k; the thread of row j+1
+      // then also finishes the next pivot L(j+1, j+1) -> one barrier per column
+      if (tid == 0) {
+        s_bad = -1;
+        if (f > 0) {
+          const double d = L[0];
+          if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) s_bad = 0;
+          L[0] = sqrt(d);
+        }
+      }
+      __syncthreads();
+      for (int jj = 0; jj < f; ++jj) {
+        const int i = jj + 1 + tid;
+        if (i <= f) {
+          const int ri = i * (i + 1) / 2, rj = jj * (jj + 1) / 2;
+          double sacc = L[ri + jj];
+          for (int k = 0; k < jj; ++k) sacc = __dsub_rn(sacc, __dmul_rn(L[ri + k], L[rj + k]));
+          sacc = sacc / L[rj + jj];
+          L[ri + jj] = sacc;
+          if (i == jj + 1 && i < f) {  // the next pivot
+            double d = L[ri + i];
+            for (int k = 0; k <= jj; ++k) d = __dsub_rn(d, __dmul_rn(L[ri + k], L[ri + k]));
+            if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) atomicMin(&s_bad, i);
+            L[ri + i] = sqrt(d);
+          }
+        }
+        __syncthreads();
+      }
+      {
+        const int bad = s_bad;
+        if (bad >= 0) {
           status = 7;
+          not_pd = bad;
         }
-        const double l = sqrt(d);
-        __syncthreads();
-        for (int i = kk + 1 + tid; i <= f; i += BT) L[pk(i, kk)] = L[pk(i, kk)] / l;
-        if (tid == 0) L[pk(kk, kk)] = l;
-        __syncthreads();
-        // trailing update, rows i in (kk, f], cols jj in (kk, min(i, f-1)]
-        const int nr = f - kk;  // rows kk+1..f
-        const int tot = nr * (nr + 1) / 2;
-        for (int q = tid; q < tot; q += BT) {
-          int ii = (int)((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
-          while (ii * (ii + 1) / 2 > q) --ii;
-          while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
-          const int jj = q - ii * (ii + 1) / 2;
-          const int i = kk + 1 + ii, j = kk + 1 + jj;
-          if (j < f) L[pk(i, j)] = __dsub_rn(L[pk(i, j)], __dmul_rn(L[pk(i, kk)], L[pk(j, kk)]));
-        }
-        __syncthreads();
       }
       if (status == 7) {
         for (int j = tid; j < n; j += BT) x[j] = 0.0;
         __syncthreads();
         break;
       }
-      // a6 back substitution L^T x_F = z (z = row f), oracle order
-      if (tid == 0) {
+      BP_MARK(4);  // gather + Cholesky
+      // a6 back substitution L^T x_F = z (z = row f): column sweep on warp 0
+      if (wid == 0) {
+        double zr[4];  // lane owns k = lane + 32 q (f <= 128)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int kq = lane + 32 * q;
+          zr[q] = kq < f ? L[f * (f + 1) / 2 + kq] : 0.0;
+        }
+        for (int i = lane; i < f; i += 32) colk[i] = 1.0 / L[i * (i + 1) / 2 + i];
+        __syncwarp();
         for (int i = f - 1; i >= 0; --i) {
-          double s = L[pk(f, i)];
-          for (int kq = i + 1; kq < f; ++kq) s = __dsub_rn(s, __dmul_rn(L[pk(kq, i)], xF[kq]));
-          xF[i] = s / L[pk(i, i)];
+          const int qi = i >> 5, li = i & 31;
+          double zi = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == qi) zi = zr[q];
+          zi = __shfl_sync(kFull, zi, li);
+          const double xi = zi * colk[i];
+          if (lane == 0) xF[i] = xi;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int kq = lane + 32 * q;
+            if (kq < i) zr[q] = __dsub_rn(zr[q], __dmul_rn(L[i * (i + 1) / 2 + kq], xi));
+          }
         }
       }
       __syncthreads();
+      BP_MARK(5);  // back substitution
       // scatter x_F, x_G = 0
       for (int aa = tid; aa < n; aa += BT) {
         if (aa < f) x[Fidx[aa]] = xF[aa];
@@ -326,9 +426,9 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
         if (mk[j]) {
           y[j] = 0.0;
         } else {
-          double s = 0.0;
-          for (int aa = 0; aa < f; ++aa) s = __dadd_rn(s, __dmul_rn(G[pk(j, Fidx[aa])], xF[aa]));
-          const double vv = s - c[j];
+          double sacc = 0.0;
+          for (int aa = 0; aa < f; ++aa) sacc = __dadd_rn(sacc, __dmul_rn(G[pk(j, Fidx[aa])], xF[aa]));
+          const double vv = sacc - c[j];
           y[j] = fabs(vv) < tol ? 0.0 : vv;
         }
       }
@@ -337,110 +437,259 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
       __syncthreads();
       ++iter;
     }
+    BP_MARK(6);  // scatter + dual (+ loop exit)
+    // ---------------------------------------------------------- hand-off
+    // the NE solution, F and the counters go to global memory with the
+    // column view; batched_lsqr_kernel (a smaller on-chip footprint, so more
+    // problems per SM) runs a10/a11
+    for (int j = tid; j < n; j += BT) {
+      a.x_out[(size_t)prob * n + j] = mk[j] ? x[j] : 0.0;
+      a.mask_out[(size_t)prob * n + j] = mk[j];
+    }
+    if (tid == 0) {
+      int32_t* ii = a.info_i + (size_t)prob * 8;
+      ii[0] = status;
+      ii[1] = iter;
+      ii[2] = singles;
+      ii[3] = f;
+      ii[7] = status == 7 ? not_pd : -1;
+    }
+    __syncthreads();
+    BP_MARK(7);  // hand-off
+    if (g_batch_prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) g_batch_prof[9] += 1;
+  }
+}
+
+// a10 LSQR on the final F and a11 report, one problem per 128-thread
+// CTA: CSR, the column view and the vectors only (~25 KB at config 4).
+struct LLay {
+  int orv, ob, ou, ox, ov, ow, oX, ored;  // double offsets
+  int doubles;
+  int irp, ico, imk, ici, icr, icx;
+  int ints;
+  size_t bytes;
+};
+__host__ __device__ inline LLay llayout(int m, int n, int nnz_max) {
+  LLay L;
+  int o = 0;
+  L.orv = o; o += nnz_max;
+  L.ob = o; o += m;
+  L.ou = o; o += m;
+  L.ox = o; o += n;
+  L.ov = o; o += n;
+  L.ow = o; o += n;
+  L.oX = o; o += n;
+  L.ored = o; o += 64;
+  L.doubles = o;
+  int q = 0;
+  L.irp = q; q += m + 1;
+  L.ico = q; q += n + 1;
+  L.imk = q; q += (n + 3) / 4;
+  L.ici = q; q += (nnz_max + 1) / 2;
+  L.icr = q; q += (nnz_max + 1) / 2;
+  L.icx = q; q += (nnz_max + 1) / 2;
+  L.ints = q + 8;
+  L.bytes = sizeof(double) * (size_t)L.doubles + sizeof(int) * (size_t)L.ints;
+  return L;
+}
+
+__global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_max) {
+  long long bp_t = clock64();
+  extern __shared__ double sm[];
+  const int m = a.m, n = a.n;
+  const LLay Ly = llayout(m, n, nnz_max);
+  double* rv = sm + Ly.orv;
+  double* bb = sm + Ly.ob;
+  double* u = sm + Ly.ou;
+  double* x = sm + Ly.ox;
+  double* v = sm + Ly.ov;
+  double* w = sm + Ly.ow;
+  double* X = sm + Ly.oX;
+  double* red = sm + Ly.ored;
+  int* ib = reinterpret_cast<int*>(sm + Ly.doubles);
+  int* rp = ib + Ly.irp;
+  int* co = ib + Ly.ico;
+  uint8_t* mk = reinterpret_cast<uint8_t*>(ib + Ly.imk);
+  uint16_t* ci = reinterpret_cast<uint16_t*>(ib + Ly.ici);
+  uint16_t* crow = reinterpret_cast<uint16_t*>(ib + Ly.icr);
+  uint16_t* cpos = reinterpret_cast<uint16_t*>(ib + Ly.icx);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double tol = a.tol;
+  for (int prob = blockIdx.x; prob < a.batch; prob += gridDim.x) {
+    const int64_t e0 = a.nnz_off[prob];
+    const int nz = (int)(a.nnz_off[prob + 1] - e0);
+    const int status = a.info_i[(size_t)prob * 8 + 0];
+    const int f = a.info_i[(size_t)prob * 8 + 3];
+    for (int r = tid; r <= m; r += BT) rp[r] = a.rowptr[(size_t)prob * (m + 1) + r];
+    for (int e = tid; e < nz; e += BT) {
+      ci[e] = (uint16_t)a.colind[e0 + e];
+      rv[e] = a.vals[e0 + e];
+    }
+    for (int r = tid; r < m; r += BT) bb[r] = a.b[(size_t)prob * m + r];
+    {
+      const int32_t* cvw = reinterpret_cast<const int32_t*>(a.colview + (size_t)prob * a.cv_stride);
+      const uint16_t* cvr = reinterpret_cast<const uint16_t*>(cvw + (n + 1));
+      for (int j = tid; j <= n; j += BT) co[j] = cvw[j];
+      for (int t = tid; t < nz; t += BT) {
+        crow[t] = cvr[t];
+        cpos[t] = cvr[nnz_max + t];
+      }
+    }
+    for (int j = tid; j < n; j += BT) {
+      mk[j] = a.mask_out[(size_t)prob * n + j];
+      x[j] = a.x_out[(size_t)prob * n + j];
+    }
+    __syncthreads();
+    BP_MARK(10);  // LSQR kernel: load
     // ---------------------------------------------------------- a10 LSQR
+    // All 4 warps.  Thread r owns row r (u), threads 2j, 2j+1 own column j
+    // (v, w, X; the pair splits A^T u).  Two CTA barriers per iteration: the
+    // norm reductions (|u|^2 | |v|^2, |d|^2, |x|^2) each end with one, and the
+    // vectors a thread reads from others were written before it; the stopping
+    // test of an iteration is evaluated after the next barrier (it needs only
+    // scalars, and x is not touched in between).
     int itn = 0, istop = 0;
     const int mode = (status == 0 && f > 0) ? a.lsqr_mode : 0;
     if (mode != 0) {
       const int itn_limit = a.itn_limit > 0 ? a.itn_limit : 4 * f;
-      for (int r = tid; r < m; r += BT) {
-        double s = 0.0;
-        if (mode == 2)
-          for (int e = rp[r]; e < rp[r + 1]; ++e)
-            if (mk[ci[e]]) s = fma(rv[e], x[ci[e]], s);
-        u[r] = bb[r] - s;
-      }
-      double pu = 0.0;
-      for (int r = tid; r < m; r += BT) pu += u[r] * u[r];
-      double beta = sqrt(block_sum(pu, red));
-      const double bnorm = beta;
-      if (beta > 0.0)
-        for (int r = tid; r < m; r += BT) u[r] /= beta;
-      __syncthreads();
-      double pv = 0.0;
-      for (int j = tid; j < n; j += BT) {
-        double s = 0.0;
-        if (mk[j] && beta > 0.0) {
-          int k = co[j];
-          for (int wq = 0; wq < W; ++wq) {
-            unsigned bits = cm[j * W + wq];
-            while (bits) {
-              const int r = wq * 32 + __ffs(bits) - 1;
-              s = fma(cv[k++], u[r], s);
-              bits &= bits - 1u;
-            }
-          }
+      int rslot = 0;  // red[] double-buffering: red[rslot*16 + 4*q + warp]
+      auto reduce3 = [&](double v0, double v1, double v2, int nv, double* out) {
+        v0 = warp_sum(v0);
+        if (nv > 1) v1 = warp_sum(v1);
+        if (nv > 2) v2 = warp_sum(v2);
+        double* rr = red + rslot * 16;
+        if (lane == 0) {
+          rr[wid] = v0;
+          if (nv > 1) rr[4 + wid] = v1;
+          if (nv > 2) rr[8 + wid] = v2;
         }
-        v[j] = s;
-        X[j] = 0.0;
-        pv += s * s;
+        __syncthreads();
+        out[0] = (rr[0] + rr[1]) + (rr[2] + rr[3]);
+        if (nv > 1) out[1] = (rr[4] + rr[5]) + (rr[6] + rr[7]);
+        if (nv > 2) out[2] = (rr[8] + rr[9]) + (rr[10] + rr[11]);
+        rslot ^= 1;
+      };
+      // row SpMV: s = A(r, :) v with 4 independent partial sums (v_G = 0)
+      auto row_dot = [&](int r, const double* vec, bool maskF) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        const int t1 = rp[r + 1];
+        int e = rp[r];
+        for (; e + 3 < t1; e += 4) {
+          const int j0 = ci[e], j1 = ci[e + 1], j2 = ci[e + 2], j3 = ci[e + 3];
+          s0 = fma(rv[e], (maskF && !mk[j0]) ? 0.0 : vec[j0], s0);
+          s1 = fma(rv[e + 1], (maskF && !mk[j1]) ? 0.0 : vec[j1], s1);
+          s2 = fma(rv[e + 2], (maskF && !mk[j2]) ? 0.0 : vec[j2], s2);
+          s3 = fma(rv[e + 3], (maskF && !mk[j3]) ? 0.0 : vec[j3], s3);
+        }
+        for (; e < t1; ++e) {
+          const int jj = ci[e];
+          s0 = fma(rv[e], (maskF && !mk[jj]) ? 0.0 : vec[jj], s0);
+        }
+        return (s0 + s1) + (s2 + s3);
+      };
+      // column SpMV half: entries t of column j with t - co[j] = half (mod 2)
+      auto col_dot = [&](int j, int half, const double* vec) {
+        double s0 = 0.0, s1 = 0.0;
+        const int t1 = co[j + 1];
+        int t = co[j] + half;
+        for (; t + 2 < t1; t += 4) {
+          s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
+          s1 = fma(rv[cpos[t + 2]], vec[crow[t + 2]], s1);
+        }
+        for (; t < t1; t += 2) s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
+        return s0 + s1;
+      };
+      const int jc = tid >> 1, half = tid & 1;  // column pair (n <= 64)
+      const bool colown = jc < n && half == 0 && mk[jc];
+      double tot[3];
+      // beta u = b - A x (mode 2) or b
+      double pu = 0.0;
+      for (int r = tid; r < m; r += BT) {
+        const double sacc = (mode == 2) ? row_dot(r, x, true) : 0.0;
+        const double uu = bb[r] - sacc;
+        u[r] = uu;
+        pu += uu * uu;
       }
-      double alpha = sqrt(block_sum(pv, red));
-      if (alpha > 0.0)
-        for (int j = tid; j < n; j += BT) v[j] /= alpha;
-      __syncthreads();
-      for (int j = tid; j < n; j += BT) w[j] = v[j];
-      __syncthreads();
+      reduce3(pu, 0.0, 0.0, 1, tot);  // B: u complete
+      double beta = sqrt(tot[0]);
+      const double bnorm = beta;
+      double ib = beta > 0.0 ? 1.0 / beta : 0.0;
+      // alpha v = A^T u
+      double pv = 0.0;
+      {
+        double sacc = 0.0;
+        if (jc < n && mk[jc] && beta > 0.0) sacc = col_dot(jc, half, u);
+        sacc += __shfl_xor_sync(kFull, sacc, 1);
+        if (half == 0 && jc < n) {
+          const double vv = mk[jc] ? sacc * ib : 0.0;
+          v[jc] = vv;
+          X[jc] = 0.0;
+          pv = vv * vv;
+        }
+      }
+      reduce3(pv, 0.0, 0.0, 1, tot);  // B: every read of u done
+      double alpha = sqrt(tot[0]);
+      const double ia0 = alpha > 0.0 ? 1.0 / alpha : 0.0;
+      for (int r = tid; r < m; r += BT) u[r] *= ib;  // own rows
+      if (half == 0 && jc < n) {
+        v[jc] *= ia0;
+        w[jc] = v[jc];
+      }
+      __syncthreads();  // v, u complete
       double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
       const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
       if (alpha * beta != 0.0) {
         while (itn < itn_limit) {
           ++itn;
+          // u' = A v - alpha u (own rows)
           pu = 0.0;
           for (int r = tid; r < m; r += BT) {
-            double s = 0.0;
-            for (int e = rp[r]; e < rp[r + 1]; ++e) s = fma(rv[e], v[ci[e]], s);  // v_G = 0
-            const double uu = s - alpha * u[r];
+            const double uu = row_dot(r, v, false) - alpha * u[r];
             u[r] = uu;
             pu += uu * uu;
           }
-          beta = sqrt(block_sum(pu, red));
+          reduce3(pu, 0.0, 0.0, 1, tot);  // B1: u' complete
+          beta = sqrt(tot[0]);
+          double alpha_new = alpha;
           if (beta > 0.0) {
-            for (int r = tid; r < m; r += BT) u[r] /= beta;
+            ib = 1.0 / beta;
             anorm = sqrt(anorm * anorm + alpha * alpha + beta * beta);
-            __syncthreads();
+            // v' = A^T u' / beta - beta v (own columns)
+            double sacc = 0.0;
+            if (jc < n && mk[jc]) sacc = col_dot(jc, half, u);
+            sacc += __shfl_xor_sync(kFull, sacc, 1);
             pv = 0.0;
-            for (int j = tid; j < n; j += BT) {
-              if (!mk[j]) continue;
-              double s = 0.0;
-              int k = co[j];
-              for (int wq = 0; wq < W; ++wq) {
-                unsigned bits = cm[j * W + wq];
-                while (bits) {
-                  const int r = wq * 32 + __ffs(bits) - 1;
-                  s = fma(cv[k++], u[r], s);
-                  bits &= bits - 1u;
-                }
-              }
-              const double vv = s - beta * v[j];
-              v[j] = vv;
-              pv += vv * vv;
+            if (colown) {
+              const double vv = sacc * ib - beta * v[jc];
+              v[jc] = vv;
+              pv = vv * vv;
             }
-            alpha = sqrt(block_sum(pv, red));
-            if (alpha > 0.0)
-              for (int j = tid; j < n; j += BT)
-                if (mk[j]) v[j] /= alpha;
+            reduce3(pv, 0.0, 0.0, 1, tot);  // B2: every read of u' done
+            alpha_new = sqrt(tot[0]);
+            for (int r = tid; r < m; r += BT) u[r] *= ib;  // own rows
+            if (alpha_new > 0.0 && colown) v[jc] *= 1.0 / alpha_new;
           }
           const double rho = sqrt(rhobar * rhobar + beta * beta);
           const double cs = rhobar / rho, sn = beta / rho;
-          const double theta = sn * alpha;
-          rhobar = -cs * alpha;
+          const double theta = sn * alpha_new;
+          rhobar = -cs * alpha_new;
           const double phi = cs * phibar;
           phibar = sn * phibar;
           const double t1 = phi / rho, t2 = -theta / rho;
-          __syncthreads();
           double pd = 0.0, px = 0.0;
-          for (int j = tid; j < n; j += BT) {
-            if (!mk[j]) continue;
-            const double ww = w[j];
-            const double d = ww / rho;
-            pd += d * d;
-            const double xx = X[j] + t1 * ww;
-            X[j] = xx;
-            w[j] = v[j] + t2 * ww;
-            px += xx * xx;
+          if (colown) {  // own column: w, x
+            const double ww = w[jc];
+            const double dd = ww / rho;
+            pd = dd * dd;
+            const double xx = X[jc] + t1 * ww;
+            X[jc] = xx;
+            w[jc] = v[jc] + t2 * ww;
+            px = xx * xx;
           }
-          ddnorm += block_sum(pd, red);
-          const double xnorm = sqrt(block_sum(px, red));
+          alpha = alpha_new;
+          reduce3(pd, px, 0.0, 2, tot);  // B3: v, w, x complete
+          ddnorm += tot[0];
+          const double xnorm = sqrt(tot[1]);
           const double acond = anorm * sqrt(ddnorm);
           const double rnorm = phibar;
           const double arnorm = alpha * fabs(sn * phi);
@@ -456,11 +705,12 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
           if (test3 <= ctol) istop = 3;
           if (test2 <= a.atol) istop = 2;
           if (test1 <= rtol) istop = 1;
-          __syncthreads();
           if (istop != 0) break;
         }
       }
+      __syncthreads();
     }
+    BP_MARK(11);  // LSQR
     // ---------------------------------------------------------- a11 output
     bool infeas = false;
     for (int j = tid; j < n; j += BT) {
@@ -473,37 +723,28 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
       if (vv < 0.0) infeas = true;
       w[j] = vv;  // final x staged in w
       a.x_out[(size_t)prob * n + j] = vv;
-      if (a.mask_out) a.mask_out[(size_t)prob * n + j] = mk[j];
     }
     const int any_infeas = __syncthreads_or(infeas);
     double obj = 0.0, mx = INFINITY, my = INFINITY, mc = 0.0, dot = 0.0;
     if (a.kkt) {
       double po = 0.0;
       for (int r = tid; r < m; r += BT) {
-        double s = 0.0;
-        for (int e = rp[r]; e < rp[r + 1]; ++e) s = fma(rv[e], w[ci[e]], s);
-        const double rr = s - bb[r];
+        double sacc = 0.0;
+        for (int e = rp[r]; e < rp[r + 1]; ++e) sacc = fma(rv[e], w[ci[e]], sacc);
+        const double rr = sacc - bb[r];
         u[r] = rr;
         po += rr * rr;
       }
       obj = block_sum(po, red);
       double lmx = INFINITY, lmy = INFINITY, lmc = 0.0, ld = 0.0;
       for (int j = tid; j < n; j += BT) {
-        double s = 0.0;
-        int k = co[j];
-        for (int wq = 0; wq < W; ++wq) {
-          unsigned bits = cm[j * W + wq];
-          while (bits) {
-            const int r = wq * 32 + __ffs(bits) - 1;
-            s = fma(cv[k++], u[r], s);
-            bits &= bits - 1u;
-          }
-        }
+        double sacc = 0.0;
+        for (int t = co[j]; t < co[j + 1]; ++t) sacc = fma(rv[cpos[t]], u[crow[t]], sacc);
         const double xj = w[j];
         lmx = fmin(lmx, xj);
-        lmy = fmin(lmy, s);
-        lmc = fmax(lmc, fabs(xj * s));
-        ld += xj * s;
+        lmy = fmin(lmy, sacc);
+        lmc = fmax(lmc, fabs(xj * sacc));
+        ld += xj * sacc;
       }
       mx = block_min(lmx, red);
       my = block_min(lmy, red);
@@ -512,14 +753,9 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
     }
     if (tid == 0) {
       int32_t* ii = a.info_i + (size_t)prob * 8;
-      ii[0] = status;
-      ii[1] = iter;
-      ii[2] = singles;
-      ii[3] = f;
       ii[4] = itn;
       ii[5] = istop;
       ii[6] = (mode != 0 && any_infeas) ? 1 : 0;
-      ii[7] = status == 7 ? not_pd : -1;
       double* dd = a.info_d + (size_t)prob * 5;
       dd[0] = 0.5 * obj;
       dd[1] = mx;
@@ -528,7 +764,13 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
       dd[4] = dot;
     }
     __syncthreads();
+    BP_MARK(12);  // output + KKT
+    if (g_batch_prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) g_batch_prof[13] += 1;
   }
+}
+
+cudaError_t batched_debug_set_profile(long long* p) {
+  return cudaMemcpyToSymbol(g_batch_prof, &p, sizeof(p));
 }
 
 __global__ void validate_batched_kernel(int batch, int m, int n, const int64_t* __restrict__ nnz_off,
@@ -576,21 +818,39 @@ cudaError_t launch_validate_batched(int batch, int m, int n, const int64_t* nnz_
 }
 
 size_t batched_smem_bytes(int m, int n, int nnz_max) { return layout(m, n, nnz_max).bytes; }
+size_t batched_gram_scratch(int n, int sm_count) { return sizeof(double) * (size_t)n * (n + 1) / 2 * (size_t)sm_count * 16; }
+
+size_t batched_colview_stride(int n, int nnz_max) {
+  return ((sizeof(int32_t) * (size_t)(n + 1) + sizeof(uint16_t) * 2 * (size_t)nnz_max) + 15) & ~(size_t)15;
+}
 
 cudaError_t launch_batched_nnz(const BatchArgs& a, int nnz_max, int sm_count, cudaStream_t s) {
   const size_t smem = layout(a.m, a.n, nnz_max).bytes;
+  const size_t smem2 = llayout(a.m, a.n, nnz_max).bytes;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(batched_lsqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
+  int per_sm = 0, per_sm2 = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batched_kernel, BT, smem);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, batched_lsqr_kernel, BT, smem2);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
+  if (per_sm2 < 1) per_sm2 = 1;
+  if (per_sm > 16) per_sm = 16;  // the Gram scratch holds 16 CTAs per SM
   int grid = sm_count * per_sm;
   if (grid > a.batch) grid = a.batch;
   if (grid < 1) grid = 1;
   batched_kernel<<<grid, BT, smem, s>>>(a, nnz_max);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int grid2 = sm_count * per_sm2;
+  if (grid2 > a.batch) grid2 = a.batch;
+  if (grid2 < 1) grid2 = 1;
+  batched_lsqr_kernel<<<grid2, BT, smem2, s>>>(a, nnz_max);
   return cudaGetLastError();
 }
 

@@ -115,11 +115,17 @@ struct BatchArgs {
   double* info_d;    // batch * 5 doubles: objective, min_x, min_y, max_comp, dot
   double tol, atol, btol, conlim;
   int p_max, max_iter, lsqr_mode, itn_limit, kkt;
+  uint8_t* colview;  // scratch: per problem the column view (batched_colview_stride bytes)
+  size_t cv_stride;
+  double* gram;      // scratch: one packed Gram per CTA (batched_gram_scratch bytes)
 };
+size_t batched_colview_stride(int n, int nnz_max);
+size_t batched_gram_scratch(int n, int sm_count);
 size_t batched_smem_bytes(int m, int n, int nnz_max);
 cudaError_t launch_validate_batched(int batch, int m, int n, const int64_t* nnz_off,
                                     const int32_t* rowptr, const int32_t* colind,
                                     const double* vals, const double* b, int* err, cudaStream_t s);
 cudaError_t launch_batched_nnz(const BatchArgs& a, int nnz_max, int sm_count, cudaStream_t s);
+cudaError_t batched_debug_set_profile(long long* p);
 
 }  // namespace nnls
