@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
   uint16_t* cpos = reinterpret_cast<uint16_t*>(ib + Ly.icx);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double tol = a.tol;
+  __shared__ int s_istop;
   for (int prob = blockIdx.x; prob < a.batch; prob += gridDim.x) {
     const int64_t e0 = a.nnz_off[prob];
     const int nz = (int)(a.nnz_off[prob + 1] - e0);
@@ -570,21 +571,18 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
         rslot ^= 1;
       };
       // row SpMV: s = A(r, :) v with 4 independent partial sums (v_G = 0)
-      auto row_dot = [&](int r, const double* vec, bool maskF) {
+      // (vec is zero outside F: x and v are, so no mask test)
+      auto row_dot = [&](int r, const double* vec) {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         const int t1 = rp[r + 1];
         int e = rp[r];
         for (; e + 3 < t1; e += 4) {
-          const int j0 = ci[e], j1 = ci[e + 1], j2 = ci[e + 2], j3 = ci[e + 3];
-          s0 = fma(rv[e], (maskF && !mk[j0]) ? 0.0 : vec[j0], s0);
-          s1 = fma(rv[e + 1], (maskF && !mk[j1]) ? 0.0 : vec[j1], s1);
-          s2 = fma(rv[e + 2], (maskF && !mk[j2]) ? 0.0 : vec[j2], s2);
-          s3 = fma(rv[e + 3], (maskF && !mk[j3]) ? 0.0 : vec[j3], s3);
+          s0 = fma(rv[e], vec[ci[e]], s0);
+          s1 = fma(rv[e + 1], vec[ci[e + 1]], s1);
+          s2 = fma(rv[e + 2], vec[ci[e + 2]], s2);
+          s3 = fma(rv[e + 3], vec[ci[e + 3]], s3);
         }
-        for (; e < t1; ++e) {
-          const int jj = ci[e];
-          s0 = fma(rv[e], (maskF && !mk[jj]) ? 0.0 : vec[jj], s0);
-        }
+        for (; e < t1; ++e) s0 = fma(rv[e], vec[ci[e]], s0);
         return (s0 + s1) + (s2 + s3);
       };
       // column SpMV half: entries t of column j with t - co[j] = half (mod 2)
@@ -605,7 +603,7 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
       // beta u = b - A x (mode 2) or b
       double pu = 0.0;
       for (int r = tid; r < m; r += BT) {
-        const double sacc = (mode == 2) ? row_dot(r, x, true) : 0.0;
+        const double sacc = (mode == 2) ? row_dot(r, x) : 0.0;
         const double uu = bb[r] - sacc;
         u[r] = uu;
         pu += uu * uu;
@@ -638,17 +636,25 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
       __syncthreads();  // v, u complete
       double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
       const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
+      // the stopping test of iteration t is evaluated by thread 0 after that
+      // iteration's last barrier and read by everyone after the next one (x
+      // is not touched in between, so breaking there returns iteration t)
+      if (tid == 0) s_istop = 0;
       if (alpha * beta != 0.0) {
-        while (itn < itn_limit) {
-          ++itn;
+        for (;;) {
           // u' = A v - alpha u (own rows)
+          const bool more = itn < itn_limit;
           pu = 0.0;
-          for (int r = tid; r < m; r += BT) {
-            const double uu = row_dot(r, v, false) - alpha * u[r];
-            u[r] = uu;
-            pu += uu * uu;
-          }
-          reduce3(pu, 0.0, 0.0, 1, tot);  // B1: u' complete
+          if (more)
+            for (int r = tid; r < m; r += BT) {
+              const double uu = row_dot(r, v) - alpha * u[r];
+              u[r] = uu;
+              pu += uu * uu;
+            }
+          reduce3(pu, 0.0, 0.0, 1, tot);  // B1: u' complete; the previous test visible
+          istop = s_istop;
+          if (istop != 0) break;
+          ++itn;
           beta = sqrt(tot[0]);
           double alpha_new = alpha;
           if (beta > 0.0) {
@@ -670,16 +676,17 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
             if (alpha_new > 0.0 && colown) v[jc] *= 1.0 / alpha_new;
           }
           const double rho = sqrt(rhobar * rhobar + beta * beta);
-          const double cs = rhobar / rho, sn = beta / rho;
+          const double irho = 1.0 / rho;
+          const double cs = rhobar * irho, sn = beta * irho;
           const double theta = sn * alpha_new;
           rhobar = -cs * alpha_new;
           const double phi = cs * phibar;
           phibar = sn * phibar;
-          const double t1 = phi / rho, t2 = -theta / rho;
+          const double t1 = phi * irho, t2 = -theta * irho;
           double pd = 0.0, px = 0.0;
           if (colown) {  // own column: w, x
             const double ww = w[jc];
-            const double dd = ww / rho;
+            const double dd = ww * irho;
             pd = dd * dd;
             const double xx = X[jc] + t1 * ww;
             X[jc] = xx;
@@ -689,23 +696,26 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
           alpha = alpha_new;
           reduce3(pd, px, 0.0, 2, tot);  // B3: v, w, x complete
           ddnorm += tot[0];
-          const double xnorm = sqrt(tot[1]);
-          const double acond = anorm * sqrt(ddnorm);
-          const double rnorm = phibar;
-          const double arnorm = alpha * fabs(sn * phi);
-          const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
-          const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
-          const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
-          const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
-          const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
-          if (itn >= itn_limit) istop = 7;
-          if (1.0 + test3 <= 1.0) istop = 6;
-          if (1.0 + test2 <= 1.0) istop = 5;
-          if (1.0 + tt1 <= 1.0) istop = 4;
-          if (test3 <= ctol) istop = 3;
-          if (test2 <= a.atol) istop = 2;
-          if (test1 <= rtol) istop = 1;
-          if (istop != 0) break;
+          if (tid == 0) {
+            const double xnorm = sqrt(tot[1]);
+            const double acond = anorm * sqrt(ddnorm);
+            const double rnorm = phibar;
+            const double arnorm = alpha * fabs(sn * phi);
+            const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+            const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
+            const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
+            const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
+            const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
+            int st = 0;
+            if (itn >= itn_limit) st = 7;
+            if (1.0 + test3 <= 1.0) st = 6;
+            if (1.0 + test2 <= 1.0) st = 5;
+            if (1.0 + tt1 <= 1.0) st = 4;
+            if (test3 <= ctol) st = 3;
+            if (test2 <= a.atol) st = 2;
+            if (test1 <= rtol) st = 1;
+            s_istop = st;
+          }
         }
       }
       __syncthreads();
