@@ -483,6 +483,7 @@ LsqrArgs lsqr_args(nnls_handle* h) {
   a.Fval = P<double>(h->Fval);
   a.Fcol = P<int32_t>(h->Fcol);
   a.Fcnt = P<int32_t>(h->Fcnt);
+  a.Fidx = P<int32_t>(h->Fidx);
   return a;
 }
 
@@ -490,11 +491,9 @@ LsqrArgs lsqr_args(nnls_handle* h) {
 // memory (configs 0, 1, 3); the full-grid cooperative kernel otherwise
 cudaError_t launch_lsqr(nnls_handle* h, cudaStream_t s) {
   const LsqrArgs a = lsqr_args(h);
-  cudaError_t e = cudaErrorNotSupported;
-  if (!h->no_cluster) {
-    e = launch_lsqr_compact(a, h->sms, s);
-    if (e == cudaSuccess) e = launch_lsqr_cluster_planned(a, h->h->plan, s);
-  }
+  cudaError_t e = launch_lsqr_compact(a, h->sms, s);  // A restricted to F (both paths)
+  if (e != cudaSuccess) return e;
+  e = h->no_cluster ? cudaErrorNotSupported : launch_lsqr_cluster_planned(a, h->h->plan, s);
   if (e == cudaErrorNotSupported) {
     cudaGetLastError();
     e = launch_lsqr_final(a, h->sms, s);

@@ -57,6 +57,42 @@ __device__ void block_partial_minmax(double v, double* partials, int slot, doubl
     if (lane == 0) partials[blockIdx.x * kSlots + slot] = s;
   }
 }
+// all CTAs: sum partials[*][slot .. slot+nv) (nv <= 3) with every thread of
+// the block (fixed order per thread, then a fixed block reduction: the
+// result is identical in every CTA).  red[] holds 3 x 16 doubles.
+__device__ void grid_sum3(const double* partials, int slot, int nv, double* out, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double sv[3] = {0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+    for (int q = 0; q < nv; ++q) sv[q] += __ldcg(&partials[b * kSlots + slot + q]);
+  for (int q = 0; q < nv; ++q) sv[q] = warp_sum(sv[q]);
+  __syncthreads();
+  if (lane == 0)
+    for (int q = 0; q < nv; ++q) red[16 * q + wid] = sv[q];
+  __syncthreads();
+  for (int q = 0; q < nv; ++q) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[16 * q + w];
+    out[q] = t;
+  }
+}
+// block-reduce nv (<= 3) values into partials[blockIdx][slot ..]
+__device__ void block_partial_sum3(const double* v, int nv, double* partials, int slot, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double x[3] = {0.0, 0.0, 0.0};
+  for (int q = 0; q < nv; ++q) x[q] = warp_sum(v[q]);
+  __syncthreads();
+  if (lane == 0)
+    for (int q = 0; q < nv; ++q) red[16 * q + wid] = x[q];
+  __syncthreads();
+  if (wid == 0) {
+    for (int q = 0; q < nv; ++q) {
+      double y = lane < (int)(blockDim.x >> 5) ? red[16 * q + lane] : 0.0;
+      y = warp_sum(y);
+      if (lane == 0) partials[blockIdx.x * kSlots + slot + q] = y;
+    }
+  }
+}
 // all CTAs: reduce partials[*][slot] in a fixed order (result identical in every CTA)
 __device__ double grid_total(const double* partials, int slot, double* bcast, int kind) {
   // kind 0 sum, 1 min, 2 max
@@ -77,9 +113,20 @@ __device__ double grid_total(const double* partials, int slot, double* bcast, in
 }
 }  // namespace
 
+// debug hook: per-phase %globaltimer stamps of CTA 0 (nnls_debug_lsqr_profile)
+__device__ unsigned long long* g_lsqr_prof = nullptr;
+#define LG_STAMP(slot)                                                                     \
+  do {                                                                                     \
+    if (g_lsqr_prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && itn < 64) {        \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_lsqr_prof[itn * 16 + (slot)] = t_;                                                 \
+    }                                                                                      \
+  } while (0)
+
 __global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[32];
+  __shared__ double red[48];
   __shared__ double bcast;
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -152,69 +199,120 @@ __global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
     grid.sync();
     double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
     const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
+    // Two grid barriers per iteration: the |d|^2, |x|^2 partials of
+    // iteration t ride on iteration t+1's first barrier, and t's stopping
+    // test is taken there (x is not touched in between).
+    double pd = 0.0, px = 0.0, last_phi = 0.0, last_sn = 0.0;
+    bool pending = false;
+    const int32_t* __restrict__ Fidx = a.Fidx;
+    // V holds v unnormalised (V = v / vscale) from phase B on, so phase C
+    // never writes it: phase A of the next iteration reads V with no barrier
+    // after phase C
+    double vscale = 1.0;
     if (alpha * beta != 0.0) {
-      while (itn < itn_limit) {
-        ++itn;
-        // ---- phase A: U = A v - alpha u, u = U / beta
+      for (;;) {
+        const bool more = itn < itn_limit;
+        LG_STAMP(0);
+        // ---- phase A: U = A v - alpha u, u = U / beta.  Four rows per warp
+        //      pass (8 lanes each), so four rows' gathers are in flight at once
         const double au = beta > 0.0 ? alpha / beta : 0.0;
         p = 0.0;
-        for (int r = gwarp; r < m; r += nwarps) {
-          double s = 0.0;
-          for (int t = a.rowptr[r] + lane; t < a.rowptr[r + 1]; t += 32)
-            s = fma(a.vals[t], __ldcg(&a.V[a.colind[t]]), s);
-          s = warp_sum(s);
-          if (lane == 0) {
-            const double u = s - au * a.U[r];
-            a.U[r] = u;
-            p += u * u;
+        if (more) {
+          const int sub = lane >> 3, sl = lane & 7;
+          for (int r0 = gwarp * 4; r0 < m; r0 += nwarps * 4) {
+            const int r = r0 + sub;
+            double s = 0.0;
+            if (r < m) {  // A restricted to F (lsqr_compact_kernel): V is zero off F
+              const int t0 = a.rowptr[r], t1 = t0 + __ldcg(&a.Fcnt[r]);
+#pragma unroll 2
+              for (int t = t0 + sl; t < t1; t += 8) s = fma(__ldcg(&a.Fval[t]), __ldcg(&a.V[__ldcg(&a.Fcol[t])]), s);
+            }
+            s += __shfl_xor_sync(kFull, s, 4);
+            s += __shfl_xor_sync(kFull, s, 2);
+            s += __shfl_xor_sync(kFull, s, 1);
+            if (sl == 0 && r < m) {
+              const double u = s * vscale - au * a.U[r];
+              a.U[r] = u;
+              p += u * u;
+            }
           }
         }
-        block_partial_sum(p, a.partials, 0, red);
+        LG_STAMP(1);
+        {
+          const double v3[3] = {p, pd, px};
+          block_partial_sum3(v3, 3, a.partials, 0, red);
+        }
         grid.sync();
-        const double beta_new = sqrt(grid_total(a.partials, 0, &bcast, 0));
-        // ---- phase B: V' = A_F^T u - beta v
+        LG_STAMP(2);
+        double gt[3];
+        grid_sum3(a.partials, 0, 3, gt, red);
+        if (pending) {  // stopping test of the previous iteration
+          ddnorm += gt[1];
+          const double xnorm = sqrt(gt[2]);
+          const double acond = anorm * sqrt(ddnorm);
+          const double rnorm = phibar;
+          const double arnorm = alpha * fabs(last_sn * last_phi);
+          const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+          const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
+          const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
+          const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
+          const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
+          if (itn >= itn_limit) istop = 7;
+          if (1.0 + test3 <= 1.0) istop = 6;
+          if (1.0 + test2 <= 1.0) istop = 5;
+          if (1.0 + tt1 <= 1.0) istop = 4;
+          if (test3 <= ctol) istop = 3;
+          if (test2 <= a.atol) istop = 2;
+          if (test1 <= rtol) istop = 1;
+          if (istop != 0) break;
+        }
+        ++itn;
+        const double beta_new = sqrt(gt[0]);
+        // ---- phase B: V' = A_F^T u - beta v (warp per F column)
         double alpha_new = alpha;
         if (beta_new > 0.0) {
           anorm = sqrt(anorm * anorm + alpha * alpha + beta_new * beta_new);
           const double ib = 1.0 / beta_new;
           p = 0.0;
-          for (int j = gwarp; j < n; j += nwarps) {
-            if (!mask[j]) continue;
+          for (int k = gwarp; k < f; k += nwarps) {
+            const int j = Fidx[k];
             double s = 0.0;
-            for (int t = a.colptr[j] + lane; t < a.colptr[j + 1]; t += 32)
-              s = fma(a.cvals[t], __ldcg(&a.U[a.rowind[t]]), s);
+            const int c1 = a.colptr[j + 1];
+#pragma unroll 2
+            for (int t = a.colptr[j] + lane; t < c1; t += 32) s = fma(a.cvals[t], __ldcg(&a.U[a.rowind[t]]), s);
             s = warp_sum(s) * ib;
             if (lane == 0) {
-              const double v = s - beta_new * __ldcg(&a.V[j]);
-              a.V[j] = v;
+              const double v = s - beta_new * (__ldcg(&a.V[j]) * vscale);
+              a.V[j] = v;  // unnormalised
               p += v * v;
             }
           }
-          block_partial_sum(p, a.partials, 1, red);
+          LG_STAMP(3);
+          block_partial_sum(p, a.partials, 4, red);
           grid.sync();
-          alpha_new = sqrt(grid_total(a.partials, 1, &bcast, 0));
+          LG_STAMP(4);
+          grid_sum3(a.partials, 4, 1, gt, red);
+          alpha_new = sqrt(gt[0]);
         }
         beta = beta_new;
         // ---- rotation (replicated scalars)
         const double rho = sqrt(rhobar * rhobar + beta * beta);
-        const double cs = rhobar / rho, sn = beta / rho;
+        const double irho = 1.0 / rho;
+        const double cs = rhobar * irho, sn = beta * irho;
         const double theta = sn * alpha_new;
         rhobar = -cs * alpha_new;
         const double phi = cs * phibar;
         phibar = sn * phibar;
-        const double t1 = phi / rho, t2 = -theta / rho;
-        // ---- phase C: v = V'/alpha, x += t1 w, w = v + t2 w
-        const double ia = alpha_new > 0.0 ? 1.0 / alpha_new : 0.0;
-        double pd = 0.0, px = 0.0;
-        for (int j = gtid; j < n; j += nthr) {
-          if (!mask[j]) continue;
-          double v = __ldcg(&a.V[j]);
-          if (beta_new > 0.0 && alpha_new > 0.0) {
-            v *= ia;
-            a.V[j] = v;
-          }
+        const double t1 = phi * irho, t2 = -theta * irho;
+        // ---- phase C: v = V'/alpha, x += t1 w, w = v + t2 w (F columns; V not written)
+        if (beta_new > 0.0 && alpha_new > 0.0) vscale = 1.0 / alpha_new;
+        pd = 0.0;
+        px = 0.0;
+        for (int k = gtid; k < f; k += nthr) {
+          const int j = Fidx[k];
+          const double v = __ldcg(&a.V[j]) * vscale;
           const double w = a.W[j];
-          const double d = w / rho;
+          const double d = w * irho;
           pd += d * d;
           const double x = a.X[j] + t1 * w;
           a.X[j] = x;
@@ -222,27 +320,10 @@ __global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
           px += x * x;
         }
         alpha = alpha_new;
-        block_partial_sum(pd, a.partials, 2, red);
-        block_partial_sum(px, a.partials, 3, red);
-        grid.sync();
-        ddnorm += grid_total(a.partials, 2, &bcast, 0);
-        const double xnorm = sqrt(grid_total(a.partials, 3, &bcast, 0));
-        const double acond = anorm * sqrt(ddnorm);
-        const double rnorm = phibar;
-        const double arnorm = alpha * fabs(sn * phi);
-        const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
-        const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
-        const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
-        const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
-        const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
-        if (itn >= itn_limit) istop = 7;
-        if (1.0 + test3 <= 1.0) istop = 6;
-        if (1.0 + test2 <= 1.0) istop = 5;
-        if (1.0 + tt1 <= 1.0) istop = 4;
-        if (test3 <= ctol) istop = 3;
-        if (test2 <= a.atol) istop = 2;
-        if (test1 <= rtol) istop = 1;
-        if (istop != 0) break;
+        last_phi = phi;
+        last_sn = sn;
+        pending = true;
+        LG_STAMP(5);
       }
     }
   }
@@ -324,7 +405,8 @@ cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s) {
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsqr_final_kernel, kThreads, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-  int grid = sm_count;  // one CTA per SM
+  if (per_sm > 4) per_sm = 4;  // partials[] holds 4 CTAs per SM
+  int grid = sm_count * per_sm;  // every co-resident CTA (latency-bound gathers)
   LsqrArgs args = a;
   void* params[] = {&args};
   return cudaLaunchCooperativeKernel((void*)lsqr_final_kernel, dim3(grid), dim3(kThreads), params, 0, s);
@@ -417,8 +499,6 @@ __global__ void lsqr_plan_kernel(int m, int n, const int32_t* rowptr, const int3
   }
 }
 
-// debug hook: per-phase %globaltimer stamps of CTA 0 (nnls_debug_lsqr_profile)
-__device__ unsigned long long* g_lsqr_prof = nullptr;
 // setup / epilogue stamps go to row 63 (slots 0..)
 #define LQ_STAMP_SETUP(slot)                                                               \
   do {                                                                                     \

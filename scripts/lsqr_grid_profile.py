@@ -1,0 +1,32 @@
+"""Per-phase timeline of the cooperative-grid LSQR (config 2 default):
+python scripts/lsqr_grid_profile.py [config]"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import nnls_gen as g  # noqa: E402
+import paper_cs_0408029_b200 as P  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+if cfg != 2:
+    os.environ["NNLS_NO_CLUSTER"] = "1"
+prob = g.make_problem(cfg, 0)
+S = P.setup(prob)
+prof = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
+P.lib.nnls_debug_lsqr_profile.argtypes = [C.c_void_p]
+for rep in range(2):
+    prof.zero_()
+    P.lib.nnls_debug_lsqr_profile(C.c_void_p(prof.data_ptr()))
+    x, info = S.solve()
+    P.lib.nnls_debug_lsqr_profile(C.c_void_p(0))
+p = prof.cpu().numpy().reshape(64, 16).astype(np.float64)
+rows = [r for r in range(1, 63) if p[r, 0] > 0 and p[r, 5] > 0 and p[r + 1, 0] > 0]
+names = ["A spmv", "A blocksum+sync", "A gridsum+test+B spmv", "B blocksum+sync", "B gridsum+C"]
+for k, nm in enumerate(names):
+    d = [(p[r, k + 1] - p[r, k]) / 1e3 for r in rows]
+    print(f"{nm:22s} {np.mean(d):8.2f} us")
+print("per iteration", np.mean([(p[r + 1, 0] - p[r, 0]) / 1e3 for r in rows]), "us; lsqr_iterations", info["lsqr_iterations"])
