@@ -245,6 +245,54 @@ __device__ int potrf_dbg(double* __restrict__ S, int rv, int cv, double* __restr
   return *s_bad;
 }
 
+// 64x64x64 update with 32x32 per warp on warps 0..3 (4 A + 4 B fragment
+// loads per 16 DMMAs instead of 2 + 4 per 8)
+__device__ __forceinline__ void dmma_tile32(double (&acc)[4][4][2], const double* __restrict__ A,
+                                            const double* __restrict__ B, int lane, int rb0, int cb0) {
+#pragma unroll 2
+  for (int kk = 0; kk < T; kk += 4) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) av[a] = -A[(rb0 + 8 * a + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bv[q] = B[(cb0 + 8 * q + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
+  }
+}
+__global__ void __launch_bounds__(256, 1) dmma_bench(double* out, long long* cyc, int reps) {
+  extern __shared__ double sm[];
+  double* S = sm;
+  double* L = sm + T * LDS;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < T * LDS; e += 256) {
+    S[e] = 0.001 * e;
+    L[e] = 0.002 * (e % 97);
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  double acc[2][4][2] = {};
+  const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
+  for (int rep = 0; rep < reps; ++rep) {
+    dmma_tile<true>(acc, L, L, lane, rb0, cb0);
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  double acc4[4][4][2] = {};
+  for (int rep = 0; rep < reps; ++rep) {
+    if (w < 4) dmma_tile32(acc4, L, L, lane, (w >> 1) * 32, (w & 1) * 32);
+    __syncthreads();
+  }
+  long long t2 = clock64();
+  if (tid == 0) {
+    cyc[0] = (t1 - t0) / reps;
+    cyc[1] = (t2 - t1) / reps;
+  }
+  out[tid] = acc[0][0][0] + acc[1][3][1] + acc4[0][0][0] + acc4[3][3][1];
+}
+
 // correctness: residual max |(L L^T)[r][c] - A[r][c]| (c <= r, c < cv) of
 // potrf64_panel8 and potrf_r8<2>, and trsm_blocked vs trsm_rows
 __global__ void __launch_bounds__(256, 1) check(double* err, int cv, int dbg) {
@@ -342,6 +390,16 @@ int main() {
          "\"resid_panel8\": [%.2e, %.2e], \"resid_r8\": [%.2e, %.2e], \"trsm_blocked_vs_rows\": [%.2e, %.2e], \"err\": \"%s\"}\n",
          h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], he[0], he[3], he[1], he[4], he[2], he[5],
          cudaGetErrorString(cudaGetLastError()));
+  {
+    cudaFuncSetAttribute(dmma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    dmma_bench<<<1, 256, smem>>>(out, cyc, 4);
+    dmma_bench<<<1, 256, smem>>>(out, cyc, 50);
+    cudaDeviceSynchronize();
+    long long hd[2];
+    cudaMemcpy(hd, cyc, sizeof(hd), cudaMemcpyDeviceToHost);
+    printf("64x64x64 DMMA update: 16x32 per warp (8 warps) %lld cycles; 32x32 per warp (4 warps) %lld cycles\n",
+           hd[0], hd[1]);
+  }
   cudaFuncSetAttribute(stamp_run, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   stamp_run<<<1, 256, smem>>>(out);
   stamp_run<<<1, 256, smem>>>(out);

@@ -1,0 +1,96 @@
+"""Full-size GPU checks at the BASELINE configurations, in bench.py's launch
+configuration (the whole problem / the whole batch), where the oracle cannot
+solve everything within a test's time budget:
+
+* config 2 (40000 x 8000, one solve): sampled Gram entries and A^T b
+  against exact column dot products (quantized inputs make every partial sum
+  exact, so any summation order gives the same bits); the KKT conditions of
+  Eq. 3 at the returned x, recomputed independently with scipy; the
+  free-set solution against an independent least-squares solve on A_F.
+* config 4 (all 65536 problems, one launch): 256 problems drawn across the
+  batch solved by the oracle one by one (F, iteration counts, x), and the KKT
+  report of every problem.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+sp = pytest.importorskip("scipy.sparse")
+spla = pytest.importorskip("scipy.sparse.linalg")
+
+import nnls_gen as g  # noqa: E402
+import oracle as O  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_cs_0408029_b200 as pkg
+    assert pkg.device_info()["cc"] >= 100
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def config2(P):
+    prob = g.make_problem(2, 0)
+    S = P.setup(prob)
+    x, info = S.solve()
+    A = sp.csr_matrix((prob.vals, prob.colind, prob.rowptr), shape=(prob.m, prob.n))
+    return dict(prob=prob, S=S, x=np.asarray(x), info=info, mask=S.free_set().astype(bool), A=A)
+
+
+def test_config2_sampled_gram_exact(config2):
+    prob, S, A = config2["prob"], config2["S"], config2["A"]
+    G, c = S.gram()
+    rng = np.random.default_rng(7)
+    Acsc = A.tocsc()
+    for i, j in zip(rng.integers(0, prob.n, 400), rng.integers(0, prob.n, 400)):
+        ci, cj = Acsc.getcol(i), Acsc.getcol(j)
+        exact = float((ci.multiply(cj)).sum())
+        assert G[i, j] == exact and G[j, i] == exact
+    cols = rng.integers(0, prob.n, 200)
+    ref_c = np.asarray(Acsc[:, cols].T @ prob.b).ravel()
+    assert np.array_equal(c[cols], ref_c)
+
+
+def test_config2_kkt(config2):
+    """x >= 0; y = A^T (A x - b) >= 0 on G and ~0 on F; x_i y_i ~ 0."""
+    prob, x, A, mask, info = config2["prob"], config2["x"], config2["A"], config2["mask"], config2["info"]
+    assert info["status"] == 0 and info["iterations"] > 0
+    assert x.min() >= 0.0
+    assert np.all(x[~mask] == 0.0)
+    r = A @ x - prob.b
+    y = A.T @ r
+    scale = np.abs(A.T @ prob.b).max()
+    assert np.abs(y[mask]).max() <= 1e-9 * scale
+    assert y[~mask].min() >= -1e-9 * scale
+    assert np.abs(x * y).max() <= 1e-9 * scale * max(1.0, x.max())
+
+
+def test_config2_free_set_least_squares(config2):
+    """x_F solves min |A_F x_F - b| (Eq. 4): against scipy's LSQR on A_F."""
+    prob, x, A, mask = config2["prob"], config2["x"], config2["A"], config2["mask"]
+    AF = A[:, np.flatnonzero(mask)]
+    ref = spla.lsqr(AF, prob.b, atol=1e-15, btol=1e-15, iter_lim=2000)[0]
+    xf = x[mask]
+    assert np.abs(xf - ref).max() <= 1e-8 * np.abs(ref).max()
+
+
+def test_config4_full_batch_sampled_parity(P):
+    B = g.make_batch(seed=0, start=0, count=65536)
+    out = P.BatchedSolver().load_batch(B).solve()
+    xs = out["x"].reshape(B.count, B.n)
+    masks = out["mask"].reshape(B.count, B.n)
+    info = out["info"]
+    assert np.all(info["status"] == 0)
+    assert info["kkt_min_x"].min() >= 0.0
+    rng = np.random.default_rng(11)
+    picks = np.sort(rng.choice(B.count, 256, replace=False))
+    for p in picks:
+        prob = B.problem(int(p))
+        r = O.solve(prob)
+        assert np.array_equal(masks[p].astype(bool), r["mask"].astype(bool)), p
+        assert info["iterations"][p] == r["iterations"], p
+        scale = max(np.abs(r["x"]).max(), 1e-300)
+        assert np.abs(xs[p] - r["x"]).max() <= 1e-9 * scale, p
