@@ -280,9 +280,19 @@ __global__ void __launch_bounds__(256) dual_kernel(
   for (int jj = gwarp; jj < g; jj += nwarps) {
     const int j = Gidx[jj];
     const double* Gj = G + (size_t)j * ldg;
-    double s = 0.0;
-    for (int a = lane; a < f; a += 32) s = fma(Gj[Fidx[a]], xF[a], s);
-    s = warp_sum(s);
+    // four independent partial sums: four loads of G_j (and of Fidx, x_F,
+    // which every warp shares through L1) in flight per lane
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int a = lane;
+    for (; a + 96 < f; a += 128) {
+      const int i0 = __ldg(&Fidx[a]), i1 = __ldg(&Fidx[a + 32]), i2 = __ldg(&Fidx[a + 64]), i3 = __ldg(&Fidx[a + 96]);
+      s0 = fma(Gj[i0], __ldg(&xF[a]), s0);
+      s1 = fma(Gj[i1], __ldg(&xF[a + 32]), s1);
+      s2 = fma(Gj[i2], __ldg(&xF[a + 64]), s2);
+      s3 = fma(Gj[i3], __ldg(&xF[a + 96]), s3);
+    }
+    for (; a < f; a += 32) s0 = fma(Gj[__ldg(&Fidx[a])], __ldg(&xF[a]), s0);
+    const double s = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) {
       const double v = s - c[j];
       const double av = fabs(v);
