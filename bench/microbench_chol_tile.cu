@@ -7,6 +7,8 @@
 
 #include "../paper_cs_0408029_b200/csrc/cholesky.cu"
 
+#include "trsm_blocked.cuh"
+
 using namespace nnls;
 
 // reference versions (previous product code) for timing / cross-checks

@@ -4,6 +4,7 @@
 #include <cstdlib>
 
 #include "../paper_cs_0408029_b200/csrc/cholesky.cu"
+#include "trsm_blocked.cuh"
 
 using namespace nnls;
 

@@ -92,7 +92,6 @@ struct nnls_handle {
   Buf U, V, W, X, R, partials, xfin;      // LSQR / report
   Buf Fval, Fcol, Fcnt;                   // A restricted to the final F (cluster LSQR)
   Buf st, err, trace;
-  size_t ntile = 0;
   int trace_cap = 0;
   HostState* h = nullptr;                 // pinned readback
   bool no_cluster = false;  // force the full-grid LSQR (tests / env NNLS_NO_CLUSTER)
@@ -213,7 +212,6 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->xF, sizeof(double) * (size_t)(n + kTile)));
   CK(ensure(h->Fidx, sizeof(int32_t) * (size_t)n));
   CK(ensure(h->Gidx, sizeof(int32_t) * (size_t)n));
-  const size_t ntile = chol_tile_count(n);
   const size_t nflags = chol_flag_count(n);
   if (h->flags.cap < sizeof(int) * nflags) {
     CK(ensure(h->flags, sizeof(int) * nflags));
@@ -222,8 +220,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
     CK(ensure(h->st, sizeof(DevState)));
     CK(cudaMemsetAsync(h->st.p, 0, sizeof(DevState), s));
   }
-  h->ntile = ntile;
-  CK(ensure(h->Lt, sizeof(double) * ntile * kTile * kTile));
+  CK(ensure(h->Lt, sizeof(double) * chol_tile_doubles(n)));
   CK(ensure(h->U, sizeof(double) * (size_t)m));
   CK(ensure(h->R, sizeof(double) * (size_t)m));
   CK(ensure(h->Fval, sizeof(double) * (size_t)(nnz > 0 ? nnz : 1)));
@@ -897,8 +894,7 @@ nnls_status nnls_step_normal_solve(int32_t n, const double* G, int32_t ldg, cons
   if (f == 0) return NNLS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   TmpBufs t;
-  const size_t ntile = chol_tile_count(n);
-  CK(ensure(t.bufs[0], sizeof(double) * ntile * kTile * kTile));
+  CK(ensure(t.bufs[0], sizeof(double) * chol_tile_doubles(n)));
   CK(ensure(t.bufs[1], sizeof(int) * chol_flag_count(n)));
   CK(ensure(t.bufs[2], sizeof(DevState)));
   CK(ensure(t.bufs[3], sizeof(double) * (size_t)(f + kTile)));

@@ -41,7 +41,8 @@ namespace {
 constexpr int T = kTile;
 constexpr int LDS = T + 4;  // smem row stride (doubles): conflict-free 8x4 fragment reads
 constexpr int kThreads = 256;
-constexpr int kSmemDoubles = 6 * T * LDS;
+constexpr int TS = T * LDS;  // a tile in global memory has the smem layout too (one bulk copy)
+constexpr int kSmemDoubles = 6 * TS;
 
 __host__ __device__ inline int tidx(int i, int j) { return i * (i + 1) / 2 + j; }
 // Barrier of the CTA's 8 warps as named barrier 1 (barrier 2 is the 7-warp
@@ -72,28 +73,26 @@ size_t chol_flag_count(int n) {
   return 2 * (size_t)tri_tiles(n) + 2 * (size_t)ntr + 4;
 }
 
-// Lower tiles L(i,j) followed by one inverse tile per tile column.
-size_t chol_tile_count(int n) {
+// Lower tiles L(i,j) followed by one inverse tile per tile column; each tile
+// T rows of stride LDS (the smem layout, so a tile moves as one bulk copy).
+size_t chol_tile_doubles(int n) {
   const int ntr = (n + 1 + T - 1) / T;
-  return (size_t)tri_tiles(n) + ntr;
+  return ((size_t)tri_tiles(n) + ntr) * TS;
 }
 
-// load a T x T tile (row-major, contiguous) from global into smem (stride LDS)
+// load a tile (global, T rows of stride LDS) into smem (same layout)
 __device__ __forceinline__ void load_tile(double* __restrict__ dst, const double* __restrict__ src) {
-  const double2* s2 = reinterpret_cast<const double2*>(src);
   for (int e = threadIdx.x; e < T * T / 2; e += kThreads) {
-    const int r = (2 * e) / T, c = (2 * e) % T;
-    const double2 v = __ldcg(&s2[e]);  // written by other CTAs: bypass L1
-    dst[r * LDS + c] = v.x;
-    dst[r * LDS + c + 1] = v.y;
+    const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(src + o));  // other CTAs' data: bypass L1
+    *reinterpret_cast<double2*>(dst + o) = v;
   }
 }
 
 __device__ __forceinline__ void store_tile(double* __restrict__ dst, const double* __restrict__ src) {
-  double2* d2 = reinterpret_cast<double2*>(dst);
   for (int e = threadIdx.x; e < T * T / 2; e += kThreads) {
-    const int r = (2 * e) / T, c = (2 * e) % T;
-    d2[e] = make_double2(src[r * LDS + c], src[r * LDS + c + 1]);
+    const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+    *reinterpret_cast<double2*>(dst + o) = *reinterpret_cast<const double2*>(src + o);
   }
 }
 
@@ -109,8 +108,8 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 __device__ __forceinline__ void tile_async(double* __restrict__ dst, const double* __restrict__ src) {
   for (int e = threadIdx.x; e < T * T / 2; e += kThreads) {
-    const int r = (2 * e) / T, c = (2 * e) % T;
-    cp_async16(dst + r * LDS + c, src + 2 * e);
+    const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+    cp_async16(dst + o, src + o);
   }
 }
 
@@ -154,29 +153,6 @@ __device__ __forceinline__ void acc_store(const double (&acc)[2][4][2], double* 
 #pragma unroll
       for (int v = 0; v < 2; ++v)
         S[(rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v] = acc[a][q][v];
-}
-
-// Inverse of a 32 x 32 lower-triangular block (smem, stride LDS) with
-// reciprocal diagonal rinvb: lane = column c computes X[:, c] by forward
-// substitution, x_i = (delta_ic - sum_{k<i} L_ik x_k) / L_ii.  ncols pivots;
-// rows/columns >= ncols are zero.  Writes X (lower) to out (stride LDS).
-__device__ __forceinline__ void warp_trtri32(const double* __restrict__ Lb,
-                                             const double* __restrict__ rinvb, int ncols, int lane,
-                                             double* __restrict__ out, double* __restrict__ outT) {
-  double x[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double s = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k) s = fma(-Lb[i * LDS + k], x[k], s);
-    x[i] = (i < ncols && lane < ncols) ? s * rinvb[i] : 0.0;
-  }
-#pragma unroll
-  for (int i = 0; i < 32; ++i) out[i * LDS + lane] = x[i];
-  if (outT != nullptr) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) outT[lane * LDS + i] = x[i];
-  }
 }
 
 // Cholesky of the diagonal 64 x 64 tile S (smem; rows < rv, pivot columns
@@ -358,52 +334,6 @@ __device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
   return *s_bad;
 }
 
-struct NoHook {
-  __device__ __forceinline__ void operator()(int, int) const {}
-};
-
-// X := X L^-T for a 64x64 smem tile X and lower L (cv valid columns), in
-// 8-column panels: warps 0-1 solve the panel row by row (thread per row,
-// the 8x8 diagonal block of L in registers), then every warp folds the
-// panel into the later column blocks with DMMA (warp w: rows 8w..8w+7).
-// hook(p, lane) runs on warp 7 during the solve phase of panel p.
-template <class Hook = NoHook>
-__device__ __forceinline__ void trsm_blocked(double* __restrict__ X, const double* __restrict__ L,
-                                             const double* __restrict__ rinv, int cv,
-                                             const Hook& hook = Hook()) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int np = (cv + 7) >> 3;
-#pragma unroll 1
-  for (int p = 0; p < np; ++p) {
-    const int c0 = 8 * p;
-    if (tid < 64) {
-      double Ld[8][8], ri[8], x[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        ri[c] = (c0 + c < cv) ? rinv[c0 + c] : 0.0;
-#pragma unroll
-        for (int c2 = c + 1; c2 < 8; ++c2) Ld[c2][c] = L[(c0 + c2) * LDS + c0 + c];
-        x[c] = X[tid * LDS + c0 + c];
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        x[c] *= ri[c];
-#pragma unroll
-        for (int c2 = c + 1; c2 < 8; ++c2) x[c2] = fma(-x[c], Ld[c2][c], x[c2]);
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) X[tid * LDS + c0 + c] = x[c];
-    } else if (w == 7) {
-      hook(p, lane);  // warp 7 is idle in the solve phase
-    }
-    csync();
-    if (p + 1 < np) {  // X(rows of warp w, J) -= X(., panel) L(J, panel)^T for J in (p, np)
-      strip8_gemm(X, X, L, c0, 8 * w, p + 1, np, lane);
-      csync();
-    }
-  }
-}
-
 // Y (lower 8x8 blocks of a 64x64 tile) -= X X^T, K = 64, on warps 0..6:
 // block b = I(I+1)/2 + J goes to warp b % 7 (slot b / 7); warps with 5
 // blocks repeat one as a dummy 6th (result dropped), so the 6 independent
@@ -449,44 +379,150 @@ __device__ __forceinline__ void syrk64_lower7(double* __restrict__ Y, const doub
   }
 }
 
-// acc[q] (rows 8w.. of a 32 x 32 product, cols 8q..) += A B^T, A and B
-// 32 x 32 row-major (B by rows n: C[m][n] += sum_k A[m][k] B[n][k]).
-__device__ __forceinline__ void dmma32(double (&acc)[4][2], const double* __restrict__ A,
-                                       const double* __restrict__ B, int lane, int w) {
-#pragma unroll
-  for (int kk = 0; kk < 32; kk += 4) {
-    const double av = A[(8 * w + (lane >> 2)) * LDS + kk + (lane & 3)];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double bv = B[(8 * q + (lane >> 2)) * LDS + kk + (lane & 3)];
-      dmma8x8x4(acc[q][0], acc[q][1], av, bv);
-    }
-  }
-}
-
-// Bulk (async-proxy) store of a smem tile (stride LDS) to a dense T x T
-// global tile: 64 row copies of 512 B issued by one thread, completed later
-// by bulk_store_release() of the same thread, so the chain never waits on
-// them.
-// The smem rows must have been made visible to the async proxy
-// (fence_proxy_async_smem() by the writers, then a barrier).
+// smem writes of this thread -> visible to the async proxy (bulk copies)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
-__device__ __forceinline__ void bulk_store_tile(double* __restrict__ dst, const double* __restrict__ src) {
-  for (int r = 0; r < T; ++r) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(src + r * LDS);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst + r * T), "r"(sa),
-                 "n"(T * 8)
-                 : "memory");
+
+// One doubling level of trtri64: for each pair of b x b diagonal blocks
+// (X11 at (o,o), X22 at (o+b,o+b), L21 at (o+b,o)), Linv21 = -X22 (L21 X11).
+// Output 8x8 blocks are spread over the 8 warps (b = 8: 4 blocks, b = 16: 8,
+// b = 32: 16 -> two per warp); Tm (scratch) holds L21 X11 transposed.
+template <int B>
+__device__ __forceinline__ void trtri_level(double* __restrict__ X, const double* __restrict__ L,
+                                            double* __restrict__ Tm, int w, int lane) {
+  constexpr int NB = B / 8;                 // 8x8 blocks per side
+  constexpr int NT = (32 / B) * NB * NB;    // output blocks in the level
+  constexpr int PER = NT >= 8 ? NT / 8 : 1; // blocks per warp
+  const int rq = lane >> 2, kq = lane & 3;
+  if (w >= NT) {  // b = 8: warps 4..7 idle in both steps
+    csync();
+    csync();
+    return;
   }
+  int o[PER], bi[PER], bj[PER], pr[PER];
+#pragma unroll
+  for (int s = 0; s < PER; ++s) {
+    const int t = w + 8 * s;
+    pr[s] = t / (NB * NB);
+    o[s] = 2 * B * pr[s];
+    bi[s] = (t % (NB * NB)) / NB;
+    bj[s] = t % NB;
+  }
+  double c0[PER], c1[PER];
+#pragma unroll
+  for (int s = 0; s < PER; ++s) c0[s] = c1[s] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < B; kk += 4) {  // Tm = L21 X11: A[m][k] = L21[m][k], B[n][k] = X11[k][n]
+#pragma unroll
+    for (int s = 0; s < PER; ++s) {
+      const double av = L[(o[s] + B + 8 * bi[s] + rq) * LDS + o[s] + kk + kq];
+      const double bv = X[(o[s] + kk + kq) * LDS + o[s] + 8 * bj[s] + rq];
+      dmma8x8x4(c0[s], c1[s], av, bv);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < PER; ++s) {  // Tmt[pair*B + n][m]
+    double* t = Tm + (B * pr[s] + 8 * bj[s] + 2 * kq) * LDS + 8 * bi[s] + rq;
+    t[0] = c0[s];
+    t[LDS] = c1[s];
+  }
+  csync();
+#pragma unroll
+  for (int s = 0; s < PER; ++s) c0[s] = c1[s] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < B; kk += 4) {  // Linv21 = -X22 Tm: A = X22, B[n][k] = Tmt[n][k]
+#pragma unroll
+    for (int s = 0; s < PER; ++s) {
+      const double av = -X[(o[s] + B + 8 * bi[s] + rq) * LDS + o[s] + B + kk + kq];
+      const double bv = Tm[(B * pr[s] + 8 * bj[s] + rq) * LDS + kk + kq];
+      dmma8x8x4(c0[s], c1[s], av, bv);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < PER; ++s) {
+    double* x = X + (o[s] + B + 8 * bi[s] + rq) * LDS + o[s] + 8 * bj[s] + 2 * kq;
+    x[0] = c0[s];
+    x[1] = c1[s];
+  }
+  if (B == 32) fence_proxy_async_smem();  // X complete -> its bulk store
+  csync();
+}
+
+// X = L^-1 for the lower 64 x 64 smem tile L with cv pivots (rows / columns
+// >= cv of X are zero), 1/l_cc in rinv (c < cv).  Blocked so that no step is
+// a 64-long column chain: warp w inverts the 8x8 diagonal block w by
+// substitution (lanes 0..7 = its columns, 28 dependent FMAs), then three
+// doubling levels b = 8, 16, 32 form Linv21 = -Linv22 L21 Linv11 on DMMA.
+// The strict upper blocks of X must be zero on entry (they are never
+// written).  All 8 warps; pj: profile row.
+__device__ __forceinline__ void trtri64(double* __restrict__ X, const double* __restrict__ L,
+                                        const double* __restrict__ rinv, int cv, double* __restrict__ Tm,
+                                        int pj) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int c0 = 8 * w;
+  if (lane < 8) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) s = fma(-L[(c0 + i) * LDS + c0 + k], x[k], s);
+      x[i] = (c0 + i < cv) ? s * rinv[c0 + i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) X[(c0 + i) * LDS + c0 + lane] = x[i];
+  }
+  csync();
+  PROF_STAMP(pj, 6);
+  trtri_level<8>(X, L, Tm, w, lane);
+  trtri_level<16>(X, L, Tm, w, lane);
+  PROF_STAMP(pj, 7);
+  trtri_level<32>(X, L, Tm, w, lane);
+}
+
+// acc (rows 8w..8w+7 of X, all 64 columns) = A Linv^T for 64 x 64 smem
+// tiles, Linv lower triangular: column block q only needs k < 8q+8, which
+// halves the DMMAs (72 per warp, 8 independent accumulators).
+__device__ __forceinline__ void gemm_linvT(double (&acc)[8][2], const double* __restrict__ A,
+                                           const double* __restrict__ Linv, int w, int lane) {
+  const int rq = lane >> 2, kq = lane & 3;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+  for (int kb = 0; kb < T / 4; ++kb) {
+    const double av = A[(8 * w + rq) * LDS + 4 * kb + kq];
+#pragma unroll
+    for (int q = kb / 2; q < 8; ++q) dmma8x8x4(acc[q][0], acc[q][1], av, Linv[(8 * q + rq) * LDS + 4 * kb + kq]);
+  }
+}
+__device__ __forceinline__ void store_rows8(const double (&acc)[8][2], double* __restrict__ X, int w, int lane) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    double* x = X + (8 * w + (lane >> 2)) * LDS + 8 * q + 2 * (lane & 3);
+    x[0] = acc[q][0];
+    x[1] = acc[q][1];
+  }
+}
+
+// Bulk (async-proxy) store of a smem tile to its global copy (same layout):
+// ONE cp.async.bulk of T*LDS doubles issued by one thread, completed later by
+// bulk_store_release() of the same thread, so the chain never waits on it.
+// The smem rows must have been made visible to the async proxy
+// (fence_proxy_async_smem() by the writers, then a barrier).
+__device__ __forceinline__ void bulk_store_tile(double* __restrict__ dst, const double* __restrict__ src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(src);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(sa),
+               "n"(TS * 8)
+               : "memory");
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
-// wait for this thread's bulk stores, then release the flag (lane 0 calls)
-__device__ __forceinline__ void bulk_store_release(int* flag, int epoch) {
+// wait for this thread's bulk stores, then release the flag(s)
+__device__ __forceinline__ void bulk_store_release(int* flag, int epoch, int* flag2 = nullptr) {
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
   st_release(flag, epoch);
+  if (flag2 != nullptr) st_release(flag2, epoch);
 }
 
 // ---------------------------------------------------------------------------
@@ -553,8 +589,8 @@ __device__ __forceinline__ void left_update(double* __restrict__ smem, double* _
         wait_flag(&full[tidx(jj, k)], epoch);
       }
       csync();
-      tile_async(LA, Lt + (size_t)tidx(i, k) * T * T);
-      tile_async(LB, Lt + (size_t)tidx(jj, k) * T * T);
+      tile_async(LA, Lt + (size_t)tidx(i, k) * TS);
+      tile_async(LB, Lt + (size_t)tidx(jj, k) * TS);
       cp_async_commit();
     }
     have_next = false;
@@ -563,8 +599,8 @@ __device__ __forceinline__ void left_update(double* __restrict__ smem, double* _
         *s_ready = (ld_acquire(&full[tidx(i, k + 1)]) == epoch) && (ld_acquire(&full[tidx(jj, k + 1)]) == epoch);
       csync();
       if (*s_ready) {
-        tile_async(smem + ((k & 1) ? 1 : 3) * (T * LDS), Lt + (size_t)tidx(i, k + 1) * T * T);
-        tile_async(smem + ((k & 1) ? 2 : 4) * (T * LDS), Lt + (size_t)tidx(jj, k + 1) * T * T);
+        tile_async(smem + ((k & 1) ? 1 : 3) * (T * LDS), Lt + (size_t)tidx(i, k + 1) * TS);
+        tile_async(smem + ((k & 1) ? 2 : 4) * (T * LDS), Lt + (size_t)tidx(jj, k + 1) * TS);
         cp_async_commit();
         have_next = true;
       }
@@ -577,11 +613,6 @@ __device__ __forceinline__ void left_update(double* __restrict__ smem, double* _
   }
   acc_store(acc, S, lane, rb0, cb0);
   csync();
-}
-
-// L (smem) -> 1/L[c][c] for c < cv
-__device__ __forceinline__ void diag_recip(const double* __restrict__ L, double* __restrict__ rinv, int cv) {
-  if (threadIdx.x < T) rinv[threadIdx.x] = (threadIdx.x < cv) ? 1.0 / L[threadIdx.x * LDS + threadIdx.x] : 0.0;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
@@ -611,8 +642,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     // L_jj's flag in a solve phase); last update of A(j+1,j+1) on warps 0-6
     // while warp 7 raises L(j+1,j)'s flag.
     double* Lnext = smem + 5 * (T * LDS);
+    double* Xinv = smem + 2 * (T * LDS);  // Linv_jj
+    double* Tm = smem + 3 * (T * LDS);    // trtri scratch
     int first_bad = -1;
-    int* pending = nullptr;  // (warp 7) flag of a stored tile not yet released
+    int* pending = nullptr;  // flag of the last stored sub tile, released after the loop
+    for (int e = tid; e < T * T; e += kThreads)  // Linv's strict upper part, never written
+      if ((e % T) > (e / T)) Xinv[(e / T) * LDS + (e % T)] = 0.0;
     for (int j = 0; j < ntc; ++j) {
       double* Sd = smem + (j & 1) * (T * LDS);
       double* Snext = smem + ((j + 1) & 1) * (T * LDS);
@@ -629,7 +664,6 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       if ((tid >> 5) == 7) {
         // ---- warp 7: release the pending flag, then prefetch both partials
         const int lane = tid & 31;
-        if (pending != nullptr && lane == 0) bulk_store_release(pending, epoch);
         int want = (has_sub ? 1 : 0) | (has_next ? 2 : 0);
         while (want) {
           int ok = 0;
@@ -639,14 +673,18 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
           }
           ok = __shfl_sync(kFull, ok, 0);
           if (ok & 1) {
-            const double* src = Lt + (size_t)tidx(j + 1, j) * T * T;
-            for (int e = lane; e < T * T / 2; e += 32)
-              cp_async16(Lnext + ((2 * e) / T) * LDS + (2 * e) % T, src + 2 * e);
+            const double* src = Lt + (size_t)tidx(j + 1, j) * TS;
+            for (int e = lane; e < T * T / 2; e += 32) {
+              const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+              cp_async16(Lnext + o, src + o);
+            }
           }
           if (ok & 2) {
-            const double* src = Lt + (size_t)tidx(j + 1, j + 1) * T * T;
-            for (int e = lane; e < T * T / 2; e += 32)
-              cp_async16(Snext + ((2 * e) / T) * LDS + (2 * e) % T, src + 2 * e);
+            const double* src = Lt + (size_t)tidx(j + 1, j + 1) * TS;
+            for (int e = lane; e < T * T / 2; e += 32) {
+              const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+              cp_async16(Snext + o, src + o);
+            }
           }
           if (ok) cp_async_commit();
           want &= ~ok;
@@ -663,33 +701,38 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
         PROF_STAMP(j, 1);
         fence_proxy_async_smem();  // L_jj (Sd) -> the bulk store below
       }
-      pending = nullptr;
       csync();  // L_jj factored; partials in smem
-      if ((tid >> 5) == 7 && (tid & 31) == 0) bulk_store_tile(Lt + (size_t)tidx(j, j) * T * T, Sd);
+      const int lane = tid & 31, w = tid >> 5;
+      if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j, j) * TS, Sd);
       PROF_STAMP(j, 2);
-      int* const fl_jj = &F.full[tidx(j, j)];
+      // Linv_jj: the sub-diagonal TRSMs become products, and the back
+      // substitution uses it
+      trtri64(Xinv, Sd, rinv, cv, Tm, j);
+      // (trtri64 fenced Xinv for the async proxy before its last barrier)
+      if (tid == kThreads - 32) bulk_store_tile(Linv + (size_t)j * TS, Xinv);
       if (!has_sub) {  // last column without a sub-diagonal tile
-        if (tid == kThreads - 32) bulk_store_release(fl_jj, epoch);
+        if (tid == kThreads - 32) bulk_store_release(&F.inv[j], epoch, &F.full[tidx(j, j)]);
         break;
       }
       PROF_STAMP(j, 3);
-      // L(j+1,j) = A(j+1,j) L_jj^-T; warp 7 releases L_jj's flag in the second
-      // solve phase (its stores have drained by then, the fence is short)
-      const int np = (cv + 7) >> 3;
-      auto trsm_hook = [&](int p, int lane) {
-        if (p == min(1, np - 1) && lane == 0) bulk_store_release(fl_jj, epoch);
-      };
-      trsm_blocked(Lnext, Sd, rinv, cv, trsm_hook);
+      {  // L(j+1,j) = A(j+1,j) L_jj^-T = A(j+1,j) Linv_jj^T; then warp 7
+         // releases L_jj and Linv_jj (their bulk stores drained meanwhile)
+        double acc[8][2];
+        gemm_linvT(acc, Lnext, Xinv, w, lane);
+        if (tid == kThreads - 32) bulk_store_release(&F.inv[j], epoch, &F.full[tidx(j, j)]);
+        csync();
+        store_rows8(acc, Lnext, w, lane);
+      }
       PROF_STAMP(j, 4);
       fence_proxy_async_smem();  // L(j+1,j) (Lnext) -> the bulk store
       csync();
-      if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j + 1, j) * T * T, Lnext);
+      if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j + 1, j) * TS, Lnext);
       if (has_next) {
         // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T on warps 0-6; warp 7 releases L(j+1,j)
-        if ((tid >> 5) == 7) {
-          if ((tid & 31) == 0) bulk_store_release(&F.full[tidx(j + 1, j)], epoch);
+        if (w == 7) {
+          if (lane == 0) bulk_store_release(&F.full[tidx(j + 1, j)], epoch);
         } else {
-          syrk64_lower7(Snext, Lnext, tid >> 5, tid & 31);
+          syrk64_lower7(Snext, Lnext, w, lane);
         }
         csync();
       } else {
@@ -707,7 +750,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   }
 
   // ============================== helpers
-  // queue per column j: [P(j+1,j+1)?, P(j+1,j)?, T(j+2..ntr-1, j), I(j)]
+  // queue per column j: [P(j+1,j+1)?, P(j+1,j)?, T(j+2..ntr-1, j)]
+  const int lane = tid & 31, w = tid >> 5;
   for (;;) {
     if (tid == 0) s_task = atomicAdd(&st->tile_counter, 1);
     csync();
@@ -718,24 +762,22 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       const int np1 = (j + 1 < ntc) ? 1 : 0;          // P(j+1,j+1)
       const int np2 = (j + 1 < ntr) ? 1 : 0;          // P(j+1,j)
       const int nT = max(0, ntr - (j + 2));           // T(i,j)
-      const int cnt = np1 + np2 + nT + 1;             // + I(j)
+      const int cnt = np1 + np2 + nT;
       if (t < cnt) {
         if (t < np1) { kind = 0; i = j + 1; }
         else if (t < np1 + np2) { kind = 1; i = j + 1; }
-        else if (t < np1 + np2 + nT) { kind = 2; i = j + 2 + (t - np1 - np2); }
-        else { kind = 3; }
+        else { kind = 2; i = j + 2 + (t - np1 - np2); }
         break;
       }
       t -= cnt;
       ++j;
     }
     if (kind < 0) break;
-    const int cv = min(T, f - j * T);
     if (kind == 0) {                 // P(j+1, j+1): diagonal tile, updates k < j
       gather_tile(S, G, ldg, cvec, Fidx, f, j + 1, j + 1);
       csync();
       left_update(smem, S, Lt, F.full, epoch, j + 1, j + 1, j, &s_ready);
-      store_tile(Lt + (size_t)tidx(j + 1, j + 1) * T * T, S);
+      store_tile(Lt + (size_t)tidx(j + 1, j + 1) * TS, S);
       publish_flag(&F.part[tidx(j + 1, j + 1)], epoch);
       PROF_STAMP(1000 + j + 1, 2);
     } else if (kind == 1) {          // P(j+1, j): updates k < j (the chain does the TRSM)
@@ -743,67 +785,26 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       csync();
       left_update(smem, S, Lt, F.full, epoch, j + 1, j, j, &s_ready);
       PROF_STAMP(1000 + j, 4);
-      store_tile(Lt + (size_t)tidx(j + 1, j) * T * T, S);
+      store_tile(Lt + (size_t)tidx(j + 1, j) * TS, S);
       publish_flag(&F.part[tidx(j + 1, j)], epoch);
       PROF_STAMP(1000 + j, 0);
-    } else if (kind == 2) {          // T(i, j): updates k < j, then TRSM with L_jj
+    } else {                         // T(i, j): updates k < j, then L(i,j) = A(i,j) Linv_jj^T
       gather_tile(S, G, ldg, cvec, Fidx, f, i, j);
       csync();
       left_update(smem, S, Lt, F.full, epoch, i, j, j, &s_ready);
       double* LB = smem + T * LDS;
-      if (tid == 0) wait_flag(&F.full[tidx(j, j)], epoch);
+      if (tid == 0) wait_flag(&F.inv[j], epoch);
       csync();
-      load_tile(LB, Lt + (size_t)tidx(j, j) * T * T);
+      load_tile(LB, Linv + (size_t)j * TS);
       csync();
-      diag_recip(LB, rinv, cv);
+      double acc[8][2];
+      gemm_linvT(acc, S, LB, w, lane);
       csync();
-      trsm_blocked(S, LB, rinv, cv);
-      store_tile(Lt + (size_t)tidx(i, j) * T * T, S);
+      store_rows8(acc, S, w, lane);
+      csync();
+      store_tile(Lt + (size_t)tidx(i, j) * TS, S);
       publish_flag(&F.full[tidx(i, j)], epoch);
       if (i == j + 2) PROF_STAMP(1000 + j + 1, 1);
-    } else {                         // I(j): Linv_jj for the back substitution
-      double* X = smem + T * LDS;
-      double* X11t = smem + 2 * T * LDS;
-      double* Tmt = smem + 3 * T * LDS;
-      const int lane = tid & 31, w = tid >> 5;
-      if (tid == 0) wait_flag(&F.full[tidx(j, j)], epoch);
-      csync();
-      load_tile(S, Lt + (size_t)tidx(j, j) * T * T);
-      csync();
-      diag_recip(S, rinv, cv);
-      csync();
-      const int n1 = min(32, cv), n2 = cv - 32;
-      if (w == 0) {
-        warp_trtri32(S, rinv, n1, lane, X, X11t);
-      } else if (w == 1) {
-        if (n2 > 0) warp_trtri32(S + 32 * LDS + 32, rinv + 32, n2, lane, X + 32 * LDS + 32, nullptr);
-        else
-          for (int r = 0; r < 32; ++r) X[(32 + r) * LDS + 32 + lane] = 0.0;
-      }
-      csync();
-      if (w < 4) {  // Tm = L21 X11 (stored transposed)
-        double acc[4][2] = {};
-        dmma32(acc, S + 32 * LDS, X11t, lane, w);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) Tmt[(8 * q + 2 * (lane & 3) + v) * LDS + 8 * w + (lane >> 2)] = acc[q][v];
-      }
-      csync();
-      if (w < 4) {  // Linv21 = -X22 Tm
-        double acc[4][2] = {};
-        dmma32(acc, X + 32 * LDS + 32, Tmt, lane, w);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int v = 0; v < 2; ++v)
-            X[(32 + 8 * w + (lane >> 2)) * LDS + 8 * q + 2 * (lane & 3) + v] = -acc[q][v];
-      } else {
-        for (int e = tid - 128; e < 32 * 32; e += 128) X[(e >> 5) * LDS + 32 + (e & 31)] = 0.0;
-      }
-      csync();
-      store_tile(Linv + (size_t)j * T * T, X);
-      publish_flag(&F.inv[j], epoch);
     }
   }
 }
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
                                                                    DevState* st) {
   extern __shared__ double bsm[];
   double* Lnext = bsm;        // L(J+1, J): the only tile on the critical path
-  double* Xinv = bsm + T * T; // Linv(J, J)
+  double* Xinv = bsm + TS;    // Linv(J, J)
   __shared__ double part[4 * T];
   __shared__ double s_rhs[T];
   __shared__ double s_x[T];
@@ -843,12 +844,12 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
     const int J = ntc - 1 - t;
     const int cv = min(T, f - J * T);
     // prefetch the critical-path tiles (the factorization is complete)
-    for (int e = tid; e < T * T / 2; e += kThreads) {
-      cp_async16(Xinv + 2 * e, Linv + (size_t)J * T * T + 2 * e);
-      if (J + 1 < ntc) cp_async16(Lnext + 2 * e, Lt + (size_t)tidx(J + 1, J) * T * T + 2 * e);
+    for (int e = tid; e < TS / 2; e += kThreads) {  // (whole padded tiles)
+      cp_async16(Xinv + 2 * e, Linv + (size_t)J * TS + 2 * e);
+      if (J + 1 < ntc) cp_async16(Lnext + 2 * e, Lt + (size_t)tidx(J + 1, J) * TS + 2 * e);
     }
     cp_async_commit();
-    if (tid < T) s_rhs[tid] = (tid < cv) ? __ldcg(&Lt[(size_t)tidx(Rf, J) * T * T + rf * T + tid]) : 0.0;
+    if (tid < T) s_rhs[tid] = (tid < cv) ? __ldcg(&Lt[(size_t)tidx(Rf, J) * TS + rf * LDS + tid]) : 0.0;
     __syncthreads();
     // subtract L_IJ^T x_I for I = ntc-1 .. J+2 straight from L2 (off the critical path)
     for (int I = ntc - 1; I > J + 1; --I) {
@@ -857,9 +858,9 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
       const int rvI = min(T, f - I * T);  // rows of L_IJ that are < f
       if (tid < T) s_x[tid] = (tid < rvI) ? __ldcg(&xF[I * T + tid]) : 0.0;
       __syncthreads();
-      const double* L = Lt + (size_t)tidx(I, J) * T * T;
+      const double* L = Lt + (size_t)tidx(I, J) * TS;
       double p = 0.0;
-      for (int r = rg; r < rvI; r += 4) p = fma(__ldcg(&L[r * T + c]), s_x[r], p);
+      for (int r = rg; r < rvI; r += 4) p = fma(__ldcg(&L[r * LDS + c]), s_x[r], p);
       part[rg * T + c] = p;
       __syncthreads();
       if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
@@ -875,7 +876,7 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
       __syncthreads();
       double p = 0.0;
 #pragma unroll 4
-      for (int r = rg; r < T; r += 4) p = fma(Lnext[r * T + c], s_x[r], p);
+      for (int r = rg; r < T; r += 4) p = fma(Lnext[r * LDS + c], s_x[r], p);
       part[rg * T + c] = p;
       __syncthreads();
       if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
     // x_J = Linv_JJ^T s : x[c] = sum_{r >= c} Linv[r][c] s[r]  (Linv is zero beyond cv)
     double p = 0.0;
 #pragma unroll 4
-    for (int r = rg; r < T; r += 4) p = fma(Xinv[r * T + c], s_rhs[r], p);
+    for (int r = rg; r < T; r += 4) p = fma(Xinv[r * LDS + c], s_rhs[r], p);
     part[rg * T + c] = p;
     __syncthreads();
     if (tid < cv) xF[J * T + tid] = (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
@@ -901,7 +902,7 @@ static cudaError_t set_attrs() {
                                        (int)(sizeof(double) * kSmemDoubles));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(double) * 2 * T * T));
+                           (int)(sizeof(double) * 2 * TS));
   if (e != cudaSuccess) return e;
   attr_set = true;
   return cudaSuccess;
@@ -916,7 +917,7 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   int grid = sm_count;  // ~204 KB smem per CTA: one persistent CTA per SM
   if (grid > tasks) grid = tasks;
   if (grid < 2) grid = 2;
-  double* Linv = Lt + (size_t)tri_tiles(n) * T * T;
+  double* Linv = Lt + (size_t)tri_tiles(n) * TS;
   chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, Linv,
                                                                           flags, tri_tiles(n), st);
   return cudaGetLastError();
@@ -926,11 +927,11 @@ cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* x
                                   int sm_count, cudaStream_t s) {
   const int ntr = (n + 1 + T - 1) / T;
   int* xflags = flags + 2 * tri_tiles(n) + (n + 1 + T - 1) / T;
-  const double* Linv = Lt + (size_t)tri_tiles(n) * T * T;
+  const double* Linv = Lt + (size_t)tri_tiles(n) * TS;
   const int g2 = ntr < sm_count ? ntr : sm_count;
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
-  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * 2 * T * T, s>>>(Lt, Linv, xflags, xF, st);
+  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * 2 * TS, s>>>(Lt, Linv, xflags, xF, st);
   return cudaGetLastError();
 }
 

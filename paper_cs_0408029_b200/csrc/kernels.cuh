@@ -53,7 +53,7 @@ cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const 
                         double* y, double tol, DevState* st, int sm_count, cudaStream_t s);
 
 // ---- a5/a6 Cholesky + solves (cholesky.cu) -------------------------------
-size_t chol_tile_count(int n);
+size_t chol_tile_doubles(int n);
 size_t chol_flag_count(int n);
 cudaError_t chol_debug_set_profile(unsigned long long* p);  // tiles needed for |F| <= n (bordered, lower)
 // Factor the bordered matrix [[G_FF, .], [c_F^T, .]] (gathered from G via
