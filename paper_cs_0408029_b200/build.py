@@ -26,7 +26,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        # NNLS_EXTRA_NVCC_FLAGS: development A/B switches (e.g. -DNAME), empty by default
+        extra = os.environ.get("NNLS_EXTRA_NVCC_FLAGS", "").split()
+        cmd = [nvcc, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

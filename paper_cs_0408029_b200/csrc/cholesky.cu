@@ -334,19 +334,19 @@ __device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
   return *s_bad;
 }
 
-// Y (lower 8x8 blocks of a 64x64 tile) -= X X^T, K = 64, on warps 0..6:
-// block b = I(I+1)/2 + J goes to warp b % 7 (slot b / 7); warps with 5
-// blocks repeat one as a dummy 6th (result dropped), so the 6 independent
+// Y (lower 8x8 blocks of a 64x64 tile) -= X X^T, K = 64, on all 8 warps:
+// block b = I(I+1)/2 + J goes to warp b % 8 (slot b / 8); warps with 4
+// blocks repeat one as a dummy 5th (result dropped), so the 5 independent
 // 16-step DMMA chains of a warp are unconditional.
-__device__ __forceinline__ void syrk64_lower7(double* __restrict__ Y, const double* __restrict__ X, int w,
+__device__ __forceinline__ void syrk64_lower(double* __restrict__ Y, const double* __restrict__ X, int w,
                                              int lane) {
-  if (w >= 7) return;
+  constexpr int NS = 5;
   const int kq = lane & 3, rq = lane >> 2;
-  int ra[6], rb[6], ci[6];
+  int ra[NS], rb[NS], ci[NS];
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    int b = w + 7 * q;
-    if (b > 35) b = w + 7 * (q - 1);  // dummy slot
+  for (int q = 0; q < NS; ++q) {
+    int b = w + 8 * q;
+    if (b > 35) b = w + 8 * (q - 1);  // dummy slot
     int I = 0;
     while ((I + 1) * (I + 2) / 2 <= b) ++I;
     const int J = b - I * (I + 1) / 2;
@@ -354,24 +354,24 @@ __device__ __forceinline__ void syrk64_lower7(double* __restrict__ Y, const doub
     rb[q] = (8 * J + rq) * LDS + kq;
     ci[q] = (8 * I + rq) * LDS + 8 * J + 2 * kq;
   }
-  double cv0[6], cv1[6];
+  double cv0[NS], cv1[NS];
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
+  for (int q = 0; q < NS; ++q) {
     cv0[q] = Y[ci[q]];
     cv1[q] = Y[ci[q] + 1];
   }
 #pragma unroll 4
   for (int kk = 0; kk < T; kk += 4) {
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
+    for (int q = 0; q < NS; ++q) {
       const double av = -X[ra[q] + kk];
       const double bv = X[rb[q] + kk];
       dmma8x8x4(cv0[q], cv1[q], av, bv);
     }
   }
-  const int nq = (w == 0) ? 6 : 5;
+  const int nq = (w < 4) ? 5 : 4;
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
+  for (int q = 0; q < NS; ++q) {
     if (q < nq) {
       Y[ci[q]] = cv0[q];
       Y[ci[q] + 1] = cv1[q];
@@ -474,7 +474,6 @@ __device__ __forceinline__ void trtri64(double* __restrict__ X, const double* __
     for (int i = 0; i < 8; ++i) X[(c0 + i) * LDS + c0 + lane] = x[i];
   }
   csync();
-  PROF_STAMP(pj, 6);
   trtri_level<8>(X, L, Tm, w, lane);
   trtri_level<16>(X, L, Tm, w, lane);
   PROF_STAMP(pj, 7);
@@ -645,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     double* Xinv = smem + 2 * (T * LDS);  // Linv_jj
     double* Tm = smem + 3 * (T * LDS);    // trtri scratch
     int first_bad = -1;
-    int* pending = nullptr;  // flag of the last stored sub tile, released after the loop
+    int* pending = nullptr;  // (tid 224) flag of the last stored sub tile, not yet released
     for (int e = tid; e < T * T; e += kThreads)  // Linv's strict upper part, never written
       if ((e % T) > (e / T)) Xinv[(e / T) * LDS + (e % T)] = 0.0;
     for (int j = 0; j < ntc; ++j) {
@@ -664,6 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       if ((tid >> 5) == 7) {
         // ---- warp 7: release the pending flag, then prefetch both partials
         const int lane = tid & 31;
+        if (pending != nullptr && lane == 0) bulk_store_release(pending, epoch);
+        pending = nullptr;
         int want = (has_sub ? 1 : 0) | (has_next ? 2 : 0);
         while (want) {
           int ok = 0;
@@ -728,16 +729,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       csync();
       if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j + 1, j) * TS, Lnext);
       if (has_next) {
-        // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T on warps 0-6; warp 7 releases L(j+1,j)
-        if (w == 7) {
-          if (lane == 0) bulk_store_release(&F.full[tidx(j + 1, j)], epoch);
-        } else {
-          syrk64_lower7(Snext, Lnext, w, lane);
-        }
+        // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T on all warps
+        syrk64_lower(Snext, Lnext, w, lane);
+        PROF_STAMP(j, 6);
         csync();
-      } else {
-        pending = &F.full[tidx(j + 1, j)];
       }
+      pending = &F.full[tidx(j + 1, j)];  // released by warp 7 in the next POTRF (or below)
       PROF_STAMP(j, 5);
     }
     if (pending != nullptr && tid == kThreads - 32) bulk_store_release(pending, epoch);  // last sub tile
