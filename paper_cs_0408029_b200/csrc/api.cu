@@ -88,6 +88,7 @@ struct nnls_handle {
   Buf colptr, rowind, cvals, cursor, tmp_row, tmp_val;  // CSC
   Buf Gc;                                 // G (n x ldg) followed by c (n)
   Buf mask, x, y, xF, Fidx, Gidx;         // pivot state
+  Buf pos, Fs, xs;                        // factor reuse: order positions, F sorted, x_F by index
   Buf Lt, flags;                          // Cholesky tiles + DAG flags
   Buf U, V, W, X, R, partials, xfin;      // LSQR / report
   Buf Fval, Fcol, Fcnt;                   // A restricted to the final F (cluster LSQR)
@@ -96,6 +97,7 @@ struct nnls_handle {
   HostState* h = nullptr;                 // pinned readback
   bool no_cluster = false;  // force the full-grid LSQR (tests / env NNLS_NO_CLUSTER)
   bool no_graph = false;    // host-driven pivot loop (env NNLS_NO_GRAPH, or capture failed)
+  bool no_reuse = false;    // F in index order, no factor reuse across iterations (env NNLS_NO_REUSE)
   cudaGraphExec_t gexec = nullptr;
   std::vector<double> gkey;
   cudaStream_t gstream = nullptr;
@@ -212,6 +214,9 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->xF, sizeof(double) * (size_t)(n + kTile)));
   CK(ensure(h->Fidx, sizeof(int32_t) * (size_t)n));
   CK(ensure(h->Gidx, sizeof(int32_t) * (size_t)n));
+  CK(ensure(h->pos, sizeof(int32_t) * (size_t)n));
+  CK(ensure(h->Fs, sizeof(int32_t) * (size_t)n));
+  CK(ensure(h->xs, sizeof(double) * (size_t)n));
   const size_t nflags = chol_flag_count(n);
   if (h->flags.cap < sizeof(int) * nflags) {
     CK(ensure(h->flags, sizeof(int) * nflags));
@@ -299,6 +304,7 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
   memset(h->h, 0, sizeof(HostState));
   h->no_cluster = getenv("NNLS_NO_CLUSTER") != nullptr;
   h->no_graph = getenv("NNLS_NO_GRAPH") != nullptr;
+  h->no_reuse = getenv("NNLS_NO_REUSE") != nullptr;
   *out = h;
   return NNLS_OK;
 }
@@ -498,6 +504,10 @@ cudaError_t launch_lsqr(nnls_handle* h, cudaStream_t s) {
   return e;
 }
 
+int32_t* pos_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<int32_t>(h->pos); }
+int32_t* fs_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<int32_t>(h->Fs); }
+double* xs_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<double>(h->xs); }
+
 // one pivot iteration: decide -> (gather + Cholesky + forward) -> back solve -> dual
 cudaError_t launch_iteration(nnls_handle* h, cudaStream_t s, const cudaGraphConditionalHandle* loop) {
   const int n = h->n;
@@ -506,15 +516,18 @@ cudaError_t launch_iteration(nnls_handle* h, cudaStream_t s, const cudaGraphCond
   DevState* st = P<DevState>(h->st);
   TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
   cudaError_t e = launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
-                                P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s, loop);
+                                P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s, loop,
+                                pos_or_null(h), fs_or_null(h));
   if (e == cudaSuccess)
     e = launch_chol_factor(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt), P<int>(h->flags), st,
                            h->sms, s);
   if (e == cudaSuccess)
-    e = launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st, h->sms, s);
+    e = launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st, h->sms, s,
+                              P<int32_t>(h->Fidx), xs_or_null(h));
   if (e == cudaSuccess)
     e = launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
-                    P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), h->prm.zero_tol, st, h->sms, s);
+                    P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), h->prm.zero_tol, st, h->sms, s,
+                    fs_or_null(h), xs_or_null(h));
   return e;
 }
 
@@ -525,9 +538,10 @@ std::vector<double> graph_key(nnls_handle* h) {
                            (double)h->h->plan[0], (double)h->h->plan[1], (double)h->h->plan[2],
                            (double)h->h->plan[3], p.zero_tol, (double)p.p_max, (double)p.max_iter,
                            (double)p.lsqr_mode, (double)p.lsqr_itn_limit, p.lsqr_atol, p.lsqr_btol,
-                           p.lsqr_conlim, (double)p.kkt, (double)h->trace_cap, (double)h->no_cluster};
+                           p.lsqr_conlim, (double)p.kkt, (double)h->trace_cap, (double)h->no_cluster,
+                           (double)h->no_reuse};
   const Buf* bufs[] = {&h->rowptr, &h->colind, &h->vals, &h->b, &h->colptr, &h->rowind, &h->cvals,
-                       &h->Gc, &h->mask, &h->x, &h->y, &h->xF, &h->Fidx, &h->Gidx, &h->Lt, &h->flags,
+                       &h->Gc, &h->mask, &h->x, &h->y, &h->xF, &h->Fidx, &h->Gidx, &h->pos, &h->Fs, &h->xs, &h->Lt, &h->flags,
                        &h->U, &h->V, &h->W, &h->X, &h->R, &h->partials, &h->xfin, &h->st, &h->trace,
                        &h->Fval, &h->Fcol, &h->Fcnt};
   for (const Buf* b : bufs) k.push_back((double)(uintptr_t)b->p);
@@ -569,7 +583,7 @@ cudaError_t build_graph(nnls_handle* h, cudaStream_t s) {
   GDBG("begin1");
   if (e == cudaSuccess) {
     cudaError_t el = launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol,
-                                 P<DevState>(h->st), p.p_max, max_iter, s);
+                                 P<DevState>(h->st), p.p_max, max_iter, s, pos_or_null(h));
     cudaGraph_t gg = g;
     e = cudaStreamEndCapture(s, &gg);
     if (e == cudaSuccess) e = el;
@@ -662,12 +676,13 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   if (!done_graph) {
     TIMED(NNLS_PH_INIT, 1,
           launch_init(n, c, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
-                      p.p_max, max_iter, s));
+                      p.p_max, max_iter, s, pos_or_null(h)));
     TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
     for (;;) {
       TIMED(NNLS_PH_DECIDE, 1,
             launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
-                          P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s));
+                          P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s, nullptr,
+                          pos_or_null(h), fs_or_null(h)));
       nnls_status rs = read_state(h);
       if (rs != NNLS_OK) return rs;
       const DevState& hs = h->h->st;
@@ -678,12 +693,12 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
                                  P<int>(h->flags), st, h->sms, s));
         TIMED(NNLS_PH_CHOL_SOLVE, 1,
               launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st,
-                                    h->sms, s));
+                                    h->sms, s, P<int32_t>(h->Fidx), xs_or_null(h)));
       }
       TIMED(NNLS_PH_DUAL, 1,
             launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
                         P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
-                        h->sms, s));
+                        h->sms, s, fs_or_null(h), xs_or_null(h)));
     }
     {
       const int ib = tm_begin(h);

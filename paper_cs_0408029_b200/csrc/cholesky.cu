@@ -569,10 +569,11 @@ __device__ __forceinline__ void gather_tile(double* __restrict__ S, const double
 }
 
 // S (smem tile i,jj) -= sum_{k < kmax} L(i,k) L(jj,k)^T, operands double-
-// buffered through BUF(1..4) with cp.async (waits on the "full" flags).
+// buffered through BUF(1..4) with cp.async (waits on the "full" flags; tiles
+// in rows < jq are kept from the previous factorization and need none).
 __device__ __forceinline__ void left_update(double* __restrict__ smem, double* __restrict__ S,
                                             const double* __restrict__ Lt, const int* __restrict__ full,
-                                            int epoch, int i, int jj, int kmax, int* s_ready) {
+                                            int epoch, int i, int jj, int kmax, int jq, int* s_ready) {
   if (kmax <= 0) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
@@ -584,8 +585,8 @@ __device__ __forceinline__ void left_update(double* __restrict__ smem, double* _
     double* LB = smem + ((k & 1) ? 4 : 2) * (T * LDS);
     if (!have_next) {
       if (tid == 0) {
-        wait_flag(&full[tidx(i, k)], epoch);
-        wait_flag(&full[tidx(jj, k)], epoch);
+        if (i >= jq) wait_flag(&full[tidx(i, k)], epoch);
+        if (jj >= jq) wait_flag(&full[tidx(jj, k)], epoch);
       }
       csync();
       tile_async(LA, Lt + (size_t)tidx(i, k) * TS);
@@ -595,7 +596,8 @@ __device__ __forceinline__ void left_update(double* __restrict__ smem, double* _
     have_next = false;
     if (k + 1 < kmax) {
       if (tid == 0)
-        *s_ready = (ld_acquire(&full[tidx(i, k + 1)]) == epoch) && (ld_acquire(&full[tidx(jj, k + 1)]) == epoch);
+        *s_ready = (i < jq || ld_acquire(&full[tidx(i, k + 1)]) == epoch) &&
+                   (jj < jq || ld_acquire(&full[tidx(jj, k + 1)]) == epoch);
       csync();
       if (*s_ready) {
         tile_async(smem + ((k & 1) ? 1 : 3) * (T * LDS), Lt + (size_t)tidx(i, k + 1) * TS);
@@ -627,6 +629,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   const int epoch = st->epoch;
   if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
   const int ntc = (f + T - 1) / T;      // tile columns to factor
+  // tile columns [0, jq) of rows [0, jq) are kept from the previous pivot
+  // iteration (same order prefix, see order_free_set in pivot.cu)
+  const int jq = (st->reuse_cols > 0 && st->reuse_cols < ntc) ? st->reuse_cols : 0;
   const int ntr = (f + 1 + T - 1) / T;  // tile rows (incl. the rhs row f)
   FlagSet F{flags, flags + tri, flags + 2 * tri};
   const int tid = threadIdx.x;
@@ -647,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     int* pending = nullptr;  // (tid 224) flag of the last stored sub tile, not yet released
     for (int e = tid; e < T * T; e += kThreads)  // Linv's strict upper part, never written
       if ((e % T) > (e / T)) Xinv[(e / T) * LDS + (e % T)] = 0.0;
-    for (int j = 0; j < ntc; ++j) {
+    for (int j = jq; j < ntc; ++j) {
       double* Sd = smem + (j & 1) * (T * LDS);
       double* Snext = smem + ((j + 1) & 1) * (T * LDS);
       const int cv = min(T, f - j * T), rv = min(T, f + 1 - j * T);
@@ -657,6 +662,11 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       PROF_STAMP(j, 0);
       if (j == 0) {
         gather_tile(Sd, G, ldg, cvec, Fidx, f, 0, 0);
+        csync();
+      } else if (j == jq) {  // restart after a kept prefix: A_jj fully updated by a helper
+        if (tid == 0) wait_flag(&F.part[tidx(j, j)], epoch);
+        csync();
+        load_tile(Sd, Lt + (size_t)tidx(j, j) * TS);
         csync();
       }
       // (j > 0: Sd holds A_jj fully updated at the end of the previous column)
@@ -747,15 +757,29 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   }
 
   // ============================== helpers
-  // queue per column j: [P(j+1,j+1)?, P(j+1,j)?, T(j+2..ntr-1, j)]
+  // queue: with a kept prefix (jq > 0) first the rows below it in the kept
+  // columns, [T(jq..ntr-1, j) for j < jq], then D(jq) = tile (jq,jq) with
+  // all its updates k < jq (the chain starts there); then per column j >= jq:
+  // [P(j+1,j+1)?, P(j+1,j)?, T(j+2..ntr-1, j)]
   const int lane = tid & 31, w = tid >> 5;
   for (;;) {
     if (tid == 0) s_task = atomicAdd(&st->tile_counter, 1);
     csync();
     int t = s_task;
     csync();
-    int j = 0, kind = -1, i = 0;
-    while (j < ntc) {
+    int j = jq, kind = -1, i = 0;
+    if (jq > 0) {
+      const int nr = ntr - jq;
+      if (t < jq * nr) {
+        kind = 2;
+        j = t / nr;
+        i = jq + t % nr;
+      } else if (t == jq * nr) {
+        kind = 3;
+      }
+      t -= jq * nr + 1;
+    }
+    while (kind < 0 && j < ntc) {
       const int np1 = (j + 1 < ntc) ? 1 : 0;          // P(j+1,j+1)
       const int np2 = (j + 1 < ntr) ? 1 : 0;          // P(j+1,j)
       const int nT = max(0, ntr - (j + 2));           // T(i,j)
@@ -770,17 +794,25 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       ++j;
     }
     if (kind < 0) break;
+    if (kind == 3) {                 // D(jq): diagonal tile jq, all updates k < jq
+      gather_tile(S, G, ldg, cvec, Fidx, f, jq, jq);
+      csync();
+      left_update(smem, S, Lt, F.full, epoch, jq, jq, jq, jq, &s_ready);
+      store_tile(Lt + (size_t)tidx(jq, jq) * TS, S);
+      publish_flag(&F.part[tidx(jq, jq)], epoch);
+      continue;
+    }
     if (kind == 0) {                 // P(j+1, j+1): diagonal tile, updates k < j
       gather_tile(S, G, ldg, cvec, Fidx, f, j + 1, j + 1);
       csync();
-      left_update(smem, S, Lt, F.full, epoch, j + 1, j + 1, j, &s_ready);
+      left_update(smem, S, Lt, F.full, epoch, j + 1, j + 1, j, jq, &s_ready);
       store_tile(Lt + (size_t)tidx(j + 1, j + 1) * TS, S);
       publish_flag(&F.part[tidx(j + 1, j + 1)], epoch);
       PROF_STAMP(1000 + j + 1, 2);
     } else if (kind == 1) {          // P(j+1, j): updates k < j (the chain does the TRSM)
       gather_tile(S, G, ldg, cvec, Fidx, f, j + 1, j);
       csync();
-      left_update(smem, S, Lt, F.full, epoch, j + 1, j, j, &s_ready);
+      left_update(smem, S, Lt, F.full, epoch, j + 1, j, j, jq, &s_ready);
       PROF_STAMP(1000 + j, 4);
       store_tile(Lt + (size_t)tidx(j + 1, j) * TS, S);
       publish_flag(&F.part[tidx(j + 1, j)], epoch);
@@ -788,9 +820,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     } else {                         // T(i, j): updates k < j, then L(i,j) = A(i,j) Linv_jj^T
       gather_tile(S, G, ldg, cvec, Fidx, f, i, j);
       csync();
-      left_update(smem, S, Lt, F.full, epoch, i, j, j, &s_ready);
+      left_update(smem, S, Lt, F.full, epoch, i, j, j, jq, &s_ready);
       double* LB = smem + T * LDS;
-      if (tid == 0) wait_flag(&F.inv[j], epoch);
+      if (tid == 0 && j >= jq) wait_flag(&F.inv[j], epoch);  // (a kept column's Linv is in place)
       csync();
       load_tile(LB, Linv + (size_t)j * TS);
       csync();
@@ -818,7 +850,9 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
                                                                    const double* __restrict__ Linv,
                                                                    int* __restrict__ xflags,
                                                                    double* __restrict__ xF,
-                                                                   DevState* st) {
+                                                                   DevState* st,
+                                                                   const int32_t* __restrict__ Fidx,
+                                                                   double* __restrict__ xs) {
   extern __shared__ double bsm[];
   double* Lnext = bsm;        // L(J+1, J): the only tile on the critical path
   double* Xinv = bsm + TS;    // Linv(J, J)
@@ -885,7 +919,11 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* 
     for (int r = rg; r < T; r += 4) p = fma(Xinv[r * LDS + c], s_rhs[r], p);
     part[rg * T + c] = p;
     __syncthreads();
-    if (tid < cv) xF[J * T + tid] = (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
+    if (tid < cv) {
+      const double v = (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
+      xF[J * T + tid] = v;
+      if (xs != nullptr) xs[Fidx[J * T + tid]] = v;
+    }
     __threadfence();
     __syncthreads();
     if (tid == 0) st_release(&xflags[J], epoch);
@@ -921,14 +959,14 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
 }
 
 cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
-                                  int sm_count, cudaStream_t s) {
+                                  int sm_count, cudaStream_t s, const int32_t* Fidx, double* xs) {
   const int ntr = (n + 1 + T - 1) / T;
   int* xflags = flags + 2 * tri_tiles(n) + (n + 1 + T - 1) / T;
   const double* Linv = Lt + (size_t)tri_tiles(n) * TS;
   const int g2 = ntr < sm_count ? ntr : sm_count;
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
-  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * 2 * TS, s>>>(Lt, Linv, xflags, xF, st);
+  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * 2 * TS, s>>>(Lt, Linv, xflags, xF, st, Fidx, xs);
   return cudaGetLastError();
 }
 

@@ -32,7 +32,8 @@ struct DevState {
   // final-step report
   int32_t lsqr_iterations, lsqr_stop, infeasible_after_lsqr, free_count;
   double objective, kkt_min_x, kkt_min_y, kkt_max_comp, kkt_dot;
-  int32_t pad[2];
+  int32_t reuse_cols;   // leading tile columns of the last factor still valid (factor reuse)
+  int32_t pad1;
 };
 
 struct TraceRec {

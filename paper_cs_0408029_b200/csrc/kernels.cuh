@@ -38,19 +38,27 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
 
 // ---- a2/a3/a4/a7/a8 pivot steps (pivot.cu) -----------------------------
 cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double* y, double tol,
-                        DevState* st, int p_max, int max_iter, cudaStream_t s);
+                        DevState* st, int p_max, int max_iter, cudaStream_t s, int32_t* pos = nullptr);
 // count + decide + exchange + compaction (one CTA); records trace[iter] head.
 // loop != nullptr: the kernel runs inside a CUDA-graph WHILE node and clears
 // its condition when the pivot loop ends (feasible, limit, or failure).
+// pos == nullptr: Fidx = F in index order.  pos != nullptr (factor reuse):
+// pos[i] = position of i in the previous factorization order (-1: not in
+// F); Fidx keeps the previous order's longest prefix that survived the
+// exchange and appends the rest by predicted stability; st->reuse_cols =
+// the whole tile columns of that prefix (see cholesky.cu).
 cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
                           int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
-                          cudaStream_t s, const cudaGraphConditionalHandle* loop = nullptr);
+                          cudaStream_t s, const cudaGraphConditionalHandle* loop = nullptr,
+                          int32_t* pos = nullptr, int32_t* Fs = nullptr);
 cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t* Fidx,
                            int32_t* Gidx, double* xF, DevState* st, cudaStream_t s);
 // y_G = G_GF x_F - c_G (Gram form of Eq. 5), zeroing, scatter x_F into x.
+// Fs/xs (factor reuse): F in index order and x_F scattered by index.
 cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
                         const int32_t* Gidx, const double* xF, uint8_t* mask, double* x,
-                        double* y, double tol, DevState* st, int sm_count, cudaStream_t s);
+                        double* y, double tol, DevState* st, int sm_count, cudaStream_t s,
+                        const int32_t* Fs = nullptr, const double* xs = nullptr);
 
 // ---- a5/a6 Cholesky + solves (cholesky.cu) -------------------------------
 size_t chol_tile_doubles(int n);
@@ -63,8 +71,10 @@ cudaError_t launch_cholesky_solve(int n, const double* G, int ldg, const double*
                                   DevState* st, int sm_count, cudaStream_t s);
 cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
                                double* Lt, int* flags, DevState* st, int sm_count, cudaStream_t s);
+// xs != nullptr: also xs[Fidx[a]] = x_F[a] (the dual's index-order view)
 cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
-                                  int sm_count, cudaStream_t s);
+                                  int sm_count, cudaStream_t s, const int32_t* Fidx = nullptr,
+                                  double* xs = nullptr);
 
 // ---- a10 LSQR + final report (lsqr.cu) ----------------------------------
 struct LsqrArgs {

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -15,9 +17,10 @@ namespace nnls {
 
 // ---------------------------------------------------------------- init (a2)
 __global__ void init_kernel(int n, const double* __restrict__ c, uint8_t* mask, double* x,
-                            double* y, double tol, DevState* st, int p_max, int max_iter) {
+                            double* y, double tol, DevState* st, int p_max, int max_iter, int32_t* pos) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     mask[i] = 0;
+    if (pos != nullptr) pos[i] = -1;
     x[i] = 0.0;
     const double v = -c[i];
     y[i] = fabs(v) < tol ? 0.0 : v;  // reading c2: the initial y is zeroed too
@@ -41,15 +44,16 @@ __global__ void init_kernel(int n, const double* __restrict__ c, uint8_t* mask, 
     st->lsqr_iterations = 0;
     st->lsqr_stop = 0;
     st->infeasible_after_lsqr = 0;
+    st->reuse_cols = 0;
   }
 }
 
 cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double* y, double tol,
-                        DevState* st, int p_max, int max_iter, cudaStream_t s) {
+                        DevState* st, int p_max, int max_iter, cudaStream_t s, int32_t* pos) {
   int blocks = (n + 255) / 256;
   if (blocks > 1024) blocks = 1024;
   if (blocks < 1) blocks = 1;
-  init_kernel<<<blocks, 256, 0, s>>>(n, c, mask, x, y, tol, st, p_max, max_iter);
+  init_kernel<<<blocks, 256, 0, s>>>(n, c, mask, x, y, tol, st, p_max, max_iter, pos);
   return cudaGetLastError();
 }
 
@@ -103,20 +107,181 @@ __device__ void block_compact(int n, const uint8_t* __restrict__ mask, int32_t* 
   }
 }
 
+// ------------------------------------------- factorization order (reuse)
+// The Cholesky factor of the permuted (A^T A)_FF is as valid as that of the
+// sorted one (the paper's TAUCS / colamd solvers factor permuted matrices,
+// P:131); choosing the order lets consecutive pivot iterations share
+// a factor prefix: if the first q members of the previous order are all
+// still in F, the leading q x q block of L -- and every tile of it -- is
+// unchanged (left-looking Cholesky: column k of L only depends on the
+// leading (k+1) x (k+1) block).  New order = that prefix, then the other
+// members of F sorted by predicted stability: old members by decreasing x
+// (those with x near 0 are the likeliest to leave next), then the newly
+// added ones in index order -- so the first factorization is in index order,
+// exactly the oracle's.  (|F|, the iterates and the termination are those of
+// P:86-104; only rounding differs.)
+constexpr int kOrderMax = 8192;  // largest sorted tail; longer tails stay in index order
+
+constexpr int kDecideThreads = 1024;
+__device__ __forceinline__ unsigned order_key(double v) {  // monotone 16-bit key of (float)v
+  unsigned u = __float_as_uint((float)v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return u >> 16;
+}
+template <int IPT>
+using TailSort = cub::BlockRadixSort<unsigned, kDecideThreads, IPT, int>;  // 4 passes of 4 bits
+
+template <int IPT>
+__device__ void sort_tail(int32_t* __restrict__ tail, int r, const double* __restrict__ x,
+                          const int32_t* __restrict__ pos, void* smem) {
+  unsigned key[IPT];
+  int val[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {  // blocked: element e = tid * IPT + k (index order)
+    const int e = threadIdx.x * IPT + k;
+    if (e < r) {
+      const int i = tail[e];
+      key[k] = pos[i] >= 0 ? order_key(-x[i]) : 0xFFFFu;
+      val[k] = i;
+    } else {
+      key[k] = 0xFFFFu;  // after every real element (stable)
+      val[k] = -1;
+    }
+  }
+  __syncthreads();  // (tail[] is rewritten below)
+  TailSort<IPT>(*reinterpret_cast<typename TailSort<IPT>::TempStorage*>(smem))
+      .SortBlockedToStriped(key, val, 0, 16);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {  // striped: rank = k * threads + tid
+    const int rank = k * kDecideThreads + threadIdx.x;
+    if (rank < r) tail[rank] = val[k];
+  }
+}
+constexpr size_t kTailSortSmem = sizeof(typename TailSort<kOrderMax / kDecideThreads>::TempStorage) >
+                                         sizeof(typename TailSort<1>::TempStorage)
+                                     ? sizeof(typename TailSort<kOrderMax / kDecideThreads>::TempStorage)
+                                     : sizeof(typename TailSort<1>::TempStorage);
+
+// Called by all threads of the decide CTA after the exchange.  fprev: |F| of
+// the previous order.  Writes Fidx (order), Gidx (sorted G), pos; returns f
+// in *s_f and the prefix length in *s_q.
+__device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const double* __restrict__ x,
+                               const double* __restrict__ y, int32_t* __restrict__ pos,
+                               int32_t* __restrict__ Fidx, int32_t* __restrict__ Gidx,
+                               int32_t* __restrict__ Fs, int fprev, int* s_wF, int* s_wG, int* s_wS,
+                               int* s_cnt, int* s_f, int* s_g, int* s_s, int* s_q, int* s_old,
+                               void* sort_smem) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  // (1) q = first position of the previous order whose member left F
+  int qloc = fprev;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const int pi = pos[i];
+    if (pi >= 0 && !mask[i]) qloc = min(qloc, pi);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) qloc = min(qloc, __shfl_xor_sync(kFull, qloc, o));
+  if (lane == 0) s_cnt[wid] = qloc;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < (int)(blockDim.x >> 5) ? s_cnt[lane] : fprev;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+    if (lane == 0) {
+      *s_q = v;
+      *s_f = v;  // running |F| (the prefix stays in place)
+      *s_g = 0;
+      *s_s = 0;
+      *s_old = 0;
+    }
+  }
+  __syncthreads();
+  const int q = *s_q;
+  // (2) the tail R = F minus the prefix -> Fidx[q..) in index order; G ->
+  // Gidx, F -> Fs (both in index order)
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + tid;
+    const bool valid = i < n;
+    const bool inF = valid && mask[i];
+    const int pi = valid ? pos[i] : -1;
+    const bool inR = inF && !(pi >= 0 && pi < q);
+    const bool inG = valid && !inF;
+    const unsigned bR = __ballot_sync(kFull, inR), bG = __ballot_sync(kFull, inG),
+                   bS = __ballot_sync(kFull, inF), bO = __ballot_sync(kFull, inR && pi >= 0);
+    if (lane == 0 && bO != 0u) atomicAdd(s_old, __popc(bO));
+    if (lane == 0) {
+      s_wF[wid] = __popc(bR);
+      s_wG[wid] = __popc(bG);
+      s_wS[wid] = __popc(bS);
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const int nw = blockDim.x >> 5;
+      int a = lane < nw ? s_wF[lane] : 0, bb = lane < nw ? s_wG[lane] : 0, cc = lane < nw ? s_wS[lane] : 0;
+      int ia = a, ib = bb, ic = cc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int ya = __shfl_up_sync(kFull, ia, o), yb = __shfl_up_sync(kFull, ib, o),
+            yc = __shfl_up_sync(kFull, ic, o);
+        if (lane >= o) {
+          ia += ya;
+          ib += yb;
+          ic += yc;
+        }
+      }
+      s_wF[lane] = ia - a;
+      s_wG[lane] = ib - bb;
+      s_wS[lane] = ic - cc;
+      if (lane == 31) {
+        s_cnt[0] = ia;
+        s_cnt[1] = ib;
+        s_cnt[2] = ic;
+      }
+    }
+    __syncthreads();
+    if (inR) Fidx[*s_f + s_wF[wid] + __popc(bR & lt)] = i;
+    if (inF) Fs[*s_s + s_wS[wid] + __popc(bS & lt)] = i;
+    if (inG) {
+      Gidx[*s_g + s_wG[wid] + __popc(bG & lt)] = i;
+      pos[i] = -1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      *s_f += s_cnt[0];
+      *s_g += s_cnt[1];
+      *s_s += s_cnt[2];
+    }
+    __syncthreads();
+  }
+  const int f = *s_f, r = f - q;
+  // (3) stable sort of the tail by a 16-bit key (the order is a heuristic:
+  // 7 mantissa bits are plenty): old members (pos >= 0) by decreasing x, new
+  // members after them in index order (the first factorization is thus in
+  // index order, as the oracle's); pos[] still holds the previous positions.
+#ifndef NO_ORDER_SORT
+  if (r > 1 && r <= kOrderMax && *s_old > 0) {  // (no old member: already in order)
+    if (r <= kDecideThreads) sort_tail<1>(Fidx + q, r, x, pos, sort_smem);
+    else sort_tail<kOrderMax / kDecideThreads>(Fidx + q, r, x, pos, sort_smem);
+    __syncthreads();
+  }
+#endif
+  for (int t = tid; t < r; t += blockDim.x) pos[Fidx[q + t]] = q + t;
+}
+
 // ------------------------------------------------- decide + exchange (a3, a4)
 // One CTA of 1024 threads.  Each thread owns the indices i = tid + 1024 q, so
 // the "snapshot before any flip" of reading c10 is automatic: a thread reads
 // its own (mask, x, y) and flips only its own entries after the block-wide
 // decision.
-constexpr int kDecideThreads = 1024;
-
 __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
     int n, uint8_t* __restrict__ mask, const double* __restrict__ x,
     const double* __restrict__ y, int32_t* __restrict__ Fidx, int32_t* __restrict__ Gidx,
-    DevState* st, TraceRec* trace, int trace_cap, cudaGraphConditionalHandle loop, int use_loop) {
+    DevState* st, TraceRec* trace, int trace_cap, cudaGraphConditionalHandle loop, int use_loop,
+    int32_t* pos, int32_t* Fs) {
+  extern __shared__ __align__(16) unsigned char s_sort[];  // (pos != nullptr) the tail sort's storage
   __shared__ int s_cnt[32], s_max[32];
-  __shared__ int s_wF[32], s_wG[32];
-  __shared__ int s_branch, s_last, s_carryF, s_carryG;
+  __shared__ int s_wF[32], s_wG[32], s_wS[32];
+  __shared__ int s_branch, s_last, s_carryF, s_carryG, s_carryS, s_q, s_fprev, s_old;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
   // close the previous iteration's trace record (extremes from the dual kernel)
@@ -175,6 +340,7 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
       }
       st->branch = branch;
       s_branch = branch;
+      s_fprev = st->f;
       s_last = ll;
       s_carryF = 0;
       s_carryG = 0;
@@ -197,10 +363,20 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
   }
   __syncthreads();
 
-  block_compact(n, mask, Fidx, Gidx, s_wF, s_wG, s_cnt, &s_carryF, &s_carryG);
+  if (pos == nullptr) {
+    block_compact(n, mask, Fidx, Gidx, s_wF, s_wG, s_cnt, &s_carryF, &s_carryG);
+  } else {
+    order_free_set(n, mask, x, y, pos, Fidx, Gidx, Fs, s_fprev, s_wF, s_wG, s_wS, s_cnt, &s_carryF, &s_carryG,
+                   &s_carryS, &s_q, &s_old, s_sort);
+  }
   if (tid == 0) {
     const int f = s_carryF;
     st->f = f;
+    // whole tile columns of the kept prefix (the factorization keeps at least
+    // its last tile column to itself)
+    int jq = 0;
+    if (pos != nullptr && f > 0) jq = min(s_q / kTile, (f + kTile - 1) / kTile - 1);
+    st->reuse_cols = jq > 0 ? jq : 0;
     st->g = s_carryG;
     st->epoch += 1;
     st->tile_counter = 0;
@@ -248,10 +424,16 @@ cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t*
 
 cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
                           int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
-                          cudaStream_t s, const cudaGraphConditionalHandle* loop) {
-  decide_kernel<<<1, kDecideThreads, 0, s>>>(n, mask, x, y, Fidx, Gidx, st, trace, trace_cap,
-                                             loop ? *loop : cudaGraphConditionalHandle{},
-                                             loop ? 1 : 0);
+                          cudaStream_t s, const cudaGraphConditionalHandle* loop, int32_t* pos,
+                          int32_t* Fs) {
+  const size_t smem = pos != nullptr ? kTailSortSmem : 0;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  decide_kernel<<<1, kDecideThreads, smem, s>>>(n, mask, x, y, Fidx, Gidx, st, trace, trace_cap,
+                                                loop ? *loop : cudaGraphConditionalHandle{},
+                                                loop ? 1 : 0, pos, Fs);
   return cudaGetLastError();
 }
 
@@ -262,7 +444,8 @@ __global__ void __launch_bounds__(256) dual_kernel(
     int n, const double* __restrict__ G, int ldg, const double* __restrict__ c,
     const int32_t* __restrict__ Fidx, const int32_t* __restrict__ Gidx,
     const double* __restrict__ xF, uint8_t* __restrict__ mask, double* __restrict__ x,
-    double* __restrict__ y, double tol, DevState* st) {
+    double* __restrict__ y, double tol, DevState* st, const int32_t* __restrict__ Fs,
+    const double* __restrict__ xs) {
   const int status = st->status;
   if (status != 0) {
     if (status == 7) {  // NOT_PD: the solve failed, x = 0 (as the oracle)
@@ -281,17 +464,33 @@ __global__ void __launch_bounds__(256) dual_kernel(
     const int j = Gidx[jj];
     const double* Gj = G + (size_t)j * ldg;
     // four independent partial sums: four loads of G_j (and of Fidx, x_F,
-    // which every warp shares through L1) in flight per lane
+    // which every warp shares through L1) in flight per lane.  With a
+    // permuted factorization order (Fs != nullptr) the sum runs over F in
+    // index order (Fs) with x_F scattered to xs, so G_j is read in order.
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int a = lane;
-    for (; a + 96 < f; a += 128) {
-      const int i0 = __ldg(&Fidx[a]), i1 = __ldg(&Fidx[a + 32]), i2 = __ldg(&Fidx[a + 64]), i3 = __ldg(&Fidx[a + 96]);
-      s0 = fma(Gj[i0], __ldg(&xF[a]), s0);
-      s1 = fma(Gj[i1], __ldg(&xF[a + 32]), s1);
-      s2 = fma(Gj[i2], __ldg(&xF[a + 64]), s2);
-      s3 = fma(Gj[i3], __ldg(&xF[a + 96]), s3);
+    if (Fs != nullptr) {
+      for (; a + 96 < f; a += 128) {
+        const int i0 = __ldg(&Fs[a]), i1 = __ldg(&Fs[a + 32]), i2 = __ldg(&Fs[a + 64]), i3 = __ldg(&Fs[a + 96]);
+        s0 = fma(Gj[i0], xs[i0], s0);
+        s1 = fma(Gj[i1], xs[i1], s1);
+        s2 = fma(Gj[i2], xs[i2], s2);
+        s3 = fma(Gj[i3], xs[i3], s3);
+      }
+      for (; a < f; a += 32) {
+        const int i = __ldg(&Fs[a]);
+        s0 = fma(Gj[i], xs[i], s0);
+      }
+    } else {
+      for (; a + 96 < f; a += 128) {
+        const int i0 = __ldg(&Fidx[a]), i1 = __ldg(&Fidx[a + 32]), i2 = __ldg(&Fidx[a + 64]), i3 = __ldg(&Fidx[a + 96]);
+        s0 = fma(Gj[i0], __ldg(&xF[a]), s0);
+        s1 = fma(Gj[i1], __ldg(&xF[a + 32]), s1);
+        s2 = fma(Gj[i2], __ldg(&xF[a + 64]), s2);
+        s3 = fma(Gj[i3], __ldg(&xF[a + 96]), s3);
+      }
+      for (; a < f; a += 32) s0 = fma(Gj[__ldg(&Fidx[a])], __ldg(&xF[a]), s0);
     }
-    for (; a < f; a += 32) s0 = fma(Gj[__ldg(&Fidx[a])], __ldg(&xF[a]), s0);
     const double s = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) {
       const double v = s - c[j];
@@ -331,11 +530,12 @@ __global__ void __launch_bounds__(256) dual_kernel(
 
 cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
                         const int32_t* Gidx, const double* xF, uint8_t* mask, double* x,
-                        double* y, double tol, DevState* st, int sm_count, cudaStream_t s) {
+                        double* y, double tol, DevState* st, int sm_count, cudaStream_t s,
+                        const int32_t* Fs, const double* xs) {
   int blocks = (n + 7) / 8;  // one warp per G index upper bound
   if (blocks > sm_count * 8) blocks = sm_count * 8;
   if (blocks < 1) blocks = 1;
-  dual_kernel<<<blocks, 256, 0, s>>>(n, G, ldg, c, Fidx, Gidx, xF, mask, x, y, tol, st);
+  dual_kernel<<<blocks, 256, 0, s>>>(n, G, ldg, c, Fidx, Gidx, xF, mask, x, y, tol, st, Fs, xs);
   return cudaGetLastError();
 }
 

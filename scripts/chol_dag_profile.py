@@ -44,7 +44,7 @@ for rep in range(3):
 print("step_normal_solve ms", t0.elapsed_time(t1))
 allp = prof.cpu().numpy().reshape(-1, 8)
 hp = allp[1000:1200]
-p = allp[:1000]
+p = allp[:600]
 p = p[p[:, 0] > 0]
 base = p[:, 0].min()
 # chain CTA: one row per tile column j
@@ -69,3 +69,16 @@ for j in range(len(p)):
         return (x - base) / 1e3 if x > 0 else float("nan")
     print(f"{j:4d}  P(j+1,j) upd-done {us(h[4]):8.1f} pub {us(h[0]):8.1f} | T(j+1,j-1) pub {us(h[1]):8.1f} | "
           f"P(j,j) pub {us(h[2]):8.1f} | chain needs sub at {us(p[j][2]):8.1f}")
+# POTRF panels of the chain (rows 600+4j, clock64 cycles: after (a), warp 0
+# panel done, (c) warps done; row 600+4j+3 slot 0: POTRF entry)
+pp = allp[600:600 + 4 * len(p)].reshape(len(p), 4, 8).astype(np.int64)
+print("POTRF per panel (cycles): (a) lookahead incl. previous sync | (b) panel factor (warp 0) | (c) strips (warp 2)")
+for j in range(1, min(4, len(p))):
+    t_start = [pp[j][3][0] if k == 0 else pp[j][1][k - 1] for k in range(8)]
+    row = []
+    for k in range(8):
+        if pp[j][0][k] <= 0:
+            break
+        row.append("%d: %d|%d|%s" % (k, pp[j][0][k] - t_start[k], pp[j][1][k] - pp[j][0][k],
+                                     str(pp[j][2][k] - pp[j][0][k]) if pp[j][2][k] > 0 else "-"))
+    print("  j=%d total %d  " % (j, pp[j][1][7] - pp[j][3][0]) + "  ".join(row))

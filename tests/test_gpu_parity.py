@@ -389,6 +389,15 @@ def test_host_driven_loop_path(P, cfg, seed, monkeypatch):
     assert_parity(P, g.make_problem(cfg, seed))
 
 
+@pytest.mark.parametrize("cfg,seed", [(0, 5), (1, 0), (3, 0)])
+def test_index_order_path(P, cfg, seed, monkeypatch):
+    """By default the factorization order keeps the previous iteration's
+    surviving prefix and reuses its factor tiles (DESIGN.md "factor reuse");
+    the plain index-order factorization (NNLS_NO_REUSE) must agree too."""
+    monkeypatch.setenv("NNLS_NO_REUSE", "1")
+    assert_parity(P, g.make_problem(cfg, seed))
+
+
 def test_graph_replay_across_loads(P):
     """One handle, the captured solve graph is reused / rebuilt across loads."""
     S = P.Solver(trace=1)
