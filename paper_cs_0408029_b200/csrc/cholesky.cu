@@ -48,6 +48,10 @@ __host__ __device__ inline int tidx(int i, int j) { return i * (i + 1) / 2 + j; 
 // Barrier of the CTA's 8 warps as named barrier 1 (barrier 2 is the 7-warp
 // barrier of the chain's POTRF, see wsync).
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+// "empty" pattern of the back-substitution mailboxes (see backsolve_chain)
+__device__ __forceinline__ unsigned long long box_empty(int epoch) {
+  return 0x7FF4000000000000ull | (unsigned)epoch;
+}
 inline int tri_tiles(int n) {
   const int ntr = (n + 1 + T - 1) / T;
   return ntr * (ntr + 1) / 2;
@@ -67,17 +71,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (g_chol_prof != nullptr && threadIdx.x == 0) g_chol_prof[(task) * 8 + (slot)] = gtimer(); \
   } while (0)
 
-// DAG flags: full[tri], part[tri], inv[ntr], back-solve x[ntr].
+// DAG flags: full[tri], part[tri], inv[ntr], back-solve x[ntr], a[ntr], N[ntr].
 size_t chol_flag_count(int n) {
   const int ntr = (n + 1 + T - 1) / T;
-  return 2 * (size_t)tri_tiles(n) + 2 * (size_t)ntr + 4;
+  return 2 * (size_t)tri_tiles(n) + 4 * (size_t)ntr + 4;
 }
 
-// Lower tiles L(i,j) followed by one inverse tile per tile column; each tile
-// T rows of stride LDS (the smem layout, so a tile moves as one bulk copy).
+// Lower tiles L(i,j), one inverse tile Linv_JJ and one back-solve tile N_J
+// per tile column (each T rows of stride LDS: the smem layout, so a tile
+// moves as one bulk copy), then the back-solve mailboxes [parity][x | a]
+// (T per tile column each).
 size_t chol_tile_doubles(int n) {
   const int ntr = (n + 1 + T - 1) / T;
-  return ((size_t)tri_tiles(n) + ntr) * TS;
+  return ((size_t)tri_tiles(n) + 2 * (size_t)ntr) * TS + 4 * (size_t)ntr * T;
 }
 
 // load a tile (global, T rows of stride LDS) into smem (same layout)
@@ -619,7 +625,7 @@ __device__ __forceinline__ void left_update(double* __restrict__ smem, double* _
 __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     const double* __restrict__ G, int ldg, const double* __restrict__ cvec,
     const int32_t* __restrict__ Fidx, double* __restrict__ Lt, double* __restrict__ Linv,
-    int* __restrict__ flags, int tri, DevState* st) {
+    int* __restrict__ flags, int tri, DevState* st, unsigned long long* __restrict__ box, int boxlen) {
   extern __shared__ double smem[];
   // helpers: BUF(0) = S, BUF(1..4) = operand double-buffers.
   // chain: BUF(0)/BUF(1) = diagonal tile of column j (alternating), BUF(5) = A/L(j+1,j)
@@ -636,6 +642,13 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   FlagSet F{flags, flags + tri, flags + 2 * tri};
   const int tid = threadIdx.x;
   double* S = smem;
+  if (blockIdx.x == 1) {  // empty this epoch's back-substitution mailboxes (see box_empty)
+    unsigned long long* xb = box + (size_t)(2 * (epoch & 1)) * boxlen;
+    for (int e = tid; e < ntc * T; e += kThreads) {
+      xb[e] = box_empty(epoch);
+      xb[boxlen + e] = box_empty(epoch);
+    }
+  }
 
   if (blockIdx.x == 0) {
     // ============================== the diagonal chain
@@ -842,91 +855,295 @@ cudaError_t chol_debug_set_profile(unsigned long long* p) {
   return cudaMemcpyToSymbol(g_chol_prof, &p, sizeof(p));
 }
 
-// L^T x = z, z = row f of the bordered factor.  Column tiles J from the last
-// to the first; task J waits for x_I (I > J), subtracts L_IJ^T x_I, then
-// x_J = Linv_JJ^T s (a GEMV, no sequential substitution).  xflags[J] == epoch:
-// x_J published.
-__global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(const double* __restrict__ Lt,
-                                                                   const double* __restrict__ Linv,
-                                                                   int* __restrict__ xflags,
-                                                                   double* __restrict__ xF,
-                                                                   DevState* st,
-                                                                   const int32_t* __restrict__ Fidx,
-                                                                   double* __restrict__ xs) {
-  extern __shared__ double bsm[];
-  double* Lnext = bsm;        // L(J+1, J): the only tile on the critical path
-  double* Xinv = bsm + TS;    // Linv(J, J)
+// ---------------------------------------------------------------------------
+// L^T x = z (z = row f of the bordered factor), column tiles J from the last
+// to the first, as a CHAIN fed by helper tasks:
+//   x_J = Linv_JJ^T (s'_J - L(J+1,J)^T x_{J+1}) = a_J - N_J^T x_{J+1},
+//   s'_J = z_J - sum_{I >= J+2} L(I,J)^T x_I,   a_J = Linv_JJ^T s'_J,
+//   N_J  = L(J+1,J) Linv_JJ.
+// Helper task J (CTAs 1..) forms N_J first (DMMA; it needs no x) and
+// publishes it, then accumulates s'_J as the x_I arrive and publishes a_J.
+// The chain (CTA 0) only does x_J = a_J - N_J^T x_{J+1}: one 64x64 GEMV per
+// tile column with x kept on chip and N_J streamed in ahead by bulk copies;
+// warp 6 feeds it (flags, bulk copies, a_J), warp 7 publishes x_J for the
+// helpers, warps 0-5 compute.  The per-column critical path has no global
+// round trip (the previous design paid ~2 us of flag + fence per column).
+namespace {
+constexpr int kBsStages = 4;
+constexpr size_t kBsSmem = sizeof(double) * 4 * (size_t)TS;  // chain: 4 stages; helper: 4 tiles
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+// arrive with the expected byte count, then one bulk copy of a whole tile
+__device__ __forceinline__ void mbar_bulk_tile(double* dst, const double* src, unsigned long long* b) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "n"(TS * 8)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "n"(TS * 8), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ int vld(const int* p) { return *(const volatile int*)p; }
+// Mailboxes: x_J and a_J pass between CTAs as 64 doubles written with plain
+// (8-byte, single-copy atomic) stores into slots that held an "empty"
+// pattern -- a signalling NaN carrying the epoch, which no arithmetic result
+// can equal -- and consumers poll the values themselves: no fence and no flag
+// on the critical path.  The factorization kernel empties the slots of the
+// epoch's parity before the back substitution starts.
+__device__ __forceinline__ unsigned long long ld_box(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_box(unsigned long long* p, double v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v))
+               : "memory");
+}
+__device__ __forceinline__ void vst(int* p, int v) { *(volatile int*)p = v; }
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 192;\n" ::: "memory"); }
+}  // namespace
+
+// acc (rows 8w..8w+7, all 64 columns) = A Linv for 64 x 64 smem tiles, Linv
+// lower triangular: column block q only needs k >= 8q (72 DMMAs per warp).
+__device__ __forceinline__ void gemm_linv(double (&acc)[8][2], const double* __restrict__ A,
+                                          const double* __restrict__ Linv, int w, int lane) {
+  const int rq = lane >> 2, kq = lane & 3;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+  for (int kb = 0; kb < T / 4; ++kb) {
+    const double av = A[(8 * w + rq) * LDS + 4 * kb + kq];
+#pragma unroll
+    for (int q = 0; q <= kb / 2 && q < 8; ++q)
+      dmma8x8x4(acc[q][0], acc[q][1], av, Linv[(4 * kb + kq) * LDS + 8 * q + rq]);
+  }
+}
+
+struct BsArgs {
+  const double* Lt;
+  const double* Linv;
+  double* Nt;    // N_J tiles
+  unsigned long long* box;   // mailboxes [epoch parity][x | a][boxlen]
+  int boxlen;                // T * tile rows of the allocation
+  unsigned long long* xbox;  // (set in the kernel: this epoch's x_J mailboxes, T per tile column)
+  unsigned long long* abox;  // (a_J mailboxes)
+  int* nflags;
+  double* xF;
+  const int32_t* Fidx;
+  double* xs;
+};
+
+__device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring) {
+  __shared__ double abuf[kBsStages][T];
+  __shared__ double xbuf[2][T];
+  __shared__ double part[3 * T];
+  __shared__ __align__(8) unsigned long long mbar[kBsStages];
+  __shared__ int s_consumed, s_xready, s_pub;
+  const int ntc = (f + T - 1) / T;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int k = 0; k < kBsStages; ++k) mbar_init(&mbar[k], 2);  // N tile (or plain) + a_J
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    s_consumed = 0;
+    s_xready = 0;
+    s_pub = 0;
+  }
+  __syncthreads();
+  if (w == 6) {
+    // ---- feeder: arm the stage of step tN with N_J (bulk copy) as soon as
+    // it is published, deliver a_J of step tA into abuf
+    int tN = 0, tA = 0;
+    const unsigned long long empty = box_empty(epoch);
+    while (tA < ntc) {
+      bool moved = false;
+      if (tN < ntc && tN - vld(&s_consumed) < kBsStages) {
+        const int J = ntc - 1 - tN, stage = tN % kBsStages;
+        int ok = 1;
+        if (lane == 0 && J < ntc - 1) ok = ld_acquire(&a.nflags[J]) == epoch;
+        ok = __shfl_sync(kFull, ok, 0);
+        if (ok) {
+          if (lane == 0) {
+            if (J < ntc - 1) mbar_bulk_tile(ring + (size_t)stage * TS, a.Nt + (size_t)J * TS, &mbar[stage]);
+            else mbar_arrive(&mbar[stage]);  // the last column has no N
+            if (g_chol_prof != nullptr) g_chol_prof[(900 + J) * 8 + 2] = gtimer();
+          }
+          ++tN;
+          moved = true;
+        }
+      }
+      if (tA < tN) {
+        const int J = ntc - 1 - tA, stage = tA % kBsStages;
+        const unsigned long long v0 = ld_box(&a.abox[J * T + lane]), v1 = ld_box(&a.abox[J * T + lane + 32]);
+        if (__all_sync(kFull, v0 != empty && v1 != empty)) {
+          abuf[stage][lane] = __longlong_as_double((long long)v0);
+          abuf[stage][lane + 32] = __longlong_as_double((long long)v1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&mbar[stage]);  // (release: abuf visible to the waiters)
+          if (lane == 0 && g_chol_prof != nullptr) g_chol_prof[(900 + J) * 8 + 1] = gtimer();
+          ++tA;
+          moved = true;
+        }
+      }
+      if (!moved) __nanosleep(32);
+    }
+  } else if (w == 7) {
+    // ---- publisher: x_J -> global, fence, flag (off the chain's path)
+    for (int t = 0; t < ntc; ++t) {
+      while (vld(&s_xready) <= t) __nanosleep(20);
+      const int J = ntc - 1 - t, cv = min(T, f - J * T);
+      for (int e = lane; e < T; e += 32) {
+        const double v = xbuf[t & 1][e];  // (0 beyond cv)
+        st_box(&a.xbox[J * T + e], v);
+        if (e < cv) {
+          a.xF[J * T + e] = v;
+          if (a.xs != nullptr) a.xs[a.Fidx[J * T + e]] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        vst(&s_pub, t + 1);
+        if (g_chol_prof != nullptr) g_chol_prof[(900 + J) * 8 + 3] = gtimer();
+      }
+    }
+  } else {
+    // ---- compute warps 0-5: x_J = a_J - N_J^T x_{J+1}
+    const int c = tid & (T - 1), rg = tid >> 6;  // 3 row groups
+    for (int t = 0; t < ntc; ++t) {
+      const int J = ntc - 1 - t, stage = t % kBsStages;
+      mbar_wait(&mbar[stage], (unsigned)((t / kBsStages) & 1));
+      double p = 0.0;
+      if (t > 0) {
+        const double* Nl = ring + (size_t)stage * TS;
+        const double* xp = xbuf[(t - 1) & 1];
+#pragma unroll 4
+        for (int r = rg; r < T; r += 3) p = fma(Nl[r * LDS + c], xp[r], p);
+      }
+      part[rg * T + c] = p;
+      bar_compute();
+      if (tid < T) {
+        if (t >= 2)
+          while (vld(&s_pub) < t - 1) __nanosleep(20);  // warp 7 has read xbuf[t & 1] (step t-2)
+        const int cv = min(T, f - J * T);
+        const double sum = (part[tid] + part[T + tid]) + part[2 * T + tid];
+        xbuf[t & 1][tid] = (tid < cv) ? abuf[stage][tid] - sum : 0.0;
+      }
+      bar_compute();
+      if (tid == 0) {
+        __threadfence_block();
+        vst(&s_consumed, t + 1);  // stage (tile, abuf) free
+        vst(&s_xready, t + 1);
+      }
+      PROF_STAMP(900 + J, 0);
+    }
+  }
+}
+
+// helper task J: N_J, then s'_J and a_J
+__device__ void backsolve_task(const BsArgs& a, int f, int epoch, int J, double* bsm) {
   __shared__ double part[4 * T];
   __shared__ double s_rhs[T];
   __shared__ double s_x[T];
+  double* Xi = bsm;            // Linv_JJ
+  double* Ls = bsm + TS;       // L(J+1, J)
+  double* ring = bsm + 2 * TS; // L(I, J), double-buffered
+  const int ntc = (f + T - 1) / T;
+  const int Rf = f / T, rf = f % T;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int c = tid & (T - 1), rg = tid >> 6;
+  const int cv = min(T, f - J * T);
+  const int nI = max(0, ntc - 1 - (J + 1));  // I = ntc-1 .. J+2
+  const unsigned long long empty = box_empty(epoch);
+  tile_async(Xi, a.Linv + (size_t)J * TS);
+  if (J + 1 < ntc) tile_async(Ls, a.Lt + (size_t)tidx(J + 1, J) * TS);
+  cp_async_commit();
+  if (nI > 0) {
+    tile_async(ring, a.Lt + (size_t)tidx(ntc - 1, J) * TS);
+    cp_async_commit();
+  }
+  if (tid < T) s_rhs[tid] = (tid < cv) ? __ldcg(&a.Lt[(size_t)tidx(Rf, J) * TS + rf * LDS + tid]) : 0.0;
+  if (nI > 0) cp_async_wait<1>();
+  else cp_async_wait<0>();
+  __syncthreads();
+  if (J + 1 < ntc) {  // N_J = L(J+1,J) Linv_JJ, straight from the fragments to global
+    double acc[8][2];
+    gemm_linv(acc, Ls, Xi, w, lane);
+    double* Ng = a.Nt + (size_t)J * TS;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<double2*>(Ng + (8 * w + (lane >> 2)) * LDS + 8 * q + 2 * (lane & 3)) =
+          make_double2(acc[q][0], acc[q][1]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(&a.nflags[J], epoch);
+  }
+  for (int k = 0; k < nI; ++k) {  // s'_J -= L(I,J)^T x_I, tiles prefetched one ahead
+    const int I = ntc - 1 - k;
+    double* Tl = ring + (size_t)(k & 1) * TS;
+    if (k + 1 < nI) {
+      tile_async(ring + (size_t)((k + 1) & 1) * TS, a.Lt + (size_t)tidx(I - 1, J) * TS);
+      cp_async_commit();
+    }
+    if (tid < T) {  // x_I from its mailbox (0 beyond its valid rows)
+      unsigned long long v;
+      while ((v = ld_box(&a.xbox[I * T + tid])) == empty) __nanosleep(20);
+      s_x[tid] = __longlong_as_double((long long)v);
+    }
+    if (k + 1 < nI) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    double p = 0.0;
+#pragma unroll 4
+    for (int r = rg; r < T; r += 4) p = fma(Tl[r * LDS + c], s_x[r], p);
+    part[rg * T + c] = p;
+    __syncthreads();
+    if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
+    __syncthreads();
+  }
+  // a_J = Linv_JJ^T s'_J
+  double p = 0.0;
+#pragma unroll 4
+  for (int r = rg; r < T; r += 4) p = fma(Xi[r * LDS + c], s_rhs[r], p);
+  part[rg * T + c] = p;
+  __syncthreads();
+  if (tid < T) st_box(&a.abox[J * T + tid], (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]));
+  __syncthreads();  // (smem reused by the next task)
+}
+
+__global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(BsArgs a, DevState* st) {
+  extern __shared__ __align__(128) double bsm[];
   __shared__ int s_task;
   const int f = st->f;
   const int epoch = st->epoch;
   if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
   const int ntc = (f + T - 1) / T;
-  const int Rf = f / T, rf = f % T;  // tile row / local row of the rhs row
-  const int tid = threadIdx.x;
-  const int c = tid & (T - 1), rg = tid >> 6;  // column, 4 row groups
+  a.xbox = a.box + (size_t)(2 * (epoch & 1)) * a.boxlen;
+  a.abox = a.xbox + a.boxlen;
+  if (blockIdx.x == 0) {
+    backsolve_chain(a, f, epoch, bsm);
+    return;
+  }
   for (;;) {
-    if (tid == 0) s_task = atomicAdd(&st->solve_counter, 1);
+    if (threadIdx.x == 0) s_task = atomicAdd(&st->solve_counter, 1);
     __syncthreads();
     const int t = s_task;
+    __syncthreads();
     if (t >= ntc) break;
-    const int J = ntc - 1 - t;
-    const int cv = min(T, f - J * T);
-    // prefetch the critical-path tiles (the factorization is complete)
-    for (int e = tid; e < TS / 2; e += kThreads) {  // (whole padded tiles)
-      cp_async16(Xinv + 2 * e, Linv + (size_t)J * TS + 2 * e);
-      if (J + 1 < ntc) cp_async16(Lnext + 2 * e, Lt + (size_t)tidx(J + 1, J) * TS + 2 * e);
-    }
-    cp_async_commit();
-    if (tid < T) s_rhs[tid] = (tid < cv) ? __ldcg(&Lt[(size_t)tidx(Rf, J) * TS + rf * LDS + tid]) : 0.0;
-    __syncthreads();
-    // subtract L_IJ^T x_I for I = ntc-1 .. J+2 straight from L2 (off the critical path)
-    for (int I = ntc - 1; I > J + 1; --I) {
-      if (tid == 0) wait_flag(&xflags[I], epoch);
-      __syncthreads();
-      const int rvI = min(T, f - I * T);  // rows of L_IJ that are < f
-      if (tid < T) s_x[tid] = (tid < rvI) ? __ldcg(&xF[I * T + tid]) : 0.0;
-      __syncthreads();
-      const double* L = Lt + (size_t)tidx(I, J) * TS;
-      double p = 0.0;
-      for (int r = rg; r < rvI; r += 4) p = fma(__ldcg(&L[r * LDS + c]), s_x[r], p);
-      part[rg * T + c] = p;
-      __syncthreads();
-      if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
-      __syncthreads();
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-    if (J + 1 < ntc) {  // the critical step: x_{J+1} from the previous task
-      if (tid == 0) wait_flag(&xflags[J + 1], epoch);
-      __syncthreads();
-      const int rvI = min(T, f - (J + 1) * T);
-      if (tid < T) s_x[tid] = (tid < rvI) ? __ldcg(&xF[(J + 1) * T + tid]) : 0.0;
-      __syncthreads();
-      double p = 0.0;
-#pragma unroll 4
-      for (int r = rg; r < T; r += 4) p = fma(Lnext[r * LDS + c], s_x[r], p);
-      part[rg * T + c] = p;
-      __syncthreads();
-      if (tid < T) s_rhs[tid] -= (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
-      __syncthreads();
-    }
-    // x_J = Linv_JJ^T s : x[c] = sum_{r >= c} Linv[r][c] s[r]  (Linv is zero beyond cv)
-    double p = 0.0;
-#pragma unroll 4
-    for (int r = rg; r < T; r += 4) p = fma(Xinv[r * LDS + c], s_rhs[r], p);
-    part[rg * T + c] = p;
-    __syncthreads();
-    if (tid < cv) {
-      const double v = (part[tid] + part[T + tid]) + (part[2 * T + tid] + part[3 * T + tid]);
-      xF[J * T + tid] = v;
-      if (xs != nullptr) xs[Fidx[J * T + tid]] = v;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(&xflags[J], epoch);
+    backsolve_task(a, f, epoch, ntc - 1 - t, bsm);
   }
 }
 
@@ -936,8 +1153,7 @@ static cudaError_t set_attrs() {
   cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * kSmemDoubles));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(double) * 2 * TS));
+  e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsSmem);
   if (e != cudaSuccess) return e;
   attr_set = true;
   return cudaSuccess;
@@ -953,20 +1169,33 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   if (grid > tasks) grid = tasks;
   if (grid < 2) grid = 2;
   double* Linv = Lt + (size_t)tri_tiles(n) * TS;
+  const int ntr = (n + 1 + T - 1) / T;
+  unsigned long long* box = reinterpret_cast<unsigned long long*>(Lt + ((size_t)tri_tiles(n) + 2 * (size_t)ntr) * TS);
   chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, Linv,
-                                                                          flags, tri_tiles(n), st);
+                                                                          flags, tri_tiles(n), st, box, ntr * T);
   return cudaGetLastError();
 }
 
 cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
                                   int sm_count, cudaStream_t s, const int32_t* Fidx, double* xs) {
   const int ntr = (n + 1 + T - 1) / T;
-  int* xflags = flags + 2 * tri_tiles(n) + (n + 1 + T - 1) / T;
-  const double* Linv = Lt + (size_t)tri_tiles(n) * TS;
-  const int g2 = ntr < sm_count ? ntr : sm_count;
+  const int tri = tri_tiles(n);
+  BsArgs a;
+  a.Lt = Lt;
+  a.Linv = Lt + (size_t)tri * TS;
+  a.Nt = const_cast<double*>(Lt) + (size_t)(tri + ntr) * TS;
+  a.nflags = flags + 2 * tri + 3 * ntr;
+  a.box = reinterpret_cast<unsigned long long*>(a.Nt + (size_t)ntr * TS);
+  a.boxlen = ntr * T;
+  a.xF = xF;
+  a.Fidx = Fidx;
+  a.xs = xs;
+  int grid = ntr + 1;  // the chain + one helper per tile column
+  if (grid > sm_count) grid = sm_count;
+  if (grid < 2) grid = 2;
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
-  chol_backsolve_kernel<<<g2, kThreads, sizeof(double) * 2 * TS, s>>>(Lt, Linv, xflags, xF, st, Fidx, xs);
+  chol_backsolve_kernel<<<grid, kThreads, kBsSmem, s>>>(a, st);
   return cudaGetLastError();
 }
 

@@ -82,3 +82,18 @@ for j in range(1, min(4, len(p))):
         row.append("%d: %d|%d|%s" % (k, pp[j][0][k] - t_start[k], pp[j][1][k] - pp[j][0][k],
                                      str(pp[j][2][k] - pp[j][0][k]) if pp[j][2][k] > 0 else "-"))
     print("  j=%d total %d  " % (j, pp[j][1][7] - pp[j][3][0]) + "  ".join(row))
+# back substitution chain (rows 900+J, slot 0): x_J computed on the chain CTA
+bs = allp[900:900 + 200, 0]
+idx = np.flatnonzero(bs > 0)
+if idx.size:
+    t = bs[idx]
+    order = np.argsort(t)
+    print("backsolve chain: x_J done at (us from the first):",
+          " ".join("J%d:%.2f" % (idx[k], (t[k] - t.min()) / 1e3) for k in order))
+    full = allp[900:900 + 200]
+    t0 = t.min()
+    print("  J   N armed   a_J in   x_J done   x_J published (us)")
+    for k in order:
+        J = idx[k]
+        r = full[J]
+        print("  %2d  %8.2f %8.2f %8.2f %8.2f" % (J, *[(v - t0) / 1e3 if v > 0 else float('nan') for v in (r[2], r[1], r[0], r[3])]))
