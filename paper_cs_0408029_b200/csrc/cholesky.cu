@@ -77,13 +77,13 @@ size_t chol_flag_count(int n) {
   return 2 * (size_t)tri_tiles(n) + 4 * (size_t)ntr + 4;
 }
 
-// Lower tiles L(i,j), one inverse tile Linv_JJ and one back-solve tile N_J
-// per tile column (each T rows of stride LDS: the smem layout, so a tile
+// Lower tiles L(i,j), one inverse tile Linv_JJ and two back-solve tiles N_J,
+// P_J per tile column (each T rows of stride LDS: the smem layout, so a tile
 // moves as one bulk copy), then the back-solve mailboxes [parity][x | a]
 // (T per tile column each).
 size_t chol_tile_doubles(int n) {
   const int ntr = (n + 1 + T - 1) / T;
-  return ((size_t)tri_tiles(n) + 2 * (size_t)ntr) * TS + 4 * (size_t)ntr * T;
+  return ((size_t)tri_tiles(n) + 3 * (size_t)ntr) * TS + 4 * (size_t)ntr * T;
 }
 
 // load a tile (global, T rows of stride LDS) into smem (same layout)
@@ -869,8 +869,8 @@ cudaError_t chol_debug_set_profile(unsigned long long* p) {
 // helpers, warps 0-5 compute.  The per-column critical path has no global
 // round trip (the previous design paid ~2 us of flag + fence per column).
 namespace {
-constexpr int kBsStages = 4;
-constexpr size_t kBsSmem = sizeof(double) * 4 * (size_t)TS;  // chain: 4 stages; helper: 4 tiles
+constexpr int kBsStages = 3;  // chain ring stages, each {N_J, P_J}
+constexpr size_t kBsSmem = sizeof(double) * 6 * (size_t)TS;  // chain: 3 x 2 tiles; helper: 5 tiles
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -879,10 +879,12 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count)
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
-// arrive with the expected byte count, then one bulk copy of a whole tile
-__device__ __forceinline__ void mbar_bulk_tile(double* dst, const double* src, unsigned long long* b) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "n"(TS * 8)
+// arrive with the expected byte count; one bulk copy of a whole tile
+__device__ __forceinline__ void mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void bulk_tile_to_smem(double* dst, const double* src, unsigned long long* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                    smem_u32(dst)),
                "l"(src), "n"(TS * 8), "r"(smem_u32(b))
@@ -937,7 +939,8 @@ __device__ __forceinline__ void gemm_linv(double (&acc)[8][2], const double* __r
 struct BsArgs {
   const double* Lt;
   const double* Linv;
-  double* Nt;    // N_J tiles
+  double* Nt;    // N_J = L(J+1,J) Linv_JJ tiles
+  double* Pt;    // P_J = L(J+2,J) Linv_JJ tiles
   unsigned long long* box;   // mailboxes [epoch parity][x | a][boxlen]
   int boxlen;                // T * tile rows of the allocation
   unsigned long long* xbox;  // (set in the kernel: this epoch's x_J mailboxes, T per tile column)
@@ -950,14 +953,14 @@ struct BsArgs {
 
 __device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring) {
   __shared__ double abuf[kBsStages][T];
-  __shared__ double xbuf[2][T];
+  __shared__ double xbuf[3][T];
   __shared__ double part[3 * T];
   __shared__ __align__(8) unsigned long long mbar[kBsStages];
   __shared__ int s_consumed, s_xready, s_pub;
   const int ntc = (f + T - 1) / T;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int k = 0; k < kBsStages; ++k) mbar_init(&mbar[k], 2);  // N tile (or plain) + a_J
+    for (int k = 0; k < kBsStages; ++k) mbar_init(&mbar[k], 2);  // tiles (or plain) + a_J
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     s_consumed = 0;
     s_xready = 0;
@@ -965,8 +968,8 @@ __device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring)
   }
   __syncthreads();
   if (w == 6) {
-    // ---- feeder: arm the stage of step tN with N_J (bulk copy) as soon as
-    // it is published, deliver a_J of step tA into abuf
+    // ---- feeder: arm the stage of step tN with N_J, P_J (bulk copies) as
+    // soon as they are published, deliver a_J of step tA into abuf
     int tN = 0, tA = 0;
     const unsigned long long empty = box_empty(epoch);
     while (tA < ntc) {
@@ -978,9 +981,15 @@ __device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring)
         ok = __shfl_sync(kFull, ok, 0);
         if (ok) {
           if (lane == 0) {
-            if (J < ntc - 1) mbar_bulk_tile(ring + (size_t)stage * TS, a.Nt + (size_t)J * TS, &mbar[stage]);
-            else mbar_arrive(&mbar[stage]);  // the last column has no N
-            if (g_chol_prof != nullptr) g_chol_prof[(900 + J) * 8 + 2] = gtimer();
+            double* dst = ring + (size_t)stage * 2 * TS;
+            const int nt = (J + 2 < ntc) ? 2 : (J + 1 < ntc ? 1 : 0);
+            if (nt > 0) {
+              mbar_expect(&mbar[stage], (unsigned)(nt * TS * 8));
+              bulk_tile_to_smem(dst, a.Nt + (size_t)J * TS, &mbar[stage]);
+              if (nt > 1) bulk_tile_to_smem(dst + TS, a.Pt + (size_t)J * TS, &mbar[stage]);
+            } else {
+              mbar_arrive(&mbar[stage]);  // the last column has neither
+            }
           }
           ++tN;
           moved = true;
@@ -994,7 +1003,6 @@ __device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring)
           abuf[stage][lane + 32] = __longlong_as_double((long long)v1);
           __syncwarp();
           if (lane == 0) mbar_arrive(&mbar[stage]);  // (release: abuf visible to the waiters)
-          if (lane == 0 && g_chol_prof != nullptr) g_chol_prof[(900 + J) * 8 + 1] = gtimer();
           ++tA;
           moved = true;
         }
@@ -1002,12 +1010,12 @@ __device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring)
       if (!moved) __nanosleep(32);
     }
   } else if (w == 7) {
-    // ---- publisher: x_J -> global, fence, flag (off the chain's path)
+    // ---- publisher: x_J -> mailbox, x_F (and xs), off the chain's path
     for (int t = 0; t < ntc; ++t) {
       while (vld(&s_xready) <= t) __nanosleep(20);
       const int J = ntc - 1 - t, cv = min(T, f - J * T);
       for (int e = lane; e < T; e += 32) {
-        const double v = xbuf[t & 1][e];  // (0 beyond cv)
+        const double v = xbuf[t % 3][e];  // (0 beyond cv)
         st_box(&a.xbox[J * T + e], v);
         if (e < cv) {
           a.xF[J * T + e] = v;
@@ -1015,37 +1023,39 @@ __device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring)
         }
       }
       __syncwarp();
-      if (lane == 0) {
-        vst(&s_pub, t + 1);
-        if (g_chol_prof != nullptr) g_chol_prof[(900 + J) * 8 + 3] = gtimer();
-      }
+      if (lane == 0) vst(&s_pub, t + 1);
     }
   } else {
-    // ---- compute warps 0-5: x_J = a_J - N_J^T x_{J+1}
+    // ---- compute warps 0-5: x_J = a_J - N_J^T x_{J+1} - P_J^T x_{J+2}
     const int c = tid & (T - 1), rg = tid >> 6;  // 3 row groups
     for (int t = 0; t < ntc; ++t) {
       const int J = ntc - 1 - t, stage = t % kBsStages;
       mbar_wait(&mbar[stage], (unsigned)((t / kBsStages) & 1));
-      double p = 0.0;
+      double p = 0.0, p2 = 0.0;
+      const double* Nl = ring + (size_t)stage * 2 * TS;
       if (t > 0) {
-        const double* Nl = ring + (size_t)stage * TS;
-        const double* xp = xbuf[(t - 1) & 1];
+        const double* xp = xbuf[(t - 1) % 3];
 #pragma unroll 4
         for (int r = rg; r < T; r += 3) p = fma(Nl[r * LDS + c], xp[r], p);
       }
-      part[rg * T + c] = p;
+      if (t > 1) {
+        const double* xp = xbuf[(t - 2) % 3];
+#pragma unroll 4
+        for (int r = rg; r < T; r += 3) p2 = fma(Nl[TS + r * LDS + c], xp[r], p2);
+      }
+      part[rg * T + c] = p + p2;
       bar_compute();
       if (tid < T) {
-        if (t >= 2)
-          while (vld(&s_pub) < t - 1) __nanosleep(20);  // warp 7 has read xbuf[t & 1] (step t-2)
+        if (t >= 3)
+          while (vld(&s_pub) < t - 2) __nanosleep(20);  // warp 7 has read xbuf[t % 3] (step t-3)
         const int cv = min(T, f - J * T);
         const double sum = (part[tid] + part[T + tid]) + part[2 * T + tid];
-        xbuf[t & 1][tid] = (tid < cv) ? abuf[stage][tid] - sum : 0.0;
+        xbuf[t % 3][tid] = (tid < cv) ? abuf[stage][tid] - sum : 0.0;
       }
       bar_compute();
       if (tid == 0) {
         __threadfence_block();
-        vst(&s_consumed, t + 1);  // stage (tile, abuf) free
+        vst(&s_consumed, t + 1);  // stage (tiles, abuf) free
         vst(&s_xready, t + 1);
       }
       PROF_STAMP(900 + J, 0);
@@ -1053,23 +1063,24 @@ __device__ void backsolve_chain(const BsArgs& a, int f, int epoch, double* ring)
   }
 }
 
-// helper task J: N_J, then s'_J and a_J
+// helper task J: N_J and P_J, then s'_J and a_J
 __device__ void backsolve_task(const BsArgs& a, int f, int epoch, int J, double* bsm) {
   __shared__ double part[4 * T];
   __shared__ double s_rhs[T];
   __shared__ double s_x[T];
   double* Xi = bsm;            // Linv_JJ
-  double* Ls = bsm + TS;       // L(J+1, J)
-  double* ring = bsm + 2 * TS; // L(I, J), double-buffered
+  double* Ls = bsm + TS;       // L(J+1, J), L(J+2, J)
+  double* ring = bsm + 3 * TS; // L(I, J), double-buffered
   const int ntc = (f + T - 1) / T;
   const int Rf = f / T, rf = f % T;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int c = tid & (T - 1), rg = tid >> 6;
   const int cv = min(T, f - J * T);
-  const int nI = max(0, ntc - 1 - (J + 1));  // I = ntc-1 .. J+2
+  const int nI = max(0, ntc - 1 - (J + 2));  // I = ntc-1 .. J+3 (the chain applies J+1, J+2)
   const unsigned long long empty = box_empty(epoch);
   tile_async(Xi, a.Linv + (size_t)J * TS);
   if (J + 1 < ntc) tile_async(Ls, a.Lt + (size_t)tidx(J + 1, J) * TS);
+  if (J + 2 < ntc) tile_async(Ls + TS, a.Lt + (size_t)tidx(J + 2, J) * TS);
   cp_async_commit();
   if (nI > 0) {
     tile_async(ring, a.Lt + (size_t)tidx(ntc - 1, J) * TS);
@@ -1079,14 +1090,17 @@ __device__ void backsolve_task(const BsArgs& a, int f, int epoch, int J, double*
   if (nI > 0) cp_async_wait<1>();
   else cp_async_wait<0>();
   __syncthreads();
-  if (J + 1 < ntc) {  // N_J = L(J+1,J) Linv_JJ, straight from the fragments to global
+  // N_J = L(J+1,J) Linv_JJ and P_J = L(J+2,J) Linv_JJ, straight from the fragments to global
+  for (int b = 1; b <= 2 && J + b < ntc; ++b) {
     double acc[8][2];
-    gemm_linv(acc, Ls, Xi, w, lane);
-    double* Ng = a.Nt + (size_t)J * TS;
+    gemm_linv(acc, Ls + (size_t)(b - 1) * TS, Xi, w, lane);
+    double* Ng = (b == 1 ? a.Nt : a.Pt) + (size_t)J * TS;
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       *reinterpret_cast<double2*>(Ng + (8 * w + (lane >> 2)) * LDS + 8 * q + 2 * (lane & 3)) =
           make_double2(acc[q][0], acc[q][1]);
+  }
+  if (J + 1 < ntc) {
     __threadfence();
     __syncthreads();
     if (tid == 0) st_release(&a.nflags[J], epoch);
@@ -1170,7 +1184,7 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   if (grid < 2) grid = 2;
   double* Linv = Lt + (size_t)tri_tiles(n) * TS;
   const int ntr = (n + 1 + T - 1) / T;
-  unsigned long long* box = reinterpret_cast<unsigned long long*>(Lt + ((size_t)tri_tiles(n) + 2 * (size_t)ntr) * TS);
+  unsigned long long* box = reinterpret_cast<unsigned long long*>(Lt + ((size_t)tri_tiles(n) + 3 * (size_t)ntr) * TS);
   chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, Linv,
                                                                           flags, tri_tiles(n), st, box, ntr * T);
   return cudaGetLastError();
@@ -1185,7 +1199,8 @@ cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* x
   a.Linv = Lt + (size_t)tri * TS;
   a.Nt = const_cast<double*>(Lt) + (size_t)(tri + ntr) * TS;
   a.nflags = flags + 2 * tri + 3 * ntr;
-  a.box = reinterpret_cast<unsigned long long*>(a.Nt + (size_t)ntr * TS);
+  a.Pt = a.Nt + (size_t)ntr * TS;
+  a.box = reinterpret_cast<unsigned long long*>(a.Pt + (size_t)ntr * TS);
   a.boxlen = ntr * T;
   a.xF = xF;
   a.Fidx = Fidx;
