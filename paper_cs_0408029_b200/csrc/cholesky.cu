@@ -651,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   }
 
   if (blockIdx.x == 0) {
+    PROF_STAMP(1198, 0);
     // ============================== the diagonal chain
     // BUF(0)/BUF(1): diagonal tile of column j (alternating), BUF(5): A/L(j+1,j).
     // Per column: POTRF on warps 0-6 while warp 7 raises the release flag of
@@ -808,11 +809,13 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     }
     if (kind < 0) break;
     if (kind == 3) {                 // D(jq): diagonal tile jq, all updates k < jq
+      PROF_STAMP(1199, 0);
       gather_tile(S, G, ldg, cvec, Fidx, f, jq, jq);
       csync();
       left_update(smem, S, Lt, F.full, epoch, jq, jq, jq, jq, &s_ready);
       store_tile(Lt + (size_t)tidx(jq, jq) * TS, S);
       publish_flag(&F.part[tidx(jq, jq)], epoch);
+      PROF_STAMP(1199, 1);
       continue;
     }
     if (kind == 0) {                 // P(j+1, j+1): diagonal tile, updates k < j

@@ -474,7 +474,7 @@ __host__ __device__ inline ClLayout cl_layout(int m, int n, const int* mx) {
   L.cols_max = mx[2];
   L.nzc_max = mx[3];
   size_t d = (size_t)m + n + L.nzr_max + L.nzc_max + 4 * (size_t)L.cols_max + 3 * 32;
-  size_t i = (size_t)L.nzr_max + L.nzc_max + L.rows_max + 1 + L.cols_max + 1 + L.cols_max;
+  size_t i = (size_t)L.nzr_max + L.nzc_max + L.rows_max + 1 + L.cols_max + 1 + 2 * (size_t)L.cols_max;
   L.bytes = 8 * d + 4 * i + 64;
   return L;
 }
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   const ClSlices S = cl_slices(kr, C, m, n, a.rowptr, a.colptr);
   const int nrows = S.r1 - S.r0, ncols = S.j1 - S.j0;
   LQ_STAMP_SETUP(1);
-  const int gR = seg_group(nrows), gC = seg_group(ncols);
+  const int gR = seg_group(nrows);
   // ---- shared memory carve-up
   double* Urep = smem;                 // m  (u replica, unnormalised)
   double* Vrep = Urep + m;             // n  (v replica, unnormalised)
@@ -579,17 +579,53 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   int* srp = sri + Ly.nzc_max;         // local rowptr (nrows + 1)
   int* scp = srp + Ly.rows_max + 1;    // local colptr (ncols + 1)
   int* smk = scp + Ly.cols_max + 1;    // own column mask
+  int* fcol = smk + Ly.cols_max;       // own F columns (local index), in order
   const uint8_t* __restrict__ mask = a.mask;
+  __shared__ int s_nfc;
 
   // ---- stage the slices (once per solve).  Every CSR product of the path
   //      multiplies a vector that is zero outside F (v, x_ne, x), so the row
   //      slice keeps only the F columns; the CSC slice (A^T u, y') is kept whole.
-  for (int t = tid; t < S.f1 - S.f0; t += kCT) {
-    scv[t] = a.cvals[S.f0 + t];
-    sri[t] = a.rowind[S.f0 + t];
-  }
-  for (int j = tid; j <= ncols; j += kCT) scp[j] = a.colptr[S.j0 + j] - S.f0;
+  // the CSC slice keeps only the F columns (every A^T product of the loop is
+  // needed on F only; the report's y' over all columns reads the global CSC)
   for (int j = tid; j < ncols; j += kCT) smk[j] = mask[S.j0 + j];
+  if (wid == 0) {
+    int carry = 0;
+    for (int b0 = 0; b0 < ncols; b0 += 32) {
+      const int j = b0 + lane;
+      const bool inF = j < ncols && mask[S.j0 + j];
+      const unsigned bal = __ballot_sync(kFull, inF);
+      if (inF) fcol[carry + __popc(bal & ((1u << lane) - 1u))] = j;
+      carry += __popc(bal);
+    }
+    if (lane == 0) s_nfc = carry;
+  }
+  __syncthreads();
+  const int nfc = s_nfc;
+  for (int q = tid; q < nfc; q += kCT) scp[q + 1] = a.colptr[S.j0 + fcol[q] + 1] - a.colptr[S.j0 + fcol[q]];
+  if (tid == 0) scp[0] = 0;
+  __syncthreads();
+  if (wid == 0) {  // inclusive scan of the F-column lengths (one warp)
+    int carry = 0;
+    for (int b0 = 0; b0 < nfc; b0 += 32) {
+      int v = (b0 + lane < nfc) ? scp[b0 + lane + 1] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += y;
+      }
+      if (b0 + lane < nfc) scp[b0 + lane + 1] = v + carry;
+      carry += __shfl_sync(kFull, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int q = wid; q < nfc; q += NW) {  // copy the F columns (warp per column, coalesced)
+    const int src = a.colptr[S.j0 + fcol[q]], dst = scp[q], cnt = scp[q + 1] - dst;
+    for (int t = lane; t < cnt; t += 32) {
+      scv[dst + t] = a.cvals[src + t];
+      sri[dst + t] = a.rowind[src + t];
+    }
+  }
   for (int r = tid; r < nrows; r += kCT) srp[r + 1] = __ldcg(&a.Fcnt[S.r0 + r]);  // F-entries per row
   if (tid == 0) srp[0] = 0;
   __syncthreads();
@@ -660,13 +696,11 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   // push own rows/cols of a replica to every CTA's copy
   // (all 512 threads share the (destination, element) space: a loop over
   //  destinations with only `cnt` active threads was 4x slower)
-  auto push = [&](double* rep, int base, int cnt) {
-    const int tot = cnt * (C - 1);
-    for (int e = tid; e < tot; e += kCT) {
-      const int qq = e / cnt, i = e - qq * cnt;
-      const int q = qq + (qq >= kr);  // skip self
+  auto push = [&](double* rep, int base, int cnt) {  // warp per destination
+    for (int d = wid; d < C - 1; d += NW) {
+      const int q = d + (d >= kr);  // skip self
       double* dst = cl.map_shared_rank(rep, q);
-      dst[base + i] = rep[base + i];
+      for (int i = lane; i < cnt; i += 32) dst[base + i] = rep[base + i];
     }
   };
 
@@ -697,7 +731,8 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
     const double bnorm = beta;
     // V' = A_F^T u on own columns
     const double ib0 = beta > 0.0 ? 1.0 / beta : 0.0;
-    seg_dots(ncols, gC, scp, scv, sri, Urep, smk, [&](int j, double s) { Vrep[S.j0 + j] = s * ib0; });
+    seg_dots(nfc, seg_group(nfc), scp, scv, sri, Urep, nullptr,
+             [&](int q, double s) { Vrep[S.j0 + fcol[q]] = s * ib0; });
     __syncthreads();
     p = 0.0;
     for (int j = tid; j < ncols; j += kCT) {
@@ -723,7 +758,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
     double last_phi = 0.0, last_sn = 0.0;  // for the deferred stopping test
     bool pending = false;
     double pd = 0.0, px = 0.0;
-    const int gCw = seg_group(ncols, kCT - 32);  // phase B runs on warps 1.. (warp 0: scalars)
+    const int gCw = seg_group(nfc, kCT - 32);  // phase B runs on warps 1.. (warp 0: scalars)
     __syncthreads();
     LQ_STAMP_SETUP(3);
     if (alpha * beta != 0.0) {
@@ -786,7 +821,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
           }
           LQ_STAMP(12);
         } else if (more) {
-          seg_dots(ncols, gCw, scp, scv, sri, Urep, smk, [&](int j, double s) { scr[j] = s; }, 32);
+          seg_dots(nfc, gCw, scp, scv, sri, Urep, nullptr, [&](int q, double s) { scr[fcol[q]] = s; }, 32);
           if (g_lsqr_prof != nullptr && kr == 0 && threadIdx.x == 32 && itn < 64) {
             unsigned long long t_;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
@@ -913,7 +948,8 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
     push(Urep, S.r0, nrows);
     publish(1, &po, K_SUM, 0);
     cl.sync();
-    seg_dots(ncols, gC, scp, scv, sri, Urep, nullptr, [&](int j, double s) { scr[j] = s; });
+    seg_dots(ncols, seg_group(ncols), a.colptr + S.j0, a.cvals, a.rowind, Urep, nullptr,
+             [&](int j, double s) { scr[j] = s; });  // all own columns, global CSC
     __syncthreads();
     double mx = INFINITY, my = INFINITY, mc = 0.0, dot = 0.0;
     for (int j = tid; j < ncols; j += kCT) {

@@ -22,15 +22,16 @@ for rep in range(2):
     x, info = S.solve()
     P.lib.nnls_debug_lsqr_profile(C.c_void_p(0))
 p = prof.cpu().numpy().reshape(64, 16).astype(np.float64)
-names = ["A.compute", "A.push+bsum", "A.clsync", "test", "B.compute(+ctotal)", "B.push+bsum", "B.clsync",
-         "ctotal(alpha)", "C.compute", "C.bsum x2"]
-rows = [r for r in range(1, 63) if p[r, 0] > 0 and p[r, 10] > 0 and p[r + 1, 0] > 0]
+names = ["A.compute", "A.push+bsum", "A.clsync", "B dots | scalars", "B.v update", "B.push+bsum", "B.clsync",
+         "ctotal(alpha)", "C.compute", "(C end)"]
+# (itn is incremented between stamps 4 and 5: slots 0-4 and 11-13 of an
+# iteration are in row r, slots 5-10 in row r + 1)
+rows = [r for r in range(1, 62) if p[r, 0] > 0 and p[r + 1, 10] > 0 and p[r + 1, 0] > 0]
 d = {n: [] for n in names}
-d["C->nextA"] = []
 for r in rows:
+    q = np.concatenate([p[r, :5], p[r + 1, 5:11]])
     for k in range(10):
-        d[names[k]].append(p[r, k + 1] - p[r, k])
-    d["C->nextA"].append(p[r + 1, 0] - p[r, 10])
+        d[names[k]].append(q[k + 1] - q[k])
 print("iterations profiled:", len(rows), "lsqr_iterations:", info["lsqr_iterations"])
 bd = [p[r, 13] - p[r, 3] for r in rows if p[r, 13] > 0]
 if bd:
