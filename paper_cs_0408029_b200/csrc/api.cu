@@ -237,7 +237,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->xfin, sizeof(double) * (size_t)n));
   CK(ensure(h->partials, sizeof(double) * 8 * (size_t)(h->sms * 4)));
   CK(ensure(h->st, sizeof(DevState)));
-  CK(ensure(h->err, sizeof(int) * 8));
+  CK(ensure(h->err, sizeof(int) * 64));  // [0..3] error bits / longest row, column; [4..] LSQR plan
   const int cap = h->prm.trace ? (h->prm.max_iter > 0 ? h->prm.max_iter : 10 * n) + 1 : 0;
   h->trace_cap = cap;
   if (cap > 0) CK(ensure(h->trace, sizeof(TraceRec) * (size_t)cap));
@@ -486,7 +486,8 @@ LsqrArgs lsqr_args(nnls_handle* h) {
   a.Fval = P<double>(h->Fval);
   a.Fcol = P<int32_t>(h->Fcol);
   a.Fcnt = P<int32_t>(h->Fcnt);
-  a.Fidx = P<int32_t>(h->Fidx);
+  a.Fidx = h->no_reuse ? P<int32_t>(h->Fidx) : P<int32_t>(h->Fs);  // F (index order when reusing)
+  a.plan = P<int>(h->err) + 4;
   return a;
 }
 

@@ -99,7 +99,8 @@ struct LsqrArgs {
   // rows of A restricted to the final F, compacted in place of each row
   // (row r: Fcnt[r] entries from offset rowptr[r]); built by launch_lsqr_compact
   double* Fval; int32_t* Fcol; int32_t* Fcnt;
-  const int32_t* Fidx;  // the final F, sorted (f entries; from the last compaction)
+  const int32_t* Fidx;  // the final F (f entries; from the last decide)
+  const int* plan;      // cluster slice plan (lsqr_plan_kernel: maxima, row bounds, column bounds)
 };
 cudaError_t launch_lsqr_compact(const LsqrArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s);

@@ -433,35 +433,6 @@ struct ClSlices {
   int j0, j1, f0, f1;   // cols [j0,j1), CSC entries [f0,f1)
 };
 
-__device__ __forceinline__ int lower_bound_i(const int32_t* __restrict__ p, int len, int key) {
-  int lo = 0, hi = len;  // first index with p[idx] >= key
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (p[mid] < key) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ ClSlices cl_slices(int k, int C, int m, int n, const int32_t* rowptr,
-                                              const int32_t* colptr) {
-  ClSlices s;
-  const long long nnz = rowptr[m];
-  s.r0 = (k == 0) ? 0 : lower_bound_i(rowptr, m + 1, (int)(nnz * k / C));
-  s.r1 = (k == C - 1) ? m : lower_bound_i(rowptr, m + 1, (int)(nnz * (k + 1) / C));
-  s.r0 = min(s.r0, m);
-  s.r1 = min(max(s.r1, s.r0), m);
-  s.e0 = rowptr[s.r0];
-  s.e1 = rowptr[s.r1];
-  s.j0 = (k == 0) ? 0 : lower_bound_i(colptr, n + 1, (int)(nnz * k / C));
-  s.j1 = (k == C - 1) ? n : lower_bound_i(colptr, n + 1, (int)(nnz * (k + 1) / C));
-  s.j0 = min(s.j0, n);
-  s.j1 = min(max(s.j1, s.j0), n);
-  s.f0 = colptr[s.j0];
-  s.f1 = colptr[s.j1];
-  return s;
-}
-
 struct ClLayout {
   int rows_max, cols_max, nzr_max, nzc_max;
   size_t bytes;
@@ -480,22 +451,53 @@ __host__ __device__ inline ClLayout cl_layout(int m, int n, const int* mx) {
 }
 }  // namespace
 
-// plan: per-CTA slice maxima for cluster size C -> out[0..3] = rows, nzr, cols, nzc
-__global__ void lsqr_plan_kernel(int m, int n, const int32_t* rowptr, const int32_t* colptr, int C,
-                                 int* out) {
-  const int k = threadIdx.x;
-  int v[4] = {0, 0, 0, 0};
-  if (k < C) {
-    const ClSlices s = cl_slices(k, C, m, n, rowptr, colptr);
-    v[0] = s.r1 - s.r0;
-    v[1] = s.e1 - s.e0;
-    v[2] = s.j1 - s.j0;
-    v[3] = s.f1 - s.f0;
+// plan: per-CTA slice bounds and maxima for cluster size C.  out[0..3] =
+// max rows, CSR nnz, cols, CSC nnz of a slice; out[4 .. 4+C] = row bounds,
+// out[5+C .. 5+2C] = column bounds (slice k: rows [rb[k], rb[k+1])).  Bound k
+// is the first row r with rowptr[r] >= nnz*k/C (nnz-balanced), found by
+// every thread checking its own rows against all C thresholds (no serial
+// binary searches).
+__global__ void __launch_bounds__(1024) lsqr_plan_kernel(int m, int n, const int32_t* rowptr,
+                                                         const int32_t* colptr, int C, int* out) {
+  int* rb = out + 4;
+  int* cb = out + 5 + C;
+  const long long nnz = rowptr[m];
+  const int tid = threadIdx.x;
+  for (int r = tid; r <= m; r += blockDim.x) {
+    const int v = rowptr[r], vp = r > 0 ? rowptr[r - 1] : (-0x7fffffff - 1);
+    for (int k = 1; k < C; ++k) {
+      const int thr = (int)(nnz * k / C);
+      if (vp < thr && v >= thr) rb[k] = r;
+    }
   }
+  for (int j = tid; j <= n; j += blockDim.x) {
+    const int v = colptr[j], vp = j > 0 ? colptr[j - 1] : (-0x7fffffff - 1);
+    for (int k = 1; k < C; ++k) {
+      const int thr = (int)(nnz * k / C);
+      if (vp < thr && v >= thr) cb[k] = j;
+    }
+  }
+  if (tid == 0) {
+    rb[0] = 0;
+    rb[C] = m;
+    cb[0] = 0;
+    cb[C] = n;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int v[4] = {0, 0, 0, 0};
+    if (tid < C) {
+      const int r0 = rb[tid], r1 = max(rb[tid + 1], r0), j0 = cb[tid], j1 = max(cb[tid + 1], j0);
+      v[0] = r1 - r0;
+      v[1] = rowptr[r1] - rowptr[r0];
+      v[2] = j1 - j0;
+      v[3] = colptr[j1] - colptr[j0];
+    }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    int x = warp_max_i(v[q]);
-    if (k == 0) out[q] = x;
+    for (int q = 0; q < 4; ++q) {
+      const int x = warp_max_i(v[q]);
+      if (tid == 0) out[q] = x;
+    }
   }
 }
 
@@ -561,7 +563,19 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kCT / 32;
   LQ_STAMP_SETUP(0);
-  const ClSlices S = cl_slices(kr, C, m, n, a.rowptr, a.colptr);
+  ClSlices S;  // this CTA's slice, from the plan (lsqr_plan_kernel)
+  {
+    const int* rb = a.plan + 4;
+    const int* cbd = a.plan + 5 + C;
+    S.r0 = rb[kr];
+    S.r1 = max(rb[kr + 1], S.r0);
+    S.j0 = cbd[kr];
+    S.j1 = max(cbd[kr + 1], S.j0);
+    S.e0 = a.rowptr[S.r0];
+    S.e1 = a.rowptr[S.r1];
+    S.f0 = a.colptr[S.j0];
+    S.f1 = a.colptr[S.j1];
+  }
   const int nrows = S.r1 - S.r0, ncols = S.j1 - S.j0;
   LQ_STAMP_SETUP(1);
   const int gR = seg_group(nrows);
@@ -1023,7 +1037,7 @@ cudaError_t launch_lsqr_compact(const LsqrArgs& a, int sm_count, cudaStream_t s)
 
 cudaError_t launch_lsqr_plan(int m, int n, const int32_t* rowptr, const int32_t* colptr, int* out,
                              cudaStream_t s) {
-  lsqr_plan_kernel<<<1, 32, 0, s>>>(m, n, rowptr, colptr, kMaxC, out);
+  lsqr_plan_kernel<<<1, 1024, 0, s>>>(m, n, rowptr, colptr, kMaxC, out);
   return cudaGetLastError();
 }
 
