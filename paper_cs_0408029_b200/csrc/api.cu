@@ -269,7 +269,8 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   TIMED(NNLS_PH_CSC, 2,
         launch_csc_fill(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                         P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                        P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s));
+                        P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s,
+                        h->h->err[2]));
   double* G = P<double>(h->Gc);
   double* c = G + (size_t)n * h->ldg;
   TIMED(NNLS_PH_GRAM, 1,

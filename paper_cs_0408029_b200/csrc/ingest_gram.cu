@@ -60,12 +60,37 @@ cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, co
 }
 
 // ---------------------------------------------------------------- CSR->CSC
+// Column counts: a shared-memory histogram per CTA (when n fits), flushed
+// with one global atomic per non-empty bin; few CTAs, so the flush stays
+// small next to the nnz shared-memory atomics.
+constexpr int kHistMax = 12288;
 __global__ void colcount_kernel(int64_t nnz, int n, const int32_t* __restrict__ colind, int32_t* cnt) {
+  extern __shared__ int hist[];
+  const bool sm = n <= kHistMax;
+  if (sm) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+  }
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int c = colind[e];
-    if (c >= 0 && c < n) atomicAdd(&cnt[c + 1], 1);  // runs before validation completes
+    if (c >= 0 && c < n) {  // (runs before validation completes)
+      if (sm) atomicAdd(&hist[c], 1);
+      else atomicAdd(&cnt[c + 1], 1);
+    }
   }
+  if (sm) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      if (hist[i] != 0) atomicAdd(&cnt[i + 1], hist[i]);
+  }
+}
+static void launch_colcount(int64_t nnz, int n, const int32_t* colind, int32_t* colptr, cudaStream_t s) {
+  long long b = nnz / (8LL * (n > 0 ? n : 1));  // ~8 entries per bin per CTA
+  if (b > 296) b = 296;
+  if (b < 1) b = 1;
+  const size_t smem = n <= kHistMax ? sizeof(int) * (size_t)n : 0;
+  colcount_kernel<<<(int)b, 1024, smem, s>>>(nnz, n, colind, colptr);
 }
 
 // In-place inclusive scan of cnt[0..len) (cnt[0] = 0 on entry) -> colptr; one CTA.
@@ -146,17 +171,39 @@ __global__ void csc_sort_kernel(int n, const int32_t* __restrict__ colptr,
   }
 }
 
+// Same ranking with the column's row indices staged in shared memory (one
+// warp per column, rank by broadcast compares): columns of up to `cap` rows.
+__global__ void csc_sort_smem_kernel(int n, const int32_t* __restrict__ colptr,
+                                     const int32_t* __restrict__ tmp_row,
+                                     const double* __restrict__ tmp_val, int32_t* rowind, double* cvals,
+                                     int cap) {
+  extern __shared__ int srow[];
+  const int lane = threadIdx.x & 31;
+  int* my = srow + (threadIdx.x >> 5) * cap;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n; c += warps) {
+    const int lo = colptr[c], len = colptr[c + 1] - lo;
+    for (int i = lane; i < len; i += 32) my[i] = tmp_row[lo + i];
+    __syncwarp();
+    for (int i = lane; i < len; i += 32) {
+      const int ri = my[i];
+      int rank = 0;
+#pragma unroll 8
+      for (int j = 0; j < len; ++j) rank += my[j] < ri;
+      rowind[lo + rank] = ri;
+      cvals[lo + rank] = tmp_val[lo + i];
+    }
+    __syncwarp();
+  }
+}
+
 cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
                               const int32_t* colind, const double* vals, int32_t* colptr,
                               int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,
                               double* tmp_val, cudaStream_t s, int* maxcnt) {
   cudaError_t e = cudaMemsetAsync(colptr, 0, sizeof(int32_t) * (size_t)(n + 1), s);
   if (e != cudaSuccess) return e;
-  if (nnz > 0) {
-    int blocks = (int)((nnz + 255) / 256);
-    if (blocks > 4096) blocks = 4096;
-    colcount_kernel<<<blocks, 256, 0, s>>>(nnz, n, colind, colptr);
-  }
+  if (nnz > 0) launch_colcount(nnz, n, colind, colptr, s);
   scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor, maxcnt);
   int rb = (int)(((int64_t)m * 32 + 255) / 256);
   if (rb > 4096) rb = 4096;
@@ -173,11 +220,7 @@ cudaError_t launch_csc_count(int m, int n, int64_t nnz, const int32_t* colind, i
   (void)m;
   cudaError_t e = cudaMemsetAsync(colptr, 0, sizeof(int32_t) * (size_t)(n + 1), s);
   if (e != cudaSuccess) return e;
-  if (nnz > 0) {
-    int blocks = (int)((nnz + 255) / 256);
-    if (blocks > 4096) blocks = 4096;
-    colcount_kernel<<<blocks, 256, 0, s>>>(nnz, n, colind, colptr);
-  }
+  if (nnz > 0) launch_colcount(nnz, n, colind, colptr, s);
   scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor, maxcnt);
   return cudaGetLastError();
 }
@@ -185,7 +228,7 @@ cudaError_t launch_csc_count(int m, int n, int64_t nnz, const int32_t* colind, i
 cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* colind,
                             const double* vals, const int32_t* colptr, int32_t* rowind,
                             double* cvals, int32_t* cursor, int32_t* tmp_row, double* tmp_val,
-                            cudaStream_t s) {
+                            cudaStream_t s, int maxcnt) {
   int rb = (int)(((int64_t)m * 32 + 255) / 256);
   if (rb > 4096) rb = 4096;
   if (rb < 1) rb = 1;
@@ -193,7 +236,13 @@ cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* 
   int cb = (int)(((int64_t)n * 32 + 255) / 256);
   if (cb > 4096) cb = 4096;
   if (cb < 1) cb = 1;
-  csc_sort_kernel<<<cb, 256, 0, s>>>(n, colptr, tmp_row, tmp_val, rowind, cvals);
+  if (maxcnt >= 0 && maxcnt <= 1536) {  // 8 warps x maxcnt rows in shared memory (<= 48 KB)
+    const int cap = maxcnt > 0 ? maxcnt : 1;
+    csc_sort_smem_kernel<<<cb, 256, sizeof(int) * 8 * (size_t)cap, s>>>(n, colptr, tmp_row, tmp_val, rowind,
+                                                                        cvals, cap);
+  } else {
+    csc_sort_kernel<<<cb, 256, 0, s>>>(n, colptr, tmp_row, tmp_val, rowind, cvals);
+  }
   return cudaGetLastError();
 }
 

@@ -23,7 +23,7 @@ cudaError_t launch_csc_count(int m, int n, int64_t nnz, const int32_t* colind, i
 cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* colind,
                             const double* vals, const int32_t* colptr, int32_t* rowind,
                             double* cvals, int32_t* cursor, int32_t* tmp_row, double* tmp_val,
-                            cudaStream_t s);
+                            cudaStream_t s, int maxcnt = -1);
 cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
                               const int32_t* colind, const double* vals, int32_t* colptr,
                               int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,

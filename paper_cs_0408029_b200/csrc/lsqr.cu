@@ -459,23 +459,23 @@ __host__ __device__ inline ClLayout cl_layout(int m, int n, const int* mx) {
 // binary searches).
 __global__ void __launch_bounds__(1024) lsqr_plan_kernel(int m, int n, const int32_t* rowptr,
                                                          const int32_t* colptr, int C, int* out) {
+  __shared__ int thr[kMaxC];
   int* rb = out + 4;
   int* cb = out + 5 + C;
-  const long long nnz = rowptr[m];
   const int tid = threadIdx.x;
+  if (tid < C) thr[tid] = (int)((long long)rowptr[m] * tid / C);
+  __syncthreads();
   for (int r = tid; r <= m; r += blockDim.x) {
     const int v = rowptr[r], vp = r > 0 ? rowptr[r - 1] : (-0x7fffffff - 1);
-    for (int k = 1; k < C; ++k) {
-      const int thr = (int)(nnz * k / C);
-      if (vp < thr && v >= thr) rb[k] = r;
-    }
+    if (v == vp) continue;  // (an empty row is never a first crossing)
+    for (int k = 1; k < C; ++k)
+      if (vp < thr[k] && v >= thr[k]) rb[k] = r;
   }
   for (int j = tid; j <= n; j += blockDim.x) {
     const int v = colptr[j], vp = j > 0 ? colptr[j - 1] : (-0x7fffffff - 1);
-    for (int k = 1; k < C; ++k) {
-      const int thr = (int)(nnz * k / C);
-      if (vp < thr && v >= thr) cb[k] = j;
-    }
+    if (v == vp) continue;
+    for (int k = 1; k < C; ++k)
+      if (vp < thr[k] && v >= thr[k]) cb[k] = j;
   }
   if (tid == 0) {
     rb[0] = 0;
