@@ -301,9 +301,35 @@ __device__ __forceinline__ void wsync() {
   else asm volatile("bar.sync 2, %0;\n" ::"n"(NW * 32) : "memory");
 }
 
+// S block (I,J) -= X(I rows) X(J rows)^T, K = 64 (the deferred last update
+// of a diagonal tile, one 8x8 block); two blocks interleaved when J2 >= 0.
+__device__ __forceinline__ void syrk_blocks(double* __restrict__ S, const double* __restrict__ X, int I, int J,
+                                            int I2, int J2, int lane) {
+  const int rq = lane >> 2, kq = lane & 3;
+  double* C1 = S + (8 * I + rq) * LDS + 8 * J + 2 * kq;
+  double* C2 = S + (8 * max(I2, 0) + rq) * LDS + 8 * max(J2, 0) + 2 * kq;
+  const double* a1 = X + (8 * I + rq) * LDS + kq;
+  const double* b1 = X + (8 * J + rq) * LDS + kq;
+  const double* a2 = X + (8 * max(I2, 0) + rq) * LDS + kq;
+  const double* b2 = X + (8 * max(J2, 0) + rq) * LDS + kq;
+  double c0 = C1[0], c1 = C1[1], d0 = C2[0], d1 = C2[1];
+#pragma unroll
+  for (int kk = 0; kk < T; kk += 4) {
+    dmma8x8x4(c0, c1, -a1[kk], b1[kk]);
+    dmma8x8x4(d0, d1, -a2[kk], b2[kk]);  // (a dummy copy of block 1 when J2 < 0)
+  }
+  C1[0] = c0;
+  C1[1] = c1;
+  if (J2 >= 0) {
+    C2[0] = d0;
+    C2[1] = d1;
+  }
+}
+
 template <int NR, int NW = 8, bool SPLIT = false>
 __device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
-                                        double* __restrict__ rinv, int* s_bad) {
+                                        double* __restrict__ rinv, int* s_bad,
+                                        const double* __restrict__ X = nullptr) {
   static_assert(NW == 7 || NW == 8, "potrf_r8 runs on 7 or 8 warps");
   static_assert(!SPLIT || NR == 1, "SPLIT: two panel warps with 32 rows each");
   // SPLIT: the panel rows are shared by warps 0 (rows c0..c0+31) and 1
@@ -314,6 +340,14 @@ __device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
   if (tid == 0) *s_bad = -1;
   const int np = (cv + 7) >> 3;
   const int nbr = (rv + 7) >> 3;
+  // X != nullptr: the tile's last update S -= X X^T (X = the previous
+  // column's sub-diagonal tile) is still pending; it is applied column block
+  // by column block just ahead of the panel that needs it: block 0 here,
+  // block p+1 by the strip warps during panel p.
+  if (X != nullptr && w < nbr) {
+    const int I2 = w + NW < nbr ? w + NW : -1;
+    syrk_blocks(S, X, w, 0, I2 < 0 ? w : I2, I2 < 0 ? -1 : 0, lane);
+  }
   wsync<NW>();
 #pragma unroll 1
   for (int p = 0; p < np; ++p) {
@@ -327,62 +361,19 @@ __device__ __forceinline__ int potrf_r8(double* __restrict__ S, int rv, int cv,
       const int bad = (c0 + 8 <= cv) ? panel_factor8<NR, true>(S, c0, r0, rv, cv, rinv, lane, w == 0)
                                      : panel_factor8<NR, false>(S, c0, r0, rv, cv, rinv, lane, w == 0);
       if (w == 0 && lane == 0 && bad >= 0 && *s_bad < 0) *s_bad = bad;
-    } else if (p > 0) {
+    } else {
       // (c) row strips I in [p+1, nbr) x column blocks [p+1, min(I, ncb-1)]
+      // (panel p-1), then the pending last update of block (I, p+1)
       const int ncb = (cv + 7) >> 3;
       for (int I = p + 1 + (w - NPW); I < nbr; I += NW - NPW) {
         const int j1 = min(I + 1, ncb);
-        if (p + 1 < j1) strip8_gemm(S, S, S, c0 - 8, 8 * I, p + 1, j1, lane);
+        if (p > 0 && p + 1 < j1) strip8_gemm(S, S, S, c0 - 8, 8 * I, p + 1, j1, lane);
+        if (X != nullptr && p + 1 < ncb) syrk_blocks(S, X, I, p + 1, I, -1, lane);
       }
     }
     wsync<NW>();
   }
   return *s_bad;
-}
-
-// Y (lower 8x8 blocks of a 64x64 tile) -= X X^T, K = 64, on all 8 warps:
-// block b = I(I+1)/2 + J goes to warp b % 8 (slot b / 8); warps with 4
-// blocks repeat one as a dummy 5th (result dropped), so the 5 independent
-// 16-step DMMA chains of a warp are unconditional.
-__device__ __forceinline__ void syrk64_lower(double* __restrict__ Y, const double* __restrict__ X, int w,
-                                             int lane) {
-  constexpr int NS = 5;
-  const int kq = lane & 3, rq = lane >> 2;
-  int ra[NS], rb[NS], ci[NS];
-#pragma unroll
-  for (int q = 0; q < NS; ++q) {
-    int b = w + 8 * q;
-    if (b > 35) b = w + 8 * (q - 1);  // dummy slot
-    int I = 0;
-    while ((I + 1) * (I + 2) / 2 <= b) ++I;
-    const int J = b - I * (I + 1) / 2;
-    ra[q] = (8 * I + rq) * LDS + kq;
-    rb[q] = (8 * J + rq) * LDS + kq;
-    ci[q] = (8 * I + rq) * LDS + 8 * J + 2 * kq;
-  }
-  double cv0[NS], cv1[NS];
-#pragma unroll
-  for (int q = 0; q < NS; ++q) {
-    cv0[q] = Y[ci[q]];
-    cv1[q] = Y[ci[q] + 1];
-  }
-#pragma unroll 4
-  for (int kk = 0; kk < T; kk += 4) {
-#pragma unroll
-    for (int q = 0; q < NS; ++q) {
-      const double av = -X[ra[q] + kk];
-      const double bv = X[rb[q] + kk];
-      dmma8x8x4(cv0[q], cv1[q], av, bv);
-    }
-  }
-  const int nq = (w < 4) ? 5 : 4;
-#pragma unroll
-  for (int q = 0; q < NS; ++q) {
-    if (q < nq) {
-      Y[ci[q]] = cv0[q];
-      Y[ci[q] + 1] = cv1[q];
-    }
-  }
 }
 
 // smem writes of this thread -> visible to the async proxy (bulk copies)
@@ -659,7 +650,6 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     // partials A(j+1,j) and A(j+1,j+1); TRSM on all warps (warp 7 raises
     // L_jj's flag in a solve phase); last update of A(j+1,j+1) on warps 0-6
     // while warp 7 raises L(j+1,j)'s flag.
-    double* Lnext = smem + 5 * (T * LDS);
     double* Xinv = smem + 2 * (T * LDS);  // Linv_jj
     double* Tm = smem + 3 * (T * LDS);    // trtri scratch
     int first_bad = -1;
@@ -669,6 +659,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     for (int j = jq; j < ntc; ++j) {
       double* Sd = smem + (j & 1) * (T * LDS);
       double* Snext = smem + ((j + 1) & 1) * (T * LDS);
+      // A/L(j+1,j) in BUF(4)/BUF(5) by column parity: L(j,j-1) stays put
+      // while column j's POTRF applies it (the deferred SYRK)
+      double* Lnext = smem + (4 + (j & 1)) * (T * LDS);
+      const double* Lprev = (j > jq) ? smem + (4 + ((j - 1) & 1)) * (T * LDS) : nullptr;
       const int cv = min(T, f - j * T), rv = min(T, f + 1 - j * T);
       const bool has_sub = j + 1 < ntr, has_next = j + 1 < ntc;
       int* const fl_sub = &F.part[tidx(j + 1, j)];
@@ -718,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
         cp_async_wait<0>();
       } else {
         // ---- warps 0..6: L_jj = chol(A_jj), stored
-        const int bad = potrf_r8<1, 7, true>(Sd, rv, cv, rinv, &s_bad);
+        const int bad = potrf_r8<1, 7, true>(Sd, rv, cv, rinv, &s_bad, Lprev);
         for (int e = tid; e < T * T; e += kThreads - 32)  // strict upper part
           if ((e % T) > (e / T)) Sd[(e / T) * LDS + (e % T)] = 0.0;
         if (bad >= 0 && first_bad < 0) first_bad = j * T + bad;
@@ -752,12 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       fence_proxy_async_smem();  // L(j+1,j) (Lnext) -> the bulk store
       csync();
       if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j + 1, j) * TS, Lnext);
-      if (has_next) {
-        // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T on all warps
-        syrk64_lower(Snext, Lnext, w, lane);
-        PROF_STAMP(j, 6);
-        csync();
-      }
+      // (A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T is applied inside the next POTRF)
       pending = &F.full[tidx(j + 1, j)];  // released by warp 7 in the next POTRF (or below)
       PROF_STAMP(j, 5);
     }
