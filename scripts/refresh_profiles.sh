@@ -13,8 +13,13 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 # launch list (cold-cache, serialised) of the same command as the bench value pass
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
   --log-file $O/launches_c1.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
-# full capture of the dominant kernels (one launch each)
-timeout 900 ncu --set full --import-source on --clock-control none \
-  -k regex:"chol_factor_kernel|lsqr_cluster_kernel|chol_backsolve_kernel|gram_kernel|dual_kernel" -c 5 \
-  -o $O/full_c1 -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_full.log 2>&1
+# full capture of the dominant kernels: one launch of each, one ncu run per
+# kernel (a single regex with -c N would stop at the first N matches)
+for k in chol_factor_kernel chol_backsolve_kernel lsqr_cluster_kernel gram_kernel dual_kernel decide_kernel; do
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$k" -c 1 \
+    -o $O/full_c1_$k -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_full_$k.log 2>&1
+done
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:chol_factor_kernel -c 1 \
+  -o $O/full_c2_chol_factor_kernel -f python bench.py --config 2 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e \
+  > $O/ncu_full_c2.log 2>&1
 echo done
