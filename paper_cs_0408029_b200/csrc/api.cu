@@ -59,7 +59,7 @@ int round_up(int v, int q) { return (v + q - 1) / q * q; }
 
 struct HostState {
   DevState st;
-  int err[4];   // validation bits, longest row, longest column
+  int err[64];  // device err block: [0] bits, [1] longest row, [2] longest column, [4..] LSQR plan, [48..] exponents
   int plan[4];  // cluster LSQR slice maxima (rows, CSR nnz, cols, CSC nnz)
 };
 
@@ -98,6 +98,7 @@ struct nnls_handle {
   bool no_cluster = false;  // force the full-grid LSQR (tests / env NNLS_NO_CLUSTER)
   bool no_graph = false;    // host-driven pivot loop (env NNLS_NO_GRAPH, or capture failed)
   bool no_reuse = false;    // F in index order, no factor reuse across iterations (env NNLS_NO_REUSE)
+  bool no_exact_gram = false;  // always the row-ordered Gram kernel (env NNLS_NO_EXACT_GRAM)
   cudaGraphExec_t gexec = nullptr;
   std::vector<double> gkey;
   cudaStream_t gstream = nullptr;
@@ -249,7 +250,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
     CK(cudaMemcpyAsync(h->vals.p, vals, sizeof(double) * (size_t)nnz, cudaMemcpyDefault, s));
   }
   CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)m, cudaMemcpyDefault, s));
-  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int) * 8, s));
+  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int) * 64, s));
   tm_end(h, NNLS_PH_UPLOAD, ib, 0);
   TIMED(NNLS_PH_VALIDATE, 1,
         launch_validate(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
@@ -262,10 +263,11 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
                          P<int32_t>(h->cursor), s, P<int>(h->err) + 2));
   CK(launch_lsqr_plan(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colptr), P<int>(h->err) + 4, s));
   tm_end(h, NNLS_PH_CSC, -1, 1);
-  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int herr = h->h->err[0];
   if (herr) return map_err_bits(herr);
+  memcpy(h->h->plan, h->h->err + 4, sizeof(h->h->plan));  // cluster LSQR slice maxima
   TIMED(NNLS_PH_CSC, 2,
         launch_csc_fill(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                         P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
@@ -276,7 +278,8 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   TIMED(NNLS_PH_GRAM, 1,
         launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                     P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                    P<double>(h->b), r0, r1, G, h->ldg, c, h->sms, s));
+                    P<double>(h->b), r0, r1, G, h->ldg, c, h->sms, s, gram_is_exact(h->h->err) && !h->no_exact_gram,
+                    gram_exact_lmin(h->h->err)));
   h->loaded = true;
   return NNLS_OK;
 }
@@ -306,6 +309,7 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
   h->no_cluster = getenv("NNLS_NO_CLUSTER") != nullptr;
   h->no_graph = getenv("NNLS_NO_GRAPH") != nullptr;
   h->no_reuse = getenv("NNLS_NO_REUSE") != nullptr;
+  h->no_exact_gram = getenv("NNLS_NO_EXACT_GRAM") != nullptr;
   *out = h;
   return NNLS_OK;
 }

@@ -13,6 +13,7 @@
 // (coalesced), so HBM traffic is the n^2 output write plus L2-resident CSR
 // reads.
 #include <cuda_runtime.h>
+#include <math.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -20,13 +21,36 @@
 namespace nnls {
 
 // ---------------------------------------------------------------- validate
+// Exponent statistics of the nonzero values: H = exponent of the leading bit,
+// L = exponent of the lowest set bit; kept biased so that 0 means "none":
+// h = max(h, H + 2048), l = max(l, 2048 - L).  Non-normal values (subnormal)
+// make L tiny, i.e. "not exact".  Used by gram_is_exact().
+__device__ __forceinline__ void exact_bits(double v, int& h, int& l) {
+  if (v == 0.0) return;
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  const int ex = (int)((u >> 52) & 0x7FF);
+  if (ex == 0) {  // subnormal
+    l = max(l, 4095);
+    return;
+  }
+  const int H = ex - 1023;
+  const unsigned long long mant = (u & ((1ull << 52) - 1)) | (1ull << 52);
+  const int L = H - 52 + (__ffsll((long long)mant) - 1);
+  h = max(h, H + 2048);
+  l = max(l, 2048 - L);
+}
+
 __global__ void validate_kernel(int m, int n, int64_t nnz, const int32_t* __restrict__ rowptr,
                                 const int32_t* __restrict__ colind,
                                 const double* __restrict__ vals, const double* __restrict__ b,
                                 int* err) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  __shared__ int s_st[4];
+  if (threadIdx.x < 4) s_st[threadIdx.x] = 0;
+  __syncthreads();
   int e_local = 0, maxlen = 0;
+  int hA = 0, lA = 0, hb = 0, lb = 0;  // biased exponent statistics (0: none), see exact_bits
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
     int64_t lo = rowptr[r], hi = rowptr[r + 1];
     if (hi - lo > maxlen) maxlen = (int)min((int64_t)0x7fffffff, hi - lo);
@@ -34,6 +58,7 @@ __global__ void validate_kernel(int m, int n, int64_t nnz, const int32_t* __rest
       if (r == 0 && lo != 0) e_local |= 1;
       if (r == m - 1 && hi != nnz) e_local |= 1;
       if (!isfinite(b[r])) e_local |= 4;
+      exact_bits(b[r], hb, lb);
     }
     if (hi < lo || lo < 0 || hi > nnz) {
       e_local |= 1;
@@ -44,10 +69,23 @@ __global__ void validate_kernel(int m, int n, int64_t nnz, const int32_t* __rest
       if (cidx < 0 || cidx >= n) e_local |= 2;
       if (t > lo && colind[t - 1] >= cidx) e_local |= 2;
       if (!isfinite(vals[t])) e_local |= 4;
+      exact_bits(vals[t], hA, lA);
     }
   }
   if (e_local) atomicOr(err, e_local);
   if (lane == 0 && maxlen > 0) atomicMax(err + 1, maxlen);  // longest row (LSQR planning)
+  hA = warp_max_i(hA);
+  lA = warp_max_i(lA);
+  hb = warp_max_i(hb);
+  lb = warp_max_i(lb);
+  if (lane == 0) {  // block first, then one global atomic per statistic per block
+    if (hA) atomicMax(&s_st[0], hA);
+    if (lA) atomicMax(&s_st[1], lA);
+    if (hb) atomicMax(&s_st[2], hb);
+    if (lb) atomicMax(&s_st[3], lb);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && s_st[threadIdx.x]) atomicMax(err + kErrExp + threadIdx.x, s_st[threadIdx.x]);
 }
 
 cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
@@ -342,11 +380,161 @@ __global__ void __launch_bounds__(256) gram_kernel(
   }
 }
 
+// Exact-arithmetic Gram: when every product a_ri a_rj and every partial sum
+// of a column is exactly representable (gram_is_exact: the inputs' exponent
+// range and the longest column bound the bits; BASELINE's 2^-12-quantized
+// inputs qualify), the sum order cannot change a single bit, so a CTA per G
+// row scatters ALL contributing A rows at once (flat over their entries, all
+// loads in flight) with shared-memory atomics.  Bit-identical to the ordered
+// kernel above and to the oracle, without its per-row dependent chain.
+constexpr int kExactTuples = 512;  // longest column handled by gram_exact_kernel
+__global__ void __launch_bounds__(512) gram_exact_kernel(
+    int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+    const double* __restrict__ vals, const int32_t* __restrict__ colptr,
+    const int32_t* __restrict__ rowind, const double* __restrict__ cvals,
+    const double* __restrict__ b, int row_begin, int row_end, double* __restrict__ G, int ldg,
+    double* __restrict__ c, double scale, double inv_scale) {
+  // Every product a_ri a_rj is an integer multiple of 2^(2 L_A) (L_A: the
+  // lowest set bit over A) and every column sum stays below 2^53 units, so
+  // the accumulator holds exact 64-bit integers (product * scale), kept as
+  // two 32-bit words updated with the native shared-memory 32-bit atomics
+  // (FP64 and 64-bit ones are CAS loops on sm_100): the low word's add
+  // returns the old value, and the thread whose add wrapped carries into the
+  // high word -- exact two's-complement arithmetic mod 2^64.
+  // Warp w scatters the contributing rows q = w, w+16, ... (lanes = the row's
+  // entries); the (a_ri, row start, length) tuples of the CTA's NEXT G row are
+  // loaded into registers while the current one is scattered.
+  extern __shared__ unsigned acc_w[];  // [lo words n][hi words n]
+  __shared__ double s_a[kExactTuples];
+  __shared__ int s_lo[kExactTuples], s_len[kExactTuples];
+  __shared__ double s_c[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+  unsigned* acc_lo = acc_w;
+  int* acc_hi = reinterpret_cast<int*>(acc_w + n);
+  // tuple of entry tid of column i -> registers (len 0: outside the shard / none)
+  auto load_tuple = [&](int i, double& a, int& lo, int& len, double& cp) {
+    a = 0.0;
+    lo = 0;
+    len = 0;
+    cp = 0.0;
+    if (i >= n) return;
+    const int e0 = colptr[i], cnt = colptr[i + 1] - e0;  // cnt <= kExactTuples (host-checked)
+    if (tid < cnt) {
+      const int r = rowind[e0 + tid];
+      a = cvals[e0 + tid];
+      if (r >= row_begin && r < row_end) {
+        lo = rowptr[r];
+        len = rowptr[r + 1] - lo;
+        cp = a * b[r];
+      }
+    }
+  };
+  double ta, tcp;
+  int tlo, tlen;
+  load_tuple(blockIdx.x, ta, tlo, tlen, tcp);
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int j = tid; j < n; j += nt) {
+      acc_lo[j] = 0u;
+      acc_hi[j] = 0;
+    }
+    if (tid < kExactTuples) {
+      s_a[tid] = ta;
+      s_lo[tid] = tlo;
+      s_len[tid] = tlen;
+    }
+    const int cnt = colptr[i + 1] - colptr[i];
+    double cp = warp_sum(tcp);  // c_i (exact: any order)
+    if (lane == 0) s_c[wid] = cp;
+    __syncthreads();
+    if (wid == 0) {
+      double cv = lane < nw ? s_c[lane] : 0.0;
+      cv = warp_sum(cv);
+      if (lane == 0) c[i] = cv;
+    }
+    load_tuple(i + gridDim.x, ta, tlo, tlen, tcp);  // next G row's tuples, in flight meanwhile
+    // scatter: warp per contributing row, two rows per pass (loads in flight together)
+    for (int q = wid; q < cnt; q += 2 * nw) {
+      const int q2 = q + nw;
+      const double a1 = s_a[q], a2 = q2 < cnt ? s_a[q2] : 0.0;
+      const int lo1 = s_lo[q], len1 = s_len[q];
+      const int lo2 = q2 < cnt ? s_lo[q2] : 0, len2 = q2 < cnt ? s_len[q2] : 0;
+      const int mx = max(len1, len2);
+      for (int t = lane; t < mx; t += 32) {
+        int j1 = -1, j2 = -1;
+        double v1 = 0.0, v2 = 0.0;
+        if (t < len1) {
+          j1 = colind[lo1 + t];
+          v1 = vals[lo1 + t];
+        }
+        if (t < len2) {
+          j2 = colind[lo2 + t];
+          v2 = vals[lo2 + t];
+        }
+        if (j1 >= 0) {
+          const long long v = __double2ll_rn((a1 * v1) * scale);  // exact integer
+          const unsigned vlo = (unsigned)v;
+          const unsigned old = atomicAdd(&acc_lo[j1], vlo);
+          const int vhi = (int)(v >> 32) + ((old + vlo < old) ? 1 : 0);
+          if (vhi != 0) atomicAdd(&acc_hi[j1], vhi);
+        }
+        if (j2 >= 0) {
+          const long long v = __double2ll_rn((a2 * v2) * scale);
+          const unsigned vlo = (unsigned)v;
+          const unsigned old = atomicAdd(&acc_lo[j2], vlo);
+          const int vhi = (int)(v >> 32) + ((old + vlo < old) ? 1 : 0);
+          if (vhi != 0) atomicAdd(&acc_hi[j2], vhi);
+        }
+      }
+    }
+    __syncthreads();
+    double* Gi = G + (size_t)i * ldg;
+    for (int j = tid; j < n; j += nt)
+      Gi[j] = (double)(long long)(((unsigned long long)(unsigned)acc_hi[j] << 32) | acc_lo[j]) * inv_scale;
+    __syncthreads();
+  }
+}
+
+bool gram_is_exact(const int* err) {
+  const int K = err[2];  // longest column
+  const int hA = err[kErrExp], lA = err[kErrExp + 1], hb = err[kErrExp + 2], lb = err[kErrExp + 3];
+  if (K > kExactTuples || lA >= 4095 || lb >= 4095) return false;
+  if (hA == 0) return true;  // A == 0
+  int lgK = 0;
+  while ((1 << lgK) < K + 1) ++lgK;
+  const int HA = hA - 2048, LA = 2048 - lA;
+  // sum of K products |a a'| < 2^(2HA+2+lgK) must stay below 2^(53 + 2LA)
+  if (2 * HA + 2 + lgK > 53 + 2 * LA) return false;
+  if (2 * LA < -1000 || 2 * HA > 1000) return false;  // (the integer scale must stay a normal double)
+  if (hb == 0) return true;  // b == 0
+  const int Hb = hb - 2048, Lb = 2048 - lb;
+  return HA + Hb + 2 + lgK <= 53 + LA + Lb;
+}
+
 cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
                         const double* vals, const int32_t* colptr, const int32_t* rowind,
                         const double* cvals, const double* b, int row_begin, int row_end,
-                        double* G, int ldg, double* c, int sm_count, cudaStream_t s) {
+                        double* G, int ldg, double* c, int sm_count, cudaStream_t s, bool exact,
+                        int exact_lmin) {
   (void)m;
+  if (exact && (size_t)n * sizeof(double) <= 160 * 1024) {
+    static bool attr_x = false;
+    if (!attr_x) {
+      cudaError_t e = cudaFuncSetAttribute(gram_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(160 * 1024));
+      if (e != cudaSuccess) return e;
+      attr_x = true;
+    }
+    const size_t smem = sizeof(double) * (size_t)n;
+    int per_sm = (int)((224 * 1024) / (smem + 9 * 1024));  // (8.3 KB static per CTA)
+    if (per_sm > 4) per_sm = 4;
+    if (per_sm < 1) per_sm = 1;
+    long long blocks = (long long)sm_count * per_sm;
+    if (blocks > n) blocks = n;
+    const double sc = ldexp(1.0, -2 * exact_lmin);
+    gram_exact_kernel<<<(int)blocks, 512, smem, s>>>(n, rowptr, colind, vals, colptr, rowind, cvals, b,
+                                                     row_begin, row_end, G, ldg, c, sc, 1.0 / sc);
+    return cudaGetLastError();
+  }
   // One chunk = the whole row when it fits (measured: splitting a row into
   // column chunks multiplies the A-row gathers and is slower at config 2).
   const int chunk = n < 1 ? 1 : (n <= 25600 ? n : 25600);

@@ -31,10 +31,15 @@ cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
 // ---- a1 Gram + c (ingest_gram.cu) ---------------------------------------
 // G (n rows of stride ldg) = A_R^T A_R and c = A_R^T b_R over rows R =
 // [row_begin, row_end) (all rows: 0, m).
+// err[kErrExp..+3]: exponent statistics of A and b from validate (see
+// exact_bits); gram_is_exact(err) -> every Gram/c sum is exact in FP64.
+constexpr int kErrExp = 48;
+bool gram_is_exact(const int* err);
+inline int gram_exact_lmin(const int* err) { return 2048 - err[kErrExp + 1]; }  // L_A
 cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
                         const double* vals, const int32_t* colptr, const int32_t* rowind,
                         const double* cvals, const double* b, int row_begin, int row_end,
-                        double* G, int ldg, double* c, int sm_count, cudaStream_t s);
+                        double* G, int ldg, double* c, int sm_count, cudaStream_t s, bool exact = false, int exact_lmin = 0);
 
 // ---- a2/a3/a4/a7/a8 pivot steps (pivot.cu) -----------------------------
 cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double* y, double tol,
