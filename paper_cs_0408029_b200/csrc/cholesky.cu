@@ -140,6 +140,23 @@ __device__ __forceinline__ void dmma_tile(double (&acc)[2][4][2], const double* 
       for (int q = 0; q < 4; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
   }
 }
+// acc += A Bm for 64 x 64 smem tiles, Bm row-major by k (C[m][n] += sum_k
+// A[m][k] Bm[k][n]: the B fragments are read transposed).
+__device__ __forceinline__ void dmma_tile_nn(double (&acc)[2][4][2], const double* __restrict__ A,
+                                             const double* __restrict__ Bm, int lane, int rb0, int cb0) {
+#pragma unroll 4
+  for (int kk = 0; kk < T; kk += 4) {
+    double av[2], bv[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) av[a] = A[(rb0 + 8 * a + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bv[q] = Bm[(kk + (lane & 3)) * LDS + cb0 + 8 * q + (lane >> 2)];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
+  }
+}
 __device__ __forceinline__ void acc_load(double (&acc)[2][4][2], const double* S, int lane, int rb0,
                                          int cb0) {
 #pragma unroll
@@ -629,6 +646,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   // tile columns [0, jq) of rows [0, jq) are kept from the previous pivot
   // iteration (same order prefix, see order_free_set in pivot.cu)
   const int jq = (st->reuse_cols > 0 && st->reuse_cols < ntc) ? st->reuse_cols : 0;
+  // W_j tiles of a restart (task W(j)) live in the back-solve's N_J region,
+  // which the back substitution only writes after the factorization
+  double* Wbuf = Linv + (size_t)(boxlen / T) * TS;
   const int ntr = (f + 1 + T - 1) / T;  // tile rows (incl. the rhs row f)
   FlagSet F{flags, flags + tri, flags + 2 * tri};
   const int tid = threadIdx.x;
@@ -771,16 +791,19 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     int t = s_task;
     csync();
     int j = jq, kind = -1, i = 0;
-    if (jq > 0) {
+    if (jq > 0) {  // [W(1..jq-1)] [T(jq..ntr-1, j) for j < jq] [D(jq)]
       const int nr = ntr - jq;
-      if (t < jq * nr) {
+      if (t < jq - 1) {
+        kind = 5;
+        j = t + 1;
+      } else if (t - (jq - 1) < jq * nr) {
         kind = 2;
-        j = t / nr;
-        i = jq + t % nr;
-      } else if (t == jq * nr) {
+        j = (t - (jq - 1)) / nr;
+        i = jq + (t - (jq - 1)) % nr;
+      } else if (t - (jq - 1) == jq * nr) {
         kind = 3;
       }
-      t -= jq * nr + 1;
+      t -= (jq - 1) + jq * nr + 1;
     }
     while (kind < 0 && j < ntc) {
       const int np1 = (j + 1 < ntc) ? 1 : 0;          // P(j+1,j+1)
@@ -797,6 +820,23 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       ++j;
     }
     if (kind < 0) break;
+    if (kind == 5) {                 // W(j) = (L(j,j-1)^T Linv_jj^T)^T = Linv_jj L(j,j-1) (kept tiles)
+      const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
+      double* Lv = smem + 5 * T * LDS;
+      double* Ls = smem + 1 * T * LDS;
+      tile_async(Lv, Linv + (size_t)j * TS);
+      tile_async(Ls, Lt + (size_t)tidx(j, j - 1) * TS);
+      cp_async_commit();
+      cp_async_wait<0>();
+      csync();
+      double acc[2][4][2] = {};
+      dmma_tile_nn(acc, Lv, Ls, lane, rb0, cb0);
+      acc_store(acc, S, lane, rb0, cb0);
+      csync();
+      store_tile(Wbuf + (size_t)j * TS, S);
+      publish_flag(&F.part[tidx(j, j - 1)], epoch);  // (a kept tile's part flag: W_j ready)
+      continue;
+    }
     if (kind == 3) {                 // D(jq): diagonal tile jq, all updates k < jq
       PROF_STAMP(1199, 0);
       gather_tile(S, G, ldg, cvec, Fidx, f, jq, jq);
@@ -822,6 +862,45 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       store_tile(Lt + (size_t)tidx(j + 1, j) * TS, S);
       publish_flag(&F.part[tidx(j + 1, j)], epoch);
       PROF_STAMP(1000 + j, 0);
+    } else if (j < jq && j > 0) {    // T(i, j) below a kept prefix: the row chain of the restart
+      // L(i,j) = B - L(i,j-1) W_j with B = (A(i,j) - sum_{k<j-1} L(i,k) L(j,k)^T) Linv_jj^T and
+      // W_j = L(j,j-1)^T Linv_jj^T (task W(j)): B is formed BEFORE L(i,j-1) arrives, so the
+      // per-column step of the chain is one product (no update + TRSM pair)
+      const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
+      double* Lv = smem + 5 * T * LDS;   // Linv_jj
+      double* Wt = smem + 2 * T * LDS;   // W_j^T
+      double* Xp = smem + 3 * T * LDS;   // L(i, j-1)
+      tile_async(Lv, Linv + (size_t)j * TS);
+      cp_async_commit();
+      gather_tile(S, G, ldg, cvec, Fidx, f, i, j);
+      csync();
+      left_update(smem, S, Lt, F.full, epoch, i, j, j - 1, jq, &s_ready);  // k < j-1
+      cp_async_wait<0>();
+      if (tid == 0) wait_flag(&F.part[tidx(j, j - 1)], epoch);
+      csync();
+      tile_async(Wt, Wbuf + (size_t)j * TS);  // (in flight during B)
+      cp_async_commit();
+      {
+        double acc8[8][2];
+        gemm_linvT(acc8, S, Lv, w, lane);
+        csync();
+        store_rows8(acc8, S, w, lane);  // S = B
+      }
+      if (tid == 0) wait_flag(&F.full[tidx(i, j - 1)], epoch);
+      csync();
+      tile_async(Xp, Lt + (size_t)tidx(i, j - 1) * TS);
+      cp_async_commit();
+      cp_async_wait<0>();
+      csync();
+      {
+        double acc[2][4][2];
+        acc_load(acc, S, lane, rb0, cb0);
+        dmma_tile<true>(acc, Xp, Wt, lane, rb0, cb0);  // S -= L(i,j-1) W_j
+        acc_store(acc, S, lane, rb0, cb0);
+      }
+      csync();
+      store_tile(Lt + (size_t)tidx(i, j) * TS, S);
+      publish_flag(&F.full[tidx(i, j)], epoch);
     } else {                         // T(i, j): updates k < j, then L(i,j) = A(i,j) Linv_jj^T
       gather_tile(S, G, ldg, cvec, Fidx, f, i, j);
       csync();
