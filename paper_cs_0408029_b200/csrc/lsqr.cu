@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks(), kr = (int)cl.block_rank();
   extern __shared__ double smem[];
-  __shared__ double red[4][32];
+  __shared__ double red[2][4][32];  // (double-buffered by publish call parity)
   __shared__ double parts[8][kMaxC];  // [slot][source CTA] partials, pushed by every CTA
   const int m = a.m, n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -672,20 +672,24 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   // block-wide and warp 0 PUSHES the block totals into slot [slot+q][kr] of
   // every CTA's parts[][] array; after the cluster barrier each thread sums
   // its local copy in rank order (deterministic, identical everywhere).
+  // (red is double-buffered: the readers of call t finish before call t+1's
+  // barrier, so call t+2 may overwrite it -- one barrier per call)
+  int red_par = 0;
   auto publish = [&](int nv, const double* v, const int* kind, int slot) {
-    __syncthreads();  // red[][] reuse
+    double (*rb)[32] = red[red_par];
+    red_par ^= 1;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       if (q < nv) {
         double x = v[q];
         x = kind[q] == 0 ? warp_sum(x) : (kind[q] == 1 ? warp_min(x) : warp_max(x));
-        if (lane == 0) red[q][wid] = x;
+        if (lane == 0) rb[q][wid] = x;
       }
     }
     __syncthreads();
     if (wid < nv) {
       const int k = kind[wid];
-      double x = lane < NW ? red[wid][lane] : (k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY));
+      double x = lane < NW ? rb[wid][lane] : (k == 0 ? 0.0 : (k == 1 ? INFINITY : -INFINITY));
       x = k == 0 ? warp_sum(x) : (k == 1 ? warp_min(x) : warp_max(x));
       if (lane < C) *cl.map_shared_rank(&parts[slot + wid][kr], lane) = x;
     }
@@ -868,13 +872,11 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
           LQ_STAMP(6);
           cl.sync();
           LQ_STAMP(7);
-          if (wid == 0) {
+          {  // every warp forms the same total (same inputs, same butterfly): no barrier
             double t1v[3];
             ctotal(1, K_SUM, 3, t1v);
-            if (lane == 0) sc[3] = sqrt(t1v[0]);
+            alpha_new = sqrt(t1v[0]);
           }
-          __syncthreads();
-          alpha_new = sc[3];
           LQ_STAMP(8);
         } else {
           cl.sync();  // keep the two-barrier rhythm (partials are reused)
