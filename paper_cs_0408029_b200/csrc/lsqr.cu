@@ -833,9 +833,18 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
             if (test1 <= rtol) stop = 1;
           }
           if (lane == 0) {
-            sc[0] = sqrt(t3[0]);   // beta_new
+            const double bn = sqrt(t3[0]);  // beta_new
+            sc[0] = bn;
             sc[1] = (double)stop;
             sc[2] = ddnorm;
+            // the part of the rotation that does not depend on alpha_new
+            // (formed here, in the shadow of the other warps' dots)
+            const double rho = sqrt(rhobar * rhobar + bn * bn);
+            sc[3] = rho;
+            sc[4] = rhobar / rho;  // cs
+            sc[5] = bn / rho;      // sn
+            sc[6] = (sc[4] * phibar) / rho;  // t1 = phi / rho
+            sc[7] = 1.0 / rho;
           }
           LQ_STAMP(12);
         } else if (more) {
@@ -853,6 +862,8 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
         if (istop != 0) break;
         ++itn;
         const double beta_new = sc[0];
+        const double rho = sc[3], cs = sc[4], sn = sc[5], t1 = sc[6], irho = sc[7];
+        const double phi = cs * phibar;
         // ---- phase B: V' = A_F^T u - beta v on own columns (u = U'/beta_new)
         double alpha_new = alpha;
         if (beta_new > 0.0) {
@@ -882,18 +893,14 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
           cl.sync();  // keep the two-barrier rhythm (partials are reused)
         }
         beta = beta_new;
-        // ---- rotation (replicated scalars)
-        const double rho = sqrt(rhobar * rhobar + beta * beta);
-        const double cs = rhobar / rho, sn = beta / rho;
+        // ---- rotation (replicated scalars; rho, cs, sn, phi, t1 formed above)
         const double theta = sn * alpha_new;
         rhobar = -cs * alpha_new;
-        const double phi = cs * phibar;
         phibar = sn * phibar;
-        const double t1 = phi / rho, t2 = -theta / rho;
+        const double t2 = -theta / rho;
         // ---- phase C: v, x, w on own columns (partials ride on the next barrier)
         const bool newv = beta_new > 0.0;
         const double ia = (newv && alpha_new > 0.0) ? 1.0 / alpha_new : 1.0;
-        const double irho = 1.0 / rho;
         pd = 0.0;
         px = 0.0;
         for (int j = tid; j < ncols; j += kCT) {
