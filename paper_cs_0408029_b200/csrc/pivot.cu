@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(256) dual_kernel(
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int a = lane;
     if (Fs != nullptr) {
+#pragma unroll 4
       for (; a + 96 < f; a += 128) {
         const int i0 = __ldg(&Fs[a]), i1 = __ldg(&Fs[a + 32]), i2 = __ldg(&Fs[a + 64]), i3 = __ldg(&Fs[a + 96]);
         s0 = fma(Gj[i0], xs[i0], s0);
@@ -518,11 +519,26 @@ __global__ void __launch_bounds__(256) dual_kernel(
     }
     y[i] = 0.0;
   }
+  // trace extremes: warp, then block, then ONE atomic pair per block (a
+  // global atomic per warp on the same two words serialised ~10 us here)
+  __shared__ double s_below[8], s_above[8];
   below = warp_max(below);
   above = warp_min(above);
+  const int wid = threadIdx.x >> 5;
   if (lane == 0) {
-    if (below > 0.0) atomicMax(&st->below_bits, dbits(below));
-    if (above < INFINITY) atomicMin(&st->above_bits, dbits(above));
+    s_below[wid] = below;
+    s_above[wid] = above;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double bl = lane < (int)(blockDim.x >> 5) ? s_below[lane] : 0.0;
+    double ab = lane < (int)(blockDim.x >> 5) ? s_above[lane] : INFINITY;
+    bl = warp_max(bl);
+    ab = warp_min(ab);
+    if (lane == 0) {
+      if (bl > 0.0) atomicMax(&st->below_bits, dbits(bl));
+      if (ab < INFINITY) atomicMin(&st->above_bits, dbits(ab));
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) st->iter += 1;
   (void)mask;
