@@ -82,6 +82,21 @@ def test_gram_bitwise_raw_inputs(P):
     assert np.array_equal(G, Go) and np.array_equal(c, co)
 
 
+@pytest.mark.parametrize("cfg", [1, dict(m=3000, n=12, density=0.5)])
+def test_gram_exact_and_ordered_paths_agree(P, cfg, monkeypatch):
+    """Quantized inputs take the exact-arithmetic Gram (any summation order,
+    integer accumulation) unless a column is too long for it (the second case:
+    columns of ~1500 entries); NNLS_NO_EXACT_GRAM forces the row-ordered
+    kernel.  Both must give the oracle's bits."""
+    prob = g.make_problem(cfg, seed=4)
+    Ge, ce = P.setup(prob).gram()
+    monkeypatch.setenv("NNLS_NO_EXACT_GRAM", "1")
+    Gs, cs = P.setup(prob).gram()
+    Go, co = O.gram(prob)
+    assert np.array_equal(Ge, Go) and np.array_equal(ce, co)
+    assert np.array_equal(Gs, Go) and np.array_equal(cs, co)
+
+
 def test_step_gram_device_buffers(P):
     prob = g.make_problem(dict(m=300, n=97, density=0.1), seed=3)
     dev = "cuda"
