@@ -402,22 +402,24 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // (X11 at (o,o), X22 at (o+b,o+b), L21 at (o+b,o)), Linv21 = -X22 (L21 X11).
 // Output 8x8 blocks are spread over the 8 warps (b = 8: 4 blocks, b = 16: 8,
 // b = 32: 16 -> two per warp); Tm (scratch) holds L21 X11 transposed.
-template <int B>
+template <int B, int NW>
 __device__ __forceinline__ void trtri_level(double* __restrict__ X, const double* __restrict__ L,
                                             double* __restrict__ Tm, int w, int lane) {
-  constexpr int NB = B / 8;                 // 8x8 blocks per side
-  constexpr int NT = (32 / B) * NB * NB;    // output blocks in the level
-  constexpr int PER = NT >= 8 ? NT / 8 : 1; // blocks per warp
+  constexpr int NB = B / 8;                         // 8x8 blocks per side
+  constexpr int NT = (32 / B) * NB * NB;            // output blocks in the level
+  constexpr int PER = (NT + NW - 1) / NW;           // blocks per warp (the last ones clamped)
   const int rq = lane >> 2, kq = lane & 3;
-  if (w >= NT) {  // b = 8: warps 4..7 idle in both steps
-    csync();
-    csync();
+  if (w >= NT) {  // b = 8: warps 4.. idle in both steps
+    wsync<NW>();
+    wsync<NW>();
     return;
   }
   int o[PER], bi[PER], bj[PER], pr[PER];
+  bool ok[PER];
 #pragma unroll
   for (int s = 0; s < PER; ++s) {
-    const int t = w + 8 * s;
+    ok[s] = w + NW * s < NT;
+    const int t = ok[s] ? w + NW * s : NT - 1;  // (a clamped duplicate: computed, not stored)
     pr[s] = t / (NB * NB);
     o[s] = 2 * B * pr[s];
     bi[s] = (t % (NB * NB)) / NB;
@@ -437,11 +439,12 @@ __device__ __forceinline__ void trtri_level(double* __restrict__ X, const double
   }
 #pragma unroll
   for (int s = 0; s < PER; ++s) {  // Tmt[pair*B + n][m]
+    if (!ok[s]) continue;
     double* t = Tm + (B * pr[s] + 8 * bj[s] + 2 * kq) * LDS + 8 * bi[s] + rq;
     t[0] = c0[s];
     t[LDS] = c1[s];
   }
-  csync();
+  wsync<NW>();
 #pragma unroll
   for (int s = 0; s < PER; ++s) c0[s] = c1[s] = 0.0;
 #pragma unroll
@@ -455,43 +458,47 @@ __device__ __forceinline__ void trtri_level(double* __restrict__ X, const double
   }
 #pragma unroll
   for (int s = 0; s < PER; ++s) {
+    if (!ok[s]) continue;
     double* x = X + (o[s] + B + 8 * bi[s] + rq) * LDS + o[s] + 8 * bj[s] + 2 * kq;
     x[0] = c0[s];
     x[1] = c1[s];
   }
   if (B == 32) fence_proxy_async_smem();  // X complete -> its bulk store
-  csync();
+  wsync<NW>();
 }
 
 // X = L^-1 for the lower 64 x 64 smem tile L with cv pivots (rows / columns
 // >= cv of X are zero), 1/l_cc in rinv (c < cv).  Blocked so that no step is
-// a 64-long column chain: warp w inverts the 8x8 diagonal block w by
-// substitution (lanes 0..7 = its columns, 28 dependent FMAs), then three
-// doubling levels b = 8, 16, 32 form Linv21 = -Linv22 L21 Linv11 on DMMA.
-// The strict upper blocks of X must be zero on entry (they are never
-// written).  All 8 warps; pj: profile row.
+// a 64-long column chain: the 8x8 diagonal blocks are inverted by
+// substitution (8 lanes = the block's columns, 28 dependent FMAs; warp w
+// takes blocks w and w + NW), then three doubling levels b = 8, 16, 32 form
+// Linv21 = -Linv22 L21 Linv11 on DMMA.  The strict upper blocks of X must be
+// zero on entry (they are never written).  Runs on warps 0..NW-1 (NW = 7: the
+// chain's warp 7 is still waiting for the helpers' partials meanwhile).
+template <int NW>
 __device__ __forceinline__ void trtri64(double* __restrict__ X, const double* __restrict__ L,
                                         const double* __restrict__ rinv, int cv, double* __restrict__ Tm,
                                         int pj) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int c0 = 8 * w;
-  if (lane < 8) {
+  const int blk = w + NW * (lane >> 3);
+  if (lane < 16 && blk < 8) {
+    const int c0 = 8 * blk, col = lane & 7;
     double x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      double s = (i == lane) ? 1.0 : 0.0;
+      double s = (i == col) ? 1.0 : 0.0;
 #pragma unroll
       for (int k = 0; k < i; ++k) s = fma(-L[(c0 + i) * LDS + c0 + k], x[k], s);
       x[i] = (c0 + i < cv) ? s * rinv[c0 + i] : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) X[(c0 + i) * LDS + c0 + lane] = x[i];
+    for (int i = 0; i < 8; ++i) X[(c0 + i) * LDS + c0 + col] = x[i];
   }
-  csync();
-  trtri_level<8>(X, L, Tm, w, lane);
-  trtri_level<16>(X, L, Tm, w, lane);
-  PROF_STAMP(pj, 7);
-  trtri_level<32>(X, L, Tm, w, lane);
+  wsync<NW>();
+  trtri_level<8, NW>(X, L, Tm, w, lane);
+  trtri_level<16, NW>(X, L, Tm, w, lane);
+  if (pj >= 0) PROF_STAMP(pj, 7);
+  trtri_level<32, NW>(X, L, Tm, w, lane);
 }
 
 // acc (rows 8w..8w+7 of X, all 64 columns) = A Linv^T for 64 x 64 smem
@@ -731,7 +738,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
         }
         cp_async_wait<0>();
       } else {
-        // ---- warps 0..6: L_jj = chol(A_jj), stored
+        // ---- warps 0..6: L_jj = chol(A_jj), then Linv_jj (while warp 7 may
+        // still be waiting for the helpers' partials)
         const int bad = potrf_r8<1, 7, true>(Sd, rv, cv, rinv, &s_bad, Lprev);
         for (int e = tid; e < T * T; e += kThreads - 32)  // strict upper part
           if ((e % T) > (e / T)) Sd[(e / T) * LDS + (e % T)] = 0.0;
@@ -739,21 +747,22 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
         wsync<7>();
         PROF_STAMP(j, 1);
         fence_proxy_async_smem();  // L_jj (Sd) -> the bulk store below
+        // Linv_jj: the sub-diagonal TRSMs become products, and the back
+        // substitution uses it (trtri64 fences Xinv for its bulk store)
+        trtri64<7>(Xinv, Sd, rinv, cv, Tm, j);
+        PROF_STAMP(j, 3);
       }
-      csync();  // L_jj factored; partials in smem
+      csync();  // L_jj, Linv_jj done; partials in smem
       const int lane = tid & 31, w = tid >> 5;
-      if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j, j) * TS, Sd);
       PROF_STAMP(j, 2);
-      // Linv_jj: the sub-diagonal TRSMs become products, and the back
-      // substitution uses it
-      trtri64(Xinv, Sd, rinv, cv, Tm, j);
-      // (trtri64 fenced Xinv for the async proxy before its last barrier)
-      if (tid == kThreads - 32) bulk_store_tile(Linv + (size_t)j * TS, Xinv);
+      if (tid == kThreads - 32) {
+        bulk_store_tile(Lt + (size_t)tidx(j, j) * TS, Sd);
+        bulk_store_tile(Linv + (size_t)j * TS, Xinv);
+      }
       if (!has_sub) {  // last column without a sub-diagonal tile
         if (tid == kThreads - 32) bulk_store_release(&F.inv[j], epoch, &F.full[tidx(j, j)]);
         break;
       }
-      PROF_STAMP(j, 3);
       {  // L(j+1,j) = A(j+1,j) L_jj^-T = A(j+1,j) Linv_jj^T; then warp 7
          // releases L_jj and Linv_jj (their bulk stores drained meanwhile)
         double acc[8][2];

@@ -48,20 +48,20 @@ p = allp[:600]
 p = p[p[:, 0] > 0]
 base = p[:, 0].min()
 # chain CTA: one row per tile column j
-print("   j    start  factored    joined  trtri-16 trtri-done  gemm-done  end (us)")
+print("   j    start  factored  trtri-16 trtri-done    joined  gemm-done  end (us)")
 for j, r in enumerate(p):
-    v = [(x - base) / 1e3 if x > 0 else float("nan") for x in (r[0], r[1], r[2], r[7], r[3], r[4], r[5])]
+    v = [(x - base) / 1e3 if x > 0 else float("nan") for x in (r[0], r[1], r[7], r[3], r[2], r[4], r[5])]
     print(f"{j:4d} " + " ".join(f"{x:9.1f}" for x in v))
 if len(p) > 1:
     d = np.diff(p[:, 0]) / 1e3
     print("per-column period us: mean %.2f  min %.2f  max %.2f" % (d.mean(), d.min(), d.max()))
     q = p[:-1]
-    print("potrf (+deferred SYRK) %.2f  join (wait partials) %.2f  trtri %.2f [diag+L8+L16 %.2f, L32 %.2f]  "
-          "gemm %.2f  end %.2f" % (
-        ((q[:, 1] - q[:, 0]) / 1e3).mean(), ((q[:, 2] - q[:, 1]) / 1e3).mean(),
-        ((q[:, 3] - q[:, 2]) / 1e3).mean(), ((q[:, 7] - q[:, 2]) / 1e3).mean(),
-        ((q[:, 3] - q[:, 7]) / 1e3).mean(),
-        ((q[:, 4] - q[:, 3]) / 1e3).mean(), ((q[:, 5] - q[:, 4]) / 1e3).mean()))
+    print("potrf (+deferred SYRK) %.2f  trtri (7 warps) %.2f [diag+L8+L16 %.2f, L32 %.2f]  "
+          "join (wait partials) %.2f  gemm %.2f  end %.2f" % (
+        ((q[:, 1] - q[:, 0]) / 1e3).mean(), ((q[:, 3] - q[:, 1]) / 1e3).mean(),
+        ((q[:, 7] - q[:, 1]) / 1e3).mean(), ((q[:, 3] - q[:, 7]) / 1e3).mean(),
+        ((q[:, 2] - q[:, 3]) / 1e3).mean(),
+        ((q[:, 4] - q[:, 2]) / 1e3).mean(), ((q[:, 5] - q[:, 4]) / 1e3).mean()))
 print("helpers, per column j (us, same base): P(j+1,j) last-update-start / published, T(j+1,j-1) published, P(j+1,j+1)... ")
 for j in range(len(p)):
     h = hp[j]
