@@ -1,7 +1,7 @@
 set -u
 O=gpurun_out/prof
 mkdir -p $O
-for k in chol_factor_kernel chol_backsolve_kernel lsqr_cluster_kernel gram_kernel dual_kernel decide_kernel; do
+for k in chol_factor_kernel chol_backsolve_kernel lsqr_cluster_kernel gram_exact_kernel dual_kernel decide_kernel; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$k" -c 1 \
     -o $O/full_c1_$k -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_full_$k.log 2>&1
 done

@@ -15,7 +15,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
   --log-file $O/launches_c1.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
 # full capture of the dominant kernels: one launch of each, one ncu run per
 # kernel (a single regex with -c N would stop at the first N matches)
-for k in chol_factor_kernel chol_backsolve_kernel lsqr_cluster_kernel gram_kernel dual_kernel decide_kernel; do
+for k in chol_factor_kernel chol_backsolve_kernel lsqr_cluster_kernel gram_exact_kernel dual_kernel decide_kernel; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$k" -c 1 \
     -o $O/full_c1_$k -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_full_$k.log 2>&1
 done
