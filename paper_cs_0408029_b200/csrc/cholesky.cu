@@ -21,14 +21,18 @@
 //     f64 kind): the left-looking update C_ij -= L_ik L_jk^T, and the
 //     triangular solve of the off-diagonal tiles, done as a product with the
 //     explicit inverse of the diagonal tile, X = C_ij L_jj^-T.
-//   * The diagonal task factors its tile (2 x 2 blocks of 32: POTRF, TRSM,
-//     SYRK, POTRF in one warp) and inverts it (TRTRI of the two 32-blocks by
-//     two warps, off-diagonal block by products).  Column-sequential work is
-//     thereby confined to the diagonal tile; the off-diagonal tiles never run
-//     a column-sequential loop.  Pivot <= 0, < 1e-300 or non-finite -> NOT_PD
-//     (reading c13).
-//   * L^T x = z by a second DAG kernel over column tiles (last to first), each
-//     step a GEMV with the published inverse diagonal tile.
+//   * The diagonal tiles are factored by ONE CTA walking the diagonal (the
+//     chain, see chol_factor_kernel): POTRF in 8-column register panels with
+//     the previous column's last update folded in, TRTRI of the diagonal
+//     block by doubling levels on DMMA, and the sub-diagonal tile as a
+//     triangular product with that inverse; helpers compute every other tile.
+//     Column-sequential work is confined to the chain's diagonal tile.
+//     Pivot <= 0, < 1e-300 or non-finite -> NOT_PD (reading c13).
+//   * Factor reuse: tile columns kept from the previous pivot iteration (same
+//     order prefix, st->reuse_cols) are not recomputed; the rows below them
+//     are (one product per column, task W(j)).
+//   * L^T x = z by a second kernel: a chain CTA (x_J = a_J - N_J^T x_{J+1}
+//     - P_J^T x_{J+2}) fed by helper tasks through mailboxes.
 #include <cuda_runtime.h>
 #include <math.h>
 
