@@ -551,19 +551,19 @@ __device__ __forceinline__ void bulk_store_release(int* flag, int epoch, int* fl
 
 // ---------------------------------------------------------------------------
 // Factorization DAG with a diagonal CHAIN.  CTA 0 walks the diagonal:
-//   for column j:  L_jj = chol(A_jj);  store;
-//                  L(j+1,j) = A(j+1,j) L_jj^-T, and in the same pass
-//                  A_(j+1)(j+1) -= L(j+1,j) L(j+1,j)^T (its last update);  store
-// so the per-column critical path is one POTRF and one TRSM with no tile
-// hand-off between CTAs; warp 7 hides the flag fences and the prefetches of
-// the helpers' partial tiles in its idle phases.  CTAs 1.. claim helper
-// tasks from a queue ordered by column:
+//   for column j:  L_jj = chol(A_jj - L(j,j-1) L(j,j-1)^T)  (the previous
+//                  column's last update folded into the POTRF panels);
+//                  Linv_jj by blocked TRTRI;  L(j+1,j) = A(j+1,j) Linv_jj^T
+// so the per-column critical path has no tile hand-off between CTAs; warp 7
+// prefetches the helpers' partial tiles and raises the flags of the chain's
+// bulk-stored tiles in its idle phases.  CTAs 1.. claim helper tasks from a
+// queue ordered by column (see the queue comment below):
 //   P(j+1,j+1): tile (j+1,j+1) with its updates k < j      -> "partial" flag
 //   P(j+1,j)  : tile (j+1,j)   with its updates k < j      -> "partial" flag
-//   T(i,j), i >= j+2: updates k < j, wait L_jj, TRSM       -> "full" flag
-//   I(j)      : Linv_jj = L_jj^-1 (for the back substitution)
-// Every wait is on a task queued earlier or on the chain, and the chain only
-// waits on queued tasks, so the DAG cannot deadlock.
+//   T(i,j), i >= j+2: updates k < j, then A(i,j) Linv_jj^T -> "full" flag
+// (plus W(j) / D(jq) after a kept prefix).  Every wait is on a task queued
+// earlier or on the chain, and the chain only waits on queued tasks, so the
+// DAG cannot deadlock.
 namespace {
 struct FlagSet {
   int* full;   // [tri]   L(i,j) final
@@ -675,12 +675,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   if (blockIdx.x == 0) {
     PROF_STAMP(1198, 0);
     // ============================== the diagonal chain
-    // BUF(0)/BUF(1): diagonal tile of column j (alternating), BUF(5): A/L(j+1,j).
-    // Per column: POTRF on warps 0-6 while warp 7 raises the release flag of
-    // the previous sub-diagonal tile and prefetches (cp.async) the helpers'
-    // partials A(j+1,j) and A(j+1,j+1); TRSM on all warps (warp 7 raises
-    // L_jj's flag in a solve phase); last update of A(j+1,j+1) on warps 0-6
-    // while warp 7 raises L(j+1,j)'s flag.
+    // BUF(0)/BUF(1): diagonal tile of column j (alternating), BUF(2): Linv_jj,
+    // BUF(3): TRTRI scratch, BUF(4)/BUF(5): A/L(j+1,j) (alternating).
+    // Per column: POTRF + TRTRI on warps 0-6 while warp 7 releases the
+    // previous sub-diagonal tile and prefetches (cp.async) the helpers'
+    // partials A(j+1,j) and A(j+1,j+1); then the product L(j+1,j) =
+    // A(j+1,j) Linv_jj^T on all warps (warp 7 releases L_jj and Linv_jj).
     double* Xinv = smem + 2 * (T * LDS);  // Linv_jj
     double* Tm = smem + 3 * (T * LDS);    // trtri scratch
     int first_bad = -1;
