@@ -150,7 +150,7 @@ __device__ void sort_tail(int32_t* __restrict__ tail, int r, const double* __res
   }
   __syncthreads();  // (tail[] is rewritten below)
   TailSort<IPT>(*reinterpret_cast<typename TailSort<IPT>::TempStorage*>(smem))
-      .SortBlockedToStriped(key, val, 0, 16);
+      .SortBlockedToStriped(key, val, 4, 16);  // the top 12 key bits (3 radix passes)
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {  // striped: rank = k * threads + tid
     const int rank = k * kDecideThreads + threadIdx.x;
@@ -254,8 +254,9 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
     __syncthreads();
   }
   const int f = *s_f, r = f - q;
-  // (3) stable sort of the tail by a 16-bit key (the order is a heuristic:
-  // 7 mantissa bits are plenty): old members (pos >= 0) by decreasing x, new
+  // (3) stable sort of the tail by the top 12 bits of a 16-bit key (the order
+  // is a heuristic: 3 mantissa bits give the same kept prefixes as the exact
+  // sort at configs 1 and 2): old members (pos >= 0) by decreasing x, new
   // members after them in index order (the first factorization is thus in
   // index order, as the oracle's); pos[] still holds the previous positions.
 #ifndef NO_ORDER_SORT
