@@ -157,6 +157,31 @@ __device__ void sort_tail(int32_t* __restrict__ tail, int r, const double* __res
     if (rank < r) tail[rank] = val[k];
   }
 }
+// Short tails (r <= threads): rank by comparison, element t -> position
+// #{u : (key_u, i_u) < (key_t, i_t)} -- the same stable order as sort_tail
+// (12-bit key, index ties), r broadcast reads per thread instead of the
+// radix sort's fixed passes.
+__device__ void rank_tail(int32_t* __restrict__ tail, int r, const double* __restrict__ x,
+                          const int32_t* __restrict__ pos, void* smem) {
+  unsigned* sk = reinterpret_cast<unsigned*>(smem);  // (key << 20) | element index t (t < 2^20)
+  const int t = threadIdx.x;
+  int i = 0;
+  unsigned kt = 0xFFFFFFFFu;
+  if (t < r) {
+    i = tail[t];
+    const unsigned key = (pos[i] >= 0 ? order_key(-x[i]) : 0xFFFFu) >> 4;  // top 12 bits
+    kt = (key << 20) | (unsigned)t;  // tail[] is in index order: t breaks ties like the index
+    sk[t] = kt;
+  }
+  __syncthreads();  // (tail[] is rewritten below)
+  if (t < r) {
+    int rank = 0;
+#pragma unroll 8
+    for (int u = 0; u < r; ++u) rank += sk[u] < kt;
+    tail[rank] = i;
+  }
+}
+
 constexpr size_t kTailSortSmem = sizeof(typename TailSort<kOrderMax / kDecideThreads>::TempStorage) >
                                          sizeof(typename TailSort<1>::TempStorage)
                                      ? sizeof(typename TailSort<kOrderMax / kDecideThreads>::TempStorage)
@@ -261,7 +286,7 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
   // index order, as the oracle's); pos[] still holds the previous positions.
 #ifndef NO_ORDER_SORT
   if (r > 1 && r <= kOrderMax && *s_old > 0) {  // (no old member: already in order)
-    if (r <= kDecideThreads) sort_tail<1>(Fidx + q, r, x, pos, sort_smem);
+    if (r <= kDecideThreads) rank_tail(Fidx + q, r, x, pos, sort_smem);
     else sort_tail<kOrderMax / kDecideThreads>(Fidx + q, r, x, pos, sort_smem);
     __syncthreads();
   }
