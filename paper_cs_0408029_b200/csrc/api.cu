@@ -510,6 +510,12 @@ cudaError_t launch_lsqr(nnls_handle* h, cudaStream_t s) {
   return e;
 }
 
+}  // namespace
+bool nnls::pdl_enabled() {
+  static const bool on = getenv("NNLS_NO_PDL") == nullptr;
+  return on;
+}
+namespace {
 int32_t* pos_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<int32_t>(h->pos); }
 int32_t* fs_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<int32_t>(h->Fs); }
 double* xs_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<double>(h->xs); }

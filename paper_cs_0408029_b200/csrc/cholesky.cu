@@ -646,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     const int32_t* __restrict__ Fidx, double* __restrict__ Lt, double* __restrict__ Linv,
     int* __restrict__ flags, int tri, DevState* st, unsigned long long* __restrict__ box, int boxlen) {
   extern __shared__ double smem[];
+  pdl_wait();
   // helpers: BUF(0) = S, BUF(1..4) = operand double-buffers.
   // chain: BUF(0)/BUF(1) = diagonal tile of column j (alternating), BUF(5) = A/L(j+1,j)
   __shared__ double rinv[T];
@@ -1224,6 +1225,7 @@ __device__ void backsolve_task(const BsArgs& a, int f, int epoch, int J, double*
 
 __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(BsArgs a, DevState* st) {
   extern __shared__ __align__(128) double bsm[];
+  pdl_wait();
   __shared__ int s_task;
   const int f = st->f;
   const int epoch = st->epoch;
@@ -1269,9 +1271,8 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   double* Linv = Lt + (size_t)tri_tiles(n) * TS;
   const int ntr = (n + 1 + T - 1) / T;
   unsigned long long* box = reinterpret_cast<unsigned long long*>(Lt + ((size_t)tri_tiles(n) + 3 * (size_t)ntr) * TS);
-  chol_factor_kernel<<<grid, kThreads, sizeof(double) * kSmemDoubles, s>>>(G, ldg, c, Fidx, Lt, Linv,
-                                                                          flags, tri_tiles(n), st, box, ntr * T);
-  return cudaGetLastError();
+  return launch_pdl(chol_factor_kernel, dim3(grid), dim3(kThreads), sizeof(double) * kSmemDoubles, s, G, ldg, c,
+                    Fidx, Lt, Linv, flags, tri_tiles(n), st, box, ntr * T);
 }
 
 cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,
@@ -1294,8 +1295,7 @@ cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* x
   if (grid < 2) grid = 2;
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
-  chol_backsolve_kernel<<<grid, kThreads, kBsSmem, s>>>(a, st);
-  return cudaGetLastError();
+  return launch_pdl(chol_backsolve_kernel, dim3(grid), dim3(kThreads), kBsSmem, s, a, st);
 }
 
 cudaError_t launch_cholesky_solve(int n, const double* G, int ldg, const double* c,

@@ -102,4 +102,27 @@ NNLS_DEV void wait_flag(const int* flag, int want) {
 // non-negative doubles compare like their bit patterns
 NNLS_DEV unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
 
+// Programmatic dependent launch: a kernel launched with launch_pdl starts
+// (CTA rasterisation, shared-memory carve-out) while its predecessor in the
+// stream drains, and waits here before touching the predecessor's results.
+// A no-op for a kernel launched without the attribute.
+NNLS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+bool pdl_enabled();  // (env NNLS_NO_PDL=1 disables; api.cu)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 }  // namespace nnls

@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
     DevState* st, TraceRec* trace, int trace_cap, cudaGraphConditionalHandle loop, int use_loop,
     int32_t* pos, int32_t* Fs) {
   extern __shared__ __align__(16) unsigned char s_sort[];  // (pos != nullptr) the tail sort's storage
+  pdl_wait();
   __shared__ int s_cnt[32], s_max[32];
   __shared__ int s_wF[32], s_wG[32], s_wS[32];
   __shared__ int s_branch, s_last, s_carryF, s_carryG, s_carryS, s_q, s_fprev, s_old;
@@ -457,9 +458,8 @@ cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y
     cudaError_t e = cudaFuncSetAttribute(decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  decide_kernel<<<1, kDecideThreads, smem, s>>>(n, mask, x, y, Fidx, Gidx, st, trace, trace_cap,
-                                                loop ? *loop : cudaGraphConditionalHandle{},
-                                                loop ? 1 : 0, pos, Fs);
+  return launch_pdl(decide_kernel, dim3(1), dim3(kDecideThreads), smem, s, n, mask, x, y, Fidx, Gidx, st, trace,
+                    trace_cap, loop ? *loop : cudaGraphConditionalHandle{}, loop ? 1 : 0, pos, Fs);
   return cudaGetLastError();
 }
 
@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(256) dual_kernel(
     const double* __restrict__ xF, uint8_t* __restrict__ mask, double* __restrict__ x,
     double* __restrict__ y, double tol, DevState* st, const int32_t* __restrict__ Fs,
     const double* __restrict__ xs) {
+  pdl_wait();
   const int status = st->status;
   if (status != 0) {
     if (status == 7) {  // NOT_PD: the solve failed, x = 0 (as the oracle)
@@ -577,8 +578,8 @@ cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const 
   int blocks = (n + 7) / 8;  // one warp per G index upper bound
   if (blocks > sm_count * 8) blocks = sm_count * 8;
   if (blocks < 1) blocks = 1;
-  dual_kernel<<<blocks, 256, 0, s>>>(n, G, ldg, c, Fidx, Gidx, xF, mask, x, y, tol, st, Fs, xs);
-  return cudaGetLastError();
+  return launch_pdl(dual_kernel, dim3(blocks), dim3(256), 0, s, n, G, ldg, c, Fidx, Gidx, xF, mask, x, y, tol, st,
+                    Fs, xs);
 }
 
 }  // namespace nnls
