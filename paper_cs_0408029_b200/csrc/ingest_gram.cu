@@ -134,6 +134,7 @@ static void launch_colcount(int64_t nnz, int n, const int32_t* colind, int32_t* 
 // In-place inclusive scan of cnt[0..len) (cnt[0] = 0 on entry) -> colptr; one CTA.
 __global__ void scan_kernel(int len, int32_t* cnt, int32_t* cursor, int* maxcnt) {
   __shared__ int32_t wsum[32];
+  pdl_wait();
   __shared__ int32_t carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) carry = 0;
@@ -178,6 +179,7 @@ __global__ void csc_scatter_kernel(int m, const int32_t* __restrict__ rowptr,
                                    const int32_t* __restrict__ colind,
                                    const double* __restrict__ vals, int32_t* cursor,
                                    int32_t* tmp_row, double* tmp_val) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
@@ -216,6 +218,7 @@ __global__ void csc_sort_smem_kernel(int n, const int32_t* __restrict__ colptr,
                                      const double* __restrict__ tmp_val, int32_t* rowind, double* cvals,
                                      int cap) {
   extern __shared__ int srow[];
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   int* my = srow + (threadIdx.x >> 5) * cap;
   const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -259,8 +262,7 @@ cudaError_t launch_csc_count(int m, int n, int64_t nnz, const int32_t* colind, i
   cudaError_t e = cudaMemsetAsync(colptr, 0, sizeof(int32_t) * (size_t)(n + 1), s);
   if (e != cudaSuccess) return e;
   if (nnz > 0) launch_colcount(nnz, n, colind, colptr, s);
-  scan_kernel<<<1, 1024, 0, s>>>(n + 1, colptr, cursor, maxcnt);
-  return cudaGetLastError();
+  return launch_pdl(scan_kernel, dim3(1), dim3(1024), 0, s, n + 1, colptr, cursor, maxcnt);
 }
 
 cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* colind,
@@ -270,14 +272,16 @@ cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* 
   int rb = (int)(((int64_t)m * 32 + 255) / 256);
   if (rb > 4096) rb = 4096;
   if (rb < 1) rb = 1;
-  csc_scatter_kernel<<<rb, 256, 0, s>>>(m, rowptr, colind, vals, cursor, tmp_row, tmp_val);
+  cudaError_t e = launch_pdl(csc_scatter_kernel, dim3(rb), dim3(256), 0, s, m, rowptr, colind, vals, cursor,
+                             tmp_row, tmp_val);
+  if (e != cudaSuccess) return e;
   int cb = (int)(((int64_t)n * 32 + 255) / 256);
   if (cb > 4096) cb = 4096;
   if (cb < 1) cb = 1;
   if (maxcnt >= 0 && maxcnt <= 1536) {  // 8 warps x maxcnt rows in shared memory (<= 48 KB)
     const int cap = maxcnt > 0 ? maxcnt : 1;
-    csc_sort_smem_kernel<<<cb, 256, sizeof(int) * 8 * (size_t)cap, s>>>(n, colptr, tmp_row, tmp_val, rowind,
-                                                                        cvals, cap);
+    return launch_pdl(csc_sort_smem_kernel, dim3(cb), dim3(256), sizeof(int) * 8 * (size_t)cap, s, n, colptr,
+                      tmp_row, tmp_val, rowind, cvals, cap);
   } else {
     csc_sort_kernel<<<cb, 256, 0, s>>>(n, colptr, tmp_row, tmp_val, rowind, cvals);
   }
@@ -394,6 +398,7 @@ __global__ void __launch_bounds__(512) gram_exact_kernel(
     const int32_t* __restrict__ rowind, const double* __restrict__ cvals,
     const double* __restrict__ b, int row_begin, int row_end, double* __restrict__ G, int ldg,
     double* __restrict__ c, double scale, double inv_scale) {
+  pdl_wait();
   // Every product a_ri a_rj is an integer multiple of 2^(2 L_A) (L_A: the
   // lowest set bit over A) and every column sum stays below 2^53 units, so
   // the accumulator holds exact 64-bit integers (product * scale), kept as
@@ -531,9 +536,8 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
     long long blocks = (long long)sm_count * per_sm;
     if (blocks > n) blocks = n;
     const double sc = ldexp(1.0, -2 * exact_lmin);
-    gram_exact_kernel<<<(int)blocks, 512, smem, s>>>(n, rowptr, colind, vals, colptr, rowind, cvals, b,
-                                                     row_begin, row_end, G, ldg, c, sc, 1.0 / sc);
-    return cudaGetLastError();
+    return launch_pdl(gram_exact_kernel, dim3((int)blocks), dim3(512), smem, s, n, rowptr, colind, vals, colptr,
+                      rowind, cvals, b, row_begin, row_end, G, ldg, c, sc, 1.0 / sc);
   }
   // One chunk = the whole row when it fits (measured: splitting a row into
   // column chunks multiplies the A-row gathers and is slower at config 2).

@@ -460,6 +460,7 @@ __host__ __device__ inline ClLayout cl_layout(int m, int n, const int* mx) {
 __global__ void __launch_bounds__(1024) lsqr_plan_kernel(int m, int n, const int32_t* rowptr,
                                                          const int32_t* colptr, int C, int* out) {
   __shared__ int thr[kMaxC];
+  pdl_wait();
   int* rb = out + 4;
   int* cb = out + 5 + C;
   const int tid = threadIdx.x;
@@ -1046,8 +1047,7 @@ cudaError_t launch_lsqr_compact(const LsqrArgs& a, int sm_count, cudaStream_t s)
 
 cudaError_t launch_lsqr_plan(int m, int n, const int32_t* rowptr, const int32_t* colptr, int* out,
                              cudaStream_t s) {
-  lsqr_plan_kernel<<<1, 1024, 0, s>>>(m, n, rowptr, colptr, kMaxC, out);
-  return cudaGetLastError();
+  return launch_pdl(lsqr_plan_kernel, dim3(1), dim3(1024), 0, s, m, n, rowptr, colptr, (int)kMaxC, out);
 }
 
 size_t lsqr_cluster_smem(int m, int n, const int* plan) { return cl_layout(m, n, plan).bytes; }
