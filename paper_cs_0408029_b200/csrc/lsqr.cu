@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
   extern __shared__ double smem[];
   __shared__ double red[2][4][32];  // (double-buffered by publish call parity)
   __shared__ double parts[8][kMaxC];  // [slot][source CTA] partials, pushed by every CTA
+  pdl_wait();
   const int m = a.m, n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kCT / 32;
@@ -1089,13 +1090,15 @@ cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host,
   cfg.blockDim = dim3(kCT);
   cfg.dynamicSmemBytes = Ly.bytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kMaxC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (see launch_pdl)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, lsqr_cluster_kernel, a, Ly);
 }
 
