@@ -75,10 +75,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (g_chol_prof != nullptr && threadIdx.x == 0) g_chol_prof[(task) * 8 + (slot)] = gtimer(); \
   } while (0)
 
-// DAG flags: full[tri], part[tri], inv[ntr], back-solve x[ntr], a[ntr], N[ntr].
+// DAG flags: full[tri], part[tri], inv[ntr], back-solve x[ntr], a[ntr], N[ntr], half1[tri].
 size_t chol_flag_count(int n) {
   const int ntr = (n + 1 + T - 1) / T;
-  return 2 * (size_t)tri_tiles(n) + 4 * (size_t)ntr + 4;
+  return 3 * (size_t)tri_tiles(n) + 4 * (size_t)ntr + 4;
 }
 
 // Lower tiles L(i,j), one inverse tile Linv_JJ and two back-solve tiles N_J,
@@ -159,6 +159,43 @@ __device__ __forceinline__ void dmma_tile_nn(double (&acc)[2][4][2], const doubl
     for (int a = 0; a < 2; ++a)
 #pragma unroll
       for (int q = 0; q < 4; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
+  }
+}
+// 32 x 64 products (a half tile): warp w owns rows rb0 = (w>>2)*16 .. +16,
+// columns cb0 = (w&3)*16 .. +16 (2 x 2 blocks of 8x8); acc -= A B^T, K = 64.
+__device__ __forceinline__ void dmma_half_sub(double (&acc)[2][2][2], const double* __restrict__ A,
+                                              const double* __restrict__ B, int lane, int rb0, int cb0) {
+#pragma unroll 4
+  for (int kk = 0; kk < T; kk += 4) {
+    double av[2], bv[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) av[a] = -A[(rb0 + 8 * a + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) bv[q] = B[(cb0 + 8 * q + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
+  }
+}
+__device__ __forceinline__ void acc_half_ls(double (&acc)[2][2][2], double* S, int lane, int rb0, int cb0,
+                                            bool store) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        double* p = S + (rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v;
+        if (store) *p = acc[a][q][v];
+        else acc[a][q][v] = *p;
+      }
+}
+// rows [r0, r0+32) of a global tile <-> rows [0, 32) of a smem buffer
+__device__ __forceinline__ void half_async(double* __restrict__ dst, const double* __restrict__ src, int r0) {
+  for (int e = threadIdx.x; e < 32 * T / 2; e += kThreads) {
+    const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+    cp_async16(dst + o, src + r0 * LDS + o);
   }
 }
 __device__ __forceinline__ void acc_load(double (&acc)[2][4][2], const double* S, int lane, int rb0,
@@ -567,8 +604,9 @@ __device__ __forceinline__ void bulk_store_release(int* flag, int epoch, int* fl
 namespace {
 struct FlagSet {
   int* full;   // [tri]   L(i,j) final
-  int* part;   // [tri]   partial tile (helper -> chain)
+  int* part;   // [tri]   partial tile (helper -> chain); rows 0-31 of a restart row-chain tile
   int* inv;    // [ntr]   Linv_jj
+  int* half1;  // [tri]   rows 32-63 of a restart row-chain tile
 };
 // all threads' stores -> barrier -> one st.release (cumulative over what the
 // barrier ordered before it) makes the tile visible with the flag
@@ -662,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   // which the back substitution only writes after the factorization
   double* Wbuf = Linv + (size_t)(boxlen / T) * TS;
   const int ntr = (f + 1 + T - 1) / T;  // tile rows (incl. the rhs row f)
-  FlagSet F{flags, flags + tri, flags + 2 * tri};
+  FlagSet F{flags, flags + tri, flags + 2 * tri, flags + 2 * tri + 4 * (boxlen / T)};
   const int tid = threadIdx.x;
   double* S = smem;
   if (blockIdx.x == 1) {  // empty this epoch's back-substitution mailboxes (see box_empty)
@@ -804,20 +842,33 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     csync();
     int t = s_task;
     csync();
-    int j = jq, kind = -1, i = 0;
-    if (jq > 0) {  // [W(1..jq-1)] [T(jq..ntr-1, j) for j < jq] [D(jq)]
+    int j = jq, kind = -1, i = 0, half = 0;
+    if (jq > 0) {
+      // [W(1..jq-1)] [T(jq..ntr-1, 0)] [row-chain tasks for 0 < j < jq] [D(jq)]; the
+      // row chain runs by half tiles (Th, kind 6) when all its tasks fit on the
+      // helpers at once, else by whole tiles (kind 2): a waiting task holds its CTA
       const int nr = ntr - jq;
+      const bool halves = 2 * nr * (jq - 1) <= (int)gridDim.x - 2;
+      const int per = halves ? 2 : 1;
+      const int nh = (jq - 1) * nr * per;
+      const int u = t - (jq - 1);
       if (t < jq - 1) {
         kind = 5;
         j = t + 1;
-      } else if (t - (jq - 1) < jq * nr) {
+      } else if (u < nr) {
         kind = 2;
-        j = (t - (jq - 1)) / nr;
-        i = jq + (t - (jq - 1)) % nr;
-      } else if (t - (jq - 1) == jq * nr) {
+        j = 0;
+        i = jq + u;
+      } else if (u - nr < nh) {
+        const int v = u - nr;
+        kind = halves ? 6 : 2;
+        j = 1 + v / (per * nr);
+        i = jq + (v % (per * nr)) / per;
+        half = v % per;
+      } else if (u - nr == nh) {
         kind = 3;
       }
-      t -= (jq - 1) + jq * nr + 1;
+      t -= (jq - 1) + nr + nh + 1;
     }
     while (kind < 0 && j < ntc) {
       const int np1 = (j + 1 < ntc) ? 1 : 0;          // P(j+1,j+1)
@@ -834,6 +885,78 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       ++j;
     }
     if (kind < 0) break;
+    if (kind == 6) {                 // Th(i, j, half): rows 32*half.. of L(i,j) below a kept prefix
+      // the restart row chain by half tiles: each step is a 32 x 64 x 64
+      // product on its own CTA (half the DMMA time of a full tile), the two
+      // halves of a row chain run independently.
+      // L(i,j)_h = B_h - L(i,j-1)_h W_j,  B_h = (A(i,j)_h - sum_{k<j-1} L(i,k)_h L(j,k)^T) Linv_jj^T
+      const int r0 = 32 * half;
+      const int rb0 = (w >> 2) * 16, cb0 = (w & 3) * 16;
+      int* const hflag = half ? F.half1 : F.part;
+      double* Lv = smem + 5 * T * LDS;   // Linv_jj
+      double* LB = smem + 1 * T * LDS;   // L(j, k) (kept)
+      double* Wt = smem + 2 * T * LDS;   // W_j^T
+      double* Xp = smem + 3 * T * LDS;   // rows of L(i, j-1) / L(i, k)
+      tile_async(Lv, Linv + (size_t)j * TS);
+      cp_async_commit();
+      {  // gather rows r0.. of A(i,j) (tile row i >= jq: never the chain's)
+        const int rv = min(T, f + 1 - i * T), cv = min(T, f - j * T);
+        for (int e = tid; e < 32 * T; e += kThreads) {
+          const int r = r0 + e / T, cc = e % T;
+          const int gi = i * T + r, gj = j * T + cc;
+          double v = 0.0;
+          if (r < rv && cc < cv) v = (gi < f) ? G[(size_t)Fidx[gi] * ldg + Fidx[gj]] : cvec[Fidx[gj]];
+          S[(e / T) * LDS + cc] = v;
+        }
+      }
+      csync();
+      double acc[2][2][2];
+      acc_half_ls(acc, S, lane, rb0, cb0, false);
+      for (int k = 0; k < j - 1; ++k) {  // (off the critical path: these rows arrived a step earlier)
+        if (tid == 0) wait_flag(&hflag[tidx(i, k)], epoch);
+        csync();
+        half_async(Xp, Lt + (size_t)tidx(i, k) * TS, r0);
+        tile_async(LB, Lt + (size_t)tidx(j, k) * TS);
+        cp_async_commit();
+        cp_async_wait<0>();
+        csync();
+        dmma_half_sub(acc, Xp, LB, lane, rb0, cb0);
+        csync();
+      }
+      acc_half_ls(acc, S, lane, rb0, cb0, true);
+      cp_async_wait<0>();
+      if (tid == 0) wait_flag(&F.part[tidx(j, j - 1)], epoch);  // W_j
+      csync();
+      tile_async(Wt, Wbuf + (size_t)j * TS);
+      cp_async_commit();
+      {
+        double acc8[8][2];
+        if (w < 4) gemm_linvT(acc8, S, Lv, w, lane);  // rows 8w.. of the half
+        csync();
+        if (w < 4) store_rows8(acc8, S, w, lane);  // S = B_h
+      }
+      if (tid == 0) wait_flag(&hflag[tidx(i, j - 1)], epoch);
+      csync();
+      half_async(Xp, Lt + (size_t)tidx(i, j - 1) * TS, r0);
+      cp_async_commit();
+      cp_async_wait<0>();
+      csync();
+      acc_half_ls(acc, S, lane, rb0, cb0, false);
+      dmma_half_sub(acc, Xp, Wt, lane, rb0, cb0);  // -= L(i,j-1)_h W_j
+      acc_half_ls(acc, S, lane, rb0, cb0, true);
+      csync();
+      double* dst = Lt + (size_t)tidx(i, j) * TS + r0 * LDS;
+      for (int e = threadIdx.x; e < 32 * T / 2; e += kThreads) {
+        const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+        *reinterpret_cast<double2*>(dst + o) = *reinterpret_cast<const double2*>(S + o);
+      }
+      publish_flag(&hflag[tidx(i, j)], epoch);
+      if (half == 1 && tid == 0) {  // the whole tile: after the other half too
+        wait_flag(&F.part[tidx(i, j)], epoch);
+        st_release(&F.full[tidx(i, j)], epoch);
+      }
+      continue;
+    }
     if (kind == 5) {                 // W(j) = (L(j,j-1)^T Linv_jj^T)^T = Linv_jj L(j,j-1) (kept tiles)
       const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
       double* Lv = smem + 5 * T * LDS;
@@ -931,6 +1054,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       csync();
       store_tile(Lt + (size_t)tidx(i, j) * TS, S);
       publish_flag(&F.full[tidx(i, j)], epoch);
+      if (jq > 0 && j == 0 && i >= jq && tid == 0) {  // (the restart's half-tile chain starts here)
+        st_release(&F.part[tidx(i, j)], epoch);
+        st_release(&F.half1[tidx(i, j)], epoch);
+      }
       if (i == j + 2) PROF_STAMP(1000 + j + 1, 1);
     }
   }
