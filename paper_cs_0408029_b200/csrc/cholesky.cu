@@ -1350,9 +1350,15 @@ __device__ void backsolve_task(const BsArgs& a, int f, int epoch, int J, double*
   __syncthreads();  // (smem reused by the next task)
 }
 
+constexpr int kDualPrefetch = 512;  // = the dual kernel's PF * 32 (pivot.cu): whole G rows prefetched
 __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(BsArgs a, DevState* st) {
   extern __shared__ __align__(128) double bsm[];
   pdl_wait();
+  // small F: let the dual kernel start now -- it gathers its whole G rows
+  // into registers while this runs (and reads nothing of ours before its own
+  // griddepcontrol.wait).  Large F: its CTAs would only compete with this
+  // kernel for the SMs and the memory system, so it starts at our exit.
+  if (st->f <= kDualPrefetch) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ int s_task;
   const int f = st->f;
   const int epoch = st->epoch;

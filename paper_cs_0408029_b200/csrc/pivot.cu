@@ -472,6 +472,33 @@ __global__ void __launch_bounds__(256) dual_kernel(
     const double* __restrict__ xF, uint8_t* __restrict__ mask, double* __restrict__ x,
     double* __restrict__ y, double tol, DevState* st, const int32_t* __restrict__ Fs,
     const double* __restrict__ xs) {
+  // Before waiting for the back substitution (PDL: it lets this grid start
+  // once it runs): gather this warp's first G row entries G[j, F] into
+  // registers -- G, F and the sets come from earlier kernels (decide).
+  constexpr int PF = 16;  // prefetched entries per lane (f <= 512: the whole row)
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int f = st->f, g = st->g;
+  const bool pre = Fs != nullptr && !st->done && gwarp < g;
+  double pg[PF];
+  int pi[PF];
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    pi[k] = 0;
+    pg[k] = 0.0;
+  }
+  if (pre) {
+    const double* Gj = G + (size_t)Gidx[gwarp] * ldg;
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int a = lane + 32 * k;
+      if (a < f) {
+        pi[k] = __ldg(&Fs[a]);
+        pg[k] = Gj[pi[k]];
+      }
+    }
+  }
   pdl_wait();
   const int status = st->status;
   if (status != 0) {
@@ -482,10 +509,26 @@ __global__ void __launch_bounds__(256) dual_kernel(
     return;
   }
   if (st->done) return;
-  const int f = st->f, g = st->g;
-  const int lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  // the prefetched entries, in the loop's own order (then dead)
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+  int pa = lane;
+  if (pre) {
+#pragma unroll
+    for (int k = 0; k < PF; k += 4) {
+      const int a0 = lane + 32 * k;
+      if (a0 + 96 < f) {
+        p0 = fma(pg[k], xs[pi[k]], p0);
+        p1 = fma(pg[k + 1], xs[pi[k + 1]], p1);
+        p2 = fma(pg[k + 2], xs[pi[k + 2]], p2);
+        p3 = fma(pg[k + 3], xs[pi[k + 3]], p3);
+      } else {  // the tail (p0), then nothing is left
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (a0 + 32 * q < f) p0 = fma(pg[k + q], xs[pi[k + q]], p0);
+      }
+    }
+    pa = (lane + 32 * (PF - 4) + 96 < f) ? lane + 32 * PF : f;  // (continue after a full last group)
+  }
   double below = 0.0, above = INFINITY;
   for (int jj = gwarp; jj < g; jj += nwarps) {
     const int j = Gidx[jj];
@@ -497,6 +540,13 @@ __global__ void __launch_bounds__(256) dual_kernel(
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int a = lane;
     if (Fs != nullptr) {
+      if (jj == gwarp && pre) {
+        s0 = p0;
+        s1 = p1;
+        s2 = p2;
+        s3 = p3;
+        a = pa;
+      }
 #pragma unroll 4
       for (; a + 96 < f; a += 128) {
         const int i0 = __ldg(&Fs[a]), i1 = __ldg(&Fs[a + 32]), i2 = __ldg(&Fs[a + 64]), i3 = __ldg(&Fs[a + 96]);
