@@ -1350,7 +1350,7 @@ __device__ void backsolve_task(const BsArgs& a, int f, int epoch, int J, double*
   __syncthreads();  // (smem reused by the next task)
 }
 
-constexpr int kDualPrefetch = 512;  // = the dual kernel's PF * 32 (pivot.cu): whole G rows prefetched
+constexpr int kDualPrefetch = 1024;  // early release while the dual prefetches a good part of its G rows (PF * 32 = 512 entries, pivot.cu)
 __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(BsArgs a, DevState* st) {
   extern __shared__ __align__(128) double bsm[];
   pdl_wait();
