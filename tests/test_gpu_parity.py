@@ -238,6 +238,18 @@ def test_solve_parity_random_shapes(P, seed):
     assert_parity(P, g.make_problem(dict(m=m, n=n, density=max(d, 2.0 / n)), seed=seed))
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_solve_parity_reuse_shapes(P, seed):
+    """|F| of a few hundred to ~700: later pivot iterations keep a factor
+    prefix (factor reuse) -- restart row chains by half or whole tiles, the
+    bordered row landing anywhere relative to the kept columns."""
+    rng = np.random.default_rng([seed, 17])
+    n = int(rng.integers(300, 1300))
+    m = n + int(rng.integers(n // 2, 3 * n))
+    d = float(rng.choice([0.03, 0.06, 0.12]))
+    assert_parity(P, g.make_problem(dict(m=m, n=n, density=d), seed=100 + seed))
+
+
 @pytest.mark.parametrize("case", SINGLES["cases"][:20], ids=lambda c: f"seed{c['seed']}")
 def test_single_exchange_parity(P, case):
     gpu, r = assert_parity(P, g.make_correlated(case["seed"], 0.05), lsqr_mode=0)
