@@ -55,6 +55,12 @@ nnls_status map_cuda(cudaError_t e) {
 
 int round_up(int v, int q) { return (v + q - 1) / q * q; }
 
+// env switch: set to anything but "" or "0"
+bool env_on(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] && !(v[0] == '0' && v[1] == 0);
+}
+
 }  // namespace
 
 struct HostState {
@@ -306,10 +312,10 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
     return s;
   }
   memset(h->h, 0, sizeof(HostState));
-  h->no_cluster = getenv("NNLS_NO_CLUSTER") != nullptr;
-  h->no_graph = getenv("NNLS_NO_GRAPH") != nullptr;
-  h->no_reuse = getenv("NNLS_NO_REUSE") != nullptr;
-  h->no_exact_gram = getenv("NNLS_NO_EXACT_GRAM") != nullptr;
+  h->no_cluster = env_on("NNLS_NO_CLUSTER");
+  h->no_graph = env_on("NNLS_NO_GRAPH");
+  h->no_reuse = env_on("NNLS_NO_REUSE");
+  h->no_exact_gram = env_on("NNLS_NO_EXACT_GRAM");
   *out = h;
   return NNLS_OK;
 }
@@ -512,7 +518,7 @@ cudaError_t launch_lsqr(nnls_handle* h, cudaStream_t s) {
 
 }  // namespace
 bool nnls::pdl_enabled() {
-  static const bool on = getenv("NNLS_NO_PDL") == nullptr;
+  static const bool on = !env_on("NNLS_NO_PDL");
   return on;
 }
 namespace {
@@ -571,7 +577,7 @@ void drop_graph(nnls_handle* h) {
 // replayed with one graph launch (no host round trip per pivot iteration).
 #define GDBG(msg)                                                                         \
   do {                                                                                    \
-    if (getenv("NNLS_DEBUG")) fprintf(stderr, "[nnls graph] %s: %s\n", msg, cudaGetErrorString(e)); \
+    if (env_on("NNLS_DEBUG")) fprintf(stderr, "[nnls graph] %s: %s\n", msg, cudaGetErrorString(e)); \
   } while (0)
 cudaError_t build_graph(nnls_handle* h, cudaStream_t s) {
   drop_graph(h);
@@ -587,7 +593,7 @@ cudaError_t build_graph(nnls_handle* h, cudaStream_t s) {
   cudaGraphNode_t init_node = nullptr, cond_node = nullptr;
   e = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
   GDBG("handle");
-  if (getenv("NNLS_DEBUG")) {
+  if (env_on("NNLS_DEBUG")) {
     fprintf(stderr, "[nnls graph] stream %p graph %p query %d\n", (void*)s, (void*)g, (int)cudaStreamQuery(s));
     fflush(stderr);
   }
