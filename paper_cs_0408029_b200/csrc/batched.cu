@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
 struct LLay {
   int orv, ob, ou, ox, ov, ow, oX, ored;  // double offsets
   int doubles;
-  int irp, ico, imk, ici, icr, icx;
+  int irp, ico, imk, ici, icr, icx, irf, ifb, ifl;
   int ints;
   size_t bytes;
 };
@@ -488,12 +488,16 @@ __host__ __device__ inline LLay llayout(int m, int n, int nnz_max) {
   L.ici = q; q += (nnz_max + 1) / 2;
   L.icr = q; q += (nnz_max + 1) / 2;
   L.icx = q; q += (nnz_max + 1) / 2;
+  L.irf = q; q += m + 1;            // row r's F entries: [rp[r], rpF[r])
+  q = (q + 1) & ~1;
+  L.ifb = q; q += 2 * m;            // row r's F-entry bits (u64)
+  L.ifl = q; q += n + 1;            // F columns in index order (compacted)
   L.ints = q + 8;
   L.bytes = sizeof(double) * (size_t)L.doubles + sizeof(int) * (size_t)L.ints;
   return L;
 }
 
-__global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_max) {
+__global__ void __launch_bounds__(BT, 7) batched_lsqr_kernel(BatchArgs a, int nnz_max) {
   long long bp_t = clock64();
   extern __shared__ double sm[];
   const int m = a.m, n = a.n;
@@ -513,6 +517,9 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
   uint16_t* ci = reinterpret_cast<uint16_t*>(ib + Ly.ici);
   uint16_t* crow = reinterpret_cast<uint16_t*>(ib + Ly.icr);
   uint16_t* cpos = reinterpret_cast<uint16_t*>(ib + Ly.icx);
+  int* rpF = ib + Ly.irf;
+  unsigned long long* fb = reinterpret_cast<unsigned long long*>(ib + Ly.ifb);
+  int* fl = ib + Ly.ifl;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double tol = a.tol;
   __shared__ int s_istop;
@@ -522,29 +529,67 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
     const int status = a.info_i[(size_t)prob * 8 + 0];
     const int f = a.info_i[(size_t)prob * 8 + 3];
     for (int r = tid; r <= m; r += BT) rp[r] = a.rowptr[(size_t)prob * (m + 1) + r];
-    for (int e = tid; e < nz; e += BT) {
-      ci[e] = (uint16_t)a.colind[e0 + e];
-      rv[e] = a.vals[e0 + e];
-    }
     for (int r = tid; r < m; r += BT) bb[r] = a.b[(size_t)prob * m + r];
+    for (int j = tid; j < n; j += BT) {
+      mk[j] = a.mask_out[(size_t)prob * n + j];
+      x[j] = a.x_out[(size_t)prob * n + j];
+      v[j] = 0.0;
+      X[j] = 0.0;
+    }
+    __syncthreads();
+    // LSQR works on A restricted to F: each row is stored F entries
+    // first, then G entries, both in their original order, so the row SpMV
+    // walks [rp[r], rpF[r]) only.  fb[r] marks row r's F entries (a row has
+    // at most n <= 64), which re-points the column view at the moved entries
+    // in O(1); the report below still reads every column.
+    const int32_t* gci = a.colind + e0;
+    const double* gvl = a.vals + e0;
+    for (int r = tid; r < m; r += BT) {
+      const int r0 = rp[r], r1 = rp[r + 1];
+      unsigned long long bits = 0ull;
+      for (int e = r0; e < r1; ++e)
+        if (mk[gci[e]]) bits |= 1ull << (e - r0);
+      const int nFr = __popcll(bits);
+      int wF = r0, wG = r0 + nFr;
+      for (int e = r0; e < r1; ++e) {
+        const int w2 = ((bits >> (e - r0)) & 1ull) ? wF++ : wG++;
+        ci[w2] = (uint16_t)gci[e];
+        rv[w2] = gvl[e];
+      }
+      rpF[r] = r0 + nFr;
+      fb[r] = bits;
+    }
+    if (wid == 0) {  // F columns in index order
+      int base = 0;
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        const bool inF = j < n && mk[j];
+        const unsigned bal = __ballot_sync(kFull, inF);
+        if (inF) fl[base + __popc(bal & ((1u << lane) - 1u))] = j;
+        base += __popc(bal);
+      }
+      if (lane == 0) fl[n] = base;
+    }
+    __syncthreads();
     {
       const int32_t* cvw = reinterpret_cast<const int32_t*>(a.colview + (size_t)prob * a.cv_stride);
       const uint16_t* cvr = reinterpret_cast<const uint16_t*>(cvw + (n + 1));
       for (int j = tid; j <= n; j += BT) co[j] = cvw[j];
       for (int t = tid; t < nz; t += BT) {
-        crow[t] = cvr[t];
-        cpos[t] = cvr[nnz_max + t];
+        const int r = cvr[t];
+        const int k = cvr[nnz_max + t] - rp[r];
+        const unsigned long long bits = fb[r];
+        const int below = __popcll(bits & ((1ull << k) - 1ull));
+        crow[t] = (uint16_t)r;
+        cpos[t] = (uint16_t)(((bits >> k) & 1ull) ? rp[r] + below : rpF[r] + (k - below));
       }
     }
-    for (int j = tid; j < n; j += BT) {
-      mk[j] = a.mask_out[(size_t)prob * n + j];
-      x[j] = a.x_out[(size_t)prob * n + j];
-    }
     __syncthreads();
+    const int nF = fl[n];
     BP_MARK(10);  // LSQR kernel: load
     // ---------------------------------------------------------- a10 LSQR
-    // All 4 warps.  Thread r owns row r (u), threads 2j, 2j+1 own column j
-    // (v, w, X; the pair splits A^T u).  Two CTA barriers per iteration: the
+    // All 4 warps.  Thread r owns row r (u); a group of tpc threads owns the
+    // F column fl[grp] (v, w, X; the group splits A^T u).  Three CTA barriers per iteration: the
     // norm reductions (|u|^2 | |v|^2, |d|^2, |x|^2) each end with one, and the
     // vectors a thread reads from others were written before it; the stopping
     // test of an iteration is evaluated after the next barrier (it needs only
@@ -574,7 +619,7 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
       // (vec is zero outside F: x and v are, so no mask test)
       auto row_dot = [&](int r, const double* vec) {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        const int t1 = rp[r + 1];
+        const int t1 = rpF[r];
         int e = rp[r];
         for (; e + 3 < t1; e += 4) {
           s0 = fma(rv[e], vec[ci[e]], s0);
@@ -585,20 +630,29 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
         for (; e < t1; ++e) s0 = fma(rv[e], vec[ci[e]], s0);
         return (s0 + s1) + (s2 + s3);
       };
-      // column SpMV half: entries t of column j with t - co[j] = half (mod 2)
-      auto col_dot = [&](int j, int half, const double* vec) {
+      // column SpMV over the F columns only: tpc threads per column (4 when
+      // |F| <= 32, else 2), thread sub takes entries t - co[j] = sub (mod tpc)
+      const int tpc = nF <= 32 ? 4 : 2;
+      const int grp = tid / tpc, sub = tid % tpc;
+      const bool colgrp = grp < nF;
+      const int jc = colgrp ? fl[grp] : 0;
+      const bool colown = colgrp && sub == 0;
+      auto col_dot = [&](const double* vec) {
         double s0 = 0.0, s1 = 0.0;
-        const int t1 = co[j + 1];
-        int t = co[j] + half;
-        for (; t + 2 < t1; t += 4) {
-          s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
-          s1 = fma(rv[cpos[t + 2]], vec[crow[t + 2]], s1);
+        if (colgrp) {
+          const int t1 = co[jc + 1];
+          int t = co[jc] + sub;
+          for (; t + tpc < t1; t += 2 * tpc) {
+            s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
+            s1 = fma(rv[cpos[t + tpc]], vec[crow[t + tpc]], s1);
+          }
+          if (t < t1) s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
         }
-        for (; t < t1; t += 2) s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
-        return s0 + s1;
+        double sacc = s0 + s1;
+        sacc += __shfl_xor_sync(kFull, sacc, 1);
+        if (tpc == 4) sacc += __shfl_xor_sync(kFull, sacc, 2);
+        return sacc;
       };
-      const int jc = tid >> 1, half = tid & 1;  // column pair (n <= 64)
-      const bool colown = jc < n && half == 0 && mk[jc];
       double tot[3];
       // beta u = b - A x (mode 2) or b
       double pu = 0.0;
@@ -615,13 +669,10 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
       // alpha v = A^T u
       double pv = 0.0;
       {
-        double sacc = 0.0;
-        if (jc < n && mk[jc] && beta > 0.0) sacc = col_dot(jc, half, u);
-        sacc += __shfl_xor_sync(kFull, sacc, 1);
-        if (half == 0 && jc < n) {
-          const double vv = mk[jc] ? sacc * ib : 0.0;
+        const double sacc = beta > 0.0 ? col_dot(u) : 0.0;
+        if (colown) {
+          const double vv = sacc * ib;
           v[jc] = vv;
-          X[jc] = 0.0;
           pv = vv * vv;
         }
       }
@@ -629,7 +680,7 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
       double alpha = sqrt(tot[0]);
       const double ia0 = alpha > 0.0 ? 1.0 / alpha : 0.0;
       for (int r = tid; r < m; r += BT) u[r] *= ib;  // own rows
-      if (half == 0 && jc < n) {
+      if (colown) {
         v[jc] *= ia0;
         w[jc] = v[jc];
       }
@@ -661,9 +712,7 @@ __global__ void __launch_bounds__(BT) batched_lsqr_kernel(BatchArgs a, int nnz_m
             ib = 1.0 / beta;
             anorm = sqrt(anorm * anorm + alpha * alpha + beta * beta);
             // v' = A^T u' / beta - beta v (own columns)
-            double sacc = 0.0;
-            if (jc < n && mk[jc]) sacc = col_dot(jc, half, u);
-            sacc += __shfl_xor_sync(kFull, sacc, 1);
+            const double sacc = col_dot(u);
             pv = 0.0;
             if (colown) {
               const double vv = sacc * ib - beta * v[jc];
