@@ -344,35 +344,45 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
         }
       }
       // left-looking by columns (the oracle's jki order per entry, so the
-      // factor is bit-identical): in step j the thread of row i > j finishes
-      // L(i, j) with a sequential dot in increasing k; the thread of row j+1
-      // then also finishes the next pivot L(j+1, j+1) -> one barrier per column
-      if (tid == 0) {
-        s_bad = -1;
-        if (f > 0) {
-          const double d = L[0];
-          if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) s_bad = 0;
-          L[0] = sqrt(d);
+      // factor is bit-identical) on warp 0 alone (f <= n <= 64: lane owns rows
+      // jj+1+lane and jj+33+lane of step jj): in step jj the owner of row
+      // i > jj finishes L(i, jj) with a sequential dot in increasing k; the
+      // owner of row jj+1 then also finishes the next pivot L(jj+1, jj+1) ->
+      // one warp barrier per column, the other warps wait once
+      __syncthreads();  // the gathered L
+      if (wid == 0) {
+        if (lane == 0) {
+          s_bad = -1;
+          if (f > 0) {
+            const double d = L[0];
+            if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) s_bad = 0;
+            L[0] = sqrt(d);
+          }
+        }
+        __syncwarp();
+        for (int jj = 0; jj < f; ++jj) {
+          const int rj = jj * (jj + 1) / 2;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = jj + 1 + lane + 32 * h;
+            if (i <= f) {
+              const int ri = i * (i + 1) / 2;
+              double sacc = L[ri + jj];
+              for (int k = 0; k < jj; ++k) sacc = __dsub_rn(sacc, __dmul_rn(L[ri + k], L[rj + k]));
+              sacc = sacc / L[rj + jj];
+              L[ri + jj] = sacc;
+              if (i == jj + 1 && i < f) {  // the next pivot
+                double d = L[ri + i];
+                for (int k = 0; k <= jj; ++k) d = __dsub_rn(d, __dmul_rn(L[ri + k], L[ri + k]));
+                if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) atomicMin(&s_bad, i);
+                L[ri + i] = sqrt(d);
+              }
+            }
+          }
+          __syncwarp();
         }
       }
       __syncthreads();
-      for (int jj = 0; jj < f; ++jj) {
-        const int i = jj + 1 + tid;
-        if (i <= f) {
-          const int ri = i * (i + 1) / 2, rj = jj * (jj + 1) / 2;
-          double sacc = L[ri + jj];
-          for (int k = 0; k < jj; ++k) sacc = __dsub_rn(sacc, __dmul_rn(L[ri + k], L[rj + k]));
-          sacc = sacc / L[rj + jj];
-          L[ri + jj] = sacc;
-          if (i == jj + 1 && i < f) {  // the next pivot
-            double d = L[ri + i];
-            for (int k = 0; k <= jj; ++k) d = __dsub_rn(d, __dmul_rn(L[ri + k], L[ri + k]));
-            if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) atomicMin(&s_bad, i);
-            L[ri + i] = sqrt(d);
-          }
-        }
-        __syncthreads();
-      }
       {
         const int bad = s_bad;
         if (bad >= 0) {
