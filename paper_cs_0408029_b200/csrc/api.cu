@@ -1043,7 +1043,7 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
   CK(ensure(h->b_gram, batched_gram_scratch(n, h->sms)));
   CK(ensure(h->b_info_i, sizeof(int32_t) * 8 * (size_t)batch));
   CK(ensure(h->b_info_d, sizeof(double) * 5 * (size_t)batch));
-  CK(ensure(h->err, sizeof(int) * 4));
+  CK(ensure(h->err, sizeof(int) * 8));
   CK(cudaMemcpyAsync(h->b_nnz_off.p, nnz_off, sizeof(int64_t) * (size_t)(batch + 1), cudaMemcpyDefault, s));
   CK(cudaMemcpyAsync(h->rowptr.p, rowptr, sizeof(int32_t) * (size_t)batch * (m + 1), cudaMemcpyDefault, s));
   if (total > 0) {
@@ -1051,14 +1051,19 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
     CK(cudaMemcpyAsync(h->vals.p, vals, sizeof(double) * (size_t)total, cudaMemcpyDefault, s));
   }
   CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)batch * m, cudaMemcpyDefault, s));
-  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int), s));
-  TIMED(NNLS_PH_VALIDATE, 1,
-        launch_validate_batched(batch, m, n, P<int64_t>(h->b_nnz_off), P<int32_t>(h->rowptr),
+  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int) * 6, s));
+  TIMED(NNLS_PH_VALIDATE, 2,
+        launch_validate_batched(batch, m, n, total, P<int64_t>(h->b_nnz_off), P<int32_t>(h->rowptr),
                                 P<int32_t>(h->colind), P<double>(h->vals), P<double>(h->b),
                                 P<int>(h->err), s));
-  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 6, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (h->h->err[0]) return map_err_bits(h->h->err[0]);
+  {  // a column index repeated or out of order inside some row
+    unsigned long long dcnt[2];
+    memcpy(dcnt, h->h->err + 2, sizeof(dcnt));
+    if (dcnt[0] != dcnt[1]) return NNLS_ERR_INDEX;
+  }
   h->loaded = true;
   return NNLS_OK;
 }

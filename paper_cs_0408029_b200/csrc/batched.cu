@@ -842,47 +842,130 @@ cudaError_t batched_debug_set_profile(long long* p) {
   return cudaMemcpyToSymbol(g_batch_prof, &p, sizeof(p));
 }
 
-__global__ void validate_batched_kernel(int batch, int m, int n, const int64_t* __restrict__ nnz_off,
-                                        const int32_t* __restrict__ rowptr,
-                                        const int32_t* __restrict__ colind,
-                                        const double* __restrict__ vals,
-                                        const double* __restrict__ b, int* err) {
+// Validation in two coalesced passes (no warp per row: rows hold ~13
+// entries).  The per-row "columns strictly increasing" test is turned into a
+// count: over the whole concatenated colind, D = #{g >= 1 : colind[g] <=
+// colind[g-1]} (entry pass); a valid batch has such descents only at the
+// first entry of a non-empty row, Ds of them (row pass) -> valid iff D == Ds
+// (rows partition each problem's entries once rowptr passes its own checks).
+// cnt[0] = D, cnt[1] = Ds.
+__global__ void validate_entries_kernel(int64_t total, int n, const int32_t* __restrict__ colind,
+                                        const double* __restrict__ vals, int* err,
+                                        unsigned long long* cnt) {
+  __shared__ int s_e;
+  __shared__ unsigned s_d;
+  if (threadIdx.x == 0) {
+    s_e = 0;
+    s_d = 0;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int e_local = 0;
-  for (int64_t gr = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gr < (int64_t)batch * m;
-       gr += warps) {
-    const int prob = (int)(gr / m), r = (int)(gr % m);
+  unsigned d_local = 0;
+  // 4 consecutive entries per thread (16-byte colind, 2 x 16-byte vals
+  // loads); whole warps iterate together (the shuffle below)
+  const int64_t q4 = (total + 3) / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t span = (q4 + 31) / 32 * 32;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < span; q += stride) {
+    const int64_t g0 = 4 * q;
+    int c[4];
+    double v[4];
+    if (g0 + 3 < total) {
+      const int4 c4 = *reinterpret_cast<const int4*>(colind + g0);
+      const double2 v0 = *reinterpret_cast<const double2*>(vals + g0);
+      const double2 v1 = *reinterpret_cast<const double2*>(vals + g0 + 2);
+      c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+      v[0] = v0.x; v[1] = v0.y; v[2] = v1.x; v[3] = v1.y;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        c[k] = g0 + k < total ? colind[g0 + k] : 0;
+        v[k] = g0 + k < total ? vals[g0 + k] : 0.0;
+      }
+    }
+    int prev = __shfl_up_sync(kFull, c[3], 1);
+    if (lane == 0 && g0 > 0 && g0 < total) prev = colind[g0 - 1];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t gk = g0 + k;
+      if (gk < total) {
+        if (c[k] < 0 || c[k] >= n) e_local |= 2;
+        if (!isfinite(v[k])) e_local |= 4;
+        if (gk > 0 && c[k] <= (k ? c[k - 1] : prev)) ++d_local;
+      }
+    }
+  }
+  d_local = warp_sum_i((int)d_local);
+  if (e_local) atomicOr(&s_e, e_local);
+  if (lane == 0 && d_local) atomicAdd(&s_d, d_local);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_e) atomicOr(err, s_e);
+    if (s_d) atomicAdd(cnt, (unsigned long long)s_d);
+  }
+}
+
+__global__ void validate_rows_kernel(int batch, int m, const int64_t* __restrict__ nnz_off,
+                                     const int32_t* __restrict__ rowptr,
+                                     const int32_t* __restrict__ colind,
+                                     const double* __restrict__ b, int* err,
+                                     unsigned long long* cnt) {
+  __shared__ int s_e;
+  __shared__ unsigned s_d;
+  if (threadIdx.x == 0) {
+    s_e = 0;
+    s_d = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  int e_local = 0;
+  unsigned d_local = 0;
+  const int64_t rows = (int64_t)batch * m;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool small = rows < (1ll << 31);
+  for (int64_t gr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gr < rows; gr += stride) {
+    const int prob = small ? (int)((unsigned)gr / (unsigned)m) : (int)(gr / m);
+    const int r = (int)(gr - (int64_t)prob * m);
     const int64_t base = nnz_off[prob];
     const int64_t nz = nnz_off[prob + 1] - base;
     const int64_t lo = rowptr[(size_t)prob * (m + 1) + r], hi = rowptr[(size_t)prob * (m + 1) + r + 1];
-    if (lane == 0) {
-      if (r == 0 && lo != 0) e_local |= 1;
-      if (r == m - 1 && hi != nz) e_local |= 1;
-      if (!isfinite(b[gr])) e_local |= 4;
-    }
+    if (r == 0 && lo != 0) e_local |= 1;
+    if (r == m - 1 && hi != nz) e_local |= 1;
+    if (!isfinite(b[gr])) e_local |= 4;
     if (hi < lo || lo < 0 || hi > nz) {
       e_local |= 1;
       continue;
     }
-    for (int64_t t = lo + lane; t < hi; t += 32) {
-      const int cidx = colind[base + t];
-      if (cidx < 0 || cidx >= n) e_local |= 2;
-      if (t > lo && colind[base + t - 1] >= cidx) e_local |= 2;
-      if (!isfinite(vals[base + t])) e_local |= 4;
-    }
+    const int64_t g = base + lo;
+    if (hi > lo && g > 0 && colind[g] <= colind[g - 1]) ++d_local;
   }
-  if (e_local) atomicOr(err, e_local);
+  d_local = warp_sum_i((int)d_local);
+  if (e_local) atomicOr(&s_e, e_local);
+  if (lane == 0 && d_local) atomicAdd(&s_d, d_local);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_e) atomicOr(err, s_e);
+    if (s_d) atomicAdd(cnt + 1, (unsigned long long)s_d);
+  }
 }
 
-cudaError_t launch_validate_batched(int batch, int m, int n, const int64_t* nnz_off,
+cudaError_t launch_validate_batched(int batch, int m, int n, int64_t total, const int64_t* nnz_off,
                                     const int32_t* rowptr, const int32_t* colind,
                                     const double* vals, const double* b, int* err, cudaStream_t s) {
-  int64_t warps = (int64_t)batch * m;
-  int blocks = (int)((warps * 32 + 255) / 256);
-  if (blocks > 8192) blocks = 8192;
+  // err[0] bits, err[2..5] the two 64-bit descent counts (zeroed by the caller)
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(err + 2);
+  int blocks = (int)((total / 4 + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  validate_batched_kernel<<<blocks, 256, 0, s>>>(batch, m, n, nnz_off, rowptr, colind, vals, b, err);
+  if (total > 0) validate_entries_kernel<<<blocks, 256, 0, s>>>(total, n, colind, vals, err, cnt);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t rows = (int64_t)batch * m;
+  blocks = (int)((rows + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  validate_rows_kernel<<<blocks, 256, 0, s>>>(batch, m, nnz_off, rowptr, colind, b, err, cnt);
   return cudaGetLastError();
 }
 

@@ -139,7 +139,9 @@ struct BatchArgs {
 size_t batched_colview_stride(int n, int nnz_max);
 size_t batched_gram_scratch(int n, int sm_count);
 size_t batched_smem_bytes(int m, int n, int nnz_max);
-cudaError_t launch_validate_batched(int batch, int m, int n, const int64_t* nnz_off,
+// err: 6 ints, zeroed: [0] error bits, [2..5] descent counts (the caller
+// reports an index error when the two 64-bit counts differ)
+cudaError_t launch_validate_batched(int batch, int m, int n, int64_t total, const int64_t* nnz_off,
                                     const int32_t* rowptr, const int32_t* colind,
                                     const double* vals, const double* b, int* err, cudaStream_t s);
 cudaError_t launch_batched_nnz(const BatchArgs& a, int nnz_max, int sm_count, cudaStream_t s);

@@ -359,6 +359,53 @@ def _batched_parity(P, B, **kw):
     return out, ref
 
 
+def test_batched_invalid_inputs(P):
+    """Batched validation: each corruption is reported with its own status,
+    wherever in the batch it sits (first / middle / last problem, first /
+    last row), and a clean batch after it loads on the same handle."""
+    B = g.make_batch(seed=5, start=0, count=40)
+    S = P.BatchedSolver()
+
+    def expect(status, **over):
+        kw = dict(nnz_off=B.nnz_off, rowptr=B.rowptr, colind=B.colind, vals=B.vals, b=B.b)
+        kw.update(over)
+        with pytest.raises(P.NNLSError) as e:
+            S.load(B.count, B.m, B.n, kw["nnz_off"], kw["rowptr"], kw["colind"], kw["vals"], kw["b"])
+        assert e.value.status == status
+
+    def row_span(prob, r):
+        base = int(B.nnz_off[prob])
+        rp = B.rowptr[prob * (B.m + 1):(prob + 1) * (B.m + 1)]
+        return base + int(rp[r]), base + int(rp[r + 1])
+
+    for prob in (0, 17, B.count - 1):
+        ci = B.colind.copy()
+        ci[row_span(prob, B.m - 1)[1] - 1] = B.n  # out of range
+        expect(P.ERR_INDEX, colind=ci)
+        for r in (0, B.m // 2, B.m - 1):
+            lo, hi = row_span(prob, r)
+            if hi - lo < 2:
+                continue
+            ci = B.colind.copy()
+            ci[lo], ci[lo + 1] = ci[lo + 1], ci[lo]  # out of order inside a row
+            expect(P.ERR_INDEX, colind=ci)
+            ci = B.colind.copy()
+            ci[hi - 1] = ci[hi - 2]  # repeated column
+            expect(P.ERR_INDEX, colind=ci)
+        v = B.vals.copy()
+        v[row_span(prob, 3)[0]] = np.inf
+        expect(P.ERR_NONFINITE, vals=v)
+        bb = B.b.copy()
+        bb[prob * B.m + B.m - 1] = np.nan
+        expect(P.ERR_NONFINITE, b=bb)
+        rp = B.rowptr.copy()
+        rp[prob * (B.m + 1) + B.m] -= 1  # last row end != nnz of the problem
+        expect(P.ERR_DIMENSION, rowptr=rp)
+    S.load_batch(B)
+    out = S.solve()
+    assert (out["info"]["status"] == 0).all()
+
+
 def test_batched_config4_slice(P):
     B = g.make_batch(seed=0, start=0, count=2048)
     out, ref = _batched_parity(P, B)
