@@ -196,6 +196,19 @@ NNLS_API nnls_status nnls_setup_batched(nnls_handle** h, int32_t batch, int32_t 
                                const nnls_params* p, void* cuda_stream);
 NNLS_API nnls_status nnls_solve_batched(nnls_handle* h, double* x_out, nnls_info* info_out,
                                uint8_t* mask_out);
+/* nnls_load_batched + nnls_solve_batched as one pipelined call: the batch is
+ * cut into chunks of `chunk` problems (<= 0: 8192); chunk k+1's inputs copy
+ * host->device on one stream and chunk k-1's x_out / mask_out copy back on
+ * another while chunk k is validated and solved on the handle's stream.
+ * Arguments and results as the two calls (inputs host -- pinned for overlap
+ * -- or device; outputs likewise).  A chunk that fails validation is not
+ * solved (a device-side guard) and the call returns the first failing
+ * chunk's status after all chunks finished; outputs are then unspecified.
+ * Returns after the outputs are written (the stream is synchronized). */
+NNLS_API nnls_status nnls_run_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n,
+                             const int64_t* nnz_off, const int32_t* rowptr, const int32_t* colind,
+                             const double* vals, const double* b, double* x_out,
+                             nnls_info* info_out, uint8_t* mask_out, int32_t chunk);
 /* nnls_setup_batched split in two, as nnls_create / nnls_load. */
 NNLS_API nnls_status nnls_create_batched(nnls_handle** h, const nnls_params* p, void* cuda_stream);
 NNLS_API nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n,

@@ -88,6 +88,7 @@ def _load():
         "nnls_create_batched": ([P, P, P], i32),
         "nnls_load_batched": ([P, i32, i32, i32, P, P, P, P, P], i32),
         "nnls_solve_batched": ([P, P, P, P], i32),
+        "nnls_run_batched": ([P, i32, i32, i32, P, P, P, P, P, P, P, P, i32], i32),
         "nnls_step_gram": ([i32, i32, i64, P, P, P, P, P, i32, P, P], i32),
         "nnls_step_normal_solve": ([i32, P, i32, P, i32, P, P, P, P], i32),
         "nnls_step_exchange": ([i32, P, P, P, i32, P, P, P, P], i32),
@@ -309,6 +310,30 @@ class BatchedSolver:
         if want_info:
             out["info"] = {k: np.array([getattr(i, k) for i in infos]) for k, _ in Info._fields_}
         return out
+
+    def run(self, batch, m, n, nnz_off, rowptr, colind, vals, b, x_out=None, mask_out=None,
+            want_info=True, chunk=0, check=True):
+        """load + solve in one pipelined call (nnls_run_batched): chunk k+1's
+        inputs copy in and chunk k-1's x copies out while chunk k solves.
+        Same results as load(...) then solve(...)."""
+        off, rp = _as(nnz_off, np.int64), _as(rowptr, np.int32)
+        ci, v, bb = _as(colind, np.int32), _as(vals, np.float64), _as(b, np.float64)
+        x = x_out if x_out is not None else np.empty(int(batch) * int(n))
+        mk = mask_out if mask_out is not None else (np.empty(int(batch) * int(n), dtype=np.uint8)
+                                                    if want_info else None)
+        infos = (Info * int(batch))() if want_info else None
+        st = lib.nnls_run_batched(self.h, int(batch), int(m), int(n), _ptr(off), _ptr(rp), _ptr(ci), _ptr(v),
+                                  _ptr(bb), _ptr(x), infos, _ptr(mk), int(chunk))
+        if check and st not in (OK, ERR_NOT_PD, ITERATION_LIMIT):
+            raise NNLSError(st, "nnls_run_batched")
+        self.batch, self.m, self.n = int(batch), int(m), int(n)
+        out = dict(x=x, mask=mk, status=st)
+        if want_info:
+            out["info"] = {k: np.array([getattr(i, k) for i in infos]) for k, _ in Info._fields_}
+        return out
+
+    def run_batch(self, B, **kw):
+        return self.run(B.count, B.m, B.n, B.nnz_off, B.rowptr, B.colind, B.vals, B.b, **kw)
 
     def close(self):
         if self.h:

@@ -113,6 +113,9 @@ struct nnls_handle {
   bool batched = false;
   int batch = 0;
   Buf b_nnz_off, b_info_i, b_info_d, b_x, b_mask, b_colview, b_gram;
+  std::vector<int64_t> b_hoff;            // host copy of nnz_off
+  cudaStream_t s_in = nullptr, s_out = nullptr;  // pipelined batched: copy streams
+  std::vector<cudaEvent_t> pev;           // pipelined batched: per-chunk events
 };
 
 namespace {
@@ -855,8 +858,14 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->cursor, &h->tmp_row, &h->tmp_val, &h->Gc, &h->mask, &h->x, &h->y, &h->xF,
                  &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
-                 &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt, &h->b_colview, &h->b_gram};
+                 &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt, &h->b_colview, &h->b_gram,
+                 &h->pos, &h->Fs, &h->xs};
   for (Buf* b : bufs) free_buf(*b);
+  if (h->s_in) cudaStreamSynchronize(h->s_in);
+  if (h->s_out) cudaStreamSynchronize(h->s_out);
+  for (cudaEvent_t e : h->pev) cudaEventDestroy(e);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
   for (cudaEvent_t e : h->tm.pool) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->gstream) cudaStreamDestroy(h->gstream);
@@ -999,22 +1008,25 @@ nnls_status nnls_step_dual(int32_t n, const double* G, int32_t ldg, const double
   return NNLS_OK;
 }
 
-nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n,
-                              const int64_t* nnz_off, const int32_t* rowptr, const int32_t* colind,
-                              const double* vals, const double* b) {
+}  // extern "C"
+
+namespace {
+
+// host checks of the batch shape and nnz offsets, device buffers for the
+// whole batch; h->b_hoff = nnz_off on the host
+nnls_status batched_prepare(nnls_handle* h, int32_t batch, int32_t m, int32_t n, const int64_t* nnz_off,
+                            const int32_t* rowptr, const int32_t* colind, const double* vals,
+                            const double* b) {
   if (!h || !h->batched) return NNLS_ERR_INVALID_ARG;
   if (batch < 1 || n < 1 || m < n || n > 64 || m > 256 || !nnz_off || !rowptr || !b)
     return NNLS_ERR_INVALID_ARG;
-  cudaStream_t s = h->stream;
   h->loaded = false;
   // nnz offsets are needed on the host to size shared memory (nnz_max)
-  int64_t* hoff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(batch + 1));
-  if (!hoff) return NNLS_ERR_OOM;
-  if (cudaMemcpy(hoff, nnz_off, sizeof(int64_t) * (size_t)(batch + 1), cudaMemcpyDefault) !=
-      cudaSuccess) {
-    free(hoff);
+  std::vector<int64_t>& hoff = h->b_hoff;
+  hoff.resize((size_t)batch + 1);
+  if (cudaMemcpy(hoff.data(), nnz_off, sizeof(int64_t) * (size_t)(batch + 1), cudaMemcpyDefault) !=
+      cudaSuccess)
     return NNLS_ERR_CUDA;
-  }
   int64_t nnz_max = 0;
   bool bad = hoff[0] != 0;
   for (int q = 0; q < batch && !bad; ++q) {
@@ -1022,9 +1034,8 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
     if (d < 0 || d > (int64_t)m * n) bad = true;
     if (d > nnz_max) nnz_max = d;
   }
-  const int64_t total = hoff[batch];
-  free(hoff);
   if (bad) return NNLS_ERR_DIMENSION;
+  const int64_t total = hoff[batch];
   if (total > 0 && (!colind || !vals)) return NNLS_ERR_INVALID_ARG;
   if (batched_smem_bytes(m, n, (int)nnz_max) > 220 * 1024) return NNLS_ERR_INVALID_ARG;
   h->m = m;
@@ -1043,6 +1054,84 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
   CK(ensure(h->b_gram, batched_gram_scratch(n, h->sms)));
   CK(ensure(h->b_info_i, sizeof(int32_t) * 8 * (size_t)batch));
   CK(ensure(h->b_info_d, sizeof(double) * 5 * (size_t)batch));
+  return NNLS_OK;
+}
+
+BatchArgs batched_args(nnls_handle* h) {
+  const nnls_params& p = h->prm;
+  BatchArgs a{};
+  a.batch = h->batch;
+  a.m = h->m;
+  a.n = h->n;
+  a.nnz_off = P<int64_t>(h->b_nnz_off);
+  a.rowptr = P<int32_t>(h->rowptr);
+  a.colind = P<int32_t>(h->colind);
+  a.vals = P<double>(h->vals);
+  a.b = P<double>(h->b);
+  a.x_out = P<double>(h->b_x);
+  a.mask_out = P<uint8_t>(h->b_mask);
+  a.info_i = P<int32_t>(h->b_info_i);
+  a.info_d = P<double>(h->b_info_d);
+  a.tol = p.zero_tol;
+  a.atol = p.lsqr_atol;
+  a.btol = p.lsqr_btol;
+  a.conlim = p.lsqr_conlim;
+  a.p_max = p.p_max;
+  a.max_iter = p.max_iter > 0 ? p.max_iter : 10 * h->n;
+  a.lsqr_mode = p.lsqr_mode;
+  a.itn_limit = p.lsqr_itn_limit;
+  a.kkt = p.kkt;
+  a.colview = P<uint8_t>(h->b_colview);
+  a.cv_stride = batched_colview_stride(h->n, h->ldg);
+  a.gram = P<double>(h->b_gram);
+  a.guard = nullptr;
+  return a;
+}
+
+// per-problem info of problems [p0, p0 + count) from the device arrays
+nnls_status batched_info(nnls_handle* h, int p0, int count, nnls_info* info_out, cudaStream_t s) {
+  const size_t nb = (size_t)count;
+  std::vector<int32_t> ii(8 * nb);
+  std::vector<double> dd(5 * nb);
+  CK(cudaMemcpyAsync(ii.data(), P<int32_t>(h->b_info_i) + (size_t)p0 * 8, sizeof(int32_t) * 8 * nb,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(dd.data(), P<double>(h->b_info_d) + (size_t)p0 * 5, sizeof(double) * 5 * nb,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  nnls_status worst = NNLS_OK;
+  for (size_t q = 0; q < nb; ++q) {
+    nnls_info& o = info_out[q];
+    memset(&o, 0, sizeof(o));
+    const int st = ii[q * 8 + 0];
+    o.status = st == 7 ? NNLS_ERR_NOT_PD : (st == 8 ? NNLS_ITERATION_LIMIT : NNLS_OK);
+    if (o.status != NNLS_OK && worst == NNLS_OK) worst = (nnls_status)o.status;
+    o.iterations = ii[q * 8 + 1];
+    o.single_exchanges = ii[q * 8 + 2];
+    o.free_count = ii[q * 8 + 3];
+    o.lsqr_iterations = ii[q * 8 + 4];
+    o.lsqr_stop = ii[q * 8 + 5];
+    o.infeasible_after_lsqr = ii[q * 8 + 6];
+    o.not_pd_column = ii[q * 8 + 7];
+    o.objective = dd[q * 5 + 0];
+    o.kkt_min_x = dd[q * 5 + 1];
+    o.kkt_min_y = dd[q * 5 + 2];
+    o.kkt_max_comp = dd[q * 5 + 3];
+    o.kkt_dot = dd[q * 5 + 4];
+  }
+  return worst;
+}
+
+}  // namespace
+
+extern "C" {
+
+nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n,
+                              const int64_t* nnz_off, const int32_t* rowptr, const int32_t* colind,
+                              const double* vals, const double* b) {
+  nnls_status st = batched_prepare(h, batch, m, n, nnz_off, rowptr, colind, vals, b);
+  if (st != NNLS_OK) return st;
+  cudaStream_t s = h->stream;
+  const int64_t total = h->nnz;
   CK(ensure(h->err, sizeof(int) * 8));
   CK(cudaMemcpyAsync(h->b_nnz_off.p, nnz_off, sizeof(int64_t) * (size_t)(batch + 1), cudaMemcpyDefault, s));
   CK(cudaMemcpyAsync(h->rowptr.p, rowptr, sizeof(int32_t) * (size_t)batch * (m + 1), cudaMemcpyDefault, s));
@@ -1052,18 +1141,13 @@ nnls_status nnls_load_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t 
   }
   CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)batch * m, cudaMemcpyDefault, s));
   CK(cudaMemsetAsync(h->err.p, 0, sizeof(int) * 6, s));
-  TIMED(NNLS_PH_VALIDATE, 2,
-        launch_validate_batched(batch, m, n, total, P<int64_t>(h->b_nnz_off), P<int32_t>(h->rowptr),
+  TIMED(NNLS_PH_VALIDATE, 3,
+        launch_validate_batched(batch, m, n, P<int64_t>(h->b_nnz_off), 0, total, P<int32_t>(h->rowptr),
                                 P<int32_t>(h->colind), P<double>(h->vals), P<double>(h->b),
                                 P<int>(h->err), s));
-  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 6, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (h->h->err[0]) return map_err_bits(h->h->err[0]);
-  {  // a column index repeated or out of order inside some row
-    unsigned long long dcnt[2];
-    memcpy(dcnt, h->h->err + 2, sizeof(dcnt));
-    if (dcnt[0] != dcnt[1]) return NNLS_ERR_INDEX;
-  }
   h->loaded = true;
   return NNLS_OK;
 }
@@ -1094,80 +1178,100 @@ nnls_status nnls_solve_batched(nnls_handle* h, double* x_out, nnls_info* info_ou
   if (!h || !h->batched) return NNLS_ERR_INVALID_ARG;
   if (!h->loaded) return NNLS_ERR_STATE;
   cudaStream_t s = h->stream;
-  const nnls_params& p = h->prm;
-  BatchArgs a{};
-  a.batch = h->batch;
-  a.m = h->m;
-  a.n = h->n;
-  a.nnz_off = P<int64_t>(h->b_nnz_off);
-  a.rowptr = P<int32_t>(h->rowptr);
-  a.colind = P<int32_t>(h->colind);
-  a.vals = P<double>(h->vals);
-  a.b = P<double>(h->b);
-  a.x_out = P<double>(h->b_x);
-  a.mask_out = P<uint8_t>(h->b_mask);
-  a.info_i = P<int32_t>(h->b_info_i);
-  a.info_d = P<double>(h->b_info_d);
-  a.tol = p.zero_tol;
-  a.atol = p.lsqr_atol;
-  a.btol = p.lsqr_btol;
-  a.conlim = p.lsqr_conlim;
-  a.p_max = p.p_max;
-  a.max_iter = p.max_iter > 0 ? p.max_iter : 10 * h->n;
-  a.lsqr_mode = p.lsqr_mode;
-  a.itn_limit = p.lsqr_itn_limit;
-  a.kkt = p.kkt;
-  a.colview = P<uint8_t>(h->b_colview);
-  a.cv_stride = batched_colview_stride(h->n, h->ldg);
-  a.gram = P<double>(h->b_gram);
+  BatchArgs a = batched_args(h);
   TIMED(NNLS_PH_BATCHED, 2, launch_batched_nnz(a, h->ldg, h->sms, s));
   const size_t nb = (size_t)h->batch;
   const int ibd = tm_begin(h);
   if (x_out) CK(cudaMemcpyAsync(x_out, h->b_x.p, sizeof(double) * nb * h->n, cudaMemcpyDefault, s));
   if (mask_out) CK(cudaMemcpyAsync(mask_out, h->b_mask.p, nb * h->n, cudaMemcpyDefault, s));
   tm_end(h, NNLS_PH_DOWNLOAD, ibd, 0);
-  nnls_status worst = NNLS_OK;
-  if (info_out) {
-    int32_t* ii = (int32_t*)malloc(sizeof(int32_t) * 8 * nb);
-    double* dd = (double*)malloc(sizeof(double) * 5 * nb);
-    if (!ii || !dd) {
-      free(ii);
-      free(dd);
-      return NNLS_ERR_OOM;
-    }
-    cudaError_t e1 = cudaMemcpyAsync(ii, h->b_info_i.p, sizeof(int32_t) * 8 * nb, cudaMemcpyDeviceToHost, s);
-    cudaError_t e2 = cudaMemcpyAsync(dd, h->b_info_d.p, sizeof(double) * 5 * nb, cudaMemcpyDeviceToHost, s);
-    cudaError_t e3 = cudaStreamSynchronize(s);
-    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
-      free(ii);
-      free(dd);
-      return NNLS_ERR_CUDA;
-    }
-    for (size_t q = 0; q < nb; ++q) {
-      nnls_info& o = info_out[q];
-      memset(&o, 0, sizeof(o));
-      const int st = ii[q * 8 + 0];
-      o.status = st == 7 ? NNLS_ERR_NOT_PD : (st == 8 ? NNLS_ITERATION_LIMIT : NNLS_OK);
-      if (o.status != NNLS_OK && worst == NNLS_OK) worst = (nnls_status)o.status;
-      o.iterations = ii[q * 8 + 1];
-      o.single_exchanges = ii[q * 8 + 2];
-      o.free_count = ii[q * 8 + 3];
-      o.lsqr_iterations = ii[q * 8 + 4];
-      o.lsqr_stop = ii[q * 8 + 5];
-      o.infeasible_after_lsqr = ii[q * 8 + 6];
-      o.not_pd_column = ii[q * 8 + 7];
-      o.objective = dd[q * 5 + 0];
-      o.kkt_min_x = dd[q * 5 + 1];
-      o.kkt_min_y = dd[q * 5 + 2];
-      o.kkt_max_comp = dd[q * 5 + 3];
-      o.kkt_dot = dd[q * 5 + 4];
-    }
-    free(ii);
-    free(dd);
-  } else {
-    CK(cudaStreamSynchronize(s));
+  if (info_out) return batched_info(h, 0, h->batch, info_out, s);
+  CK(cudaStreamSynchronize(s));
+  return NNLS_OK;
+}
+
+nnls_status nnls_run_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n, const int64_t* nnz_off,
+                             const int32_t* rowptr, const int32_t* colind, const double* vals,
+                             const double* b, double* x_out, nnls_info* info_out, uint8_t* mask_out,
+                             int32_t chunk) {
+  nnls_status st = batched_prepare(h, batch, m, n, nnz_off, rowptr, colind, vals, b);
+  if (st != NNLS_OK) return st;
+  if (chunk <= 0) chunk = 8192;
+  const int nch = (batch + chunk - 1) / chunk;
+  cudaStream_t s = h->stream;
+  if (!h->s_in) CK(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+  if (!h->s_out) CK(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+  while (h->pev.size() < (size_t)(2 * nch + 1)) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->pev.push_back(e);
   }
-  return worst;
+  CK(ensure(h->err, sizeof(int) * 8 * (size_t)nch));
+  const std::vector<int64_t>& off = h->b_hoff;
+  // the copy streams start after everything already queued on the stream
+  // (an earlier call still reading these buffers)
+  cudaEvent_t e0 = h->pev[2 * nch];
+  CK(cudaEventRecord(e0, s));
+  CK(cudaStreamWaitEvent(h->s_in, e0, 0));
+  CK(cudaMemsetAsync(h->err.p, 0, sizeof(int) * 8 * (size_t)nch, s));
+  CK(cudaMemcpyAsync(h->b_nnz_off.p, nnz_off, sizeof(int64_t) * (size_t)(batch + 1), cudaMemcpyDefault,
+                     h->s_in));
+  BatchArgs a0 = batched_args(h);
+  const size_t cvs = a0.cv_stride;
+  for (int c = 0; c < nch; ++c) {
+    const int p0 = c * chunk, p1 = p0 + chunk < batch ? p0 + chunk : batch, cnt = p1 - p0;
+    const int64_t o0 = off[p0], o1 = off[p1];
+    // stage c in: its CSR slice and b
+    CK(cudaMemcpyAsync(P<int32_t>(h->rowptr) + (size_t)p0 * (m + 1), rowptr + (size_t)p0 * (m + 1),
+                       sizeof(int32_t) * (size_t)cnt * (m + 1), cudaMemcpyDefault, h->s_in));
+    if (o1 > o0) {
+      CK(cudaMemcpyAsync(P<int32_t>(h->colind) + o0, colind + o0, sizeof(int32_t) * (size_t)(o1 - o0),
+                         cudaMemcpyDefault, h->s_in));
+      CK(cudaMemcpyAsync(P<double>(h->vals) + o0, vals + o0, sizeof(double) * (size_t)(o1 - o0),
+                         cudaMemcpyDefault, h->s_in));
+    }
+    CK(cudaMemcpyAsync(P<double>(h->b) + (size_t)p0 * m, b + (size_t)p0 * m, sizeof(double) * (size_t)cnt * m,
+                       cudaMemcpyDefault, h->s_in));
+    CK(cudaEventRecord(h->pev[2 * c], h->s_in));
+    // stage c compute: validate, then solve unless validation failed
+    CK(cudaStreamWaitEvent(s, h->pev[2 * c], 0));
+    int* err = P<int>(h->err) + 8 * c;
+    TIMED(NNLS_PH_VALIDATE, 3,
+          launch_validate_batched(cnt, m, n, P<int64_t>(h->b_nnz_off) + p0, o0, o1,
+                                  P<int32_t>(h->rowptr) + (size_t)p0 * (m + 1), P<int32_t>(h->colind),
+                                  P<double>(h->vals), P<double>(h->b) + (size_t)p0 * m, err, s));
+    BatchArgs a = a0;
+    a.batch = cnt;
+    a.nnz_off = a0.nnz_off + p0;
+    a.rowptr = a0.rowptr + (size_t)p0 * (m + 1);
+    a.b = a0.b + (size_t)p0 * m;
+    a.x_out = a0.x_out + (size_t)p0 * n;
+    a.mask_out = a0.mask_out + (size_t)p0 * n;
+    a.info_i = a0.info_i + (size_t)p0 * 8;
+    a.info_d = a0.info_d + (size_t)p0 * 5;
+    a.colview = a0.colview + (size_t)p0 * cvs;
+    a.guard = err;
+    TIMED(NNLS_PH_BATCHED, 2, launch_batched_nnz(a, h->ldg, h->sms, s));
+    CK(cudaEventRecord(h->pev[2 * c + 1], s));
+    // stage c out
+    CK(cudaStreamWaitEvent(h->s_out, h->pev[2 * c + 1], 0));
+    if (x_out)
+      CK(cudaMemcpyAsync(x_out + (size_t)p0 * n, a.x_out, sizeof(double) * (size_t)cnt * n, cudaMemcpyDefault,
+                         h->s_out));
+    if (mask_out)
+      CK(cudaMemcpyAsync(mask_out + (size_t)p0 * n, a.mask_out, (size_t)cnt * n, cudaMemcpyDefault, h->s_out));
+  }
+  // the stream orders after the outputs (the caller's view of completion)
+  CK(cudaEventRecord(h->pev[2 * nch], h->s_out));
+  CK(cudaStreamWaitEvent(s, h->pev[2 * nch], 0));
+  std::vector<int> herr(8 * (size_t)nch);
+  CK(cudaMemcpyAsync(herr.data(), h->err.p, sizeof(int) * 8 * (size_t)nch, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int c = 0; c < nch; ++c)
+    if (herr[8 * c]) return map_err_bits(herr[8 * c]);
+  h->loaded = true;
+  if (info_out) return batched_info(h, 0, batch, info_out, s);
+  return NNLS_OK;
 }
 
 }  // extern "C"

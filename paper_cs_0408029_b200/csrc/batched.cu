@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double tol = a.tol;
 
+  if (a.guard && *(volatile const int*)a.guard) return;  // invalid input (pipelined path)
   for (int prob = blockIdx.x; prob < a.batch; prob += gridDim.x) {
     // ---------------------------------------------------------- load
     const int64_t e0 = a.nnz_off[prob];
@@ -533,6 +534,7 @@ __global__ void __launch_bounds__(BT, 7) batched_lsqr_kernel(BatchArgs a, int nn
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double tol = a.tol;
   __shared__ int s_istop;
+  if (a.guard && *(volatile const int*)a.guard) return;  // invalid input (pipelined path)
   for (int prob = blockIdx.x; prob < a.batch; prob += gridDim.x) {
     const int64_t e0 = a.nnz_off[prob];
     const int nz = (int)(a.nnz_off[prob + 1] - e0);
@@ -849,9 +851,11 @@ cudaError_t batched_debug_set_profile(long long* p) {
 // first entry of a non-empty row, Ds of them (row pass) -> valid iff D == Ds
 // (rows partition each problem's entries once rowptr passes its own checks).
 // cnt[0] = D, cnt[1] = Ds.
-__global__ void validate_entries_kernel(int64_t total, int n, const int32_t* __restrict__ colind,
+__global__ void validate_entries_kernel(int64_t g_begin, int64_t g_end, int n,
+                                        const int32_t* __restrict__ colind,
                                         const double* __restrict__ vals, int* err,
                                         unsigned long long* cnt) {
+  // entries [g_begin, g_end) of the (16-byte aligned) arrays
   __shared__ int s_e;
   __shared__ unsigned s_d;
   if (threadIdx.x == 0) {
@@ -862,16 +866,16 @@ __global__ void validate_entries_kernel(int64_t total, int n, const int32_t* __r
   const int lane = threadIdx.x & 31;
   int e_local = 0;
   unsigned d_local = 0;
-  // 4 consecutive entries per thread (16-byte colind, 2 x 16-byte vals
+  // aligned quads of 4 entries per thread (16-byte colind, 2 x 16-byte vals
   // loads); whole warps iterate together (the shuffle below)
-  const int64_t q4 = (total + 3) / 4;
+  const int64_t qa = g_begin / 4, qb = (g_end + 3) / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t span = (q4 + 31) / 32 * 32;
+  const int64_t span = (qb - qa + 31) / 32 * 32;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < span; q += stride) {
-    const int64_t g0 = 4 * q;
+    const int64_t g0 = 4 * (qa + q);
     int c[4];
     double v[4];
-    if (g0 + 3 < total) {
+    if (g0 >= g_begin && g0 + 3 < g_end) {
       const int4 c4 = *reinterpret_cast<const int4*>(colind + g0);
       const double2 v0 = *reinterpret_cast<const double2*>(vals + g0);
       const double2 v1 = *reinterpret_cast<const double2*>(vals + g0 + 2);
@@ -880,19 +884,20 @@ __global__ void validate_entries_kernel(int64_t total, int n, const int32_t* __r
     } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        c[k] = g0 + k < total ? colind[g0 + k] : 0;
-        v[k] = g0 + k < total ? vals[g0 + k] : 0.0;
+        const bool in = g0 + k >= g_begin && g0 + k < g_end;
+        c[k] = in ? colind[g0 + k] : 0;
+        v[k] = in ? vals[g0 + k] : 0.0;
       }
     }
     int prev = __shfl_up_sync(kFull, c[3], 1);
-    if (lane == 0 && g0 > 0 && g0 < total) prev = colind[g0 - 1];
+    if (lane == 0 && g0 > g_begin && g0 <= g_end) prev = colind[g0 - 1];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t gk = g0 + k;
-      if (gk < total) {
+      if (gk >= g_begin && gk < g_end) {
         if (c[k] < 0 || c[k] >= n) e_local |= 2;
         if (!isfinite(v[k])) e_local |= 4;
-        if (gk > 0 && c[k] <= (k ? c[k - 1] : prev)) ++d_local;
+        if (gk > g_begin && c[k] <= (k ? c[k - 1] : prev)) ++d_local;
       }
     }
   }
@@ -910,7 +915,7 @@ __global__ void validate_rows_kernel(int batch, int m, const int64_t* __restrict
                                      const int32_t* __restrict__ rowptr,
                                      const int32_t* __restrict__ colind,
                                      const double* __restrict__ b, int* err,
-                                     unsigned long long* cnt) {
+                                     unsigned long long* cnt, int64_t g_begin) {
   __shared__ int s_e;
   __shared__ unsigned s_d;
   if (threadIdx.x == 0) {
@@ -938,7 +943,7 @@ __global__ void validate_rows_kernel(int batch, int m, const int64_t* __restrict
       continue;
     }
     const int64_t g = base + lo;
-    if (hi > lo && g > 0 && colind[g] <= colind[g - 1]) ++d_local;
+    if (hi > lo && g > g_begin && colind[g] <= colind[g - 1]) ++d_local;
   }
   d_local = warp_sum_i((int)d_local);
   if (e_local) atomicOr(&s_e, e_local);
@@ -950,22 +955,32 @@ __global__ void validate_rows_kernel(int batch, int m, const int64_t* __restrict
   }
 }
 
-cudaError_t launch_validate_batched(int batch, int m, int n, int64_t total, const int64_t* nnz_off,
-                                    const int32_t* rowptr, const int32_t* colind,
+__global__ void validate_finalize_kernel(int* err) {
+  const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(err + 2);
+  if (cnt[0] != cnt[1]) err[0] |= 2;
+}
+
+cudaError_t launch_validate_batched(int batch, int m, int n, const int64_t* nnz_off, int64_t g_begin,
+                                    int64_t g_end, const int32_t* rowptr, const int32_t* colind,
                                     const double* vals, const double* b, int* err, cudaStream_t s) {
   // err[0] bits, err[2..5] the two 64-bit descent counts (zeroed by the caller)
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(err + 2);
-  int blocks = (int)((total / 4 + 255) / 256);
+  const int64_t quads = (g_end + 3) / 4 - g_begin / 4;
+  int blocks = (int)((quads + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  if (total > 0) validate_entries_kernel<<<blocks, 256, 0, s>>>(total, n, colind, vals, err, cnt);
+  if (g_end > g_begin)
+    validate_entries_kernel<<<blocks, 256, 0, s>>>(g_begin, g_end, n, colind, vals, err, cnt);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t rows = (int64_t)batch * m;
   blocks = (int)((rows + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  validate_rows_kernel<<<blocks, 256, 0, s>>>(batch, m, nnz_off, rowptr, colind, b, err, cnt);
+  validate_rows_kernel<<<blocks, 256, 0, s>>>(batch, m, nnz_off, rowptr, colind, b, err, cnt, g_begin);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  validate_finalize_kernel<<<1, 1, 0, s>>>(err);
   return cudaGetLastError();
 }
 

@@ -135,14 +135,18 @@ struct BatchArgs {
   uint8_t* colview;  // scratch: per problem the column view (batched_colview_stride bytes)
   size_t cv_stride;
   double* gram;      // scratch: one packed Gram per CTA (batched_gram_scratch bytes)
+  const int* guard;  // non-null: skip the whole launch when *guard != 0 (validation failed)
 };
 size_t batched_colview_stride(int n, int nnz_max);
 size_t batched_gram_scratch(int n, int sm_count);
 size_t batched_smem_bytes(int m, int n, int nnz_max);
-// err: 6 ints, zeroed: [0] error bits, [2..5] descent counts (the caller
-// reports an index error when the two 64-bit counts differ)
-cudaError_t launch_validate_batched(int batch, int m, int n, int64_t total, const int64_t* nnz_off,
-                                    const int32_t* rowptr, const int32_t* colind,
+// err: 6 ints, zeroed: [0] error bits (an out-of-order / repeated column
+// inside a row sets bit 2 via the [2..5] descent counts).  The problems of
+// this slice: nnz_off / rowptr / b at its first problem; its entries are
+// [g_begin, g_end) of colind / vals (absolute offsets; the pipelined path
+// validates chunks).
+cudaError_t launch_validate_batched(int batch, int m, int n, const int64_t* nnz_off, int64_t g_begin,
+                                    int64_t g_end, const int32_t* rowptr, const int32_t* colind,
                                     const double* vals, const double* b, int* err, cudaStream_t s);
 cudaError_t launch_batched_nnz(const BatchArgs& a, int nnz_max, int sm_count, cudaStream_t s);
 cudaError_t batched_debug_set_profile(long long* p);

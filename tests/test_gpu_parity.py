@@ -406,6 +406,49 @@ def test_batched_invalid_inputs(P):
     assert (out["info"]["status"] == 0).all()
 
 
+@pytest.mark.parametrize("chunk", [1, 7, 100, 0])
+def test_batched_pipelined_run_matches_load_solve(P, chunk):
+    """nnls_run_batched (chunked copy/compute pipeline) gives the bits of
+    load + solve, pinned or pageable host buffers alike."""
+    B = g.make_batch(seed=6, start=0, count=300)
+    ref = P.BatchedSolver().load_batch(B).solve()
+    S = P.BatchedSolver()
+    for pinned in (False, True):
+        arrs = [B.nnz_off, B.rowptr, B.colind, B.vals, B.b]
+        if pinned:
+            arrs = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrs]
+        x = torch.empty(B.count * B.n, dtype=torch.float64).pin_memory() if pinned else None
+        out = S.run(B.count, B.m, B.n, *arrs, x_out=x, chunk=chunk)
+        xo = out["x"].numpy() if pinned else out["x"]
+        assert np.array_equal(xo, ref["x"])
+        assert np.array_equal(out["mask"], ref["mask"])
+        for k in ref["info"]:
+            assert np.array_equal(out["info"][k], ref["info"][k], equal_nan=True), k
+    # the handle is loaded afterwards: a plain solve repeats the result
+    again = S.solve()
+    assert np.array_equal(again["x"], ref["x"])
+
+
+def test_batched_pipelined_run_invalid_chunk(P):
+    """A corrupt problem in a middle chunk: the call reports it, the other
+    chunks still run, and the handle works for the next batch."""
+    B = g.make_batch(seed=7, start=0, count=64)
+    S = P.BatchedSolver()
+    ci = B.colind.copy()
+    ci[int(B.nnz_off[40]) + 5] = -1
+    with pytest.raises(P.NNLSError) as e:
+        S.run(B.count, B.m, B.n, B.nnz_off, B.rowptr, ci, B.vals, B.b, chunk=16)
+    assert e.value.status == P.ERR_INDEX
+    v = B.vals.copy()
+    v[int(B.nnz_off[63]) + 1] = np.nan
+    with pytest.raises(P.NNLSError) as e:
+        S.run(B.count, B.m, B.n, B.nnz_off, B.rowptr, B.colind, v, B.b, chunk=16)
+    assert e.value.status == P.ERR_NONFINITE
+    out = S.run_batch(B, chunk=16)
+    ref = O.solve_batched(B, O.default_params(), threads=0)
+    assert np.array_equal(out["mask"].reshape(B.count, B.n), ref["mask"])
+
+
 def test_batched_config4_slice(P):
     B = g.make_batch(seed=0, start=0, count=2048)
     out, ref = _batched_parity(P, B)
