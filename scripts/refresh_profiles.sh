@@ -22,4 +22,9 @@ done
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:chol_factor_kernel -c 1 \
   -o $O/full_c2_chol_factor_kernel -f python bench.py --config 2 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e \
   > $O/ncu_full_c2.log 2>&1
+for k in batched_kernel batched_lsqr_kernel; do
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$k" --launch-skip 1 -c 1 \
+    -o $O/full_c4_$k -f python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
+    > $O/ncu_full_c4_$k.log 2>&1
+done
 echo done
