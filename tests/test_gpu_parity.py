@@ -449,6 +449,18 @@ def test_batched_pipelined_run_invalid_chunk(P):
     assert np.array_equal(out["mask"].reshape(B.count, B.n), ref["mask"])
 
 
+@pytest.mark.parametrize("m,n,density,count", [(256, 64, 0.2, 64), (64, 64, 0.3, 64), (10, 1, 0.5, 33),
+                                               (33, 17, 0.25, 100), (200, 40, 0.05, 50)])
+def test_batched_shapes(P, m, n, density, count):
+    """Batched limits and odd shapes (m = n, n = 1, m at its 256 cap, very
+    sparse rows incl. empty ones): parity with the oracle, through both the
+    load + solve path and the pipelined run."""
+    B = g.make_batch(seed=8, start=0, count=count, m=m, n=n, density=density, total=count)
+    out, ref = _batched_parity(P, B)
+    run = P.BatchedSolver().run_batch(B, chunk=16)
+    assert np.array_equal(run["x"], out["x"]) and np.array_equal(run["mask"], out["mask"])
+
+
 def test_batched_config4_slice(P):
     B = g.make_batch(seed=0, start=0, count=2048)
     out, ref = _batched_parity(P, B)
