@@ -474,9 +474,9 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
 // a10 LSQR on the final F and a11 report, one problem per 128-thread
 // CTA: CSR, the column view and the vectors only (~25 KB at config 4).
 struct LLay {
-  int orv, ob, ou, ox, ov, ow, oX, ored;  // double offsets
+  int orv, ou, ov, ow, oX, ored;  // double offsets (b and the NE x stay in global memory)
   int doubles;
-  int irp, ico, imk, ici, icr, icx, irf, ifb, ifl;
+  int irp, ico, imk, ici, icr, icx, irf, ifl;
   int ints;
   size_t bytes;
 };
@@ -484,13 +484,11 @@ __host__ __device__ inline LLay llayout(int m, int n, int nnz_max) {
   LLay L;
   int o = 0;
   L.orv = o; o += nnz_max;
-  L.ob = o; o += m;
-  L.ou = o; o += m;
-  L.ox = o; o += n;
+  L.ou = o; o += m;                 // (during the load: the rows' F-entry bits, u64)
   L.ov = o; o += n;
   L.ow = o; o += n;
   L.oX = o; o += n;
-  L.ored = o; o += 64;
+  L.ored = o; o += 32;
   L.doubles = o;
   int q = 0;
   L.irp = q; q += m + 1;
@@ -500,23 +498,19 @@ __host__ __device__ inline LLay llayout(int m, int n, int nnz_max) {
   L.icr = q; q += (nnz_max + 1) / 2;
   L.icx = q; q += (nnz_max + 1) / 2;
   L.irf = q; q += m + 1;            // row r's F entries: [rp[r], rpF[r])
-  q = (q + 1) & ~1;
-  L.ifb = q; q += 2 * m;            // row r's F-entry bits (u64)
   L.ifl = q; q += n + 1;            // F columns in index order (compacted)
   L.ints = q + 8;
   L.bytes = sizeof(double) * (size_t)L.doubles + sizeof(int) * (size_t)L.ints;
   return L;
 }
 
-__global__ void __launch_bounds__(BT, 7) batched_lsqr_kernel(BatchArgs a, int nnz_max) {
+__global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nnz_max) {
   long long bp_t = clock64();
   extern __shared__ double sm[];
   const int m = a.m, n = a.n;
   const LLay Ly = llayout(m, n, nnz_max);
   double* rv = sm + Ly.orv;
-  double* bb = sm + Ly.ob;
   double* u = sm + Ly.ou;
-  double* x = sm + Ly.ox;
   double* v = sm + Ly.ov;
   double* w = sm + Ly.ow;
   double* X = sm + Ly.oX;
@@ -529,7 +523,7 @@ __global__ void __launch_bounds__(BT, 7) batched_lsqr_kernel(BatchArgs a, int nn
   uint16_t* crow = reinterpret_cast<uint16_t*>(ib + Ly.icr);
   uint16_t* cpos = reinterpret_cast<uint16_t*>(ib + Ly.icx);
   int* rpF = ib + Ly.irf;
-  unsigned long long* fb = reinterpret_cast<unsigned long long*>(ib + Ly.ifb);
+  unsigned long long* fb = reinterpret_cast<unsigned long long*>(u);  // load phase only
   int* fl = ib + Ly.ifl;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double tol = a.tol;
@@ -541,10 +535,10 @@ __global__ void __launch_bounds__(BT, 7) batched_lsqr_kernel(BatchArgs a, int nn
     const int status = a.info_i[(size_t)prob * 8 + 0];
     const int f = a.info_i[(size_t)prob * 8 + 3];
     for (int r = tid; r <= m; r += BT) rp[r] = a.rowptr[(size_t)prob * (m + 1) + r];
-    for (int r = tid; r < m; r += BT) bb[r] = a.b[(size_t)prob * m + r];
+    const double* bb = a.b + (size_t)prob * m;       // b (global, read twice)
+    const double* x = a.x_out + (size_t)prob * n;    // the NE x (global; overwritten by the output below)
     for (int j = tid; j < n; j += BT) {
       mk[j] = a.mask_out[(size_t)prob * n + j];
-      x[j] = a.x_out[(size_t)prob * n + j];
       v[j] = 0.0;
       X[j] = 0.0;
     }
