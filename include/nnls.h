@@ -103,6 +103,11 @@ typedef struct {
   int32_t f;          /* |F| after the exchange                            */
   double below_tol;   /* largest |v| < zero_tol over x_F, y_G before zeroing (0 if none) */
   double above_tol;   /* smallest |v| >= zero_tol over x_F, y_G (inf if none) */
+  int32_t kept;       /* leading rows/columns of the previous iteration's
+                         Cholesky factor reused unchanged by this one (factor
+                         reuse, reading c22; 0 = full factorization).
+                         Implementation record, not part of the paper's state */
+  int32_t pad;
 } nnls_iter_rec;
 
 typedef struct nnls_handle nnls_handle;
@@ -157,28 +162,50 @@ NNLS_API nnls_status nnls_get_gram(nnls_handle* h, double* G_out, double* c_out)
 NNLS_API nnls_status nnls_destroy(nnls_handle* h);
 
 /* ---------------------------------------------------------------------------
- * Row-sharded Gram (config 2 across GPUs, BASELINE north_star): like
- * nnls_setup (the full A and b are given, validated and kept for the final
- * LSQR/KKT), but G and c are formed only from rows [row_begin, row_end): the
- * partial sums G_r = A_r^T A_r, c_r = A_r^T b_r of this rank's row block.
- * The caller all-reduces (SUM, float64) the contiguous device buffer returned
- * by nnls_gram_buffer -- G (n rows of stride *ld) followed by c (n) --
- * through torch.distributed / NCCL, then calls nnls_gram_finalize; after that
- * nnls_solve runs on the full Gram.  With quantized inputs every partial sum
- * is exact, so the reduced Gram is bitwise identical for any rank count.
- * nnls_solve before nnls_gram_finalize returns NNLS_ERR_STATE.
+ * Row-sharded Gram (config 2 across GPUs, BASELINE north_star; "A^T A
+ * ... is computed once": the one step of the method that shards).  The Gram
+ * is a sum over rows, G = sum_r a_r a_r^T, c = sum_r a_r b_r, so rank k forms
+ * the partial sums of its row block and the ranks SUM them with one
+ * collective through torch.distributed / NCCL (a reduce to the root, or an
+ * all-reduce); only the root runs the pivot loop.
+ *
+ *   root:      nnls_setup_shard / nnls_load_shard with the FULL A and b (kept
+ *              for the final LSQR and the report) and its own row range
+ *              [row_begin, row_end);
+ *   non-root:  nnls_create + nnls_load_block with ONLY its row block (local
+ *              CSR of m_block rows, its slice of b; m_block < n allowed);
+ *   all:       reduce (SUM, float64) the device buffer of nnls_gram_buffer;
+ *   root:      nnls_gram_finalize, then nnls_solve.
+ *
+ * The buffer is the PACKED lower triangle (row i = G[i][0..i] at offset
+ * i(i+1)/2) followed by c (n): n(n+1)/2 + n doubles, half the bytes of the
+ * square.  With quantized (exact-sum) inputs the reduced Gram is bitwise
+ * identical for any rank count.  nnls_solve before nnls_gram_finalize, and
+ * finalize/solve on a block-only handle, return NNLS_ERR_STATE.
  */
 NNLS_API nnls_status nnls_setup_shard(nnls_handle** h, int32_t m, int32_t n, int64_t nnz,
                              const int32_t* rowptr, const int32_t* colind, const double* vals,
                              const double* b, int32_t row_begin, int32_t row_end,
                              const nnls_params* p, void* cuda_stream);
-/* Reload a (new) problem into a handle as a row shard (as nnls_load, Gram
- * over rows [row_begin, row_end) only; finalize required again). */
+/* Reload a (new) problem into a handle as the shard root (as nnls_load, the
+ * partial Gram over rows [row_begin, row_end) only; finalize required again). */
 NNLS_API nnls_status nnls_load_shard(nnls_handle* h, int32_t m, int32_t n, int64_t nnz,
                                      const int32_t* rowptr, const int32_t* colind,
                                      const double* vals, const double* b, int32_t row_begin,
                                      int32_t row_end);
-NNLS_API nnls_status nnls_gram_buffer(nnls_handle* h, double** dev_ptr, size_t* count, int32_t* ld);
+/* A non-root rank's row block: CSR of m_block rows (rowptr local, starting
+ * at 0), b_block[m_block]; validated like nnls_load (same error codes), then
+ * its packed partial Gram is formed.  The handle can only serve
+ * nnls_gram_buffer afterwards. */
+NNLS_API nnls_status nnls_load_block(nnls_handle* h, int32_t m_block, int32_t n, int64_t nnz,
+                                     const int32_t* rowptr, const int32_t* colind,
+                                     const double* vals, const double* b_block);
+/* Device pointer and element count (n(n+1)/2 + n) of the packed [G | c]
+ * partial of a shard or block handle (owned by the handle; valid until the
+ * next load or destroy). */
+NNLS_API nnls_status nnls_gram_buffer(nnls_handle* h, double** dev_ptr, size_t* count);
+/* Root only, after the reduction: expands the packed sum into the full
+ * symmetric Gram the pivot loop reads (stream-ordered). */
 NNLS_API nnls_status nnls_gram_finalize(nnls_handle* h);
 
 /* ---------------------------------------------------------------------------

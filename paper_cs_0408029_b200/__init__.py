@@ -57,7 +57,8 @@ class Info(C.Structure):
 
 class IterRec(C.Structure):
     _fields_ = [("iter", C.c_int32), ("k", C.c_int32), ("branch", C.c_int32), ("f", C.c_int32),
-                ("below_tol", C.c_double), ("above_tol", C.c_double)]
+                ("below_tol", C.c_double), ("above_tol", C.c_double), ("kept", C.c_int32),
+                ("pad", C.c_int32)]
 
 
 def _load():
@@ -81,7 +82,8 @@ def _load():
         "nnls_get_gram": ([P, P, P], i32),
         "nnls_destroy": ([P], i32),
         "nnls_setup_shard": ([P, i32, i32, i64, P, P, P, P, i32, i32, P, P], i32),
-        "nnls_gram_buffer": ([P, P, P, P], i32),
+        "nnls_gram_buffer": ([P, P, P], i32),
+        "nnls_load_block": ([P, i32, i32, i64, P, P, P, P], i32),
         "nnls_load_shard": ([P, i32, i32, i64, P, P, P, P, i32, i32], i32),
         "nnls_gram_finalize": ([P], i32),
         "nnls_setup_batched": ([P, i32, i32, i32, P, P, P, P, P, P, P], i32),
@@ -211,7 +213,7 @@ class Solver:
         cnt = C.c_int32()
         _check(lib.nnls_get_trace(self.h, recs, cap, C.byref(cnt)), "nnls_get_trace")
         return [dict(iter=r.iter, k=r.k, branch=r.branch, f=r.f, below_tol=r.below_tol,
-                     above_tol=r.above_tol) for r in recs[:cnt.value]]
+                     above_tol=r.above_tol, kept=r.kept) for r in recs[:cnt.value]]
 
     def gram(self):
         G = np.empty((self.n, self.n))
@@ -248,8 +250,10 @@ def setup(prob, params: Params | None = None, stream=None, **kw) -> Solver:
 
 
 class ShardSolver(Solver):
-    """Row-sharded Gram: partial A_R^T A_R, c_R on this rank; all-reduce the
-    buffer from gram_buffer() (torch.distributed), then finalize()."""
+    """Row-sharded Gram, shard ROOT (include/nnls.h): holds the full A and b,
+    forms the packed partial Gram of its own rows [row_begin, row_end); after
+    the ranks' reduction (paper_cs_0408029_b200.dist.reduce_gram) finalize()
+    expands it and solve() runs the pivot loop."""
 
     def __init__(self, m, n, rowptr, colind, vals, b, row_begin, row_end, params=None, stream=None, **kw):
         self.params = params if params is not None else default_params(**kw)
@@ -268,13 +272,28 @@ class ShardSolver(Solver):
         return self
 
     def gram_buffer(self):
-        """(device pointer, element count, row stride) of [G | c]."""
-        p, cnt, ld = C.c_void_p(), C.c_size_t(), C.c_int32()
-        _check(lib.nnls_gram_buffer(self.h, C.byref(p), C.byref(cnt), C.byref(ld)), "nnls_gram_buffer")
-        return p.value, cnt.value, ld.value
+        """(device pointer, element count) of the packed [G lower | c] partial."""
+        p, cnt = C.c_void_p(), C.c_size_t()
+        _check(lib.nnls_gram_buffer(self.h, C.byref(p), C.byref(cnt)), "nnls_gram_buffer")
+        return p.value, cnt.value
 
     def finalize(self):
         _check(lib.nnls_gram_finalize(self.h), "nnls_gram_finalize")
+
+
+class BlockSolver(Solver):
+    """Row-sharded Gram, NON-ROOT rank: only its row block (local CSR of
+    m_block rows and b_block) is uploaded; it contributes the packed partial
+    Gram to the reduction and never solves."""
+
+    def load_block(self, m_block, n, rowptr, colind, vals, b_block):
+        rp, ci, v, bb = _as(rowptr, np.int32), _as(colind, np.int32), _as(vals, np.float64), _as(b_block, np.float64)
+        _check(lib.nnls_load_block(self.h, int(m_block), int(n), int(ci.shape[0]), _ptr(rp), _ptr(ci), _ptr(v),
+                                   _ptr(bb)), "nnls_load_block")
+        self.m, self.n = int(m_block), int(n)
+        return self
+
+    gram_buffer = ShardSolver.gram_buffer
 
 
 class BatchedSolver:

@@ -93,6 +93,8 @@ struct nnls_handle {
   Buf rowptr, colind, vals, b;           // CSR + rhs
   Buf colptr, rowind, cvals, cursor, tmp_row, tmp_val;  // CSC
   Buf Gc;                                 // G (n x ldg) followed by c (n)
+  Buf Gp;                                 // row-shard partial: packed lower G (n(n+1)/2) then c (n)
+  int shard = 0;                          // 0 whole problem, 1 shard root (full A), 2 row block only
   Buf mask, x, y, xF, Fidx, Gidx;         // pivot state
   Buf pos, Fs, xs;                        // factor reuse: order positions, F sorted, x_F by index
   Buf Lt, flags;                          // Cholesky tiles + DAG flags
@@ -193,9 +195,13 @@ nnls_status map_err_bits(int e) {
 }
 
 // upload + validate + CSC + Gram over rows [r0, r1)
+// shard: 0 whole problem (full Gram); 1 shard root (full A kept for the
+// loop and LSQR, packed partial Gram over rows [r0, r1)); 2 a row block only
+// (packed partial Gram over all its rows; m < n allowed; cannot solve)
 nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const int32_t* rowptr,
-                      const int32_t* colind, const double* vals, const double* b, int r0, int r1) {
-  if (!h || m < 1 || n < 1 || m < n || nnz < 0 || !rowptr || !b) return NNLS_ERR_INVALID_ARG;
+                      const int32_t* colind, const double* vals, const double* b, int r0, int r1,
+                      int shard = 0) {
+  if (!h || m < 1 || n < 1 || (m < n && shard != 2) || nnz < 0 || !rowptr || !b) return NNLS_ERR_INVALID_ARG;
   if (nnz > 0 && (!colind || !vals)) return NNLS_ERR_INVALID_ARG;
   if (nnz > 0x7fffffffLL) return NNLS_ERR_INVALID_ARG;
   if ((int64_t)n * 8 > 200 * 1024) return NNLS_ERR_INVALID_ARG;  // Gram row accumulator in smem
@@ -207,6 +213,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   h->ldg = round_up(n, 4);
   h->gram_ready = false;
   h->loaded = false;
+  h->shard = shard;
   CK(ensure(h->rowptr, sizeof(int32_t) * (size_t)(m + 1)));
   CK(ensure(h->colind, sizeof(int32_t) * (size_t)nnz));
   CK(ensure(h->vals, sizeof(double) * (size_t)nnz));
@@ -284,10 +291,17 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
                         h->h->err[2]));
   double* G = P<double>(h->Gc);
   double* c = G + (size_t)n * h->ldg;
+  int ldg = h->ldg;
+  if (shard != 0) {  // packed partial [P | c]: what the ranks reduce (half the bytes of the square)
+    CK(ensure(h->Gp, sizeof(double) * ((size_t)n * (n + 1) / 2 + n)));
+    G = P<double>(h->Gp);
+    c = G + (size_t)n * (n + 1) / 2;
+    ldg = 0;
+  }
   TIMED(NNLS_PH_GRAM, 1,
         launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                     P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                    P<double>(h->b), r0, r1, G, h->ldg, c, h->sms, s, gram_is_exact(h->h->err) && !h->no_exact_gram,
+                    P<double>(h->b), r0, r1, G, ldg, c, h->sms, s, gram_is_exact(h->h->err) && !h->no_exact_gram,
                     gram_exact_lmin(h->h->err)));
   h->loaded = true;
   return NNLS_OK;
@@ -418,7 +432,7 @@ nnls_status nnls_setup_shard(nnls_handle** h, int32_t m, int32_t n, int64_t nnz,
                              const nnls_params* p, void* cuda_stream) {
   nnls_status s = create_impl(h, p, cuda_stream);
   if (s != NNLS_OK) return s;
-  s = load_impl(*h, m, n, nnz, rowptr, colind, vals, b, row_begin, row_end);
+  s = load_impl(*h, m, n, nnz, rowptr, colind, vals, b, row_begin, row_end, 1);
   if (s != NNLS_OK) {
     nnls_destroy(*h);
     *h = nullptr;
@@ -430,19 +444,32 @@ nnls_status nnls_load_shard(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, c
                             const int32_t* colind, const double* vals, const double* b,
                             int32_t row_begin, int32_t row_end) {
   if (!h || h->batched) return NNLS_ERR_INVALID_ARG;
-  return load_impl(h, m, n, nnz, rowptr, colind, vals, b, row_begin, row_end);
+  return load_impl(h, m, n, nnz, rowptr, colind, vals, b, row_begin, row_end, 1);
 }
 
-nnls_status nnls_gram_buffer(nnls_handle* h, double** dev_ptr, size_t* count, int32_t* ld) {
-  if (!h || !h->loaded || h->batched) return NNLS_ERR_STATE;
-  if (dev_ptr) *dev_ptr = P<double>(h->Gc);
-  if (count) *count = (size_t)h->n * h->ldg + h->n;
-  if (ld) *ld = h->ldg;
+nnls_status nnls_load_block(nnls_handle* h, int32_t m_block, int32_t n, int64_t nnz, const int32_t* rowptr,
+                            const int32_t* colind, const double* vals, const double* b) {
+  if (!h || h->batched) return NNLS_ERR_INVALID_ARG;
+  return load_impl(h, m_block, n, nnz, rowptr, colind, vals, b, 0, m_block, 2);
+}
+
+nnls_status nnls_gram_buffer(nnls_handle* h, double** dev_ptr, size_t* count) {
+  if (!h || !h->loaded || h->batched || h->shard == 0) return NNLS_ERR_STATE;
+  if (dev_ptr) *dev_ptr = P<double>(h->Gp);
+  if (count) *count = (size_t)h->n * (h->n + 1) / 2 + h->n;
   return NNLS_OK;
 }
 
 nnls_status nnls_gram_finalize(nnls_handle* h) {
-  if (!h || !h->loaded || h->batched) return NNLS_ERR_STATE;
+  if (!h || !h->loaded || h->batched || h->shard != 1) return NNLS_ERR_STATE;
+  const int n = h->n;
+  const double* Pk = P<double>(h->Gp);
+  double* G = P<double>(h->Gc);
+  int ib = tm_begin(h);
+  CK(launch_gram_unpack(n, Pk, G, h->ldg, h->sms, h->stream));
+  CK(cudaMemcpyAsync(G + (size_t)n * h->ldg, Pk + (size_t)n * (n + 1) / 2, sizeof(double) * (size_t)n,
+                     cudaMemcpyDeviceToDevice, h->stream));
+  tm_end(h, NNLS_PH_GRAM, ib, 1);
   h->gram_ready = true;
   return NNLS_OK;
 }
@@ -859,7 +886,7 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
                  &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt, &h->b_colview, &h->b_gram,
-                 &h->pos, &h->Fs, &h->xs};
+                 &h->pos, &h->Fs, &h->xs, &h->Gp};
   for (Buf* b : bufs) free_buf(*b);
   if (h->s_in) cudaStreamSynchronize(h->s_in);
   if (h->s_out) cudaStreamSynchronize(h->s_out);

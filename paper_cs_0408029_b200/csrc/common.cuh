@@ -39,6 +39,8 @@ struct DevState {
 struct TraceRec {
   int32_t iter, k, branch, f;
   double below_tol, above_tol;
+  int32_t kept;   // leading columns of the previous factor reused (0: full factorization)
+  int32_t pad;
 };
 
 NNLS_DEV double warp_sum(double v) {

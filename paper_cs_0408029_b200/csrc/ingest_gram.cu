@@ -375,9 +375,12 @@ __global__ void __launch_bounds__(256) gram_kernel(
       }
     }
     if (lane == 0 && j0 == 0) c[i] = ci;
-    double* Gi = G + (size_t)i * ldg + j0;
+    // ldg > 0: full row i (stride ldg); ldg <= 0: packed lower triangle, row
+    // i = entries j <= i at offset i(i+1)/2 (the row-shard all-reduce buffer)
+    double* Gi = (ldg > 0 ? G + (size_t)i * ldg : G + (size_t)i * (i + 1) / 2) + j0;
+    const int jst = ldg > 0 ? jw : max(0, min(jw, i + 1 - j0));
     for (int j = lane; j < jw; j += 32) {
-      Gi[j] = acc[j];
+      if (j < jst) Gi[j] = acc[j];
       acc[j] = 0.0;
     }
     __syncwarp();
@@ -492,11 +495,52 @@ __global__ void __launch_bounds__(512) gram_exact_kernel(
       }
     }
     __syncthreads();
-    double* Gi = G + (size_t)i * ldg;
-    for (int j = tid; j < n; j += nt)
+    double* Gi = ldg > 0 ? G + (size_t)i * ldg : G + (size_t)i * (i + 1) / 2;  // (packed: j <= i)
+    const int jn = ldg > 0 ? n : i + 1;
+    for (int j = tid; j < jn; j += nt)
       Gi[j] = (double)(long long)(((unsigned long long)(unsigned)acc_hi[j] << 32) | acc_lo[j]) * inv_scale;
     __syncthreads();
   }
+}
+
+// Packed lower triangle (row i at offset i(i+1)/2, j <= i) -> full symmetric
+// n x ldg matrix.  32 x 32 blocks (bi >= bj) through shared memory so both the
+// lower block (row copy) and its mirror (transposed) are written coalesced.
+__global__ void __launch_bounds__(256) gram_unpack_kernel(int n, const double* __restrict__ P,
+                                                          double* __restrict__ G, int ldg) {
+  __shared__ double t[32][33];
+  const int nb = (n + 31) / 32;
+  const long long nblk = (long long)nb * (nb + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 row groups
+  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    // blk -> (bi, bj), bj <= bi, row-major over the lower block triangle
+    int bi = (int)((sqrt(8.0 * (double)blk + 1.0) - 1.0) * 0.5);
+    while ((long long)bi * (bi + 1) / 2 > blk) --bi;
+    while ((long long)(bi + 1) * (bi + 2) / 2 <= blk) ++bi;
+    const int bj = (int)(blk - (long long)bi * (bi + 1) / 2);
+    for (int r = ty; r < 32; r += 8) {
+      const int i = 32 * bi + r, j = 32 * bj + tx;
+      double v = 0.0;
+      if (i < n && j <= i) v = P[(size_t)i * (i + 1) / 2 + j];
+      t[r][tx] = v;
+      if (i < n && j < n && (bi != bj || j <= i)) G[(size_t)i * ldg + j] = v;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {  // mirror: G[j][i] = P(i, j) for the block's j rows
+      const int j = 32 * bj + r, i = 32 * bi + tx;
+      if (j < n && i < n && (bi != bj || i > j)) G[(size_t)j * ldg + i] = t[tx][r];
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_gram_unpack(int n, const double* P, double* G, int ldg, int sm_count, cudaStream_t s) {
+  const int nb = (n + 31) / 32;
+  long long blocks = (long long)nb * (nb + 1) / 2;
+  if (blocks > (long long)sm_count * 8) blocks = (long long)sm_count * 8;
+  if (blocks < 1) blocks = 1;
+  gram_unpack_kernel<<<(int)blocks, 256, 0, s>>>(n, P, G, ldg);
+  return cudaGetLastError();
 }
 
 bool gram_is_exact(const int* err) {

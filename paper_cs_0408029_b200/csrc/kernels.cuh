@@ -36,6 +36,10 @@ cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
 constexpr int kErrExp = 48;
 bool gram_is_exact(const int* err);
 inline int gram_exact_lmin(const int* err) { return 2048 - err[kErrExp + 1]; }  // L_A
+// ldg <= 0: G is the packed lower triangle (row i = entries j <= i at offset
+// i(i+1)/2) -- the row-shard partial Gram that ranks reduce.
+// launch_gram_unpack: packed -> full symmetric n x ldg.
+cudaError_t launch_gram_unpack(int n, const double* P, double* G, int ldg, int sm_count, cudaStream_t s);
 cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
                         const double* vals, const int32_t* colptr, const int32_t* rowind,
                         const double* cvals, const double* b, int row_begin, int row_end,

@@ -418,6 +418,8 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
       trace[it].f = f;
       trace[it].below_tol = 0.0;
       trace[it].above_tol = INFINITY;
+      trace[it].kept = (jq > 0 ? jq : 0) * kTile;
+      trace[it].pad = 0;
     }
   }
 }

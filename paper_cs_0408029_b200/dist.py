@@ -1,18 +1,25 @@
 """Multi-GPU plumbing for the NNLS hot path (one process per GPU,
-torch.distributed over NCCL on NVLink; gloo for CPU tests).
+torch.distributed over NCCL on NVLink; gloo for CPU tests).  Argument
+marshalling and collectives only -- no arithmetic of the method.
 
-Two ways the path uses several GPUs (BASELINE.json north_star):
+Two ways the path uses several GPUs (BASELINE.json north_star; SURVEY.md §8(e);
+DESIGN.md §8):
 
-* Row-sharded Gram: rank r forms G_r = A_r^T A_r, c_r = A_r^T b_r over its
-  row block (nnls_setup_shard), the [G | c] buffers are summed with ONE
-  all-reduce (the only GPU<->GPU exchange of the method), nnls_gram_finalize,
-  then the pivot loop runs on the full Gram.  With quantized inputs every
-  partial sum is exact, so the reduced Gram is bitwise independent of the
-  number of ranks.
-* Independent problems (batched config 4, or one problem per rank): disjoint
-  slices, no communication.
+* Row-sharded Gram (A^T A is formed once, and it is a sum over the
+  rows of A): rank k forms the packed partial G_k = A_k^T A_k, c_k = A_k^T b_k
+  of its row block -- the root from the full A it keeps for the loop
+  (ShardSolver), every other rank from ONLY its block (BlockSolver) -- and the
+  partials are summed with ONE collective: a reduce to the root (default:
+  only the root runs the pivot loop) or an all-reduce (every rank holds the
+  sum).  The buffer is the packed lower triangle + c, n(n+1)/2 + n doubles.
+  With quantized inputs every partial sum is exact, so the reduced Gram is
+  bitwise independent of the number of ranks.
+* Independent problems (batched config 4): disjoint slices of the batch, no
+  communication.
 """
 from __future__ import annotations
+
+import numpy as np
 
 
 def row_shards(m: int, world: int) -> list[tuple[int, int]]:
@@ -30,9 +37,25 @@ def row_shards(m: int, world: int) -> list[tuple[int, int]]:
 
 
 def batch_shard(total: int, world: int, rank: int) -> tuple[int, int]:
-    """(start, count) of rank's slice of `total` independent problems."""
+    """(start, count) of rank's slice of `total` independent problems; the
+    remainder is spread one problem each over the first ranks (nothing is
+    dropped)."""
     r0, r1 = row_shards(total, world)[rank]
     return r0, r1 - r0
+
+
+def row_block(rowptr, colind, vals, b, r0: int, r1: int):
+    """Local CSR (rowptr rebased to 0) and b of rows [r0, r1): what a non-root
+    rank uploads (numpy arrays)."""
+    rowptr = np.asarray(rowptr)
+    e0, e1 = int(rowptr[r0]), int(rowptr[r1])
+    return ((rowptr[r0:r1 + 1] - e0).astype(np.int32), np.ascontiguousarray(colind[e0:e1], dtype=np.int32),
+            np.ascontiguousarray(vals[e0:e1], dtype=np.float64), np.ascontiguousarray(b[r0:r1], dtype=np.float64))
+
+
+def packed_count(n: int) -> int:
+    """Doubles in the reduction buffer: packed lower triangle + c."""
+    return n * (n + 1) // 2 + n
 
 
 class _CudaArray:
@@ -43,21 +66,51 @@ class _CudaArray:
                                          "data": (int(ptr), False), "version": 3}
 
 
-def gram_tensor(shard_solver):
-    """torch tensor aliasing the solver's device [G | c] buffer."""
+def gram_tensor(solver, device=None):
+    """torch tensor aliasing the handle's device [G packed | c] buffer."""
     import torch
-    ptr, count, _ = shard_solver.gram_buffer()
-    return torch.as_tensor(_CudaArray(ptr, count), device="cuda")
+    ptr, count = solver.gram_buffer()
+    return torch.as_tensor(_CudaArray(ptr, count), device=device or "cuda")
 
 
-def allreduce_gram(shard_solver, group=None):
-    """Sum the row-shard partial Grams of all ranks in place (one
-    all_reduce(SUM, float64)), then finalize the handle."""
+def reduce_gram_buffer(buf, mode: str = "reduce", root: int = 0, group=None):
+    """SUM the ranks' packed partial-Gram buffers in place: mode "reduce" ->
+    the sum lands on `root` only, "allreduce" -> on every rank.  Device
+    agnostic (NCCL for CUDA tensors, gloo for CPU tensors)."""
+    import torch.distributed as dist
+    if mode == "reduce":
+        dist.reduce(buf, dst=root, op=dist.ReduceOp.SUM, group=group)
+    elif mode == "allreduce":
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    else:
+        raise ValueError(f"unknown reduction mode {mode!r}")
+    return buf
+
+
+def reduce_gram(solver, mode: str = "reduce", root: int = 0, group=None, stream=None):
+    """The sharded-Gram exchange for a ShardSolver (root) or BlockSolver:
+    reduce the packed partials, then (root) finalize the handle.  `stream`:
+    the torch stream the handle was created on -- the collective is issued
+    on it, so it orders after the partial-Gram kernels and the finalize after
+    the collective without a host synchronisation."""
+    import contextlib
+
     import torch
     import torch.distributed as dist
-    t = gram_tensor(shard_solver)
-    torch.cuda.synchronize()  # the partial Gram kernels ran on the handle's stream
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    torch.cuda.synchronize()
-    shard_solver.finalize()
+    t = gram_tensor(solver)
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:
+        if stream is None:
+            torch.cuda.synchronize()  # (handle on another stream: order by a host sync)
+        reduce_gram_buffer(t, mode, root, group)
+    rank = dist.get_rank(group)
+    if hasattr(solver, "finalize") and (mode == "allreduce" or rank == root):
+        if stream is None:
+            torch.cuda.synchronize()
+        solver.finalize()
     return t
+
+
+# backwards-compatible name (round 1): all-reduce + finalize
+def allreduce_gram(solver, group=None, stream=None):
+    return reduce_gram(solver, "allreduce", 0, group, stream)

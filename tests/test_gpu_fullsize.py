@@ -11,6 +11,8 @@ solve everything within a test's time budget:
   batch solved by the oracle one by one (F, iteration counts, x), and the KKT
   report of every problem.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -94,3 +96,36 @@ def test_config4_full_batch_sampled_parity(P):
         assert info["iterations"][p] == r["iterations"], p
         scale = max(np.abs(r["x"]).max(), 1e-300)
         assert np.abs(xs[p] - r["x"]).max() <= 1e-9 * scale, p
+
+
+# ------------------------------------------------ config 2 against the oracle
+# The oracle solves config 2 in ~25 s, so its results for seeds 0-2 are cached
+# by tests/golden/make_config2_golden.py (calls only oracle/).  Bar (BASELINE
+# north_star): F and the iteration count identical, x within 1e-9 relative
+# inf-norm; the per-iteration trace (k, branch, |F|) identical.
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_config2_oracle_parity(P, seed):
+    import hashlib
+    gold = np.load(os.path.join(GOLDEN, f"config2_seed{seed}.npz"))
+    prob = g.make_problem(2, seed)
+    h = hashlib.sha256()
+    for a in (prob.rowptr, prob.colind, prob.vals, prob.b):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == str(gold["digest"]), "generator changed: regenerate the golden files"
+    S = P.setup(prob, trace=1)
+    x, info = S.solve()
+    mask_or = np.unpackbits(gold["mask_bits"])[: prob.n]
+    assert info["status"] == int(gold["status"]) == 0
+    assert np.array_equal(S.free_set().astype(np.uint8), mask_or), "final free set differs"
+    assert info["iterations"] == int(gold["iterations"])
+    assert info["single_exchanges"] == int(gold["single_exchanges"])
+    assert info["free_count"] == int(gold["free_count"])
+    tr = [(t["k"], t["branch"], t["f"]) for t in S.trace()]
+    assert tr == [tuple(int(v) for v in row) for row in gold["trace_kbf"]]
+    xo, xne = gold["x"], gold["x_ne"]
+    assert np.abs(np.asarray(x) - xo).max() <= 1e-9 * np.abs(xo).max()
+    assert np.abs(S.x_ne() - xne).max() <= 1e-9 * np.abs(xne).max()
+    assert abs(info["objective"] - float(gold["objective"])) <= 1e-9 * float(gold["objective"])

@@ -184,3 +184,89 @@ def test_iteration_limit_and_not_pd():
     # start; c_0 = c_dup so they move together -> NOT_PD on that solve
     if (A.T @ p.b)[0] > 0:
         assert r["status"] == 7
+
+
+# ---------------------------------------------------------------- or_kkt pins
+# KKT report of Eq. 3 with the independent dual y' = A^T (A x - b).
+# Hand-computed on the S:334 matrix A = [[1,0],[0,1],[1,1]], b = (-1,1,0):
+#   x = (0, .5):  r = A x - b = (1, -.5, .5),  y' = A^T r = (1.5, 0)
+#   x = (1, 1):   r = (2, 0, 2),               y' = (4, 2)
+#   x = (.5, -1): r = (1.5, -2, -.5),          y' = (1, -2.5)
+# Every field is distinct across the cases, so a sign error in y' (or r), a
+# dropped |.| in the complementarity, or a min/max swap fails one of them.
+KKT_HAND = [
+    ((0.0, 0.5), dict(objective=0.75, kkt_min_x=0.0, kkt_min_y=0.0, kkt_max_comp=0.0, kkt_dot=0.0)),
+    ((1.0, 1.0), dict(objective=4.0, kkt_min_x=1.0, kkt_min_y=2.0, kkt_max_comp=4.0, kkt_dot=6.0)),
+    ((0.5, -1.0), dict(objective=3.25, kkt_min_x=-1.0, kkt_min_y=-2.5, kkt_max_comp=2.5, kkt_dot=3.0)),
+]
+
+
+@pytest.mark.parametrize("x,want", KKT_HAND, ids=["S334-optimum", "x=(1,1)", "x=(.5,-1)"])
+def test_kkt_hand_cases(x, want):
+    p = g.from_dense([[1, 0], [0, 1], [1, 1]], [-1, 1, 0])
+    got = O.kkt(p, np.array(x))
+    for k, v in want.items():
+        assert got[k] == v, (k, got[k], v)
+
+
+def test_kkt_matches_dense_definition():
+    """Random x on a config-0 problem: every field equals its definition
+    evaluated densely with numpy (y' = A^T (A x - b))."""
+    p = g.make_problem(0, 3)
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal(p.n)
+    A = p.dense()
+    r = A @ x - p.b
+    yp = A.T @ r
+    got = O.kkt(p, x)
+    assert abs(got["objective"] - 0.5 * r @ r) <= 1e-12 * (r @ r)
+    assert got["kkt_min_x"] == x.min()
+    assert abs(got["kkt_min_y"] - yp.min()) <= 1e-12 * np.abs(yp).max()
+    assert abs(got["kkt_max_comp"] - np.abs(x * yp).max()) <= 1e-12 * np.abs(x * yp).max()
+    assert abs(got["kkt_dot"] - x @ yp) <= 1e-12 * np.abs(x * yp).sum()
+
+
+# --------------------------------------------------------- or_brute_force pins
+def test_brute_force_identity_closed_form():
+    """A = I: the feasible partition is unique, F = {i : b_i > 0},
+    x = max(b, 0); every b_i = 0 exactly doubles the count (i in F or in G
+    both give x_i = y_i = 0)."""
+    b = np.array([3.0, -2.0, 0.5, -0.25, 1.0, -7.0])
+    cnt, masks, x = O.brute_force(g.from_dense(np.eye(6), b))
+    assert cnt == 1
+    assert np.array_equal(masks[0], (b > 0).astype(np.uint8))
+    assert np.array_equal(x, np.maximum(b, 0))
+    b0 = np.array([3.0, 0.0, -1.0, 0.0])
+    cnt, masks, _ = O.brute_force(g.from_dense(np.eye(4), b0))
+    assert cnt == 4
+    got = sorted(tuple(m) for m in masks)
+    assert got == sorted([(1, a, 0, c) for a in (0, 1) for c in (0, 1)])
+
+
+def test_brute_force_diagonal_gram_closed_form():
+    """Columns with disjoint row supports: G = diag(g_i), y_i = g_i x_i - c_i,
+    so F = {i : c_i > 0} and x_i = c_i / g_i there (no enumeration needed)."""
+    rng = np.random.default_rng(12)
+    n, per = 9, 2
+    A = np.zeros((n * per, n))
+    for j in range(n):
+        A[j * per:(j + 1) * per, j] = np.round(rng.standard_normal(per) * 16) / 16 + 2.0
+    b = np.round(rng.standard_normal(n * per) * 16) / 16
+    c = A.T @ b
+    gd = (A * A).sum(0)
+    cnt, masks, x = O.brute_force(g.from_dense(A, b))
+    assert cnt == 1
+    assert np.array_equal(masks[0], (c > 0).astype(np.uint8))
+    assert np.allclose(x, np.where(c > 0, c / gd, 0.0), rtol=1e-15, atol=0)
+
+
+def test_brute_force_counts_all_feasible_partitions():
+    """A problem with two KKT points is impossible for full-rank A (unique
+    minimiser), so a rank-deficient A (two equal columns) with c > 0 on them
+    has exactly the F's that put the weight on either copy -- but both copies
+    together make the Gram singular (skipped, NOT_PD).  Expect 2 partitions."""
+    A = np.array([[1.0, 1.0], [2.0, 2.0], [0.0, 0.0]])
+    b = np.array([1.0, 1.0, 0.0])
+    cnt, masks, _ = O.brute_force(g.from_dense(A, b))
+    assert cnt == 2
+    assert sorted(tuple(m) for m in masks) == [(0, 1), (1, 0)]
