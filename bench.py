@@ -8,14 +8,19 @@ one synthetic problem already resident in HBM: ingest (validation, CSC), Gram
 A^T A and A^T b, the pivot loop (decide/exchange, gather+Cholesky+solves,
 dual update, zeroing), the final LSQR and the KKT report, x left in HBM.
 
-Default workload (N = 1): BASELINE.json configs[1], a single 2000 x 1000 CSR
-problem with 5% N(0,1) nonzeros (quantized to 2^-12), b = A x0 + 0.01 noise.
-Under torchrun (N > 1) every rank solves its own independent problem (seed +
-rank): the single-problem path does not shard ("replicas", weak scaling).
---config 4 runs the batched config (65536 problems of 128 x 64; problems
-sharded over ranks, no communication).
+Default workload: BASELINE.json configs[2], the largest single-GPU
+configuration -- one 40000 x 8000 CSR problem with 0.5% N(0,1) nonzeros
+(quantized to 2^-12), b = A x0 + 0.01 noise; the Cholesky of |F| ~ 4000 and
+the HBM kernels carry §8(d)'s targets there.  The same line carries configs
+1, 3 and 4 (the batched 65536 x (128x64) config) under "other_configs".
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+Multi-GPU (`--gpus N`, re-launched through torchrun when WORLD_SIZE is
+unset): config 2 forms A^T A row-sharded over the ranks (each rank uploads
+only its row block; the packed partial Grams are reduced to rank 0 with one
+NCCL reduce; rank 0 runs the pivot loop: strong scaling), and the config-4
+batch is sharded over the ranks with no communication ("config4_sharded").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
 only reference this paper-derived build has) on the host cores, rank 0 only.
@@ -25,7 +30,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -38,23 +45,24 @@ import numpy as np  # noqa: E402
 METRIC = "NNLS solves/s and pivot iterations/s (FP64); % of FP64-TC / HBM roofline"
 L2_FLUSH_BYTES = 256 << 20
 HBM_FALLBACK_GBS = 6650.0
+REF_BUDGET_S = 150.0   # reference arm: timed oracle work per run (a bounded sample)
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--batch", type=int, default=65536, help="config 4: total problems (all ranks)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--shard-gram", action="store_true",
-                    help="single problem: row-shard A^T A over the ranks + one NCCL all-reduce "
-                         "(strong scaling) instead of one independent problem per rank")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configs / alternatives")
+    ap.add_argument("--reduce", choices=["reduce", "allreduce"], default="reduce",
+                    help="N>1 config 2: collective for the packed partial Grams")
     return ap.parse_args()
 
 
@@ -64,6 +72,17 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def relaunch_torchrun(args):
+    """--gpus N > 1 without a torchrun environment: start N ranks here."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def workload_desc(cfg, batch=None):
@@ -77,6 +96,25 @@ def workload_desc(cfg, batch=None):
             f"(2^-12 grid), {rhs}")
 
 
+def config_dict(cfg, args, world):
+    """The `config` object -- identical in both arms (--impl ours / reference)."""
+    import nnls_gen as g
+    c = g.CONFIGS[cfg]
+    d = {"workload": workload_desc(cfg, args.batch), "config_index": cfg, "seed": args.seed,
+         "m": c["m"], "n": c["n"], "density": c["density"],
+         "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+    if cfg == 4:
+        d.update(problems=args.batch, parallelism="problems sharded over ranks, no communication")
+    elif world > 1 and cfg == 2:
+        d["parallelism"] = (f"A^T A row-sharded over {world} ranks (packed partial Grams, NCCL {args.reduce} "
+                            "to rank 0); pivot loop on rank 0")
+    elif world > 1:
+        d["parallelism"] = "replicas: one independent problem per GPU"
+    else:
+        d["parallelism"] = "one GPU"
+    return d
+
+
 class ClockSampler:
     """nvidia-smi-equivalent sampling (NVML) of SM clocks and throttle reasons
     during the timed region."""
@@ -87,7 +125,7 @@ class ClockSampler:
         0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, device_index, period=0.02):
+    def __init__(self, device_index, period=0.01):
         self.period = period
         self.samples = []
         self.reasons = 0
@@ -141,7 +179,7 @@ def load_peaks():
             src = "MEASURED_PEAKS.json hbm_gbs (measured)"
         except Exception:
             pass
-    fp64, fsrc = 37.139, "profiles/r01_microbench_fp64.json dmma_tflops (measured, this pool)"
+    fp64, fsrc = 37.139, "profiles/r01_microbench_fp64.json dmma_tflops (DMMA 8x8x4 peak measured on this pool)"
     mb = os.path.join(ROOT, "profiles", "r01_microbench_fp64.json")
     if os.path.exists(mb):
         try:
@@ -164,19 +202,22 @@ def load_traffic():
 
 
 # ------------------------------------------------- algorithmic work models
-# (DESIGN.md §"Roofline": bytes a step must move / flops it must do; avoided
-#  dense work is not counted)
+# (bytes a step must move / flops it must do)
+def chol_flops(f, q=0):
+    """Executed Cholesky flops of the bordered (f+1) x (f+1) factorization when
+    the leading q columns of the previous factor are reused: the left-looking
+    column j costs 2 j (f - j) flops, of which the kept columns only redo the
+    rows below q, 2 j (f - q): sum = (f^3 - q^3)/3; plus the bordered
+    (forward-substitution) row, f^2 - q^2.  q = 0: the method's f^3/3 + f^2."""
+    return (f ** 3 - q ** 3) / 3.0 + (f * f - q * q)
+
+
 def phase_work(phase, prob, traces, lsqr_itns, nnzF_list):
     m, n, nnz = prob.m, prob.n, prob.nnz
     if phase == "gram":       # read CSR+CSC+b, write full G (n*n) and c
         return "hbm", float(2 * 12 * nnz + 4 * (m + n) + 8 * m + 8 * n * n + 8 * n)
     if phase == "chol_factor":
-        fl = 0.0
-        for tr in traces:
-            for t in tr:
-                f = t["f"]
-                fl += f ** 3 / 3.0 + f * f  # Cholesky f^3/3 + bordered forward row
-        return "tensor", fl
+        return "tensor", float(sum(chol_flops(t["f"], t.get("kept", 0)) for tr in traces for t in tr))
     if phase == "chol_solve":
         return "hbm", float(sum(8 * t["f"] * (t["f"] + 1) / 2 for tr in traces for t in tr))
     if phase == "dual":
@@ -194,234 +235,382 @@ def phase_work(phase, prob, traces, lsqr_itns, nnzF_list):
     return "hbm", 0.0
 
 
-# ----------------------------------------------------------------- ours
-def run_ours(args):
-    import torch
+KERNEL_PHASES = ["validate", "csc", "gram", "init", "decide", "chol_factor", "chol_solve", "dual", "lsqr",
+                 "batched"]
 
+
+# ----------------------------------------------------------------- ours
+class Ctx:
+    def __init__(self, args):
+        import torch
+        self.torch = torch
+        self.args = args
+        self.world, self.rank, self.local = dist_env()
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+        self.dev = torch.device("cuda", self.local)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=self.dev)
+        self.peaks = load_peaks()
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max_over_ranks(self, v):
+        if self.dist is None:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(self, step, steps, inputs, x_out, after=None):
+        """K steps, each bracketed by CUDA events on the library's stream, L2
+        flushed before each (outside the events).  Returns total device ms."""
+        torch = self.torch
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for k in range(steps):
+            with torch.cuda.stream(self.stream):
+                self.flush.zero_()
+            ev[k][0].record(self.stream)
+            step(inputs, x_out)
+            ev[k][1].record(self.stream)
+            if after is not None:
+                after()
+        torch.cuda.synchronize(self.dev)
+        return sum(a.elapsed_time(b) for a, b in ev)
+
+
+def measure_single(C, cfg, steps, warmup, shard=False, with_e2e=True, full_fact=True, trace=True):
+    """Single problem (configs 0-3).  shard (N > 1, config 2): row-sharded Gram
+    + reduce to rank 0, the loop on rank 0."""
     import nnls_gen as g
     import paper_cs_0408029_b200 as P
-
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.Stream(device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    hbm_gbs, hbm_src, fp64_tf, fp64_src = load_peaks()
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    cfg = args.config
-    batched = cfg == 4
-    if batched:
-        per = args.batch // world
-        start = rank * per
-        B = g.make_batch(seed=args.seed, start=start, count=per)
-        host = dict(nnz_off=B.nnz_off, rowptr=B.rowptr, colind=B.colind, vals=B.vals, b=B.b)
-        solver = P.BatchedSolver(stream=stream)
-        units_per_step = per
-    elif args.shard_gram:
-        from paper_cs_0408029_b200.dist import allreduce_gram, row_shards
-        prob = g.make_problem(cfg, seed=args.seed)          # the same problem on every rank
-        host = dict(rowptr=prob.rowptr, colind=prob.colind, vals=prob.vals, b=prob.b)
+    torch, args = C.torch, C.args
+    world, rank = C.world, C.rank
+    prob = g.make_problem(cfg, seed=args.seed + (0 if shard else rank))
+    host = dict(rowptr=prob.rowptr, colind=prob.colind, vals=prob.vals, b=prob.b)
+    if shard:
+        from paper_cs_0408029_b200.dist import reduce_gram, row_block, row_shards
         r0, r1 = row_shards(prob.m, world)[rank]
-        solver = P.ShardSolver(prob.m, prob.n, prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1,
-                               stream=stream, trace=1)
-        units_per_step = 1
+        if rank == 0:
+            solver = P.ShardSolver(prob.m, prob.n, prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1,
+                                   stream=C.stream, trace=1)
+        else:  # only this rank's row block travels to its GPU
+            rp, ci, v, bb = row_block(prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1)
+            host = dict(rowptr=rp, colind=ci, vals=v, b=bb)
+            solver = P.BlockSolver(stream=C.stream).load_block(r1 - r0, prob.n, rp, ci, v, bb)
     else:
-        prob = g.make_problem(cfg, seed=args.seed + rank)
-        host = dict(rowptr=prob.rowptr, colind=prob.colind, vals=prob.vals, b=prob.b)
-        solver = P.Solver(stream=stream, trace=1)
-        units_per_step = 1
-    devt = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in host.items()}
+        solver = P.Solver(stream=C.stream, trace=1 if trace else 0)
+    devt = {k: torch.from_numpy(np.ascontiguousarray(v)).to(C.dev) for k, v in host.items()}
     pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in host.items()}
-    nx = (B.count * B.n) if batched else prob.n
-    x_dev = torch.empty(nx, dtype=torch.float64, device=dev)
-    x_pin = torch.empty(nx, dtype=torch.float64).pin_memory()
+    x_dev = torch.empty(prob.n, dtype=torch.float64, device=C.dev)
+    x_pin = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+    infos = []
+    mode = [args.reduce]
 
-    def step(inputs, x_out):
-        if args.shard_gram and not batched:
-            solver.load_shard(prob.m, prob.n, inputs["rowptr"], inputs["colind"], inputs["vals"], inputs["b"],
-                              r0, r1)
-            if world > 1:
-                allreduce_gram(solver)
+    def step(inp, x_out):
+        if shard:
+            if rank == 0:
+                solver.load_shard(prob.m, prob.n, inp["rowptr"], inp["colind"], inp["vals"], inp["b"], r0, r1)
             else:
-                solver.finalize()
-            _, info = solver.solve(x_out=x_out)
-            return info
-        if batched:
-            if not inputs["b"].is_cuda:
-                # host buffers: the pipelined load + solve (chunk k+1 copies in
-                # and chunk k-1 copies out while chunk k solves)
-                solver.run(B.count, B.m, B.n, inputs["nnz_off"], inputs["rowptr"], inputs["colind"],
-                           inputs["vals"], inputs["b"], x_out=x_out, want_info=False)
-                return None
-            solver.load(B.count, B.m, B.n, inputs["nnz_off"], inputs["rowptr"], inputs["colind"],
-                        inputs["vals"], inputs["b"])
-            solver.solve(x_out=x_out, want_info=False)
-            return None
-        solver.load(prob.m, prob.n, inputs["rowptr"], inputs["colind"], inputs["vals"], inputs["b"])
-        _, info = solver.solve(x_out=x_out)
-        return info
+                solver.load_block(r1 - r0, prob.n, inp["rowptr"], inp["colind"], inp["vals"], inp["b"])
+            reduce_gram(solver, mode[0], 0, stream=C.stream)
+            if rank == 0:
+                infos.append(solver.solve(x_out=x_out)[1])
+            return
+        solver.load(prob.m, prob.n, inp["rowptr"], inp["colind"], inp["vals"], inp["b"])
+        infos.append(solver.solve(x_out=x_out)[1])
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-
-    def timed_pass(inputs, x_out, collect):
-        infos, traces = [], []
-        total_ms = 0.0
-        for k in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.zero_()                      # evict L2 (256 MiB > 126 MB L2) between steps
-            e0, e1 = ev[k]
-            e0.record(stream)
-            info = step(inputs, x_out)
-            e1.record(stream)
-            if collect and not batched:
-                infos.append(info)
-                traces.append(solver.trace())
-        torch.cuda.synchronize(dev)
-        for e0, e1 in ev:
-            total_ms += e0.elapsed_time(e1)
-        return total_ms, infos, traces
-
-    # warm-up
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step(devt, x_dev)
-    torch.cuda.synchronize(dev)
-
-    # ---- device-resident timed pass (value): the production path (the pivot
-    #      loop runs inside one CUDA graph with a device-side WHILE node)
+    torch.cuda.synchronize(C.dev)
+    # ---- value pass: the production path (pivot loop inside one CUDA graph)
     P.timing_enable(solver.h, False)  # resets the launch counters
-    barrier()
-    with ClockSampler(local) as clk:
-        total_ms, infos, traces = timed_pass(devt, x_dev, collect=True)
-    barrier()
-    launches_timed = P.timing_read(solver.h)
-    t_max = total_ms
-    if dist is not None:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-    # ---- instrumented pass (same K steps): per-phase CUDA events on the
-    #      library's stream (host-driven pivot loop, so each kernel is bracketed)
+    infos.clear()
+    C.barrier()
+    with ClockSampler(C.local) as clk:
+        total = C.timed(step, steps, devt, x_dev)
+    C.barrier()
+    launches = P.timing_read(solver.h)
+    t_max = C.max_over_ranks(total)
+    res = {"ms_per_step": t_max / steps, "value": steps / (t_max / 1e3), "clocks": clk.summary(),
+           "gpu_launches": int(sum(launches[p][1] for p in KERNEL_PHASES))}
+    if shard and world > 1 and not args.no_extra:
+        other = "allreduce" if args.reduce == "reduce" else "reduce"
+        mode[0] = other
+        C.barrier()
+        alt = C.max_over_ranks(C.timed(step, steps, devt, x_dev))
+        mode[0] = args.reduce
+        res["alternative_collective"] = {"collective": other, "ms_per_step": round(alt / steps, 5),
+                                         "value": round(steps / (alt / 1e3), 3)}
+    if rank == 0:
+        info = infos[0]
+        trace = solver.trace()
+        res["pivot_iterations_per_s"] = info["iterations"] * steps / (t_max / 1e3)
+        res["per_solve"] = {k: info[k] for k in ("iterations", "free_count", "lsqr_iterations", "status",
+                                                 "single_exchanges")}
+        res["per_solve"]["trace"] = [{"k": t["k"], "branch": t["branch"], "f": t["f"], "kept": t["kept"]}
+                                     for t in trace]
+    # ---- instrumented pass: per-phase CUDA events (host-driven pivot loop)
     P.timing_enable(solver.h, True)
-    barrier()
-    instr_ms, _, _ = timed_pass(devt, x_dev, collect=False)
-    barrier()
+    C.barrier()
+    instr = C.timed(step, steps, devt, x_dev)
+    C.barrier()
     phases = P.timing_read(solver.h)
     P.timing_enable(solver.h, False)
-
-    # ---- end-to-end pass through the public API with HOST buffers (value e2e)
-    e2e_ms = None
-    if not args.no_e2e:
+    res["phase_timing"] = {"pass": "instrumented (host-driven loop, CUDA events per phase)",
+                           "ms_per_step": round(instr / steps, 5)}
+    res["phase_ms_per_step"] = {p: round(phases[p][0] / steps, 5) for p in P.PHASES
+                                if phases[p][1] or phases[p][0]}
+    if rank == 0:
+        hbm, hsrc, fp64, fsrc = C.peaks
+        dom = max(KERNEL_PHASES, key=lambda p: phases[p][0])
+        mask = solver.free_set()
+        nnzF = int(mask[prob.colind].sum())
+        traces = [trace] * steps
+        bound, work = phase_work(dom, prob, traces, [info["lsqr_iterations"]] * steps, [nnzF] * steps)
+        nl = max(1, phases[dom][1])
+        dom_s = phases[dom][0] / 1e3
+        tensor = bound == "tensor"
+        achieved = work / dom_s / (1e12 if tensor else 1e9)
+        peak = fp64 if tensor else hbm
+        res["roofline"] = {
+            "kernel": dom, "bound": bound, "achieved": round(achieved, 4), "peak": peak,
+            "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(achieved / peak, 6),
+            "peak_source": fsrc if tensor else hsrc,
+            "algorithmic_per_launch": work / nl, "avg_launch_ms": round(phases[dom][0] / nl, 5),
+            "launches_per_step": nl / steps, "share_of_step": round(phases[dom][0] / max(instr, 1e-9), 4),
+            "traffic": load_traffic().get("config%d" % cfg, {}).get(dom, {}).get("dram_bytes_per_launch"),
+            "work_model": ("executed Cholesky flops: sum over launches of (f^3 - q^3)/3 + f^2 - q^2, q = factor "
+                           "prefix reused from the previous pivot iteration (trace 'kept')" if tensor else
+                           "algorithmic bytes (DESIGN.md §8)")}
+        # every kernel's rate against its own roofline (DESIGN.md §8 work models)
+        per = {}
+        for p in ("gram", "chol_factor", "chol_solve", "dual", "lsqr", "decide"):
+            if not phases[p][1]:
+                continue
+            b, w = phase_work(p, prob, traces, [info["lsqr_iterations"]] * steps, [nnzF] * steps)
+            s = phases[p][0] / 1e3
+            a = w / s / (1e12 if b == "tensor" else 1e9)
+            per[p] = {"bound": b, "achieved": round(a, 3), "frac": round(a / (fp64 if b == "tensor" else hbm), 4),
+                      "avg_launch_ms": round(phases[p][0] / phases[p][1], 5)}
+        res["kernel_rooflines"] = per
+    # ---- full factorizations (no prefix reuse): the FP64-TC target of §8(d)
+    if rank == 0 and full_fact and not shard:
+        os.environ["NNLS_NO_REUSE"] = "1"
+        try:
+            s2 = P.Solver(stream=C.stream, trace=1)
+        finally:
+            del os.environ["NNLS_NO_REUSE"]
+        s2.load(prob.m, prob.n, devt["rowptr"], devt["colind"], devt["vals"], devt["b"])
+        s2.solve(x_out=x_dev)
+        P.timing_enable(s2.h, True)
+        nrep = max(2, min(steps, 5))
+        for _ in range(nrep):
+            with torch.cuda.stream(C.stream):
+                C.flush.zero_()
+            s2.solve(x_out=x_dev)
+        torch.cuda.synchronize(C.dev)
+        ph2 = P.timing_read(s2.h)
+        tr2 = s2.trace()
+        fl = sum(chol_flops(t["f"]) for t in tr2) * nrep
+        ms = ph2["chol_factor"][0]
+        fp64 = C.peaks[2]
+        res["full_factorization"] = {
+            "f": [t["f"] for t in tr2], "launches": ph2["chol_factor"][1],
+            "avg_launch_ms": round(ms / max(1, ph2["chol_factor"][1]), 5),
+            "tflops": round(fl / (ms / 1e3) / 1e12, 4), "frac": round(fl / (ms / 1e3) / 1e12 / fp64, 4),
+            "note": "NNLS_NO_REUSE handle: every pivot iteration factors (A^T A)_FF from scratch; "
+                    "flops f^3/3 + f^2 per launch"}
+        s2.close()
+    # ---- end-to-end through the public API with HOST buffers
+    if with_e2e:
         for _ in range(2):
             step(pinned, x_pin)
-        barrier()
-        e2e_ms, _, _ = timed_pass(pinned, x_pin, collect=False)
-        barrier()
-        if dist is not None:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-
-    shard = args.shard_gram and not batched
-    units = units_per_step * args.steps * (1 if shard else world)
-    value = units / (t_max / 1e3)
-    out = {"metric": METRIC, "value": round(value, 3), "unit": "solves/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5),
-           "higher_is_better": True, "scaling": "strong" if shard else "weak", "vs_baseline": None,
-           "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)", "impl": "ours"}
-    if not batched:
-        iters = sum(i["iterations"] for i in infos) * (1 if shard else world)
-        out["pivot_iterations_per_s"] = round(iters / (t_max / 1e3), 3)
-        out["per_solve"] = {"iterations": infos[0]["iterations"], "free_count": infos[0]["free_count"],
-                            "lsqr_iterations": infos[0]["lsqr_iterations"], "status": infos[0]["status"]}
-    out["config"] = {"workload": workload_desc(cfg, args.batch), "config_index": cfg,
-                     "seed": args.seed, "l2": "flushed between timed steps (256 MiB write, outside events)",
-                     "parallelism": ("problems sharded over ranks, no communication" if batched
-                                     else ("A^T A row-sharded over ranks + NCCL all-reduce of [G|c]"
-                                           if shard else "replicas: one independent problem per GPU"))}
-    if batched:
-        out["config"].update(m=B.m, n=B.n, problems_per_gpu=B.count)
-    else:
-        out["config"].update(m=prob.m, n=prob.n, nnz=prob.nnz)
-
-    # ---- phases, dominant kernel, roofline
-    kernel_phases = ["validate", "csc", "gram", "init", "decide", "chol_factor", "chol_solve", "dual",
-                     "lsqr", "batched"]
-    out["gpu_launches"] = int(sum(launches_timed[p][1] for p in kernel_phases))
-    out["phase_timing"] = {"pass": "instrumented (host-driven loop, CUDA events per phase)",
-                           "ms_per_step": round(instr_ms / args.steps, 5)}
-    out["phase_ms_per_step"] = {p: round(phases[p][0] / args.steps, 5) for p in P.PHASES if phases[p][1] or phases[p][0]}
-    dom = max(kernel_phases, key=lambda p: phases[p][0])
-    traffic = load_traffic()
-    if batched:
-        # per problem: CSR + b in, x + info out (G, factor, vectors stay on chip)
-        nzp = int(B.nnz_off[1] - B.nnz_off[0])
-        bytes_per = 12 * nzp + 4 * (B.m + 1) + 8 * B.m + 8 * B.n + B.n + 8 * 8 + 5 * 8
-        bound, work = "hbm", float(bytes_per * B.count * args.steps)
-    else:
-        nnzF = []
-        rp = prob.rowptr
-        for _ in infos:
-            mask = solver.free_set()
-            nnzF.append(int(mask[prob.colind].sum()))
-        bound, work = phase_work(dom, prob, traces, [i["lsqr_iterations"] for i in infos], nnzF)
-    dom_s = phases[dom][0] / 1e3
-    if bound == "tensor":
-        achieved = work / dom_s / 1e12
-        peak, unit, psrc = fp64_tf, "TFLOP/s", fp64_src
-    else:
-        achieved = work / dom_s / 1e9
-        peak, unit, psrc = hbm_gbs, "GB/s", hbm_src
-    launches = max(1, phases[dom][1])
-    out["roofline"] = {"kernel": dom, "bound": bound, "achieved": round(achieved, 4), "peak": peak,
-                       "unit": unit, "frac": round(achieved / peak, 6), "peak_source": psrc,
-                       "algorithmic_per_launch": work / launches,
-                       "avg_launch_ms": round(phases[dom][0] / launches, 5),
-                       "share_of_step": round(phases[dom][0] / max(instr_ms, 1e-9), 4),
-                       "traffic": traffic.get("config%d" % args.config, {}).get(dom, {}).get("dram_bytes_per_launch")}
-    if e2e_ms is not None:
+        C.barrier()
+        e2e = C.max_over_ranks(C.timed(step, steps, pinned, x_pin))
         h2d = sum(int(v.nbytes) for v in host.values())
-        out["e2e"] = {"value": round(units / (e2e_ms / 1e3), 3), "unit": "solves/s",
-                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(nx * 8),
-                      "path": ("BatchedSolver.run(pinned host CSR,b; x_out=pinned host): chunked copy/compute pipeline"
-                               if batched else "Solver.load(pinned host CSR,b) + Solver.solve(x_out=pinned host)")}
-    out["clocks"] = clk.summary()
+        res["e2e"] = {"value": round(steps / (e2e / 1e3), 3), "unit": "solves/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": int(prob.n * 8) if rank == 0 else 0,
+                      "path": "Solver.load(pinned host CSR, b) + Solver.solve(x_out=pinned host)"}
+    res["_prob"] = prob
+    solver.close()
+    return res
 
+
+def measure_batched(C, steps, warmup, with_e2e=True):
+    import nnls_gen as g
+    import paper_cs_0408029_b200 as P
+    from paper_cs_0408029_b200.dist import batch_shard
+    torch, args = C.torch, C.args
+    start, per = batch_shard(args.batch, C.world, C.rank)
+    B = g.make_batch(seed=args.seed, start=start, count=per)
+    host = dict(nnz_off=B.nnz_off, rowptr=B.rowptr, colind=B.colind, vals=B.vals, b=B.b)
+    solver = P.BatchedSolver(stream=C.stream)
+    devt = {k: torch.from_numpy(np.ascontiguousarray(v)).to(C.dev) for k, v in host.items()}
+    pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in host.items()}
+    x_dev = torch.empty(B.count * B.n, dtype=torch.float64, device=C.dev)
+    x_pin = torch.empty(B.count * B.n, dtype=torch.float64).pin_memory()
+
+    def step(inp, x_out):
+        if not inp["b"].is_cuda:  # host buffers: the pipelined load + solve
+            solver.run(B.count, B.m, B.n, inp["nnz_off"], inp["rowptr"], inp["colind"], inp["vals"], inp["b"],
+                       x_out=x_out, want_info=False)
+            return
+        solver.load(B.count, B.m, B.n, inp["nnz_off"], inp["rowptr"], inp["colind"], inp["vals"], inp["b"])
+        solver.solve(x_out=x_out, want_info=False)
+
+    for _ in range(warmup):
+        step(devt, x_dev)
+    torch.cuda.synchronize(C.dev)
+    P.timing_enable(solver.h, False)
+    C.barrier()
+    with ClockSampler(C.local) as clk:
+        total = C.timed(step, steps, devt, x_dev)
+    C.barrier()
+    launches = P.timing_read(solver.h)
+    t_max = C.max_over_ranks(total)
+    res = {"ms_per_step": t_max / steps, "value": args.batch * steps / (t_max / 1e3), "clocks": clk.summary(),
+           "gpu_launches": int(sum(launches[p][1] for p in KERNEL_PHASES)), "problems_per_gpu": per}
+    out = solver.solve(x_out=x_dev, want_info=True)
+    its = float(out["info"]["iterations"].sum())
+    if C.dist is not None:  # pivot iterations of all ranks' problems
+        t = torch.tensor([its], dtype=torch.float64, device=C.dev)
+        C.dist.all_reduce(t)
+        its = float(t.item())
+    res["pivot_iterations_per_s"] = its * steps / (t_max / 1e3)
+    P.timing_enable(solver.h, True)
+    C.barrier()
+    instr = C.timed(step, steps, devt, x_dev)
+    C.barrier()
+    phases = P.timing_read(solver.h)
+    P.timing_enable(solver.h, False)
+    res["phase_ms_per_step"] = {p: round(phases[p][0] / steps, 5) for p in P.PHASES if phases[p][1] or phases[p][0]}
+    dom = max(KERNEL_PHASES, key=lambda p: phases[p][0])
+    nzp = float(B.nnz_off[-1] - B.nnz_off[0]) / B.count
+    bytes_per = 12 * nzp + 4 * (B.m + 1) + 8 * B.m + 8 * B.n + B.n + 8 * 8 + 5 * 8
+    hbm, hsrc, fp64, fsrc = C.peaks
+    nl = max(1, phases[dom][1])
+    work = bytes_per * B.count * steps
+    achieved = work / (phases[dom][0] / 1e3) / 1e9
+    res["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 4), "peak": hbm, "unit": "GB/s",
+                       "frac": round(achieved / hbm, 6), "peak_source": hsrc,
+                       "algorithmic_per_launch": work / nl, "avg_launch_ms": round(phases[dom][0] / nl, 5),
+                       "share_of_step": round(phases[dom][0] / max(instr, 1e-9), 4),
+                       "traffic": load_traffic().get("config4", {}).get(dom, {}).get("dram_bytes_per_launch"),
+                       "work_model": "per problem: CSR + b in, x + info out (G, factor, vectors stay on chip)"}
+    if with_e2e:
+        for _ in range(2):
+            step(pinned, x_pin)
+        C.barrier()
+        e2e = C.max_over_ranks(C.timed(step, steps, pinned, x_pin))
+        res["e2e"] = {"value": round(args.batch * steps / (e2e / 1e3), 3), "unit": "solves/s",
+                      "h2d_bytes_per_step": sum(int(v.nbytes) for v in host.values()),
+                      "d2h_bytes_per_step": int(B.count * B.n * 8),
+                      "path": "BatchedSolver.run(pinned host CSR, b; x_out=pinned host): chunked copy/compute pipeline"}
+    res["_batch"] = B
+    solver.close()
+    return res
+
+
+def round_res(r):
+    out = {}
+    for k, v in r.items():
+        if k.startswith("_"):
+            continue
+        out[k] = round(v, 5) if isinstance(v, float) else v
+    return out
+
+
+def run_ours(args):
+    C = Ctx(args)
+    world, rank = C.world, C.rank
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    cfg = args.config
+    if cfg == 4:
+        res = measure_batched(C, args.steps, args.warmup, with_e2e=not args.no_e2e)
+        args._batch = res.get("_batch")
+    else:
+        res = measure_single(C, cfg, args.steps, args.warmup, shard=(world > 1 and cfg == 2),
+                             with_e2e=not args.no_e2e)
+    shard = world > 1 and cfg == 2
+    out = {"metric": METRIC, "value": round(res["value"], 3), "unit": "solves/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 5),
+           "higher_is_better": True,
+           "scaling": "strong" if (shard or cfg == 4) else "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)",
+           "impl": "ours", "config": config_dict(cfg, args, world)}
+    for k, v in round_res(res).items():
+        if k not in ("value", "ms_per_step"):
+            out[k] = v
+    # ---- the other BASELINE configs (N = 1) / the sharded batch (N > 1)
+    if not args.no_extra:
+        extra = {}
+        if world == 1:
+            for c2 in [c for c in (1, 3, 4, 2) if c != cfg]:
+                if c2 == 4:
+                    r = measure_batched(C, max(3, args.steps // 4), 3, with_e2e=not args.no_e2e)
+                else:
+                    r = measure_single(C, c2, args.steps, 3, with_e2e=not args.no_e2e, full_fact=False)
+                extra[f"config{c2}"] = {k: v for k, v in round_res(r).items()
+                                        if k in ("value", "ms_per_step", "pivot_iterations_per_s", "e2e",
+                                                 "roofline", "per_solve", "phase_ms_per_step", "problems_per_gpu",
+                                                 "full_factorization")}
+                extra[f"config{c2}"]["workload"] = workload_desc(c2, args.batch)
+                if "per_solve" in extra[f"config{c2}"]:
+                    extra[f"config{c2}"]["per_solve"].pop("trace", None)
+        elif cfg != 4:
+            r = measure_batched(C, max(3, args.steps // 4), 3, with_e2e=False)
+            extra["config4_sharded"] = {k: v for k, v in round_res(r).items()
+                                        if k in ("value", "ms_per_step", "pivot_iterations_per_s", "roofline",
+                                                 "problems_per_gpu")}
+            extra["config4_sharded"]["workload"] = workload_desc(4, args.batch) + f", {world} ranks"
+        out["other_configs"] = extra
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, cfg, budget=args.cpu_seconds)
+        out["cpu_baseline"] = cpu_baseline(args, cfg, budget=args.cpu_seconds, batch=getattr(args, "_batch", None))
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+    if C.dist is not None:
+        C.dist.barrier()
+        C.dist.destroy_process_group()
 
 
 # ------------------------------------------------------------ oracle (CPU)
-def cpu_baseline(args, cfg, budget):
+def cpu_baseline(args, cfg, budget, batch=None):
     import nnls_gen as g
     import oracle as O
     if cfg == 4:
-        count = 2048
-        B = g.make_batch(seed=args.seed, start=0, count=count)
-        t0 = time.perf_counter()
-        out = O.solve_batched(B, threads=0)
-        dt = time.perf_counter() - t0
-        return {"value": round(count / dt, 3), "unit": "solves/s", "cores": out["threads"],
-                "kind": "oracle", "sample": f"{count} config-4 problems (OpenMP over problems)",
-                "seconds": round(dt, 3)}
+        # the oracle on 1 core and on all cores, each on a slice of the same
+        # batch sized to ~budget/2 seconds of CPU work (a 256-problem probe first)
+        B = batch if batch is not None else g.make_batch(seed=args.seed, start=0, count=16384)
+        out = {}
+        for label, thr in (("1core", 1), ("all", 0)):
+            probe = g.make_batch(seed=args.seed, start=0, count=256)
+            t1 = time.perf_counter()
+            O.solve_batched(probe, threads=thr)
+            rate = 256 / (time.perf_counter() - t1)
+            cnt = int(min(B.count, max(256, rate * budget / 2)))
+            sub = B if cnt == B.count else g.make_batch(seed=args.seed, start=0, count=cnt)
+            t1 = time.perf_counter()
+            used = O.solve_batched(sub, threads=thr)["threads"]
+            dt = time.perf_counter() - t1
+            out[label] = (cnt / dt, used, cnt, dt)
+        v, used, done, dt = out["all"]
+        return {"value": round(v, 3), "unit": "solves/s", "cores": used, "kind": "oracle",
+                "sample": f"{done} config-4 problems (OpenMP over problems, {used} threads)",
+                "seconds": round(dt, 3), "one_core": {"value": round(out["1core"][0], 3), "cores": 1,
+                                                      "sample": f"{out['1core'][2]} problems",
+                                                      "seconds": round(out["1core"][3], 3)}}
     prob = g.make_problem(cfg, seed=args.seed)
-    done, t0 = 0, time.perf_counter()
-    iters = 0
+    done, t0, iters = 0, time.perf_counter(), 0
     while True:
         r = O.solve(prob)
         done += 1
@@ -435,6 +624,10 @@ def cpu_baseline(args, cfg, budget):
 
 
 def run_reference(args):
+    """The CPU oracle on the host cores, as it stands, on this arm's workload;
+    each step is one full solve (config 4: a fixed sample of the batch).  The
+    run is bounded: timed steps stop once REF_BUDGET_S of oracle work is spent
+    (config 2: one solve is ~25-40 s), so `steps` reports those actually timed."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
@@ -442,34 +635,37 @@ def run_reference(args):
     import oracle as O
     cfg = args.config
     if cfg == 4:
-        count = 1024
+        count = 2048
         B = g.make_batch(seed=args.seed, start=0, count=count)
-        for _ in range(args.warmup):
-            O.solve_batched(B, threads=0)
-        t0 = time.perf_counter()
-        threads = 1
-        for _ in range(args.steps):
-            threads = O.solve_batched(B, threads=0)["threads"]
-        dt = time.perf_counter() - t0
-        value = count * args.steps / dt
+        work = lambda: O.solve_batched(B, threads=0)["threads"]  # noqa: E731
         sample = f"{count} config-4 problems per step (OpenMP over problems)"
-        cores = threads
+        units = count
     else:
         prob = g.make_problem(cfg, seed=args.seed)
-        for _ in range(args.warmup):
-            O.solve(prob)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            O.solve(prob)
-        dt = time.perf_counter() - t0
-        value = args.steps / dt
+        work = lambda: (O.solve(prob), 1)[1]  # noqa: E731
         sample = f"one full oracle solve of the config-{cfg} problem per step (single thread)"
-        cores = 1
+        units = 1
+    t_w0 = time.perf_counter()
+    cores = 1
+    for i in range(args.warmup):
+        cores = work()
+        if time.perf_counter() - t_w0 > REF_BUDGET_S / 5:   # one warm-up is enough for a slow solve
+            break
+    done, t0 = 0, time.perf_counter()
+    while done < args.steps:
+        cores = work()
+        done += 1
+        if time.perf_counter() - t0 > REF_BUDGET_S:
+            break
+    dt = time.perf_counter() - t0
+    value = units * done / dt
+    if done < args.steps:
+        sample += f"; {done} of the {args.steps} requested steps timed (bounded at {REF_BUDGET_S:.0f} s)"
     out = {"metric": METRIC, "value": round(value, 4), "unit": "solves/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 4),
+           "steps": done, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / done, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded, BASELINE config shapes)", "impl": "reference",
-           "config": {"workload": workload_desc(cfg, args.batch), "config_index": cfg, "seed": args.seed},
+           "config": config_dict(cfg, args, world),
            "cpu_baseline": {"value": round(value, 4), "unit": "solves/s", "cores": cores, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": round(value, 4), "unit": "solves/s", "h2d_bytes_per_step": 0,
@@ -481,6 +677,8 @@ def main():
     args = parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:

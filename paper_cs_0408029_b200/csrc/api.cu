@@ -1224,6 +1224,7 @@ nnls_status nnls_run_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n
   nnls_status st = batched_prepare(h, batch, m, n, nnz_off, rowptr, colind, vals, b);
   if (st != NNLS_OK) return st;
   if (chunk <= 0) chunk = 8192;
+  if (chunk > batch) chunk = batch;  // (a huge chunk means one chunk; no int overflow below)
   const int nch = (batch + chunk - 1) / chunk;
   cudaStream_t s = h->stream;
   if (!h->s_in) CK(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));

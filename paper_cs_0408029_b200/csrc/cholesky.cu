@@ -688,10 +688,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   // helpers: BUF(0) = S, BUF(1..4) = operand double-buffers.
   // chain: BUF(0)/BUF(1) = diagonal tile of column j (alternating), BUF(5) = A/L(j+1,j)
   __shared__ double rinv[T];
-  __shared__ int s_task, s_ready, s_bad;
+  __shared__ int s_task, s_ready, s_bad, s_role;
   const int f = st->f;
   const int epoch = st->epoch;
   if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
+  // Role by arrival, not by blockIdx: the first CTA that runs walks the
+  // diagonal (helpers spin on its flags, so it must be a CTA that is already
+  // resident -- a CTA with a fixed index might not be, under MPS or beside
+  // other kernels); the second empties the back-substitution mailboxes.
+  if (threadIdx.x == 0) s_role = atomicAdd(&st->role_factor, 1);
+  __syncthreads();
+  const int role = s_role;
   const int ntc = (f + T - 1) / T;      // tile columns to factor
   // tile columns [0, jq) of rows [0, jq) are kept from the previous pivot
   // iteration (same order prefix, see order_free_set in pivot.cu)
@@ -703,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   FlagSet F{flags, flags + tri, flags + 2 * tri, flags + 2 * tri + 4 * (boxlen / T)};
   const int tid = threadIdx.x;
   double* S = smem;
-  if (blockIdx.x == 1) {  // empty this epoch's back-substitution mailboxes (see box_empty)
+  if (role == 1) {  // empty this epoch's back-substitution mailboxes (see box_empty)
     unsigned long long* xb = box + (size_t)(2 * (epoch & 1)) * boxlen;
     for (int e = tid; e < ntc * T; e += kThreads) {
       xb[e] = box_empty(epoch);
@@ -711,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
     }
   }
 
-  if (blockIdx.x == 0) {
+  if (role == 0) {
     PROF_STAMP(1198, 0);
     // ============================== the diagonal chain
     // BUF(0)/BUF(1): diagonal tile of column j (alternating), BUF(2): Linv_jj,
@@ -1359,14 +1366,16 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(BsArgs a, DevS
   // griddepcontrol.wait).  Large F: its CTAs would only compete with this
   // kernel for the SMs and the memory system, so it starts at our exit.
   if (st->f <= kDualPrefetch) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  __shared__ int s_task;
+  __shared__ int s_task, s_role;
   const int f = st->f;
   const int epoch = st->epoch;
   if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
   const int ntc = (f + T - 1) / T;
   a.xbox = a.box + (size_t)(2 * (epoch & 1)) * a.boxlen;
   a.abox = a.xbox + a.boxlen;
-  if (blockIdx.x == 0) {
+  if (threadIdx.x == 0) s_role = atomicAdd(&st->role_solve, 1);  // first CTA to run: the chain
+  __syncthreads();
+  if (s_role == 0) {
     backsolve_chain(a, f, epoch, bsm);
     return;
   }
@@ -1381,15 +1390,16 @@ __global__ void __launch_bounds__(kThreads) chol_backsolve_kernel(BsArgs a, DevS
 }
 
 static cudaError_t set_attrs() {
-  static bool attr_set = false;
-  if (attr_set) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(chol_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * kSmemDoubles));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsSmem);
-  if (e != cudaSuccess) return e;
-  attr_set = true;
-  return cudaSuccess;
+  static DeviceOnce once;  // (per device: attributes are per device)
+  cudaError_t err = cudaSuccess;
+  const int ok = device_once(once, [&]() {
+    err = cudaFuncSetAttribute(chol_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(sizeof(double) * kSmemDoubles));
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(chol_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsSmem);
+    return err == cudaSuccess ? 1 : 0;
+  });
+  return ok ? cudaSuccess : err;
 }
 
 cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,

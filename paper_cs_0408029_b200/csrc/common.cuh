@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+
 #define NNLS_DEV __device__ __forceinline__
 
 namespace nnls {
@@ -33,6 +36,8 @@ struct DevState {
   int32_t lsqr_iterations, lsqr_stop, infeasible_after_lsqr, free_count;
   double objective, kkt_min_x, kkt_min_y, kkt_max_comp, kkt_dot;
   int32_t reuse_cols;   // leading tile columns of the last factor still valid (factor reuse)
+  int32_t role_factor;  // CTA role tickets of the factorization / back-substitution kernels:
+  int32_t role_solve;   // the first CTA to run takes the chain (reset with the task counters)
   int32_t pad1;
 };
 
@@ -109,6 +114,33 @@ NNLS_DEV unsigned long long dbits(double v) { return (unsigned long long)__doubl
 // stream drains, and waits here before touching the predecessor's results.
 // A no-op for a kernel launched without the attribute.
 NNLS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+// Per-device cached host setup (kernel attributes set with
+// cudaFuncSetAttribute are per device): state[dev] = the value init()
+// returned for the CURRENT device (0 = not yet / failed: retried next call),
+// computed once under a mutex.
+constexpr int kMaxDevices = 64;
+struct DeviceOnce {
+  std::atomic<int> state[kMaxDevices];
+  std::mutex mu;
+  DeviceOnce() {
+    for (auto& v : state) v.store(0, std::memory_order_relaxed);
+  }
+};
+template <typename F>
+inline int device_once(DeviceOnce& o, F init) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return init();
+  int v = o.state[dev].load(std::memory_order_acquire);
+  if (v != 0) return v;
+  std::lock_guard<std::mutex> g(o.mu);
+  v = o.state[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    v = init();
+    o.state[dev].store(v, std::memory_order_release);
+  }
+  return v;
+}
 
 bool pdl_enabled();  // (env NNLS_NO_PDL=1 disables; api.cu)
 template <typename... KArgs, typename... Args>

@@ -566,13 +566,13 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
                         int exact_lmin) {
   (void)m;
   if (exact && (size_t)n * sizeof(double) <= 160 * 1024) {
-    static bool attr_x = false;
-    if (!attr_x) {
-      cudaError_t e = cudaFuncSetAttribute(gram_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(160 * 1024));
-      if (e != cudaSuccess) return e;
-      attr_x = true;
-    }
+    static DeviceOnce attr_x;
+    cudaError_t ea = cudaSuccess;
+    if (!device_once(attr_x, [&]() {
+          ea = cudaFuncSetAttribute(gram_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(160 * 1024));
+          return ea == cudaSuccess ? 1 : 0;
+        }))
+      return ea;
     const size_t smem = sizeof(double) * (size_t)n;
     int per_sm = (int)((224 * 1024) / (smem + 9 * 1024));  // (8.3 KB static per CTA)
     if (per_sm > 4) per_sm = 4;
@@ -590,13 +590,13 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
   const size_t smem = sizeof(double) * (size_t)chunk * wpb;
-  static bool attr = false;  // once, at the maximum (a driver round trip per call otherwise)
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(200 * 1024));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static DeviceOnce attr;  // once per device, at the maximum (a driver round trip per call otherwise)
+  cudaError_t ea = cudaSuccess;
+  if (!device_once(attr, [&]() {
+        ea = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024));
+        return ea == cudaSuccess ? 1 : 0;
+      }))
+    return ea;
   int per_sm = (int)(220 * 1024 / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
   if (per_sm * wpb > 16) per_sm = 16 / wpb;  // ~126 registers: at most 16 warps per SM

@@ -1058,11 +1058,10 @@ cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host,
   if (Ly.bytes > 220 * 1024) return cudaErrorNotSupported;
   // attributes and the co-residency check are host round trips: do them once
   // at the maximum shared-memory size (valid for every smaller launch)
-  static int checked = 0;  // 0 unknown, 1 supported, -1 not supported
+  static DeviceOnce once;  // per device: 1 supported, -1 not supported
   constexpr size_t kMaxSmem = 220 * 1024;
-  cudaError_t e;
-  if (checked == 0) {
-    e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int checked = device_once(once, [&]() {
+    cudaError_t e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kMaxSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lsqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1081,9 +1080,9 @@ cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host,
       q.numAttrs = 1;
       e = cudaOccupancyMaxActiveClusters(&nclusters, lsqr_cluster_kernel, &q);
     }
-    checked = (e == cudaSuccess && nclusters >= 1) ? 1 : -1;
     cudaGetLastError();
-  }
+    return (e == cudaSuccess && nclusters >= 1) ? 1 : -1;
+  });
   if (checked < 0) return cudaErrorNotSupported;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kMaxC);

@@ -408,6 +408,8 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
     st->epoch += 1;
     st->tile_counter = 0;
     st->solve_counter = 0;
+    st->role_factor = 0;
+    st->role_solve = 0;
     st->below_bits = 0ull;
     st->above_bits = dbits(INFINITY);
     const int it = st->iter;

@@ -542,25 +542,40 @@ def test_graph_replay_across_loads(P):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_row_sharded_gram_path(P, world):
-    """nnls_setup_shard on each row block + summed [G | c] buffers (the
-    all-reduce, done here by torch on one GPU) + nnls_gram_finalize: the Gram
+    """Root ShardSolver (full A, its own rows) + BlockSolver ranks (ONLY their
+    row block uploaded) -> packed partial [G | c] buffers, summed here by torch
+    on one GPU (what dist.reduce_gram does across GPUs) -> nnls_gram_finalize:
+    the packed partials equal the oracle's row-block Grams, the finalized Gram
     is bitwise the full one and the solve matches the oracle."""
-    from paper_cs_0408029_b200.dist import gram_tensor, row_shards
+    from paper_cs_0408029_b200.dist import gram_tensor, packed_count, row_block, row_shards
     prob = g.make_problem(1, 5)
-    shards = [P.ShardSolver(prob.m, prob.n, prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1)
-              for r0, r1 in row_shards(prob.m, world)]
+    sh = row_shards(prob.m, world)
+    root = P.ShardSolver(prob.m, prob.n, prob.rowptr, prob.colind, prob.vals, prob.b, *sh[0])
+    blocks = []
+    for r0, r1 in sh[1:]:
+        rp, ci, v, b = row_block(prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1)
+        blocks.append((P.BlockSolver().load_block(r1 - r0, prob.n, rp, ci, v, b), (rp, ci, v, b, r1 - r0)))
     torch.cuda.synchronize()
     with pytest.raises(P.NNLSError):
-        shards[0].solve()                                  # not finalized yet
-    acc = gram_tensor(shards[0])
-    for s in shards[1:]:
-        acc += gram_tensor(s)
+        root.solve()                                       # not finalized yet
+    with pytest.raises(P.NNLSError):
+        blocks[0][0].solve()                               # a block-only handle never solves
+    n = prob.n
+    tril = np.tril_indices(n)
+    for S, (rp, ci, v, b, mb) in blocks:                   # packed layout: row i = G[i, :i+1]
+        buf = gram_tensor(S).cpu().numpy()
+        assert buf.size == packed_count(n)
+        Gb, cb = O.gram(g.Problem(mb, n, rp, ci, v, b, prob.x_gen, prob.kind, prob.seed))
+        assert np.array_equal(buf[:n * (n + 1) // 2], Gb[tril]) and np.array_equal(buf[n * (n + 1) // 2:], cb)
+    acc = gram_tensor(root)
+    for S, _ in blocks:
+        acc += gram_tensor(S)
     torch.cuda.synchronize()
-    shards[0].finalize()
-    G, c = shards[0].gram()
+    root.finalize()
+    G, c = root.gram()
     Go, co = O.gram(prob)
     assert np.array_equal(G, Go) and np.array_equal(c, co)
-    x, info = shards[0].solve()
+    x, info = root.solve()
     r = O.solve(prob)
-    assert np.array_equal(shards[0].free_set(), r["mask"]) and info["iterations"] == r["iterations"]
+    assert np.array_equal(root.free_set(), r["mask"]) and info["iterations"] == r["iterations"]
     assert rel(x, r["x"]) <= TOL_X
