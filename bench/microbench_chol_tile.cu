@@ -10,6 +10,7 @@
 #include "trsm_blocked.cuh"
 
 using namespace nnls;
+bool nnls::pdl_enabled() { return false; }
 
 // reference versions (previous product code) for timing / cross-checks
 namespace nnls {

@@ -679,7 +679,128 @@ __device__ __forceinline__ void left_update(double* __restrict__ smem, double* _
   csync();
 }
 
-__global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
+// ---------------------------------------------------------------------------
+// Helper operand pipeline (warp-specialized).  A helper CTA is 8 consumer
+// warps (the DMMA updates, 256 threads as everywhere in this file) plus one
+// PRODUCER warp: per left-looking update k of the task's tile (i, jj) it polls
+// the release flags of L(i,k) and L(jj,k), then moves both tiles into a ring
+// stage with ONE bulk copy each (cp.async.bulk, completion on the stage's
+// "full" mbarrier); the consumers wait on that mbarrier, run the 64x64x64
+// DMMA update with the accumulator in registers, and release the stage on
+// its "empty" mbarrier.  No CTA-wide barrier per update; up to kStages
+// updates' operands are in flight while one is computed.  Linv_jj (T tasks)
+// is one more stage.
+constexpr int kStages = 3;              // ring stages of two tile slots (6 tiles = the whole smem)
+constexpr int kHelperThreads = kThreads + 32;
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ring_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void ring_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void ring_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void ring_wait(unsigned long long* b, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void ring_load_tile(double* dst, const double* src, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "n"(TS * 8), "r"(smem_addr(b))
+               : "memory");
+}
+// the 9-warp barrier of a helper CTA (task hand-off)
+__device__ __forceinline__ void hsync() { asm volatile("bar.sync 3, %0;\n" ::"n"(kHelperThreads) : "memory"); }
+
+struct HelperRing {
+  unsigned long long full[kStages], empty[kStages];
+};
+
+// producer (lane 0 of warp 8): stage `cnt` of the running sequence <- L(i,k),
+// L(jj,k) for k < kmax (flags waited only for rows >= jq: kept rows need
+// none), then (linv_j >= 0) Linv_{linv_j} alone.  cnt advances by the stages used.
+__device__ __forceinline__ void ring_produce(HelperRing& R, double* ring, const double* __restrict__ Lt,
+                                             const double* __restrict__ Linv, const FlagSet& F, int epoch, int i,
+                                             int jj, int kmax, int jq, int linv_j, unsigned& cnt) {
+  for (int k = 0; k < kmax + (linv_j >= 0 ? 1 : 0); ++k, ++cnt) {
+    const int sidx = (int)(cnt % kStages);
+    const unsigned use = cnt / kStages;
+    if (use > 0) ring_wait(&R.empty[sidx], (use - 1) & 1);
+    double* slot = ring + (size_t)(2 * sidx) * TS;
+    if (k < kmax) {
+      if (i >= jq) wait_flag(&F.full[tidx(i, k)], epoch);
+      if (jj >= jq) wait_flag(&F.full[tidx(jj, k)], epoch);
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");  // (acquired data -> async-proxy reads)
+      ring_expect(&R.full[sidx], 2u * TS * 8);
+      ring_load_tile(slot, Lt + (size_t)tidx(i, k) * TS, &R.full[sidx]);
+      ring_load_tile(slot + TS, Lt + (size_t)tidx(jj, k) * TS, &R.full[sidx]);
+    } else {
+      if (linv_j >= jq) wait_flag(&F.inv[linv_j], epoch);
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      ring_expect(&R.full[sidx], 1u * TS * 8);
+      ring_load_tile(slot, Linv + (size_t)linv_j * TS, &R.full[sidx]);
+    }
+  }
+}
+
+// [G_FF; c_F^T] tile (i, jj) gathered straight into this warp's accumulator
+// fragment (rows rb0.., columns cb0.., as acc_load would read them from S)
+__device__ __forceinline__ void gather_acc(double (&acc)[2][4][2], const double* __restrict__ G, int ldg,
+                                           const double* __restrict__ cvec, const int32_t* __restrict__ Fidx,
+                                           int f, int i, int jj, int lane, int rb0, int cb0) {
+  const int rv = min(T, f + 1 - i * T), cv = min(T, f - jj * T);
+  int gr[2], gc[8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int r = rb0 + 8 * a + (lane >> 2);
+    gr[a] = (r < rv) ? ((i * T + r < f) ? Fidx[i * T + r] : -1) : -2;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int cc = cb0 + 8 * q + 2 * (lane & 3) + v;
+      gc[2 * q + v] = (cc < cv) ? Fidx[jj * T + cc] : -1;
+    }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int r = rb0 + 8 * a + (lane >> 2), cc = cb0 + 8 * q + 2 * (lane & 3) + v;
+        const int gcv = gc[2 * q + v];
+        double x = 0.0;
+        if (gr[a] != -2 && gcv >= 0 && (i != jj || cc <= r))
+          x = (gr[a] >= 0) ? G[(size_t)gr[a] * ldg + gcv] : cvec[gcv];
+        acc[a][q][v] = x;
+      }
+}
+
+// consumers: the kmax updates acc -= L(i,k) L(jj,k)^T from the ring
+__device__ __forceinline__ void ring_consume_updates(HelperRing& R, const double* ring, double (&acc)[2][4][2],
+                                                     int kmax, unsigned& cnt, int lane, int rb0, int cb0) {
+  for (int k = 0; k < kmax; ++k, ++cnt) {
+    const int sidx = (int)(cnt % kStages);
+    ring_wait(&R.full[sidx], (cnt / kStages) & 1);
+    const double* slot = ring + (size_t)(2 * sidx) * TS;
+    dmma_tile<true>(acc, slot, slot + TS, lane, rb0, cb0);
+    __syncwarp();
+    if (lane == 0) ring_arrive(&R.empty[sidx]);
+  }
+}
+
+__global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
     const double* __restrict__ G, int ldg, const double* __restrict__ cvec,
     const int32_t* __restrict__ Fidx, double* __restrict__ Lt, double* __restrict__ Linv,
     int* __restrict__ flags, int tri, DevState* st, unsigned long long* __restrict__ box, int boxlen) {
@@ -710,7 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   FlagSet F{flags, flags + tri, flags + 2 * tri, flags + 2 * tri + 4 * (boxlen / T)};
   const int tid = threadIdx.x;
   double* S = smem;
-  if (role == 1) {  // empty this epoch's back-substitution mailboxes (see box_empty)
+  if (role == 1 && tid < kThreads) {  // empty this epoch's back-substitution mailboxes (see box_empty)
     unsigned long long* xb = box + (size_t)(2 * (epoch & 1)) * boxlen;
     for (int e = tid; e < ntc * T; e += kThreads) {
       xb[e] = box_empty(epoch);
@@ -719,6 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   }
 
   if (role == 0) {
+    if (tid >= kThreads) return;  // (the chain runs on 8 warps; its named barriers count 256 / 224 threads)
     PROF_STAMP(1198, 0);
     // ============================== the diagonal chain
     // BUF(0)/BUF(1): diagonal tile of column j (alternating), BUF(2): Linv_jj,
@@ -844,11 +966,23 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
   // all its updates k < jq (the chain starts there); then per column j >= jq:
   // [P(j+1,j+1)?, P(j+1,j)?, T(j+2..ntr-1, j)]
   const int lane = tid & 31, w = tid >> 5;
+  __shared__ HelperRing R;
+  if (tid == 0) {
+    for (int k = 0; k < kStages; ++k) {
+      ring_mbar_init(&R.full[k], 1);
+      ring_mbar_init(&R.empty[k], kThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  unsigned rcnt = 0;  // ring stages used so far (identical sequence on both sides)
   for (;;) {
+    // (this thread's generic smem accesses of the last task -> before the
+    // bulk copies the producer issues into the same memory after the barrier)
+    fence_proxy_async_smem();
     if (tid == 0) s_task = atomicAdd(&st->tile_counter, 1);
-    csync();
+    hsync();
     int t = s_task;
-    csync();
+    hsync();
     int j = jq, kind = -1, i = 0, half = 0;
     if (jq > 0) {
       // [W(1..jq-1)] [T(jq..ntr-1, 0)] [row-chain tasks for 0 < j < jq] [D(jq)]; the
@@ -892,6 +1026,58 @@ __global__ void __launch_bounds__(kThreads, 1) chol_factor_kernel(
       ++j;
     }
     if (kind < 0) break;
+    // ---- pipelined kinds: P(j+1,j+1), P(j+1,j), T(i,j) outside a restart row chain, D(jq)
+    const bool piped = kind == 0 || kind == 1 || kind == 3 || (kind == 2 && !(j < jq && j > 0));
+    if (piped) {
+      const int ti = kind == 3 ? jq : (kind == 2 ? i : j + 1);
+      const int tj = kind == 3 ? jq : (kind == 0 ? j + 1 : j);
+      const int kmax = kind == 3 ? jq : j;
+      const bool trsm = kind == 2;
+      double* ring = smem;
+      if (w == kThreads / 32) {  // ---- producer warp
+        if (lane == 0) ring_produce(R, ring, Lt, Linv, F, epoch, ti, tj, kmax, jq, trsm ? tj : -1, rcnt);
+        else rcnt += kmax + (trsm ? 1 : 0);
+        continue;
+      }
+      // ---- consumer warps 0..7
+      const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
+      double acc[2][4][2];
+      gather_acc(acc, G, ldg, cvec, Fidx, f, ti, tj, lane, rb0, cb0);
+      ring_consume_updates(R, ring, acc, kmax, rcnt, lane, rb0, cb0);
+      // S: slot B of the next stage (free: the producer waits for the next task)
+      double* Sx = ring + (size_t)(2 * (rcnt % kStages) + 1) * TS;
+      if (trsm) {
+        const int sidx = (int)(rcnt % kStages);
+        csync();  // every warp is past its updates (a fast warp runs up to kStages ahead): Sx is free
+        acc_store(acc, Sx, lane, rb0, cb0);
+        ring_wait(&R.full[sidx], (rcnt / kStages) & 1);  // Linv_jj in slot A
+        csync();
+        double acc8[8][2];
+        gemm_linvT(acc8, Sx, ring + (size_t)(2 * sidx) * TS, w, lane);
+        csync();
+        store_rows8(acc8, Sx, w, lane);
+        csync();
+        store_tile(Lt + (size_t)tidx(ti, tj) * TS, Sx);
+        __syncwarp();
+        if (lane == 0) ring_arrive(&R.empty[sidx]);
+        ++rcnt;
+        publish_flag(&F.full[tidx(ti, tj)], epoch);
+        if (jq > 0 && tj == 0 && ti >= jq && tid == 0) {  // (the restart's half-tile chain starts here)
+          st_release(&F.part[tidx(ti, tj)], epoch);
+          st_release(&F.half1[tidx(ti, tj)], epoch);
+        }
+        if (ti == tj + 2) PROF_STAMP(1000 + tj + 1, 1);
+      } else {
+        // partial tiles go out in the global tile layout straight from the fragments
+        double* dst = Lt + (size_t)tidx(ti, tj) * TS;
+        acc_store(acc, dst, lane, rb0, cb0);
+        publish_flag(&F.part[tidx(ti, tj)], epoch);
+        if (kind == 0) PROF_STAMP(1000 + ti, 2);
+        else if (kind == 1) PROF_STAMP(1000 + tj, 0);
+      }
+      continue;
+    }
+    if (w >= kThreads / 32) continue;  // the producer warp idles through the restart kinds
     if (kind == 6) {                 // Th(i, j, half): rows 32*half.. of L(i,j) below a kept prefix
       // the restart row chain by half tiles: each step is a 32 x 64 x 64
       // product on its own CTA (half the DMMA time of a full tile), the two
@@ -1414,7 +1600,7 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   double* Linv = Lt + (size_t)tri_tiles(n) * TS;
   const int ntr = (n + 1 + T - 1) / T;
   unsigned long long* box = reinterpret_cast<unsigned long long*>(Lt + ((size_t)tri_tiles(n) + 3 * (size_t)ntr) * TS);
-  return launch_pdl(chol_factor_kernel, dim3(grid), dim3(kThreads), sizeof(double) * kSmemDoubles, s, G, ldg, c,
+  return launch_pdl(chol_factor_kernel, dim3(grid), dim3(kHelperThreads), sizeof(double) * kSmemDoubles, s, G, ldg, c,
                     Fidx, Lt, Linv, flags, tri_tiles(n), st, box, ntr * T);
 }
 
