@@ -23,7 +23,9 @@ for r in rows[1:]:
     if n in want:
         kern.setdefault(k, {})[n] = (r[ix["Metric Value"]] + " " + r[ix["Metric Unit"]]).strip()
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
-                      "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                      "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+                      "sm__ops_path_tensor_src_fp64.sum,sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed,"
+                      "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"],
                      capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
 if len(rr) > 2:
@@ -31,7 +33,9 @@ if len(rr) > 2:
     for r in rr[2:]:
         d = dict(zip(h, r))
         k = d.get("Kernel Name", "").split("(")[0] + "#" + d.get("ID", "")
-        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                  "sm__ops_path_tensor_src_fp64.sum", "sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed",
+                  "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"):
             if m in d:
                 kern.setdefault(k, {})[m] = d[m] + " " + rr[1][h.index(m)]
 for k, v in kern.items():
