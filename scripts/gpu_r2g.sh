@@ -1,0 +1,7 @@
+set -u
+O=gpurun_out/r2g
+mkdir -p $O
+timeout 300 python scripts/lsqr_grid_profile.py 2 > $O/lsqr_grid_c2.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "lsqr or config2 or grid or whole" > $O/pytest.log 2>&1
+timeout 300 python bench.py --no-extra --no-cpu-baseline --steps 10 > $O/bench.json 2> $O/bench.err
+echo done
