@@ -27,7 +27,8 @@ STATUS = {0: "OK", 6: "OOM", 7: "NOT_PD", 8: "ITERATION_LIMIT"}
 class Params(C.Structure):
     _fields_ = [("zero_tol", C.c_double), ("p_max", C.c_int32), ("max_iter", C.c_int32),
                 ("lsqr_mode", C.c_int32), ("lsqr_atol", C.c_double), ("lsqr_btol", C.c_double),
-                ("lsqr_conlim", C.c_double), ("lsqr_itn_limit", C.c_int32)]
+                ("lsqr_conlim", C.c_double), ("lsqr_itn_limit", C.c_int32), ("notpd_fallback", C.c_int32),
+                ("adaptive_threshold", C.c_double)]
 
 
 class Info(C.Structure):
@@ -35,7 +36,8 @@ class Info(C.Structure):
                 ("free_count", C.c_int32), ("lsqr_iterations", C.c_int32), ("lsqr_stop", C.c_int32),
                 ("infeasible_after_lsqr", C.c_int32), ("pad", C.c_int32),
                 ("objective", C.c_double), ("kkt_min_x", C.c_double), ("kkt_min_y", C.c_double),
-                ("kkt_max_comp", C.c_double), ("kkt_dot", C.c_double)]
+                ("kkt_max_comp", C.c_double), ("kkt_dot", C.c_double), ("kappa", C.c_double),
+                ("refined", C.c_int32), ("lsqr_fallbacks", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
@@ -77,6 +79,10 @@ def lib():
                               P, P, P, P, P, i32]
         L.or_lsqr.restype = i32
         L.or_kkt.argtypes = [i32, i32, P, P, P, P, P, P]
+        L.or_condest.argtypes = [i32, P, C.c_double]
+        L.or_condest.restype = C.c_double
+        L.or_norm1.argtypes = [i32, P]
+        L.or_norm1.restype = C.c_double
         L.or_bpp_solve.argtypes = [i32, i32, P, P, P, P, P, P, P, P, P, P, P, i32]
         L.or_bpp_solve.restype = i32
         L.or_bpp_solve_batched.argtypes = [i32, i32, i32, P, P, P, P, P, P, P, P, P, i32]
@@ -100,7 +106,8 @@ def _csr(prob):
 
 def default_params(**kw) -> Params:
     p = Params(zero_tol=1e-12, p_max=3, max_iter=0, lsqr_mode=1, lsqr_atol=1e-15,
-               lsqr_btol=1e-15, lsqr_conlim=1e8, lsqr_itn_limit=0)
+               lsqr_btol=1e-15, lsqr_conlim=1e8, lsqr_itn_limit=0, notpd_fallback=0,
+               adaptive_threshold=1e-8)
     for k, v in kw.items():
         setattr(p, k, v)
     return p
@@ -186,6 +193,17 @@ def lsqr(prob, mask=None, rhs=None, atol=1e-15, btol=1e-15, conlim=1e8, itn_limi
                           itn_limit, _p(x), C.byref(itn), C.byref(rn), C.byref(arn), _p(hist), itn_limit)
     return dict(x=x, istop=int(istop), itn=itn.value, rnorm=rn.value, arnorm=arn.value,
                 rnorm_hist=hist[:itn.value].copy())
+
+
+def condest(L, norm1_M):
+    """kappa_1 estimate of M = L L^T (Hager/Higham, as LAPACK dpocon): norm1_M * est(||M^-1||_1)."""
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    return float(lib().or_condest(L.shape[0], _p(L), float(norm1_M)))
+
+
+def norm1(M):
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    return float(lib().or_norm1(M.shape[0], _p(M)))
 
 
 def kkt(prob, x):

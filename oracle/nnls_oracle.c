@@ -46,12 +46,21 @@ typedef struct {
   int32_t lsqr_mode;    /* 0 none, 1 cold recompute, 2 warm   */
   double lsqr_atol, lsqr_btol, lsqr_conlim;
   int32_t lsqr_itn_limit; /* <=0 -> 4*|F|                             */
+  int32_t notpd_fallback; /* 1: a failed Cholesky is replaced by an
+                             LSQR solve on A_F for that iteration  */
+  double adaptive_threshold; /* lsqr_mode 3: LSQR iff kappa*2^-52 > this
+                                ("when a switch ... is necessary";
+                                default 1e-8)                      */
 } or_params;
 
 typedef struct {
   int32_t status, iterations, single_exchanges, free_count;
   int32_t lsqr_iterations, lsqr_stop, infeasible_after_lsqr, pad;
   double objective, kkt_min_x, kkt_min_y, kkt_max_comp, kkt_dot;
+  double kappa;                /* lsqr_mode 3: condition estimate of the final
+                                  (A^T A)_FF (or_condest); else 0           */
+  int32_t refined;             /* 1 if the final x came from LSQR           */
+  int32_t lsqr_fallbacks;      /* NOT_PD iterations solved by LSQR instead  */
 } or_info;
 
 typedef struct {
@@ -190,6 +199,87 @@ int32_t or_exchange(int32_t n, uint8_t* mask, const double* x, const double* y,
   }
   free(infeas);
   return k;
+}
+
+/* ------------------------------------------------------------------------ */
+/* 1-norm condition estimate of M = L L^T (Section 3: "We can estimate
+ * the relative error kappa^2 eps of each normal equations solution by
+ * computing the condition number kappa^2 of A_F^T A_F with the LAPACK
+ * function dpocon").  dpocon returns 1/(||M||_1 est(||M^-1||_1)) where est is
+ * Hager's estimator with Higham's refinements (LAPACK dlacn2, at most 5
+ * iterations, then the alternating-sign test vector); B = M^-1 is applied by
+ * the forward and back substitutions of or_chol_solve (M is symmetric, so
+ * B^T = B).  Written out step by step in dlacn2's order:
+ *   1. x = (1/f, ..., 1/f); y = B x; est = ||y||_1 (f == 1: est = |y_1|, stop)
+ *   2. xi = sign(y); z = B xi; j = argmax_i |z_i|; iter = 2
+ *   3. x = e_j; y = B x; est_old = est; est = ||y||_1
+ *      if sign(y) == xi or est <= est_old: go to 5
+ *      xi = sign(y); z = B xi; jlast = j; j = argmax |z_i|
+ *      if z_jlast != |z_j| and iter < 5: iter += 1, go to 3
+ *   5. x_i = (-1)^(i) (1 + i/(f-1)), i = 0..f-1 (x_0 = +1); y = B x;
+ *      est = max(est, 2 ||y||_1 / (3 f))
+ * sign(0) = +1 (dlacn2).  Returns kappa = norm1_M * est (>= 1 for SPD M). */
+static double asum(int32_t f, const double* v) {
+  double s = 0.0;
+  for (int32_t i = 0; i < f; ++i) s += fabs(v[i]);
+  return s;
+}
+static int32_t iamax(int32_t f, const double* v) {
+  int32_t j = 0;
+  for (int32_t i = 1; i < f; ++i)
+    if (fabs(v[i]) > fabs(v[j])) j = i;
+  return j;
+}
+double or_condest(int32_t f, const double* L, double norm1_M) {
+  if (f <= 0) return 0.0;
+  double* x = (double*)malloc(sizeof(double) * (size_t)f);
+  double* y = (double*)malloc(sizeof(double) * (size_t)f);
+  double* xi = (double*)malloc(sizeof(double) * (size_t)f);
+  double est;
+  for (int32_t i = 0; i < f; ++i) x[i] = 1.0 / (double)f;
+  or_chol_solve(f, L, x, y);                                     /* step 1 */
+  if (f == 1) {
+    est = fabs(y[0]);
+  } else {
+    est = asum(f, y);
+    for (int32_t i = 0; i < f; ++i) xi[i] = y[i] >= 0.0 ? 1.0 : -1.0; /* step 2 */
+    or_chol_solve(f, L, xi, y);
+    int32_t j = iamax(f, y), iter = 2;
+    for (;;) {                                                   /* step 3 */
+      for (int32_t i = 0; i < f; ++i) x[i] = (i == j) ? 1.0 : 0.0;
+      or_chol_solve(f, L, x, y);
+      const double est_old = est;
+      est = asum(f, y);
+      int32_t same = 1;
+      for (int32_t i = 0; i < f; ++i)
+        if ((y[i] >= 0.0 ? 1.0 : -1.0) != xi[i]) { same = 0; break; }
+      if (same || est <= est_old) break;   /* converged / cycling (dlacn2 keeps est) */
+      for (int32_t i = 0; i < f; ++i) xi[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+      or_chol_solve(f, L, xi, y);
+      const int32_t jlast = j;
+      j = iamax(f, y);
+      if (y[jlast] != fabs(y[j]) && iter < 5) { iter += 1; continue; }   /* (signed z_jlast, as dlacn2) */
+      break;
+    }
+    double sgn = 1.0;                                            /* step 5 */
+    for (int32_t i = 0; i < f; ++i) { x[i] = sgn * (1.0 + (double)i / (double)(f - 1)); sgn = -sgn; }
+    or_chol_solve(f, L, x, y);
+    const double temp = 2.0 * asum(f, y) / (3.0 * (double)f);
+    if (temp > est) est = temp;
+  }
+  free(x); free(y); free(xi);
+  return norm1_M * est;
+}
+
+/* ||M||_1 = max_j sum_i |M_ij| (M symmetric f x f, row-major).            */
+double or_norm1(int32_t f, const double* M) {
+  double mx = 0.0;
+  for (int32_t j = 0; j < f; ++j) {
+    double s = 0.0;
+    for (int32_t i = 0; i < f; ++i) s += fabs(M[(size_t)i * f + j]);
+    if (s > mx) mx = s;
+  }
+  return mx;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -368,9 +458,11 @@ int32_t or_bpp_solve(int32_t m, int32_t n, const int32_t* rowptr, const int32_t*
   double* L = (double*)malloc(sizeof(double) * (size_t)n * n);
   double* rhs = (double*)malloc(sizeof(double) * (size_t)n);
   double* xf = (double*)malloc(sizeof(double) * (size_t)n);
-  if (!G || !c || !x || !y || !mask || !Fidx || !M || !L || !rhs || !xf) {
+  double* xfb = (double*)malloc(sizeof(double) * (size_t)n);
+  int32_t last_factored = 0;  /* the last update solved the normal equations (L, M hold its factor) */
+  if (!G || !c || !x || !y || !mask || !Fidx || !M || !L || !rhs || !xf || !xfb) {
     info->status = OR_OOM;
-    free(G); free(c); free(x); free(y); free(mask); free(Fidx); free(M); free(L); free(rhs); free(xf);
+    free(G); free(c); free(x); free(y); free(mask); free(Fidx); free(M); free(L); free(rhs); free(xf); free(xfb);
     return OR_OOM;
   }
   /* Gram caching: A^T A and A^T b formed once. */
@@ -392,13 +484,27 @@ int32_t or_bpp_solve(int32_t m, int32_t n, const int32_t* rowptr, const int32_t*
     int32_t f = 0;
     for (int32_t i = 0; i < n; ++i) if (mask[i]) Fidx[f++] = i;
     for (int32_t j = 0; j < n; ++j) x[j] = 0.0;
+    last_factored = 0;
     if (f > 0) {
       or_gather(n, G, f, Fidx, M);
       int32_t rc = or_cholesky(f, M, L);
-      if (rc != 0) { status = OR_NOT_PD; break; }   /* iterations = completed solves */
-      for (int32_t a = 0; a < f; ++a) rhs[a] = c[Fidx[a]];
-      or_chol_solve(f, L, rhs, xf);
-      for (int32_t a = 0; a < f; ++a) x[Fidx[a]] = xf[a];
+      if (rc != 0 && !prm->notpd_fallback) { status = OR_NOT_PD; break; }   /* iterations = completed solves */
+      if (rc != 0) {
+        /* S:366 reading c13b: the normal equations failed ("may fail
+         * entirely when kappa^2 eps >= 1"), so x_F for this iteration comes
+         * from LSQR on A_F (cold start, the final step's tolerances) */
+        int32_t itn_fb = 0, lim = prm->lsqr_itn_limit > 0 ? prm->lsqr_itn_limit : 4 * f;
+        double rn_fb, arn_fb;
+        or_lsqr(m, n, rowptr, colind, vals, mask, b, prm->lsqr_atol, prm->lsqr_btol, prm->lsqr_conlim, lim,
+                xfb, &itn_fb, &rn_fb, &arn_fb, NULL, 0);
+        for (int32_t a = 0; a < f; ++a) x[Fidx[a]] = xfb[Fidx[a]];
+        info->lsqr_fallbacks += 1;
+      } else {
+        for (int32_t a = 0; a < f; ++a) rhs[a] = c[Fidx[a]];
+        or_chol_solve(f, L, rhs, xf);
+        for (int32_t a = 0; a < f; ++a) x[Fidx[a]] = xf[a];
+        last_factored = 1;
+      }
     }
     /* ... and y_G by Eq. 5 (Gram form), from the unclamped x_F (c3) */
     or_dual_gram(n, G, c, mask, x, y);
@@ -420,14 +526,24 @@ int32_t or_bpp_solve(int32_t m, int32_t n, const int32_t* rowptr, const int32_t*
   int32_t fcount = 0;
   for (int32_t i = 0; i < n; ++i) fcount += mask[i];
   if (x_ne_out) for (int32_t j = 0; j < n; ++j) x_ne_out[j] = x[j];
+  /* lsqr_mode 3 (reading c23): the condition estimate of the final
+   * (A^T A)_FF decides whether the final LSQR is needed: predicted relative
+   * error kappa * 2^-52 ("c kappa^2 eps") above the threshold.
+   * A final F solved by the LSQR fallback has no factor: kappa = inf. */
+  int32_t do_lsqr = prm->lsqr_mode == 1 || prm->lsqr_mode == 2;
+  if (status == OR_OK && prm->lsqr_mode == 3 && fcount > 0) {
+    info->kappa = last_factored ? or_condest(fcount, L, or_norm1(fcount, M)) : INFINITY;
+    do_lsqr = info->kappa * ldexp(1.0, -52) > prm->adaptive_threshold;
+  }
   /* recompute the final solution on the final F with LSQR (c15, c16) */
-  if (status == OR_OK && prm->lsqr_mode != 0 && fcount > 0) {
+  if (status == OR_OK && do_lsqr && fcount > 0) {
+    info->refined = 1;
     int32_t itn_lim = prm->lsqr_itn_limit > 0 ? prm->lsqr_itn_limit : 4 * fcount;
     double* rhs_m = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
     double* dx = (double*)malloc(sizeof(double) * (size_t)n);
     double rn, arn;
     int32_t itn = 0, istop;
-    if (prm->lsqr_mode == 1) {                 /* cold start: rhs = b */
+    if (prm->lsqr_mode != 2) {                 /* cold start: rhs = b (modes 1, 3) */
       for (int32_t i = 0; i < m; ++i) rhs_m[i] = b[i];
       istop = or_lsqr(m, n, rowptr, colind, vals, mask, rhs_m, prm->lsqr_atol, prm->lsqr_btol,
                       prm->lsqr_conlim, itn_lim, dx, &itn, &rn, &arn, NULL, 0);
@@ -465,7 +581,7 @@ int32_t or_bpp_solve(int32_t m, int32_t n, const int32_t* rowptr, const int32_t*
   info->single_exchanges = singles;
   info->free_count = fcount;
   or_kkt(m, n, rowptr, colind, vals, b, x, info);
-  free(G); free(c); free(x); free(y); free(mask); free(Fidx); free(M); free(L); free(rhs); free(xf);
+  free(G); free(c); free(x); free(y); free(mask); free(Fidx); free(M); free(L); free(rhs); free(xf); free(xfb);
   return status;
 }
 
