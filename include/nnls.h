@@ -68,13 +68,27 @@ typedef struct {
                              1 (default): recompute x on the final F with
                              LSQR from x = 0 ("recomputing the final
                              solution");  2: LSQR correction started from
-                             the normal-equations x                          */
+                             the normal-equations x;  3: adaptive -- a
+                             1-norm condition estimate kappa of the final
+                             (A^T A)_FF from its Cholesky factor (P:129,
+                             LAPACK dpocon's estimator) decides: LSQR as in
+                             mode 1 iff kappa * 2^-52 > adaptive_threshold,
+                             else the normal-equations x                    */
   int32_t lsqr_itn_limit; /* 0 -> 4*|F|                              */
   double lsqr_atol;       /* 1e-15                                   */
   double lsqr_btol;       /* 1e-15                                           */
   double lsqr_conlim;     /* 1e8                                             */
   int32_t trace;          /* != 0: record one nnls_iter_rec per pivot       */
   int32_t kkt;            /* != 0 (default): fill the KKT fields of nnls_info */
+  double adaptive_threshold; /* lsqr_mode 3: predicted relative error above
+                                which LSQR runs (default 1e-8)       */
+  int32_t notpd_fallback; /* != 0: a Cholesky failure ("may fail
+                             entirely when kappa^2 eps >= 1") no longer ends
+                             the solve: that iteration's x_F comes from LSQR
+                             on A_F (cold start, the lsqr_* tolerances) and
+                             pivoting continues.  Single-problem
+                             handles only; batched handles return NOT_PD. */
+  int32_t reserved;
 } nnls_params;
 
 /* Per-solve report. */
@@ -93,6 +107,10 @@ typedef struct {
   double kkt_min_y;           /* min_i y'_i, y' = A^T (A x - b) recomputed  */
   double kkt_max_comp;        /* max_i |x_i y'_i|                           */
   double kkt_dot;             /* <x, y'>                                    */
+  double kappa;               /* lsqr_mode 3: the condition estimate of the
+                                 final (A^T A)_FF (0 in the other modes)    */
+  int32_t refined;            /* 1 if the final x came from LSQR            */
+  int32_t lsqr_fallbacks;     /* NOT_PD iterations solved by LSQR instead   */
 } nnls_info;
 
 /* One pivot iteration (for parity tests against the oracle's trace). */

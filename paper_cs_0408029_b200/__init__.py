@@ -41,7 +41,8 @@ class Params(C.Structure):
     _fields_ = [("zero_tol", C.c_double), ("p_max", C.c_int32), ("max_iter", C.c_int32),
                 ("lsqr_mode", C.c_int32), ("lsqr_itn_limit", C.c_int32), ("lsqr_atol", C.c_double),
                 ("lsqr_btol", C.c_double), ("lsqr_conlim", C.c_double), ("trace", C.c_int32),
-                ("kkt", C.c_int32)]
+                ("kkt", C.c_int32), ("adaptive_threshold", C.c_double), ("notpd_fallback", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -49,7 +50,8 @@ class Info(C.Structure):
                 ("free_count", C.c_int32), ("lsqr_iterations", C.c_int32), ("lsqr_stop", C.c_int32),
                 ("infeasible_after_lsqr", C.c_int32), ("not_pd_column", C.c_int32),
                 ("objective", C.c_double), ("kkt_min_x", C.c_double), ("kkt_min_y", C.c_double),
-                ("kkt_max_comp", C.c_double), ("kkt_dot", C.c_double)]
+                ("kkt_max_comp", C.c_double), ("kkt_dot", C.c_double), ("kappa", C.c_double),
+                ("refined", C.c_int32), ("lsqr_fallbacks", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

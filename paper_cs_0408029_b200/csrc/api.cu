@@ -100,6 +100,7 @@ struct nnls_handle {
   Buf Lt, flags;                          // Cholesky tiles + DAG flags
   Buf U, V, W, X, R, partials, xfin;      // LSQR / report
   Buf Fval, Fcol, Fcnt;                   // A restricted to the final F (cluster LSQR)
+  Buf cwork;                              // condest vectors (6 n doubles) + ||M||_1 bits; fallback x
   Buf st, err, trace;
   int trace_cap = 0;
   HostState* h = nullptr;                 // pinned readback
@@ -182,7 +183,7 @@ nnls_status set_stream_device(nnls_handle* h, void* stream) {
 
 nnls_status check_params(const nnls_params* p) {
   if (!(p->zero_tol >= 0.0) || p->p_max < 0 || p->max_iter < 0 || p->lsqr_mode < 0 ||
-      p->lsqr_mode > 2)
+      p->lsqr_mode > 3 || !(p->adaptive_threshold >= 0.0))
     return NNLS_ERR_INVALID_ARG;
   return NNLS_OK;
 }
@@ -252,6 +253,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->W, sizeof(double) * (size_t)n));
   CK(ensure(h->X, sizeof(double) * (size_t)n));
   CK(ensure(h->xfin, sizeof(double) * (size_t)n));
+  CK(ensure(h->cwork, sizeof(double) * (7 * (size_t)n + 1)));
   CK(ensure(h->partials, sizeof(double) * 8 * (size_t)(h->sms * 4)));
   CK(ensure(h->st, sizeof(DevState)));
   CK(ensure(h->err, sizeof(int) * 64));  // [0..3] error bits / longest row, column; [4..] LSQR plan
@@ -384,6 +386,8 @@ nnls_status nnls_params_default(nnls_params* p) {
   p->lsqr_conlim = 1e8;
   p->trace = 0;
   p->kkt = 1;
+  p->adaptive_threshold = 1e-8;
+  p->notpd_fallback = 0;
   return NNLS_OK;
 }
 
@@ -534,8 +538,43 @@ LsqrArgs lsqr_args(nnls_handle* h) {
 
 // cluster-resident LSQR when A's slices fit in one 16-CTA cluster's shared
 // memory (configs 0, 1, 3); the full-grid cooperative kernel otherwise
+cudaError_t launch_lsqr_args(nnls_handle* h, const LsqrArgs& a, cudaStream_t s);
+double* xs_or_null(nnls_handle* h);
+// NOT_PD fallback (notpd_fallback): x_F of the failed iteration from
+// a cold LSQR on A_F (no report), then the pivot loop continues; the next
+// factorization starts from scratch (the failed factor's prefix is not reused)
+cudaError_t launch_fallback(nnls_handle* h, cudaStream_t s) {
+  DevState* st = P<DevState>(h->st);
+  double* xl = P<double>(h->cwork);
+  cudaError_t e = launch_fallback_prep(st, s);
+  if (e != cudaSuccess) return e;
+  LsqrArgs a = lsqr_args(h);
+  a.mode = 1;
+  a.kkt = 0;
+  a.x_out = xl;
+  e = launch_lsqr_args(h, a, s);
+  if (e != cudaSuccess) return e;
+  e = launch_fallback_fixup(h->n, P<int32_t>(h->Fidx), xl, P<double>(h->xF), xs_or_null(h), st, s);
+  if (e != cudaSuccess) return e;
+  if (!h->no_reuse) e = cudaMemsetAsync(h->pos.p, 0xFF, sizeof(int32_t) * (size_t)h->n, s);
+  return e;
+}
+// the final step: (mode 3) the condition estimate, then LSQR + report
+cudaError_t launch_condest_h(nnls_handle* h, cudaStream_t s) {
+  const int n = h->n;
+  double* w = P<double>(h->cwork);
+  return launch_condest(P<double>(h->Gc), h->ldg, P<int32_t>(h->Fidx), P<double>(h->Lt), n, P<DevState>(h->st),
+                        w, reinterpret_cast<unsigned long long*>(w + 7 * (size_t)n), h->prm.adaptive_threshold,
+                        h->sms, s);
+}
 cudaError_t launch_lsqr(nnls_handle* h, cudaStream_t s) {
-  const LsqrArgs a = lsqr_args(h);
+  if (h->prm.lsqr_mode == 3) {
+    cudaError_t ec = launch_condest_h(h, s);
+    if (ec != cudaSuccess) return ec;
+  }
+  return launch_lsqr_args(h, lsqr_args(h), s);
+}
+cudaError_t launch_lsqr_args(nnls_handle* h, const LsqrArgs& a, cudaStream_t s) {
   cudaError_t e = launch_lsqr_compact(a, h->sms, s);  // A restricted to F (both paths)
   if (e != cudaSuccess) return e;
   e = h->no_cluster ? cudaErrorNotSupported : launch_lsqr_cluster_planned(a, h->h->plan, s);
@@ -587,11 +626,11 @@ std::vector<double> graph_key(nnls_handle* h) {
                            (double)h->h->plan[3], p.zero_tol, (double)p.p_max, (double)p.max_iter,
                            (double)p.lsqr_mode, (double)p.lsqr_itn_limit, p.lsqr_atol, p.lsqr_btol,
                            p.lsqr_conlim, (double)p.kkt, (double)h->trace_cap, (double)h->no_cluster,
-                           (double)h->no_reuse};
+                           (double)h->no_reuse, p.adaptive_threshold, (double)p.notpd_fallback};
   const Buf* bufs[] = {&h->rowptr, &h->colind, &h->vals, &h->b, &h->colptr, &h->rowind, &h->cvals,
                        &h->Gc, &h->mask, &h->x, &h->y, &h->xF, &h->Fidx, &h->Gidx, &h->pos, &h->Fs, &h->xs, &h->Lt, &h->flags,
                        &h->U, &h->V, &h->W, &h->X, &h->R, &h->partials, &h->xfin, &h->st, &h->trace,
-                       &h->Fval, &h->Fcol, &h->Fcnt};
+                       &h->Fval, &h->Fcol, &h->Fcnt, &h->cwork};
   for (const Buf* b : bufs) k.push_back((double)(uintptr_t)b->p);
   return k;
 }
@@ -697,8 +736,9 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
   double* c = G + (size_t)n * h->ldg;
   DevState* st = P<DevState>(h->st);
   bool done_graph = false;
-  if (!h->tm.on && !h->no_graph) {
-    // device-resident loop (one graph launch); per-phase timing uses the host loop
+  if (!h->tm.on && !h->no_graph && !p.notpd_fallback) {
+    // device-resident loop (one graph launch); per-phase timing uses the host
+    // loop, and so does the NOT_PD fallback (it needs the host between steps)
     // graphs are captured and launched on a private stream fenced to the
     // caller's stream with events (capture is not allowed on the legacy stream)
     if (!h->gstream) {
@@ -742,6 +782,11 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
         TIMED(NNLS_PH_CHOL_SOLVE, 1,
               launch_chol_backsolve(n, P<double>(h->Lt), P<int>(h->flags), P<double>(h->xF), st,
                                     h->sms, s, P<int32_t>(h->Fidx), xs_or_null(h)));
+        if (p.notpd_fallback) {
+          nnls_status rs2 = read_state(h);
+          if (rs2 != NNLS_OK) return rs2;
+          if (h->h->st.status == 7) TIMED(NNLS_PH_LSQR, 2, launch_fallback(h, s));
+        }
       }
       TIMED(NNLS_PH_DUAL, 1,
             launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
@@ -788,6 +833,11 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
     info->kkt_min_y = hs.kkt_min_y;
     info->kkt_max_comp = hs.kkt_max_comp;
     info->kkt_dot = hs.kkt_dot;
+    info->kappa = hs.kappa;
+    info->refined = (hs.status == 0 && hs.free_count > 0 &&
+                     (h->prm.lsqr_mode == 1 || h->prm.lsqr_mode == 2 || (h->prm.lsqr_mode == 3 && hs.refined)))
+                        ? 1 : 0;
+    info->lsqr_fallbacks = hs.lsqr_fallbacks;
   }
   return status;
 }
@@ -886,7 +936,7 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
                  &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt, &h->b_colview, &h->b_gram,
-                 &h->pos, &h->Fs, &h->xs, &h->Gp};
+                 &h->pos, &h->Fs, &h->xs, &h->Gp, &h->cwork};
   for (Buf* b : bufs) free_buf(*b);
   if (h->s_in) cudaStreamSynchronize(h->s_in);
   if (h->s_out) cudaStreamSynchronize(h->s_out);
@@ -1079,8 +1129,8 @@ nnls_status batched_prepare(nnls_handle* h, int32_t batch, int32_t m, int32_t n,
   CK(ensure(h->b_mask, (size_t)batch * n));
   CK(ensure(h->b_colview, batched_colview_stride(n, (int)nnz_max) * (size_t)batch));
   CK(ensure(h->b_gram, batched_gram_scratch(n, h->sms)));
-  CK(ensure(h->b_info_i, sizeof(int32_t) * 8 * (size_t)batch));
-  CK(ensure(h->b_info_d, sizeof(double) * 5 * (size_t)batch));
+  CK(ensure(h->b_info_i, sizeof(int32_t) * kInfoI * (size_t)batch));
+  CK(ensure(h->b_info_d, sizeof(double) * kInfoD * (size_t)batch));
   return NNLS_OK;
 }
 
@@ -1108,6 +1158,7 @@ BatchArgs batched_args(nnls_handle* h) {
   a.lsqr_mode = p.lsqr_mode;
   a.itn_limit = p.lsqr_itn_limit;
   a.kkt = p.kkt;
+  a.adaptive_threshold = p.adaptive_threshold;
   a.colview = P<uint8_t>(h->b_colview);
   a.cv_stride = batched_colview_stride(h->n, h->ldg);
   a.gram = P<double>(h->b_gram);
@@ -1118,32 +1169,34 @@ BatchArgs batched_args(nnls_handle* h) {
 // per-problem info of problems [p0, p0 + count) from the device arrays
 nnls_status batched_info(nnls_handle* h, int p0, int count, nnls_info* info_out, cudaStream_t s) {
   const size_t nb = (size_t)count;
-  std::vector<int32_t> ii(8 * nb);
-  std::vector<double> dd(5 * nb);
-  CK(cudaMemcpyAsync(ii.data(), P<int32_t>(h->b_info_i) + (size_t)p0 * 8, sizeof(int32_t) * 8 * nb,
+  std::vector<int32_t> ii(kInfoI * nb);
+  std::vector<double> dd(kInfoD * nb);
+  CK(cudaMemcpyAsync(ii.data(), P<int32_t>(h->b_info_i) + (size_t)p0 * kInfoI, sizeof(int32_t) * kInfoI * nb,
                      cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(dd.data(), P<double>(h->b_info_d) + (size_t)p0 * 5, sizeof(double) * 5 * nb,
+  CK(cudaMemcpyAsync(dd.data(), P<double>(h->b_info_d) + (size_t)p0 * kInfoD, sizeof(double) * kInfoD * nb,
                      cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   nnls_status worst = NNLS_OK;
   for (size_t q = 0; q < nb; ++q) {
     nnls_info& o = info_out[q];
     memset(&o, 0, sizeof(o));
-    const int st = ii[q * 8 + 0];
+    const int st = ii[q * kInfoI + 0];
     o.status = st == 7 ? NNLS_ERR_NOT_PD : (st == 8 ? NNLS_ITERATION_LIMIT : NNLS_OK);
     if (o.status != NNLS_OK && worst == NNLS_OK) worst = (nnls_status)o.status;
-    o.iterations = ii[q * 8 + 1];
-    o.single_exchanges = ii[q * 8 + 2];
-    o.free_count = ii[q * 8 + 3];
-    o.lsqr_iterations = ii[q * 8 + 4];
-    o.lsqr_stop = ii[q * 8 + 5];
-    o.infeasible_after_lsqr = ii[q * 8 + 6];
-    o.not_pd_column = ii[q * 8 + 7];
-    o.objective = dd[q * 5 + 0];
-    o.kkt_min_x = dd[q * 5 + 1];
-    o.kkt_min_y = dd[q * 5 + 2];
-    o.kkt_max_comp = dd[q * 5 + 3];
-    o.kkt_dot = dd[q * 5 + 4];
+    o.iterations = ii[q * kInfoI + 1];
+    o.single_exchanges = ii[q * kInfoI + 2];
+    o.free_count = ii[q * kInfoI + 3];
+    o.lsqr_iterations = ii[q * kInfoI + 4];
+    o.lsqr_stop = ii[q * kInfoI + 5];
+    o.infeasible_after_lsqr = ii[q * kInfoI + 6];
+    o.not_pd_column = ii[q * kInfoI + 7];
+    o.objective = dd[q * kInfoD + 0];
+    o.kkt_min_x = dd[q * kInfoD + 1];
+    o.kkt_min_y = dd[q * kInfoD + 2];
+    o.kkt_max_comp = dd[q * kInfoD + 3];
+    o.kkt_dot = dd[q * kInfoD + 4];
+    o.refined = ii[q * kInfoI + 8];
+    o.kappa = dd[q * kInfoD + 5];
   }
   return worst;
 }
@@ -1275,8 +1328,8 @@ nnls_status nnls_run_batched(nnls_handle* h, int32_t batch, int32_t m, int32_t n
     a.b = a0.b + (size_t)p0 * m;
     a.x_out = a0.x_out + (size_t)p0 * n;
     a.mask_out = a0.mask_out + (size_t)p0 * n;
-    a.info_i = a0.info_i + (size_t)p0 * 8;
-    a.info_d = a0.info_d + (size_t)p0 * 5;
+    a.info_i = a0.info_i + (size_t)p0 * kInfoI;
+    a.info_d = a0.info_d + (size_t)p0 * kInfoD;
     a.colview = a0.colview + (size_t)p0 * cvs;
     a.guard = err;
     TIMED(NNLS_PH_BATCHED, 2, launch_batched_nnz(a, h->ldg, h->sms, s));

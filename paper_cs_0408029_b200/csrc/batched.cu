@@ -124,7 +124,7 @@ __device__ long long* g_batch_prof = nullptr;
     }                                                                      \
   } while (0)
 
-__global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
+__global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max) {
   long long bp_t = clock64();
   extern __shared__ double sm[];
   unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
@@ -449,6 +449,120 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
       ++iter;
     }
     BP_MARK(6);  // scatter + dual (+ loop exit)
+    // ---------------------------------------------------------- NEXT-2
+    // lsqr_mode 3: Hager/Higham estimate of kappa_1((A^T A)_FF) from the
+    // final factor (dpocon's estimator, LAPACK dlacn2's steps) on warp 0,
+    // vectors in registers (lane l holds entries l and l+32; f <= 64).
+    double kappa = 0.0;
+    int refined = (status == 0 && f > 0 && (a.lsqr_mode == 1 || a.lsqr_mode == 2)) ? 1 : 0;
+    if (a.lsqr_mode == 3 && status == 0 && f > 0) {
+      if (wid == 0) {
+        // ||M||_1: column j's sum in increasing i (the oracle's order), then the max
+        double cs = 0.0;
+        for (int jq = lane; jq < f; jq += 32) {
+          double t = 0.0;
+          for (int i = 0; i < f; ++i) t += fabs(G[pk(Fidx[i], Fidx[jq])]);
+          cs = fmax(cs, t);
+        }
+        const double norm1 = warp_max(cs);
+        // B v = M^-1 v: forward L z = v (column sweep: each z_i gets its terms in
+        // increasing k, as the oracle), then L^T x = z (column sweep, descending)
+        auto applyB = [&](double v0, double v1, double& o0, double& o1) {
+          double s0 = v0, s1 = v1;
+          for (int j = 0; j < f; ++j) {
+            const int rj = j * (j + 1) / 2;
+            const double own = (j < 32) ? s0 : s1;
+            const double zj = __shfl_sync(kFull, own, j & 31) / L[rj + j];
+            if (lane == (j & 31)) {
+              if (j < 32) s0 = zj;
+              else s1 = zj;
+            }
+            const int i0 = lane, i1 = lane + 32;
+            if (i0 > j && i0 < f) s0 = __dsub_rn(s0, __dmul_rn(L[i0 * (i0 + 1) / 2 + j], zj));
+            if (i1 > j && i1 < f) s1 = __dsub_rn(s1, __dmul_rn(L[i1 * (i1 + 1) / 2 + j], zj));
+          }
+          for (int i = f - 1; i >= 0; --i) {
+            const int ri = i * (i + 1) / 2;
+            const double own = (i < 32) ? s0 : s1;
+            const double xi_ = __shfl_sync(kFull, own, i & 31) / L[ri + i];
+            if (lane == (i & 31)) {
+              if (i < 32) s0 = xi_;
+              else s1 = xi_;
+            }
+            const int k0 = lane, k1 = lane + 32;
+            if (k0 < i) s0 = __dsub_rn(s0, __dmul_rn(L[ri + k0], xi_));
+            if (k1 < i) s1 = __dsub_rn(s1, __dmul_rn(L[ri + k1], xi_));
+          }
+          o0 = (lane < f) ? s0 : 0.0;
+          o1 = (lane + 32 < f) ? s1 : 0.0;
+        };
+        auto asum = [&](double a0, double a1) { return warp_sum(fabs(a0) + fabs(a1)); };
+        auto iamax = [&](double a0, double a1) {  // first index of max |v|
+          double b = fabs(a0);
+          int bi = lane;
+          if (lane + 32 < f && fabs(a1) > b) {
+            b = fabs(a1);
+            bi = lane + 32;
+          }
+          if (lane >= f) b = -1.0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(kFull, b, o);
+            const int oi = __shfl_xor_sync(kFull, bi, o);
+            if (ob > b || (ob == b && oi < bi)) {
+              b = ob;
+              bi = oi;
+            }
+          }
+          return bi;
+        };
+        auto sgn = [](double v) { return v >= 0.0 ? 1.0 : -1.0; };
+        const double inv_f = 1.0 / (double)f;
+        double x0 = lane < f ? inv_f : 0.0, x1 = lane + 32 < f ? inv_f : 0.0, y0, y1;
+        applyB(x0, x1, y0, y1);
+        double est;
+        if (f == 1) {
+          est = fabs(__shfl_sync(kFull, y0, 0));
+        } else {
+          est = asum(y0, y1);
+          double xi0 = lane < f ? sgn(y0) : 0.0, xi1 = lane + 32 < f ? sgn(y1) : 0.0;
+          applyB(xi0, xi1, y0, y1);
+          int jj = iamax(y0, y1), iter = 2;
+          for (;;) {
+            x0 = (lane == jj) ? 1.0 : 0.0;
+            x1 = (lane + 32 == jj) ? 1.0 : 0.0;
+            applyB(x0, x1, y0, y1);
+            const double est_old = est;
+            est = asum(y0, y1);
+            const bool diff = (lane < f && sgn(y0) != xi0) || (lane + 32 < f && sgn(y1) != xi1);
+            if (!__any_sync(kFull, diff) || est <= est_old) break;
+            xi0 = lane < f ? sgn(y0) : 0.0;
+            xi1 = lane + 32 < f ? sgn(y1) : 0.0;
+            applyB(xi0, xi1, y0, y1);
+            const int jlast = jj;
+            jj = iamax(y0, y1);
+            const double zl = __shfl_sync(kFull, jlast < 32 ? y0 : y1, jlast & 31);
+            const double zj = __shfl_sync(kFull, jj < 32 ? y0 : y1, jj & 31);
+            if (zl != fabs(zj) && iter < 5) {
+              ++iter;
+              continue;
+            }
+            break;
+          }
+          x0 = lane < f ? ((lane & 1) ? -1.0 : 1.0) * (1.0 + (double)lane / (double)(f - 1)) : 0.0;
+          x1 = lane + 32 < f ? (((lane + 32) & 1) ? -1.0 : 1.0) * (1.0 + (double)(lane + 32) / (double)(f - 1))
+                             : 0.0;
+          applyB(x0, x1, y0, y1);
+          const double temp = 2.0 * asum(y0, y1) / (3.0 * (double)f);
+          if (temp > est) est = temp;
+        }
+        if (lane == 0) colk[0] = norm1 * est;
+      }
+      __syncthreads();
+      kappa = colk[0];
+      refined = (kappa * 0x1p-52 > a.adaptive_threshold) ? 1 : 0;
+      __syncthreads();
+    }
     // ---------------------------------------------------------- hand-off
     // the NE solution, F and the counters go to global memory with the
     // column view; batched_lsqr_kernel (a smaller on-chip footprint, so more
@@ -458,12 +572,15 @@ __global__ void __launch_bounds__(BT) batched_kernel(BatchArgs a, int nnz_max) {
       a.mask_out[(size_t)prob * n + j] = mk[j];
     }
     if (tid == 0) {
-      int32_t* ii = a.info_i + (size_t)prob * 8;
+      int32_t* ii = a.info_i + (size_t)prob * kInfoI;
       ii[0] = status;
       ii[1] = iter;
       ii[2] = singles;
       ii[3] = f;
       ii[7] = status == 7 ? not_pd : -1;
+      ii[8] = refined;
+      ii[9] = 0;
+      a.info_d[(size_t)prob * kInfoD + 5] = kappa;
     }
     __syncthreads();
     BP_MARK(7);  // hand-off
@@ -532,8 +649,8 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
   for (int prob = blockIdx.x; prob < a.batch; prob += gridDim.x) {
     const int64_t e0 = a.nnz_off[prob];
     const int nz = (int)(a.nnz_off[prob + 1] - e0);
-    const int status = a.info_i[(size_t)prob * 8 + 0];
-    const int f = a.info_i[(size_t)prob * 8 + 3];
+    const int status = a.info_i[(size_t)prob * kInfoI + 0];
+    const int f = a.info_i[(size_t)prob * kInfoI + 3];
     for (int r = tid; r <= m; r += BT) rp[r] = a.rowptr[(size_t)prob * (m + 1) + r];
     const double* bb = a.b + (size_t)prob * m;       // b (global, read twice)
     const double* x = a.x_out + (size_t)prob * n;    // the NE x (global; overwritten by the output below)
@@ -601,7 +718,9 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
     // test of an iteration is evaluated after the next barrier (it needs only
     // scalars, and x is not touched in between).
     int itn = 0, istop = 0;
-    const int mode = (status == 0 && f > 0) ? a.lsqr_mode : 0;
+    const int mode0 = (status == 0 && f > 0) ? a.lsqr_mode : 0;
+    // mode 3 (adaptive): the pivot kernel's condition estimate decided
+    const int mode = mode0 == 3 ? (a.info_i[(size_t)prob * kInfoI + 8] ? 1 : 0) : mode0;
     if (mode != 0) {
       const int itn_limit = a.itn_limit > 0 ? a.itn_limit : 4 * f;
       int rslot = 0;  // red[] double-buffering: red[rslot*16 + 4*q + warp]
@@ -817,11 +936,11 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
       dot = block_sum(ld, red);
     }
     if (tid == 0) {
-      int32_t* ii = a.info_i + (size_t)prob * 8;
+      int32_t* ii = a.info_i + (size_t)prob * kInfoI;
       ii[4] = itn;
       ii[5] = istop;
       ii[6] = (mode != 0 && any_infeas) ? 1 : 0;
-      double* dd = a.info_d + (size_t)prob * 5;
+      double* dd = a.info_d + (size_t)prob * kInfoD;
       dd[0] = 0.5 * obj;
       dd[1] = mx;
       dd[2] = my;

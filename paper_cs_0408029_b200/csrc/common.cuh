@@ -39,6 +39,9 @@ struct DevState {
   int32_t role_factor;  // CTA role tickets of the factorization / back-substitution kernels:
   int32_t role_solve;   // the first CTA to run takes the chain (reset with the task counters)
   int32_t pad1;
+  double kappa;           // lsqr_mode 3: condition estimate of the final (A^T A)_FF (condest.cu)
+  int32_t refined;        // 1: the final x comes from LSQR
+  int32_t lsqr_fallbacks; // NOT_PD iterations solved by LSQR instead (notpd_fallback)
 };
 
 struct TraceRec {

@@ -85,6 +85,19 @@ cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* x
                                   int sm_count, cudaStream_t s, const int32_t* Fidx = nullptr,
                                   double* xs = nullptr);
 
+// ---- NEXT-2 condition estimate (condest.cu) --------------------------------
+// kappa_1 estimate of the final (A^T A)_FF = L L^T from the factor tiles Lt
+// (layout of cholesky.cu, n = the handle's size), written to st->kappa, and
+// st->refined = kappa * 2^-52 > threshold.  work: 6 n doubles; norm1: one u64.
+cudaError_t launch_condest(const double* G, int ldg, const int32_t* Fidx, const double* Lt, int n, DevState* st,
+                           double* work, unsigned long long* norm1, double threshold, int sm_count, cudaStream_t s);
+// NOT_PD fallback steps (pivot.cu): before the LSQR on the failed F (status
+// cleared, done raised so the LSQR kernels take it as a final F) and after it
+// (x_F from the LSQR x, done cleared, counter).
+cudaError_t launch_fallback_prep(DevState* st, cudaStream_t s);
+cudaError_t launch_fallback_fixup(int n, const int32_t* Fidx, const double* xl, double* xF, double* xs,
+                                  DevState* st, cudaStream_t s);
+
 // ---- a10 LSQR + final report (lsqr.cu) ----------------------------------
 struct LsqrArgs {
   int m, n;
@@ -123,6 +136,7 @@ size_t lsqr_cluster_smem(int m, int n, const int* plan);
 cudaError_t launch_lsqr_cluster_planned(const LsqrArgs& a, const int* plan_host, cudaStream_t s);
 
 // ---- batched whole solve (batched.cu) ------------------------------------
+constexpr int kInfoI = 10, kInfoD = 6;  // per-problem report slots of the batched kernels
 struct BatchArgs {
   int batch, m, n;
   const int64_t* nnz_off;
@@ -132,10 +146,11 @@ struct BatchArgs {
   const double* b;
   double* x_out;
   uint8_t* mask_out;
-  int32_t* info_i;   // batch * 8 ints: status, iter, singles, f, lsqr_itn, lsqr_stop, infeas, notpd
-  double* info_d;    // batch * 5 doubles: objective, min_x, min_y, max_comp, dot
+  int32_t* info_i;   // batch * kInfoI ints: status, iter, singles, f, lsqr_itn, lsqr_stop, infeas, notpd, refined, -
+  double* info_d;    // batch * kInfoD doubles: objective, min_x, min_y, max_comp, dot, kappa
   double tol, atol, btol, conlim;
   int p_max, max_iter, lsqr_mode, itn_limit, kkt;
+  double adaptive_threshold;  // lsqr_mode 3
   uint8_t* colview;  // scratch: per problem the column view (batched_colview_stride bytes)
   size_t cv_stride;
   double* gram;      // scratch: one packed Gram per CTA (batched_gram_scratch bytes)

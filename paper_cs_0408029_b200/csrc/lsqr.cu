@@ -137,7 +137,9 @@ __global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
   const int status = a.st->status;
   const int f = a.st->f;
   const uint8_t* __restrict__ mask = a.mask;
-  const int mode = (status == 0 && a.st->done && f > 0) ? a.mode : 0;
+  const int mode0 = (status == 0 && a.st->done && f > 0) ? a.mode : 0;
+  // mode 3 (adaptive): condest.cu decided -- LSQR as mode 1, or the NE x
+  const int mode = mode0 == 3 ? (a.st->refined ? 1 : 0) : mode0;
 
   int itn = 0, istop = 0;
   if (mode != 0) {
@@ -726,7 +728,9 @@ __global__ void __launch_bounds__(kCT, 1) lsqr_cluster_kernel(LsqrArgs a, ClLayo
 
   const int f = a.st->f;
   const int status = a.st->status;
-  const int mode = (status == 0 && a.st->done && f > 0) ? a.mode : 0;
+  const int mode0 = (status == 0 && a.st->done && f > 0) ? a.mode : 0;
+  // mode 3 (adaptive): condest.cu decided -- LSQR as mode 1, or the NE x
+  const int mode = mode0 == 3 ? (a.st->refined ? 1 : 0) : mode0;
   int itn = 0, istop = 0;
 
   if (mode != 0) {

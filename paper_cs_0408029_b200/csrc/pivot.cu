@@ -45,6 +45,9 @@ __global__ void init_kernel(int n, const double* __restrict__ c, uint8_t* mask, 
     st->lsqr_stop = 0;
     st->infeasible_after_lsqr = 0;
     st->reuse_cols = 0;
+    st->kappa = 0.0;
+    st->refined = 0;
+    st->lsqr_fallbacks = 0;
   }
 }
 
@@ -634,6 +637,35 @@ cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const 
   if (blocks < 1) blocks = 1;
   return launch_pdl(dual_kernel, dim3(blocks), dim3(256), 0, s, n, G, ldg, c, Fidx, Gidx, xF, mask, x, y, tol, st,
                     Fs, xs);
+}
+
+// --------------------------------------------- NOT_PD fallback
+__global__ void fallback_prep_kernel(DevState* st) {
+  st->status = 0;
+  st->done = 1;  // the LSQR kernels take the current F as the final one
+}
+__global__ void __launch_bounds__(256) fallback_fixup_kernel(int n, const int32_t* __restrict__ Fidx,
+                                                             const double* __restrict__ xl, double* __restrict__ xF,
+                                                             double* __restrict__ xs, DevState* st) {
+  const int f = st->f;
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < f; a += gridDim.x * blockDim.x) xF[a] = xl[Fidx[a]];
+  if (xs != nullptr)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) xs[i] = xl[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->done = 0;
+    st->lsqr_fallbacks += 1;
+  }
+}
+cudaError_t launch_fallback_prep(DevState* st, cudaStream_t s) {
+  fallback_prep_kernel<<<1, 1, 0, s>>>(st);
+  return cudaGetLastError();
+}
+cudaError_t launch_fallback_fixup(int n, const int32_t* Fidx, const double* xl, double* xF, double* xs,
+                                  DevState* st, cudaStream_t s) {
+  int blocks = (n + 255) / 256;
+  if (blocks > 64) blocks = 64;
+  fallback_fixup_kernel<<<blocks, 256, 0, s>>>(n, Fidx, xl, xF, xs, st);
+  return cudaGetLastError();
 }
 
 }  // namespace nnls

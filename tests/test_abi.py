@@ -42,8 +42,8 @@ def test_sass_is_sm100a_with_dmma(P):
 
 
 def test_struct_layouts(P):
-    assert ctypes.sizeof(P.Params) == 56
-    assert ctypes.sizeof(P.Info) == 72
+    assert ctypes.sizeof(P.Params) == 72
+    assert ctypes.sizeof(P.Info) == 88
     assert ctypes.sizeof(P.IterRec) == 40
     p = P.default_params()
     assert p.zero_tol == 1e-12 and p.p_max == 3 and p.lsqr_mode == 1 and p.kkt == 1

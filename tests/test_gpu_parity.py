@@ -579,3 +579,69 @@ def test_row_sharded_gram_path(P, world):
     r = O.solve(prob)
     assert np.array_equal(root.free_set(), r["mask"]) and info["iterations"] == r["iterations"]
     assert rel(x, r["x"]) <= TOL_X
+
+
+# ------------------------------------------------------------------ NEXT-2
+# lsqr_mode 3 (adaptive final step) and the NOT_PD LSQR fallback
+# against the oracle extension (oracle/nnls_oracle.c or_condest).
+# kappa: the forward solve is bit-identical to the oracle's, the backward
+# sweep sums in another order -> relative 1e-6 (decisions are far from it).
+@pytest.mark.parametrize("cfg,seed", [(0, 0), (1, 0), (3, 1), ("ill", 5)])
+@pytest.mark.parametrize("thr", [1e-8, 1e-14])
+def test_adaptive_mode_single(P, cfg, seed, thr):
+    if cfg == "ill":
+        rng = np.random.default_rng(seed)
+        A = np.round(rng.standard_normal((200, 60)) * 64) / 64
+        A[:, 0] *= 1e-5
+        b = A @ (1.0 + np.abs(rng.standard_normal(60))) + 1e-9 * rng.standard_normal(200)
+        prob = g.from_dense(A, b)
+    else:
+        prob = g.make_problem(cfg, seed)
+    r = O.solve(prob, lsqr_mode=3, adaptive_threshold=thr, trace_cap=10 * prob.n + 2)
+    S = P.setup(prob, lsqr_mode=3, adaptive_threshold=thr)
+    x, info = S.solve()
+    assert info["status"] == r["status"] == 0
+    assert np.array_equal(S.free_set(), r["mask"]) and info["iterations"] == r["iterations"]
+    assert info["refined"] == r["refined"]
+    assert abs(info["kappa"] - r["kappa"]) <= 1e-6 * r["kappa"]
+    assert rel(x, r["x"]) <= TOL_X
+    if not r["refined"]:
+        assert info["lsqr_iterations"] == 0 and rel(x, S.x_ne()) == 0.0
+
+
+def test_adaptive_mode_batched(P):
+    B = g.make_batch(seed=2, start=0, count=512)
+    thr = 1e-14                              # kappa ~ 10-100 at config 4: some refine, some not
+    out = P.BatchedSolver(lsqr_mode=3, adaptive_threshold=thr).load_batch(B).solve()
+    info = out["info"]
+    xs = out["x"].reshape(B.count, B.n)
+    nref = 0
+    for q in range(B.count):
+        r = O.solve(B.problem(q), lsqr_mode=3, adaptive_threshold=thr)
+        assert info["refined"][q] == r["refined"], q
+        assert abs(info["kappa"][q] - r["kappa"]) <= 1e-6 * r["kappa"], q
+        assert rel(xs[q], r["x"]) <= TOL_X, q
+        nref += r["refined"]
+    assert 0 < nref < B.count
+
+
+def test_notpd_fallback_single(P):
+    """Duplicate column: the default stops at NOT_PD (as the oracle); with
+    notpd_fallback the LSQR solve replaces the failed factorization and the
+    solve reaches the oracle's F, iteration count and optimal objective."""
+    base = g.make_problem(0, 0)
+    A = base.dense()
+    A = np.concatenate([A, A[:, :1]], axis=1)
+    prob = g.from_dense(A, base.b)
+    S = P.setup(prob)
+    _, info = S.solve()
+    assert info["status"] == P.ERR_NOT_PD
+    r = O.solve(prob, notpd_fallback=1)
+    S2 = P.setup(prob, notpd_fallback=1)
+    x, info2 = S2.solve()
+    assert info2["status"] == r["status"] == 0
+    assert info2["lsqr_fallbacks"] == r["lsqr_fallbacks"] >= 1
+    assert info2["iterations"] == r["iterations"]
+    assert np.array_equal(S2.free_set(), r["mask"])
+    assert abs(info2["objective"] - r["objective"]) <= 1e-9 * r["objective"]
+    assert x.min() >= 0.0
