@@ -273,3 +273,43 @@ def make_correlated(seed: int, corr: float = 0.05, nmin: int = 4, nmax: int = 9,
     p.seed = int(seed)
     p.kind = "correlated"
     return p
+
+
+def _householder_apply(vs, M):
+    """(H_1 H_2 ... H_k) M for reflections H_i = I - 2 v v^T / v^T v (v in vs)."""
+    for v in reversed(vs):
+        M = M - np.outer(2.0 * v / (v @ v), v @ M)
+    return M
+
+
+def make_p_problem(m: int = 80, n: int = 70, d: int = 4, cond: float = 1e4, seed: int = 0,
+                   resid: float = 0.25) -> Problem:
+    """The paper's accuracy test family P(m, n, d, x) (Section 4:
+    "each singular value is repeated 4 times, and x is a parameter which
+    controls the condition number"; the original LSQR generator is not
+    available -- this is SPEC.md's gen_p substitute):
+    A = Y D Z^T with Y (m x m), Z (n x n) products of seeded Householder
+    reflections, D = diag of ceil(n/d) singular values geometrically spaced
+    from 1 down to 1/cond, each repeated d times; x_true_j = 1 + j/n; b =
+    A x_true + r with r = Y (0_n; c) orthogonal to range(A), ||r|| = resid *
+    ||A x_true|| (SPEC's 1/4 by default; the LSQR generator's residual size is
+    not in the paper) -- so the NNLS solution is exactly x_true (y = A^T r = 0)
+    and kappa(A) = cond.  Dense, unquantized (stored as CSR)."""
+    assert m > n >= 1 and d >= 1 and cond >= 1.0
+    rng = np.random.default_rng([int(seed), 8080, m, n, d])
+    k = (n + d - 1) // d
+    levels = cond ** (-np.arange(k) / max(k - 1, 1)) if k > 1 else np.ones(1)
+    sig = np.repeat(levels, d)[:n]
+    Y = _householder_apply([rng.standard_normal(m) for _ in range(m)], np.eye(m))
+    Z = _householder_apply([rng.standard_normal(n) for _ in range(n)], np.eye(n))
+    A = (Y[:, :n] * sig) @ Z.T
+    x_true = 1.0 + np.arange(n) / n
+    Ax = A @ x_true
+    c = rng.standard_normal(m - n)
+    r = Y[:, n:] @ c
+    r *= (resid * np.linalg.norm(Ax)) / np.linalg.norm(r)
+    p = from_dense(A, Ax + r)
+    p.x_gen = x_true
+    p.kind = "p_family"
+    p.seed = int(seed)
+    return p

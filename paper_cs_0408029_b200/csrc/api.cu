@@ -47,10 +47,13 @@ nnls_status map_cuda(cudaError_t e) {
   return NNLS_ERR_CUDA;
 }
 
-#define CK(expr)                                  \
-  do {                                            \
-    cudaError_t e_ = (expr);                      \
-    if (e_ != cudaSuccess) return map_cuda(e_);   \
+#define CK(expr)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      if (getenv("NNLS_DEBUG")) fprintf(stderr, "[nnls] %s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+      return map_cuda(e_);                                                                   \
+    }                                                                                        \
   } while (0)
 
 int round_up(int v, int q) { return (v + q - 1) / q * q; }
@@ -555,8 +558,6 @@ cudaError_t launch_fallback(nnls_handle* h, cudaStream_t s) {
   e = launch_lsqr_args(h, a, s);
   if (e != cudaSuccess) return e;
   e = launch_fallback_fixup(h->n, P<int32_t>(h->Fidx), xl, P<double>(h->xF), xs_or_null(h), st, s);
-  if (e != cudaSuccess) return e;
-  if (!h->no_reuse) e = cudaMemsetAsync(h->pos.p, 0xFF, sizeof(int32_t) * (size_t)h->n, s);
   return e;
 }
 // the final step: (mode 3) the condition estimate, then LSQR + report

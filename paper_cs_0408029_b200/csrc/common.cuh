@@ -38,7 +38,7 @@ struct DevState {
   int32_t reuse_cols;   // leading tile columns of the last factor still valid (factor reuse)
   int32_t role_factor;  // CTA role tickets of the factorization / back-substitution kernels:
   int32_t role_solve;   // the first CTA to run takes the chain (reset with the task counters)
-  int32_t pad1;
+  int32_t keep_none;      // 1: the next decide keeps no factor prefix (set after a NOT_PD fallback)
   double kappa;           // lsqr_mode 3: condition estimate of the final (A^T A)_FF (condest.cu)
   int32_t refined;        // 1: the final x comes from LSQR
   int32_t lsqr_fallbacks; // NOT_PD iterations solved by LSQR instead (notpd_fallback)

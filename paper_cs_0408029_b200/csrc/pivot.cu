@@ -370,7 +370,8 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
       }
       st->branch = branch;
       s_branch = branch;
-      s_fprev = st->f;
+      s_fprev = st->keep_none ? 0 : st->f;  // (keep_none: the previous factor failed, nothing is kept)
+      st->keep_none = 0;
       s_last = ll;
       s_carryF = 0;
       s_carryG = 0;
@@ -654,6 +655,7 @@ __global__ void __launch_bounds__(256) fallback_fixup_kernel(int n, const int32_
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->done = 0;
     st->lsqr_fallbacks += 1;
+    st->keep_none = 1;  // the failed factor's prefix is not reused by the next decide
   }
 }
 cudaError_t launch_fallback_prep(DevState* st, cudaStream_t s) {
