@@ -286,7 +286,7 @@ class Ctx:
         return sum(a.elapsed_time(b) for a, b in ev)
 
 
-def measure_single(C, cfg, steps, warmup, shard=False, with_e2e=True, full_fact=True, trace=True):
+def measure_single(C, cfg, steps, warmup, shard=False, with_e2e=True, full_fact=True, trace=True, **solver_kw):
     """Single problem (configs 0-3).  shard (N > 1, config 2): row-sharded Gram
     + reduce to rank 0, the loop on rank 0."""
     import nnls_gen as g
@@ -306,7 +306,7 @@ def measure_single(C, cfg, steps, warmup, shard=False, with_e2e=True, full_fact=
             host = dict(rowptr=rp, colind=ci, vals=v, b=bb)
             solver = P.BlockSolver(stream=C.stream).load_block(r1 - r0, prob.n, rp, ci, v, bb)
     else:
-        solver = P.Solver(stream=C.stream, trace=1 if trace else 0)
+        solver = P.Solver(stream=C.stream, trace=1 if trace else 0, **solver_kw)
     devt = {k: torch.from_numpy(np.ascontiguousarray(v)).to(C.dev) for k, v in host.items()}
     pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in host.items()}
     x_dev = torch.empty(prob.n, dtype=torch.float64, device=C.dev)
@@ -354,7 +354,7 @@ def measure_single(C, cfg, steps, warmup, shard=False, with_e2e=True, full_fact=
         trace = solver.trace()
         res["pivot_iterations_per_s"] = info["iterations"] * steps / (t_max / 1e3)
         res["per_solve"] = {k: info[k] for k in ("iterations", "free_count", "lsqr_iterations", "status",
-                                                 "single_exchanges")}
+                                                 "single_exchanges", "kappa", "refined")}
         res["per_solve"]["trace"] = [{"k": t["k"], "branch": t["branch"], "f": t["f"], "kept": t["kept"]}
                                      for t in trace]
     # ---- instrumented pass: per-phase CUDA events (host-driven pivot loop)
@@ -566,6 +566,14 @@ def run_ours(args):
                 extra[f"config{c2}"]["workload"] = workload_desc(c2, args.batch)
                 if "per_solve" in extra[f"config{c2}"]:
                     extra[f"config{c2}"]["per_solve"].pop("trace", None)
+        if world == 1 and cfg != 4:
+            # NEXT-2: the adaptive final step (condition estimate of the final
+            # (A^T A)_FF, LSQR only when kappa 2^-52 > 1e-8) on the same problem
+            r = measure_single(C, cfg, args.steps, 3, with_e2e=False, full_fact=False, lsqr_mode=3)
+            extra["adaptive_lsqr_mode3"] = {k: v for k, v in round_res(r).items()
+                                            if k in ("value", "ms_per_step", "phase_ms_per_step", "per_solve")}
+            extra["adaptive_lsqr_mode3"]["per_solve"].pop("trace", None)
+            extra["adaptive_lsqr_mode3"]["workload"] = workload_desc(cfg, args.batch) + ", lsqr_mode 3"
         elif cfg != 4:
             r = measure_batched(C, max(3, args.steps // 4), 3, with_e2e=False)
             extra["config4_sharded"] = {k: v for k, v in round_res(r).items()

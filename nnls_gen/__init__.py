@@ -313,3 +313,13 @@ def make_p_problem(m: int = 80, n: int = 70, d: int = 4, cond: float = 1e4, seed
     p.kind = "p_family"
     p.seed = int(seed)
     return p
+
+
+def make_fig2(n: int, density: float, seed: int = 0) -> Problem:
+    """The paper's timing workloads (Fig. 2): "randomly
+    generated, well-conditioned matrices from MATLAB's sprandn ... of size
+    n x (n-10)", density 1 ("general dense") and 0.01 ("sparse").  Stand-in:
+    this module's seeded N(0,1) recipe (2^-12 grid) at that shape; the paper
+    does not say how b was drawn -- b = A x0 + 0.01 N(0,1) as for the BASELINE
+    configs (reading c25)."""
+    return make_problem(dict(m=int(n), n=int(n) - 10, density=float(density)), seed=seed)

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnnls_b200.so")
-SOURCES = ["api.cu", "ingest_gram.cu", "pivot.cu", "cholesky.cu", "lsqr.cu", "batched.cu", "condest.cu"]
+SOURCES = ["api.cu", "ingest_gram.cu", "pivot.cu", "cholesky.cu", "lsqr.cu", "batched.cu", "condest.cu", "gram_dense.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
 

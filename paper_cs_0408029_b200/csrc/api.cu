@@ -104,6 +104,8 @@ struct nnls_handle {
   Buf U, V, W, X, R, partials, xfin;      // LSQR / report
   Buf Fval, Fcol, Fcnt;                   // A restricted to the final F (cluster LSQR)
   Buf cwork;                              // condest vectors (6 n doubles) + ||M||_1 bits; fallback x
+  Buf Adense;                             // tiled dense copy of A (dense Gram path)
+  bool gram_dense = false;                // the last load formed G with the dense DMMA SYRK
   Buf st, err, trace;
   int trace_cap = 0;
   HostState* h = nullptr;                 // pinned readback
@@ -303,11 +305,26 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
     c = G + (size_t)n * (n + 1) / 2;
     ldg = 0;
   }
-  TIMED(NNLS_PH_GRAM, 1,
-        launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
-                    P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                    P<double>(h->b), r0, r1, G, ldg, c, h->sms, s, gram_is_exact(h->h->err) && !h->no_exact_gram,
-                    gram_exact_lmin(h->h->err)));
+  const bool exact = gram_is_exact(h->h->err) && !h->no_exact_gram;
+  const bool bits_exact = gram_bits_exact(h->h->err) && !h->no_exact_gram;
+  // dense A (NEXT-1, the Fig. 2 density-1 workloads): the Gram is an O(m n^2)
+  // SYRK -> DMMA on a tiled dense copy; exact inputs only (bitwise = oracle)
+  const double density = (double)nnz / ((double)m * (double)n);
+  const size_t dense_bytes = sizeof(double) * gram_dense_doubles(r1 - r0, n);
+  if (bits_exact && density >= 0.25 && n >= 32 && dense_bytes <= ((size_t)16 << 30) && !env_on("NNLS_NO_DENSE_GRAM")) {
+    CK(ensure(h->Adense, dense_bytes));
+    TIMED(NNLS_PH_GRAM, 4,
+          launch_gram_dense(n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                            P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals), P<double>(h->b), r0,
+                            r1, P<double>(h->Adense), G, ldg, c, h->sms, s));
+    h->gram_dense = true;
+  } else {
+    TIMED(NNLS_PH_GRAM, 1,
+          launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                      P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
+                      P<double>(h->b), r0, r1, G, ldg, c, h->sms, s, exact, gram_exact_lmin(h->h->err)));
+    h->gram_dense = false;
+  }
   h->loaded = true;
   return NNLS_OK;
 }
@@ -937,7 +954,7 @@ nnls_status nnls_destroy(nnls_handle* h) {
                  &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
                  &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt, &h->b_colview, &h->b_gram,
-                 &h->pos, &h->Fs, &h->xs, &h->Gp, &h->cwork};
+                 &h->pos, &h->Fs, &h->xs, &h->Gp, &h->cwork, &h->Adense};
   for (Buf* b : bufs) free_buf(*b);
   if (h->s_in) cudaStreamSynchronize(h->s_in);
   if (h->s_out) cudaStreamSynchronize(h->s_out);

@@ -543,10 +543,14 @@ cudaError_t launch_gram_unpack(int n, const double* P, double* G, int ldg, int s
   return cudaGetLastError();
 }
 
-bool gram_is_exact(const int* err) {
+bool gram_is_exact(const int* err) { return err[2] <= kExactTuples && gram_bits_exact(err); }
+
+// every product a_ri a_rj and every column partial sum exact in FP64 (the
+// bit budget alone, any kernel / summation order)
+bool gram_bits_exact(const int* err) {
   const int K = err[2];  // longest column
   const int hA = err[kErrExp], lA = err[kErrExp + 1], hb = err[kErrExp + 2], lb = err[kErrExp + 3];
-  if (K > kExactTuples || lA >= 4095 || lb >= 4095) return false;
+  if (lA >= 4095 || lb >= 4095) return false;
   if (hA == 0) return true;  // A == 0
   int lgK = 0;
   while ((1 << lgK) < K + 1) ++lgK;

@@ -34,12 +34,21 @@ cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
 // err[kErrExp..+3]: exponent statistics of A and b from validate (see
 // exact_bits); gram_is_exact(err) -> every Gram/c sum is exact in FP64.
 constexpr int kErrExp = 48;
-bool gram_is_exact(const int* err);
+bool gram_is_exact(const int* err);    // exact AND the column fits gram_exact_kernel
+bool gram_bits_exact(const int* err);  // exact (bit budget only)
 inline int gram_exact_lmin(const int* err) { return 2048 - err[kErrExp + 1]; }  // L_A
 // ldg <= 0: G is the packed lower triangle (row i = entries j <= i at offset
 // i(i+1)/2) -- the row-shard partial Gram that ranks reduce.
 // launch_gram_unpack: packed -> full symmetric n x ldg.
 cudaError_t launch_gram_unpack(int n, const double* P, double* G, int ldg, int sm_count, cudaStream_t s);
+// dense A (gram_dense.cu): G = A^T A over rows [row_begin, row_end) as a DMMA
+// SYRK on a tiled dense copy At (gram_dense_doubles(rows, n) doubles), c from
+// the CSC.  Exact-arithmetic inputs only (the order differs from the oracle's).
+size_t gram_dense_doubles(int rows, int n);
+cudaError_t launch_gram_dense(int n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                              const int32_t* colptr, const int32_t* rowind, const double* cvals, const double* b,
+                              int row_begin, int row_end, double* At, double* G, int ldg, double* c, int sm_count,
+                              cudaStream_t s);
 cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
                         const double* vals, const int32_t* colptr, const int32_t* rowind,
                         const double* cvals, const double* b, int row_begin, int row_end,

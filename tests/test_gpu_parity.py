@@ -645,3 +645,34 @@ def test_notpd_fallback_single(P):
     assert np.array_equal(S2.free_set(), r["mask"])
     assert abs(info2["objective"] - r["objective"]) <= 1e-9 * r["objective"]
     assert x.min() >= 0.0
+
+
+# ------------------------------------------------------------------ NEXT-1
+# The Fig. 2 workloads (n x (n-10), density 1 and 0.01).  Density 1
+# takes the dense DMMA SYRK Gram (gram_dense.cu): with exact inputs its sums
+# are bitwise the oracle's, for the full Gram and for a row shard's packed one.
+@pytest.mark.parametrize("n,d", [(100, 1.0), (300, 1.0), (700, 1.0), (1000, 1.0), (800, 0.01), (1420, 0.01)])
+def test_fig2_workloads(P, n, d):
+    prob = g.make_fig2(n, d, seed=1)
+    S = P.setup(prob, trace=1)
+    G, c = S.gram()
+    Go, co = O.gram(prob)
+    assert np.array_equal(G, Go) and np.array_equal(c, co)
+    x, info = S.solve()
+    r = O.solve(prob, trace_cap=10 * prob.n + 2)
+    assert info["status"] == r["status"] == 0
+    assert np.array_equal(S.free_set(), r["mask"]) and info["iterations"] == r["iterations"]
+    assert rel(x, r["x"]) <= TOL_X
+
+
+def test_dense_gram_row_shard_packed(P):
+    from paper_cs_0408029_b200.dist import gram_tensor, row_block, row_shards
+    prob = g.make_fig2(400, 1.0, seed=2)
+    n = prob.n
+    tril = np.tril_indices(n)
+    for r0, r1 in row_shards(prob.m, 3)[1:]:
+        rp, ci, v, b = row_block(prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1)
+        S = P.BlockSolver().load_block(r1 - r0, n, rp, ci, v, b)
+        buf = gram_tensor(S).cpu().numpy()
+        Gb, cb = O.gram(g.Problem(r1 - r0, n, rp, ci, v, b, prob.x_gen, prob.kind, prob.seed))
+        assert np.array_equal(buf[:n * (n + 1) // 2], Gb[tril]) and np.array_equal(buf[n * (n + 1) // 2:], cb)
