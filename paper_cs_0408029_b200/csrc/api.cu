@@ -306,17 +306,17 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
     ldg = 0;
   }
   const bool exact = gram_is_exact(h->h->err) && !h->no_exact_gram;
-  const bool bits_exact = gram_bits_exact(h->h->err) && !h->no_exact_gram;
+  const bool a_exact = gram_A_exact(h->h->err) && !h->no_exact_gram;
   // dense A (NEXT-1, the Fig. 2 density-1 workloads): the Gram is an O(m n^2)
   // SYRK -> DMMA on a tiled dense copy; exact inputs only (bitwise = oracle)
   const double density = (double)nnz / ((double)m * (double)n);
   const size_t dense_bytes = sizeof(double) * gram_dense_doubles(r1 - r0, n);
-  if (bits_exact && density >= 0.25 && n >= 32 && dense_bytes <= ((size_t)16 << 30) && !env_on("NNLS_NO_DENSE_GRAM")) {
+  if (a_exact && density >= 0.25 && n >= 32 && dense_bytes <= ((size_t)16 << 30) && !env_on("NNLS_NO_DENSE_GRAM")) {
     CK(ensure(h->Adense, dense_bytes));
     TIMED(NNLS_PH_GRAM, 4,
           launch_gram_dense(n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                             P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals), P<double>(h->b), r0,
-                            r1, P<double>(h->Adense), G, ldg, c, h->sms, s));
+                            r1, P<double>(h->Adense), G, ldg, c, h->sms, s, gram_c_exact(h->h->err)));
     h->gram_dense = true;
   } else {
     TIMED(NNLS_PH_GRAM, 1,

@@ -6,9 +6,10 @@
 // form A^T A requires n^2 m flops" -- at density 1 the Gram is the dominant
 // O(m n^2) step (the sparse scatter kernels of ingest_gram.cu are built for
 // m d^2 ~ 1-5 MACs per output entry).  Used when the load's exactness check
-// passes (gram_is_exact: every product and partial sum exact in FP64, as for
-// BASELINE's 2^-12-quantized inputs), so the DMMA summation order gives the
-// same bits as the oracle's sequential sum; and when A is dense enough.
+// passes for A (gram_A_exact: every product and partial sum of A^T A exact in
+// FP64, as for BASELINE's 2^-12-quantized inputs), so the DMMA summation
+// order gives the same bits as the oracle's sequential sum; and when A is
+// dense enough.
 //
 // B200 design
 //   * densify: CSR rows [r0, r1) -> a TILED dense copy, tile (kb, jb) = rows
@@ -23,7 +24,8 @@
 //     leaves through shared memory: the lower block row-coalesced, its mirror
 //     transposed (full symmetric output), or only j <= i into the packed row
 //     shard buffer.
-//   * c = A^T b: a warp per column over the CSC (exact, any order).
+//   * c = A^T b: a warp per column over the CSC when its sums are exact, else
+//     a thread per column in increasing row order (the oracle's sequence).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -102,6 +104,24 @@ __global__ void __launch_bounds__(256) densify_kernel(const int32_t* __restrict_
       const int c = colind[e];
       At[((size_t)kb * ntc + c / T) * TS + ri * LDS + c % T] = vals[e];
     }
+  }
+}
+
+// c_i = sum over column i of a_ri b_r in increasing row order, separate
+// multiply / add (the oracle's sequence: bitwise for any inputs) -- a thread
+// per column, for when the products or sums are not exact
+__global__ void __launch_bounds__(128) dense_c_ordered_kernel(int n, const int32_t* __restrict__ colptr,
+                                                              const int32_t* __restrict__ rowind,
+                                                              const double* __restrict__ cvals,
+                                                              const double* __restrict__ b, int r0, int r1,
+                                                              double* __restrict__ c) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = colptr[j]; t < colptr[j + 1]; ++t) {
+      const int r = rowind[t];
+      if (r >= r0 && r < r1) s = __dadd_rn(s, __dmul_rn(cvals[t], b[r]));
+    }
+    c[j] = s;
   }
 }
 
@@ -206,7 +226,7 @@ size_t gram_dense_doubles(int rows, int n) {
 cudaError_t launch_gram_dense(int n, const int32_t* rowptr, const int32_t* colind, const double* vals,
                               const int32_t* colptr, const int32_t* rowind, const double* cvals, const double* b,
                               int row_begin, int row_end, double* At, double* G, int ldg, double* c, int sm_count,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool c_exact) {
   const int rows = row_end - row_begin;
   const int nkb = (rows + T - 1) / T, ntc = (n + T - 1) / T;
   cudaError_t e = cudaMemsetAsync(At, 0, sizeof(double) * gram_dense_doubles(rows, n), s);
@@ -219,7 +239,8 @@ cudaError_t launch_gram_dense(int n, const int32_t* rowptr, const int32_t* colin
   int cb = (n + 7) / 8;
   if (cb > sm_count * 8) cb = sm_count * 8;
   if (cb < 1) cb = 1;
-  dense_c_kernel<<<cb, 256, 0, s>>>(n, colptr, rowind, cvals, b, row_begin, row_end, c);
+  if (c_exact) dense_c_kernel<<<cb, 256, 0, s>>>(n, colptr, rowind, cvals, b, row_begin, row_end, c);
+  else dense_c_ordered_kernel<<<(n + 127) / 128, 128, 0, s>>>(n, colptr, rowind, cvals, b, row_begin, row_end, c);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t smem = sizeof(double) * (size_t)(2 * kStagesD + 1) * TS;
   static DeviceOnce once;

@@ -547,10 +547,13 @@ bool gram_is_exact(const int* err) { return err[2] <= kExactTuples && gram_bits_
 
 // every product a_ri a_rj and every column partial sum exact in FP64 (the
 // bit budget alone, any kernel / summation order)
-bool gram_bits_exact(const int* err) {
+bool gram_bits_exact(const int* err) { return gram_A_exact(err) && gram_c_exact(err); }
+
+// A^T A alone: every product a_ri a_rj and every column partial sum exact
+bool gram_A_exact(const int* err) {
   const int K = err[2];  // longest column
-  const int hA = err[kErrExp], lA = err[kErrExp + 1], hb = err[kErrExp + 2], lb = err[kErrExp + 3];
-  if (lA >= 4095 || lb >= 4095) return false;
+  const int hA = err[kErrExp], lA = err[kErrExp + 1];
+  if (lA >= 4095) return false;
   if (hA == 0) return true;  // A == 0
   int lgK = 0;
   while ((1 << lgK) < K + 1) ++lgK;
@@ -558,8 +561,18 @@ bool gram_bits_exact(const int* err) {
   // sum of K products |a a'| < 2^(2HA+2+lgK) must stay below 2^(53 + 2LA)
   if (2 * HA + 2 + lgK > 53 + 2 * LA) return false;
   if (2 * LA < -1000 || 2 * HA > 1000) return false;  // (the integer scale must stay a normal double)
-  if (hb == 0) return true;  // b == 0
-  const int Hb = hb - 2048, Lb = 2048 - lb;
+  return true;
+}
+
+// A^T b: every product a_ri b_r and partial sum exact
+bool gram_c_exact(const int* err) {
+  const int K = err[2];
+  const int hA = err[kErrExp], lA = err[kErrExp + 1], hb = err[kErrExp + 2], lb = err[kErrExp + 3];
+  if (lA >= 4095 || lb >= 4095) return false;
+  if (hA == 0 || hb == 0) return true;  // A == 0 or b == 0
+  int lgK = 0;
+  while ((1 << lgK) < K + 1) ++lgK;
+  const int HA = hA - 2048, LA = 2048 - lA, Hb = hb - 2048, Lb = 2048 - lb;
   return HA + Hb + 2 + lgK <= 53 + LA + Lb;
 }
 

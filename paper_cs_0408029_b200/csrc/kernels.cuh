@@ -35,7 +35,9 @@ cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
 // exact_bits); gram_is_exact(err) -> every Gram/c sum is exact in FP64.
 constexpr int kErrExp = 48;
 bool gram_is_exact(const int* err);    // exact AND the column fits gram_exact_kernel
-bool gram_bits_exact(const int* err);  // exact (bit budget only)
+bool gram_bits_exact(const int* err);  // exact (bit budget only): A^T A and A^T b
+bool gram_A_exact(const int* err);     // A^T A exact
+bool gram_c_exact(const int* err);     // A^T b exact
 inline int gram_exact_lmin(const int* err) { return 2048 - err[kErrExp + 1]; }  // L_A
 // ldg <= 0: G is the packed lower triangle (row i = entries j <= i at offset
 // i(i+1)/2) -- the row-shard partial Gram that ranks reduce.
@@ -45,10 +47,12 @@ cudaError_t launch_gram_unpack(int n, const double* P, double* G, int ldg, int s
 // SYRK on a tiled dense copy At (gram_dense_doubles(rows, n) doubles), c from
 // the CSC.  Exact-arithmetic inputs only (the order differs from the oracle's).
 size_t gram_dense_doubles(int rows, int n);
+// c_exact: A^T b exact in any order (else summed per column in increasing
+// row order, the oracle's order: bitwise either way)
 cudaError_t launch_gram_dense(int n, const int32_t* rowptr, const int32_t* colind, const double* vals,
                               const int32_t* colptr, const int32_t* rowind, const double* cvals, const double* b,
                               int row_begin, int row_end, double* At, double* G, int ldg, double* c, int sm_count,
-                              cudaStream_t s);
+                              cudaStream_t s, bool c_exact);
 cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
                         const double* vals, const int32_t* colptr, const int32_t* rowind,
                         const double* cvals, const double* b, int row_begin, int row_end,

@@ -654,7 +654,12 @@ def test_notpd_fallback_single(P):
 @pytest.mark.parametrize("n,d", [(100, 1.0), (300, 1.0), (700, 1.0), (1000, 1.0), (800, 0.01), (1420, 0.01)])
 def test_fig2_workloads(P, n, d):
     prob = g.make_fig2(n, d, seed=1)
-    S = P.setup(prob, trace=1)
+    S = P.Solver(trace=1)
+    P.timing_enable(S.h, True)
+    S.load_problem(prob)
+    gram_launches = P.timing_read(S.h)["gram"][1]
+    P.timing_enable(S.h, False)
+    assert gram_launches == (4 if d == 1.0 else 1)      # density 1: the dense DMMA SYRK path
     G, c = S.gram()
     Go, co = O.gram(prob)
     assert np.array_equal(G, Go) and np.array_equal(c, co)
@@ -672,7 +677,10 @@ def test_dense_gram_row_shard_packed(P):
     tril = np.tril_indices(n)
     for r0, r1 in row_shards(prob.m, 3)[1:]:
         rp, ci, v, b = row_block(prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1)
-        S = P.BlockSolver().load_block(r1 - r0, n, rp, ci, v, b)
+        S = P.BlockSolver()
+        P.timing_enable(S.h, True)
+        S.load_block(r1 - r0, n, rp, ci, v, b)
+        assert P.timing_read(S.h)["gram"][1] == 4            # the dense path, packed output
         buf = gram_tensor(S).cpu().numpy()
         Gb, cb = O.gram(g.Problem(r1 - r0, n, rp, ci, v, b, prob.x_gen, prob.kind, prob.seed))
         assert np.array_equal(buf[:n * (n + 1) // 2], Gb[tril]) and np.array_equal(buf[n * (n + 1) // 2:], cb)
