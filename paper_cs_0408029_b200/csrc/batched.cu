@@ -2,24 +2,30 @@
 // per CTA, for batches of independent problems (BASELINE config 4: 65536
 // problems of 128 x 64, 20% dense; "one warp-group per problem").
 //
-// Everything for a problem lives in shared memory: CSR rows (values, 16-bit
-// column indices), a column view (per-column row bitmasks for the Gram, and
-// row index / CSR position lists for A^T u), the packed Gram, the packed
-// bordered factor and all vectors.  Steps, following PAPER.md:
-//   a1 Gram  G_ij = sum over rows set in mask_i & mask_j, increasing
-//                    row order, separate multiply/add -> same terms, same
-//                    order, same roundings as the CPU oracle (bit-identical).
+// Two kernels, one 128-thread CTA per problem each (grid-stride over the
+// batch); everything but the Gram lives in shared memory.  Steps, following
+// PAPER.md:
+//   batched_kernel (the pivot loop):
+//   a1 Gram  G_ij = sum over rows set in mask_i & mask_j (a column
+//                    view of per-column row bitmasks), increasing row order,
+//                    separate multiply/add -> the oracle's terms, order and
+//                    roundings (bit-identical); packed, in a per-CTA global
+//                    scratch that stays L2-resident, so the CSR's smem region
+//                    is reused by the factor (~24 KB per problem).
 //   a2 init, a3 decide/exchange, a4 compaction (ballot)
-//   a5 Cholesky of the bordered [G_FF; c_F^T], right-looking, each entry
-//                    updated in increasing k with separate mul/sub (the
-//                    oracle's jki rounding sequence: bit-identical factor);
-//                    two CTA barriers per column, no index decoding (every
-//                    thread steps through its own packed entries).
+//   a5 Cholesky of the bordered [G_FF; c_F^T], LEFT-looking by columns in the
+//                    oracle's jki order (bit-identical factor) on warp 0
+//                    alone (a lane owns two rows; one __syncwarp per column,
+//                    the other warps wait once)
 //   a6 back substitution L^T x = z by a column sweep on one warp (lane k
-//                    owns z_k; x_i is broadcast by a shuffle)
+//                    owns z_k; its summation order differs from the oracle's)
 //   a7/a8 dual y_G = G_GF x_F - c_G (oracle order per entry), zeroing
-//   a10 LSQR on the final F on warp 0 alone: warp-shuffle norms, no
-//                    CTA barriers inside the iteration
+//   NEXT-2 (lsqr_mode 3) the condition estimate of the final factor on warp 0
+//   batched_lsqr_kernel:
+//   a10 LSQR on the final F on all four warps (thread r owns row r,
+//                    2-4 threads per F column; three CTA barriers per
+//                    iteration), A restricted to F (rows stored F entries
+//                    first)
 //   a11 report (objective, KKT of Eq. 3)
 // Problems are independent: CTAs grid-stride over the batch; no inter-CTA
 // communication.
