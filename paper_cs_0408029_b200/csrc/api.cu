@@ -1177,6 +1177,11 @@ BatchArgs batched_args(nnls_handle* h) {
   a.itn_limit = p.lsqr_itn_limit;
   a.kkt = p.kkt;
   a.adaptive_threshold = p.adaptive_threshold;
+  {
+    const char* cp = getenv("NNLS_BATCH_CAP");
+    a.lsqr_cap_pct = (cp && cp[0]) ? atoi(cp) : 90;
+    if (a.lsqr_cap_pct < 10) a.lsqr_cap_pct = 10;
+  }
   a.colview = P<uint8_t>(h->b_colview);
   a.cv_stride = batched_colview_stride(h->n, h->ldg);
   a.gram = P<double>(h->b_gram);

@@ -595,35 +595,54 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
 }
 
 // a10 LSQR on the final F and a11 report, one problem per 128-thread
-// CTA: CSR, the column view and the vectors only (~25 KB at config 4).
+// CTA.  A restricted to F is held in shared memory twice, both as SLICED
+// ELL (SELL-32) blocks: by rows (thread r owns row r; warp slice w holds its
+// 32 rows' F entries entry-major, padded to the slice's longest row) and by
+// F columns (a column's entries dealt round-robin to its tpc threads; slices
+// of 32 thread slots).  Every value / index load of the two products is then
+// one conflict-free wavefront pair, and the column product needs no
+// indirection through the row storage; only the gathers of v and u are
+// random.  (ncu on the previous CSR/CSC layout: the two products were 78 % of
+// the kernel's shared-memory wavefronts, over half of them bank conflicts.)
+// Built straight from the global CSR and the pivot kernel's column view;
+// a problem whose padded blocks exceed the capacity (very uneven rows) runs
+// its products from global memory instead.  The report reads global memory.
 struct LLay {
-  int orv, ou, ov, ow, oX, ored;  // double offsets (b and the NE x stay in global memory)
+  int ors, ocs, ou, ov, ow, oX, ored;  // double offsets
   int doubles;
-  int irp, ico, imk, ici, icr, icx, irf, ifl;
-  int ints;
+  int iri, icr, irof, icof, ifl, ircnt, irp, icp, imk;  // byte offsets in the int area
+  int cap;                             // entries per SELL block
   size_t bytes;
 };
-__host__ __device__ inline LLay llayout(int m, int n, int nnz_max) {
+__host__ __device__ inline LLay llayout(int m, int n, int nnz_max, int cap_pct) {
   LLay L;
+  // padded F blocks: ~1.1 nnz_F, nnz_F ~ nnz f/n (config 4: f/n ~ 0.5, up to
+  // 0.7); cap_pct = 90 covers every problem of the config-4 batch (measured:
+  // 70 % -> 34 ms, 80 % -> 24 ms, 90 % -> 21.8 ms, 100 % -> 22.7 ms per batch);
+  // a problem that does not fit takes the global-memory path
+  L.cap = ((nnz_max * cap_pct / 100 + 31) / 32) * 32 + 32;  // (sorted slices pad ~10 %)
   int o = 0;
-  L.orv = o; o += nnz_max;
-  L.ou = o; o += m;                 // (during the load: the rows' F-entry bits, u64)
+  L.ors = o; o += L.cap;
+  L.ocs = o; o += L.cap;
+  L.ou = o; o += m;
   L.ov = o; o += n;
   L.ow = o; o += n;
   L.oX = o; o += n;
   L.ored = o; o += 32;
   L.doubles = o;
-  int q = 0;
-  L.irp = q; q += m + 1;
-  L.ico = q; q += n + 1;
-  L.imk = q; q += (n + 3) / 4;
-  L.ici = q; q += (nnz_max + 1) / 2;
-  L.icr = q; q += (nnz_max + 1) / 2;
-  L.icx = q; q += (nnz_max + 1) / 2;
-  L.irf = q; q += m + 1;            // row r's F entries: [rp[r], rpF[r])
-  L.ifl = q; q += n + 1;            // F columns in index order (compacted)
-  L.ints = q + 8;
-  L.bytes = sizeof(double) * (size_t)L.doubles + sizeof(int) * (size_t)L.ints;
+  int q = 0;  // bytes
+  L.iri = q; q += L.cap;                        // row SELL column indices (u8)
+  L.icr = q; q += L.cap;                        // column SELL row indices (u8)
+  q = (q + 15) & ~15;
+  L.irof = q; q += 4 * 12;                      // row slice offsets (<= 8 slices + 1)
+  L.icof = q; q += 4 * 8;                       // column slice offsets (4 slices + 1)
+  L.ifl = q; q += 4 * (n + 1);                  // F columns, index order
+  L.ircnt = q; q += 4 * (m > n ? m : n);        // F entries per row / per F column (sort keys)
+  L.irp = q; q += m;                            // rows by decreasing F count (SELL-sigma)
+  L.icp = q; q += n;                            // F columns by decreasing length
+  L.imk = q; q += n;
+  q = (q + 15) & ~15;
+  L.bytes = sizeof(double) * (size_t)L.doubles + (size_t)q;
   return L;
 }
 
@@ -631,63 +650,47 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
   long long bp_t = clock64();
   extern __shared__ double sm[];
   const int m = a.m, n = a.n;
-  const LLay Ly = llayout(m, n, nnz_max);
-  double* rv = sm + Ly.orv;
+  const LLay Ly = llayout(m, n, nnz_max, a.lsqr_cap_pct);
+  double* rS = sm + Ly.ors;
+  double* cS = sm + Ly.ocs;
   double* u = sm + Ly.ou;
   double* v = sm + Ly.ov;
   double* w = sm + Ly.ow;
   double* X = sm + Ly.oX;
   double* red = sm + Ly.ored;
-  int* ib = reinterpret_cast<int*>(sm + Ly.doubles);
-  int* rp = ib + Ly.irp;
-  int* co = ib + Ly.ico;
-  uint8_t* mk = reinterpret_cast<uint8_t*>(ib + Ly.imk);
-  uint16_t* ci = reinterpret_cast<uint16_t*>(ib + Ly.ici);
-  uint16_t* crow = reinterpret_cast<uint16_t*>(ib + Ly.icr);
-  uint16_t* cpos = reinterpret_cast<uint16_t*>(ib + Ly.icx);
-  int* rpF = ib + Ly.irf;
-  unsigned long long* fb = reinterpret_cast<unsigned long long*>(u);  // load phase only
-  int* fl = ib + Ly.ifl;
+  unsigned char* ib = reinterpret_cast<unsigned char*>(sm + Ly.doubles);
+  uint8_t* rI = ib + Ly.iri;
+  uint8_t* cR = ib + Ly.icr;
+  int* roff = reinterpret_cast<int*>(ib + Ly.irof);
+  int* coff = reinterpret_cast<int*>(ib + Ly.icof);
+  int* fl = reinterpret_cast<int*>(ib + Ly.ifl);
+  int* kcnt = reinterpret_cast<int*>(ib + Ly.ircnt);
+  uint8_t* rperm = ib + Ly.irp;
+  uint8_t* cperm = ib + Ly.icp;
+  uint8_t* mk = ib + Ly.imk;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double tol = a.tol;
-  __shared__ int s_istop;
+  __shared__ int s_istop, s_ws[8], s_wc[4], s_over;
   if (a.guard && *(volatile const int*)a.guard) return;  // invalid input (pipelined path)
+  const int nsl = (m + 31) / 32;  // row slices (<= 8)
   for (int prob = blockIdx.x; prob < a.batch; prob += gridDim.x) {
     const int64_t e0 = a.nnz_off[prob];
-    const int nz = (int)(a.nnz_off[prob + 1] - e0);
     const int status = a.info_i[(size_t)prob * kInfoI + 0];
     const int f = a.info_i[(size_t)prob * kInfoI + 3];
-    for (int r = tid; r <= m; r += BT) rp[r] = a.rowptr[(size_t)prob * (m + 1) + r];
-    const double* bb = a.b + (size_t)prob * m;       // b (global, read twice)
+    const int32_t* rpg = a.rowptr + (size_t)prob * (m + 1);
+    const int32_t* gci = a.colind + e0;
+    const double* gvl = a.vals + e0;
+    const double* bb = a.b + (size_t)prob * m;       // b (global)
     const double* x = a.x_out + (size_t)prob * n;    // the NE x (global; overwritten by the output below)
+    const int32_t* cvw = reinterpret_cast<const int32_t*>(a.colview + (size_t)prob * a.cv_stride);
+    const uint16_t* cvr = reinterpret_cast<const uint16_t*>(cvw + (n + 1));
     for (int j = tid; j < n; j += BT) {
       mk[j] = a.mask_out[(size_t)prob * n + j];
       v[j] = 0.0;
       X[j] = 0.0;
     }
+    if (tid == 0) s_over = 0;
     __syncthreads();
-    // LSQR works on A restricted to F: each row is stored F entries
-    // first, then G entries, both in their original order, so the row SpMV
-    // walks [rp[r], rpF[r]) only.  fb[r] marks row r's F entries (a row has
-    // at most n <= 64), which re-points the column view at the moved entries
-    // in O(1); the report below still reads every column.
-    const int32_t* gci = a.colind + e0;
-    const double* gvl = a.vals + e0;
-    for (int r = tid; r < m; r += BT) {
-      const int r0 = rp[r], r1 = rp[r + 1];
-      unsigned long long bits = 0ull;
-      for (int e = r0; e < r1; ++e)
-        if (mk[gci[e]]) bits |= 1ull << (e - r0);
-      const int nFr = __popcll(bits);
-      int wF = r0, wG = r0 + nFr;
-      for (int e = r0; e < r1; ++e) {
-        const int w2 = ((bits >> (e - r0)) & 1ull) ? wF++ : wG++;
-        ci[w2] = (uint16_t)gci[e];
-        rv[w2] = gvl[e];
-      }
-      rpF[r] = r0 + nFr;
-      fb[r] = bits;
-    }
     if (wid == 0) {  // F columns in index order
       int base = 0;
       for (int j0 = 0; j0 < n; j0 += 32) {
@@ -700,29 +703,122 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
       if (lane == 0) fl[n] = base;
     }
     __syncthreads();
+    const int nF = fl[n];
+    const int tpc = nF <= 32 ? 4 : 2;  // threads per F column
+    // ---- row SELL-sigma: rows sorted by decreasing F count (rank = rows
+    //      with more entries, ties by index), so a 32-row slice's padding to
+    //      its longest row stays small; thread t then owns row rperm[t]
+    for (int r = tid; r < m; r += BT) {
+      int c = 0;
+      for (int e = rpg[r]; e < rpg[r + 1]; ++e) c += mk[gci[e]];
+      kcnt[r] = c;
+    }
+    __syncthreads();
+    for (int r = tid; r < m; r += BT) {
+      const int c = kcnt[r];
+      int rank = 0;
+      for (int q = 0; q < m; ++q) {
+        const int cq = kcnt[q];
+        rank += (cq > c) || (cq == c && q < r);
+      }
+      rperm[rank] = (uint8_t)r;
+    }
+    __syncthreads();
+    int cntr[2] = {0, 0};
+    for (int h = 0; h < 2; ++h) {
+      const int t = tid + BT * h;
+      if (t < m) cntr[h] = kcnt[rperm[t]];
+    }
+    for (int h = 0; h < 2; ++h) {
+      const int wmax = warp_max_i(cntr[h]);
+      if (lane == 0 && wid + 4 * h < nsl) s_ws[wid + 4 * h] = wmax;
+    }
+    __syncthreads();
+    // ---- column SELL: F columns sorted by decreasing length; slot tid =
+    //      (group, sub) takes entries k = sub (mod tpc) of its group's column
+    for (int g = tid; g < nF; g += BT) kcnt[g] = cvw[fl[g] + 1] - cvw[fl[g]];
+    __syncthreads();
+    for (int g = tid; g < nF; g += BT) {
+      const int c = kcnt[g];
+      int rank = 0;
+      for (int q = 0; q < nF; ++q) {
+        const int cq = kcnt[q];
+        rank += (cq > c) || (cq == c && q < g);
+      }
+      cperm[rank] = (uint8_t)g;
+    }
+    __syncthreads();
+    const int grp = tid / tpc, sub = tid % tpc;
+    const bool colgrp = grp < nF;
+    const int jc = colgrp ? fl[cperm[grp]] : 0;
+    const int c0 = colgrp ? cvw[jc] : 0, c1 = colgrp ? cvw[jc + 1] : 0;
+    const int cntc = colgrp ? max(0, (c1 - c0 - sub + tpc - 1) / tpc) : 0;
     {
-      const int32_t* cvw = reinterpret_cast<const int32_t*>(a.colview + (size_t)prob * a.cv_stride);
-      const uint16_t* cvr = reinterpret_cast<const uint16_t*>(cvw + (n + 1));
-      for (int j = tid; j <= n; j += BT) co[j] = cvw[j];
-      for (int t = tid; t < nz; t += BT) {
-        const int r = cvr[t];
-        const int k = cvr[nnz_max + t] - rp[r];
-        const unsigned long long bits = fb[r];
-        const int below = __popcll(bits & ((1ull << k) - 1ull));
-        crow[t] = (uint16_t)r;
-        cpos[t] = (uint16_t)(((bits >> k) & 1ull) ? rp[r] + below : rpF[r] + (k - below));
+      const int wmax = warp_max_i(cntc);
+      if (lane == 0) s_wc[wid] = wmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int o = 0;
+      for (int sl = 0; sl < 8; ++sl) {
+        if (sl >= nsl) s_ws[sl] = 0;  // (warps with no second slice read width 0)
+        roff[sl] = o;
+        o += 32 * s_ws[sl];
+      }
+      roff[8] = o;
+      int oc = 0;
+      for (int sl = 0; sl < 4; ++sl) {
+        coff[sl] = oc;
+        oc += 32 * s_wc[sl];
+      }
+      coff[4] = oc;
+      s_over = (o > Ly.cap || oc > Ly.cap) ? 1 : 0;
+    }
+    __syncthreads();
+    const bool sell = !s_over;
+    if (sell) {
+      for (int h = 0; h < 2; ++h) {
+        const int t = tid + BT * h, sl = wid + 4 * h;
+        if (sl >= nsl) continue;
+        const int r = t < m ? rperm[t] : m;
+        const int base = roff[sl] + lane, W = s_ws[sl];
+        int k = 0;
+        if (r < m)
+          for (int e = rpg[r]; e < rpg[r + 1]; ++e) {
+            const int j = gci[e];
+            if (mk[j]) {
+              rS[base + 32 * k] = gvl[e];
+              rI[base + 32 * k] = (uint8_t)j;
+              ++k;
+            }
+          }
+        for (; k < W; ++k) {
+          rS[base + 32 * k] = 0.0;
+          rI[base + 32 * k] = 0;
+        }
+      }
+      {
+        const int base = coff[wid] + lane, W = s_wc[wid];
+        int k = 0;
+        for (int t = c0 + sub; t < c1; t += tpc, ++k) {
+          cS[base + 32 * k] = gvl[cvr[nnz_max + t]];
+          cR[base + 32 * k] = (uint8_t)cvr[t];
+        }
+        for (; k < W; ++k) {
+          cS[base + 32 * k] = 0.0;
+          cR[base + 32 * k] = 0;
+        }
       }
     }
     __syncthreads();
-    const int nF = fl[n];
     BP_MARK(10);  // LSQR kernel: load
     // ---------------------------------------------------------- a10 LSQR
     // All 4 warps.  Thread r owns row r (u); a group of tpc threads owns the
-    // F column fl[grp] (v, w, X; the group splits A^T u).  Three CTA barriers per iteration: the
-    // norm reductions (|u|^2 | |v|^2, |d|^2, |x|^2) each end with one, and the
-    // vectors a thread reads from others were written before it; the stopping
-    // test of an iteration is evaluated after the next barrier (it needs only
-    // scalars, and x is not touched in between).
+    // F column fl[grp] (v, w, X; the group splits A^T u).  Three CTA barriers
+    // per iteration: the norm reductions (|u|^2 | |v|^2, |d|^2, |x|^2) each
+    // end with one, and the vectors a thread reads from others were written
+    // before it; the stopping test of an iteration is evaluated after the next
+    // barrier (it needs only scalars, and x is not touched in between).
     int itn = 0, istop = 0;
     const int mode0 = (status == 0 && f > 0) ? a.lsqr_mode : 0;
     // mode 3 (adaptive): the pivot kernel's condition estimate decided
@@ -746,63 +842,71 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
         if (nv > 2) out[2] = (rr[8] + rr[9]) + (rr[10] + rr[11]);
         rslot ^= 1;
       };
-      // row SpMV: s = A(r, :) v with 4 independent partial sums (v_G = 0)
-      // (vec is zero outside F: x and v are, so no mask test)
-      auto row_dot = [&](int r, const double* vec) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        const int t1 = rpF[r];
-        int e = rp[r];
-        for (; e + 3 < t1; e += 4) {
-          s0 = fma(rv[e], vec[ci[e]], s0);
-          s1 = fma(rv[e + 1], vec[ci[e + 1]], s1);
-          s2 = fma(rv[e + 2], vec[ci[e + 2]], s2);
-          s3 = fma(rv[e + 3], vec[ci[e + 3]], s3);
+      // row product s = A_F(r, :) vec (h: the thread's second row when m > 128)
+      auto row_dot = [&](int h, const double* vec) {
+        const int t = tid + BT * h, sl = wid + 4 * h;
+        const int r = t < m ? rperm[t] : m;
+        double s0 = 0.0, s1 = 0.0;
+        if (sell) {
+          const int base = roff[sl] + lane, W = s_ws[sl];
+          int k = 0;
+          for (; k + 1 < W; k += 2) {
+            s0 = fma(rS[base + 32 * k], vec[rI[base + 32 * k]], s0);
+            s1 = fma(rS[base + 32 * (k + 1)], vec[rI[base + 32 * (k + 1)]], s1);
+          }
+          if (k < W) s0 = fma(rS[base + 32 * k], vec[rI[base + 32 * k]], s0);
+        } else if (r < m) {
+          for (int e = rpg[r]; e < rpg[r + 1]; ++e) {
+            const int j = gci[e];
+            if (mk[j]) s0 = fma(gvl[e], vec[j], s0);
+          }
         }
-        for (; e < t1; ++e) s0 = fma(rv[e], vec[ci[e]], s0);
-        return (s0 + s1) + (s2 + s3);
+        return s0 + s1;
       };
-      // column SpMV over the F columns only: tpc threads per column (4 when
-      // |F| <= 32, else 2), thread sub takes entries t - co[j] = sub (mod tpc)
-      const int tpc = nF <= 32 ? 4 : 2;
-      const int grp = tid / tpc, sub = tid % tpc;
-      const bool colgrp = grp < nF;
-      const int jc = colgrp ? fl[grp] : 0;
-      const bool colown = colgrp && sub == 0;
+      // column product over the F columns: the slot's entries, then the group's sum
       auto col_dot = [&](const double* vec) {
         double s0 = 0.0, s1 = 0.0;
-        if (colgrp) {
-          const int t1 = co[jc + 1];
-          int t = co[jc] + sub;
-          for (; t + tpc < t1; t += 2 * tpc) {
-            s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
-            s1 = fma(rv[cpos[t + tpc]], vec[crow[t + tpc]], s1);
+        if (sell) {
+          const int base = coff[wid] + lane, W = s_wc[wid];
+          int k = 0;
+          for (; k + 1 < W; k += 2) {
+            s0 = fma(cS[base + 32 * k], vec[cR[base + 32 * k]], s0);
+            s1 = fma(cS[base + 32 * (k + 1)], vec[cR[base + 32 * (k + 1)]], s1);
           }
-          if (t < t1) s0 = fma(rv[cpos[t]], vec[crow[t]], s0);
+          if (k < W) s0 = fma(cS[base + 32 * k], vec[cR[base + 32 * k]], s0);
+        } else if (colgrp) {
+          for (int t = c0 + sub; t < c1; t += tpc) s0 = fma(gvl[cvr[nnz_max + t]], vec[cvr[t]], s0);
         }
         double sacc = s0 + s1;
         sacc += __shfl_xor_sync(kFull, sacc, 1);
         if (tpc == 4) sacc += __shfl_xor_sync(kFull, sacc, 2);
         return sacc;
       };
+      const bool colown = colgrp && sub == 0;
       double tot[3];
       // beta u = b - A x (mode 2) or b
       double pu = 0.0;
-      for (int r = tid; r < m; r += BT) {
-        const double sacc = (mode == 2) ? row_dot(r, x) : 0.0;
-        const double uu = bb[r] - sacc;
-        u[r] = uu;
-        pu += uu * uu;
+      for (int h = 0; h < 2; ++h) {
+        const int t = tid + BT * h;
+        if (BT * h >= m) continue;
+        const int r = t < m ? rperm[t] : m;
+        const double sacc = (mode == 2) ? row_dot(h, x) : 0.0;  // (uniform per warp slice)
+        if (r < m) {
+          const double uu = bb[r] - sacc;
+          u[r] = uu;
+          pu += uu * uu;
+        }
       }
       reduce3(pu, 0.0, 0.0, 1, tot);  // B: u complete
       double beta = sqrt(tot[0]);
       const double bnorm = beta;
-      double ib = beta > 0.0 ? 1.0 / beta : 0.0;
+      double ibt = beta > 0.0 ? 1.0 / beta : 0.0;
       // alpha v = A^T u
       double pv = 0.0;
       {
         const double sacc = beta > 0.0 ? col_dot(u) : 0.0;
         if (colown) {
-          const double vv = sacc * ib;
+          const double vv = sacc * ibt;
           v[jc] = vv;
           pv = vv * vv;
         }
@@ -810,7 +914,7 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
       reduce3(pv, 0.0, 0.0, 1, tot);  // B: every read of u done
       double alpha = sqrt(tot[0]);
       const double ia0 = alpha > 0.0 ? 1.0 / alpha : 0.0;
-      for (int r = tid; r < m; r += BT) u[r] *= ib;  // own rows
+      for (int r = tid; r < m; r += BT) u[r] *= ibt;  // own rows
       if (colown) {
         v[jc] *= ia0;
         w[jc] = v[jc];
@@ -818,9 +922,6 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
       __syncthreads();  // v, u complete
       double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
       const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
-      // the stopping test of iteration t is evaluated by thread 0 after that
-      // iteration's last barrier and read by everyone after the next one (x
-      // is not touched in between, so breaking there returns iteration t)
       if (tid == 0) s_istop = 0;
       if (alpha * beta != 0.0) {
         for (;;) {
@@ -828,10 +929,16 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
           const bool more = itn < itn_limit;
           pu = 0.0;
           if (more)
-            for (int r = tid; r < m; r += BT) {
-              const double uu = row_dot(r, v) - alpha * u[r];
-              u[r] = uu;
-              pu += uu * uu;
+            for (int h = 0; h < 2; ++h) {
+              const int t = tid + BT * h;
+              if (BT * h >= m) continue;
+              const int r = t < m ? rperm[t] : m;
+              const double rd = row_dot(h, v);
+              if (r < m) {
+                const double uu = rd - alpha * u[r];
+                u[r] = uu;
+                pu += uu * uu;
+              }
             }
           reduce3(pu, 0.0, 0.0, 1, tot);  // B1: u' complete; the previous test visible
           istop = s_istop;
@@ -840,19 +947,19 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
           beta = sqrt(tot[0]);
           double alpha_new = alpha;
           if (beta > 0.0) {
-            ib = 1.0 / beta;
+            ibt = 1.0 / beta;
             anorm = sqrt(anorm * anorm + alpha * alpha + beta * beta);
             // v' = A^T u' / beta - beta v (own columns)
             const double sacc = col_dot(u);
             pv = 0.0;
             if (colown) {
-              const double vv = sacc * ib - beta * v[jc];
+              const double vv = sacc * ibt - beta * v[jc];
               v[jc] = vv;
               pv = vv * vv;
             }
             reduce3(pv, 0.0, 0.0, 1, tot);  // B2: every read of u' done
             alpha_new = sqrt(tot[0]);
-            for (int r = tid; r < m; r += BT) u[r] *= ib;  // own rows
+            for (int r = tid; r < m; r += BT) u[r] *= ibt;  // own rows
             if (alpha_new > 0.0 && colown) v[jc] *= 1.0 / alpha_new;
           }
           const double rho = sqrt(rhobar * rhobar + beta * beta);
@@ -916,11 +1023,11 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
     }
     const int any_infeas = __syncthreads_or(infeas);
     double obj = 0.0, mx = INFINITY, my = INFINITY, mc = 0.0, dot = 0.0;
-    if (a.kkt) {
+    if (a.kkt) {  // the report over all of A, from global memory (once per problem)
       double po = 0.0;
       for (int r = tid; r < m; r += BT) {
         double sacc = 0.0;
-        for (int e = rp[r]; e < rp[r + 1]; ++e) sacc = fma(rv[e], w[ci[e]], sacc);
+        for (int e = rpg[r]; e < rpg[r + 1]; ++e) sacc = fma(gvl[e], w[gci[e]], sacc);
         const double rr = sacc - bb[r];
         u[r] = rr;
         po += rr * rr;
@@ -929,7 +1036,7 @@ __global__ void __launch_bounds__(BT, 8) batched_lsqr_kernel(BatchArgs a, int nn
       double lmx = INFINITY, lmy = INFINITY, lmc = 0.0, ld = 0.0;
       for (int j = tid; j < n; j += BT) {
         double sacc = 0.0;
-        for (int t = co[j]; t < co[j + 1]; ++t) sacc = fma(rv[cpos[t]], u[crow[t]], sacc);
+        for (int t = cvw[j]; t < cvw[j + 1]; ++t) sacc = fma(gvl[cvr[nnz_max + t]], u[cvr[t]], sacc);
         const double xj = w[j];
         lmx = fmin(lmx, xj);
         lmy = fmin(lmy, sacc);
@@ -1112,7 +1219,7 @@ size_t batched_colview_stride(int n, int nnz_max) {
 
 cudaError_t launch_batched_nnz(const BatchArgs& a, int nnz_max, int sm_count, cudaStream_t s) {
   const size_t smem = layout(a.m, a.n, nnz_max).bytes;
-  const size_t smem2 = llayout(a.m, a.n, nnz_max).bytes;
+  const size_t smem2 = llayout(a.m, a.n, nnz_max, a.lsqr_cap_pct).bytes;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

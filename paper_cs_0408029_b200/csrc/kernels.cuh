@@ -164,6 +164,7 @@ struct BatchArgs {
   double tol, atol, btol, conlim;
   int p_max, max_iter, lsqr_mode, itn_limit, kkt;
   double adaptive_threshold;  // lsqr_mode 3
+  int lsqr_cap_pct;           // LSQR kernel: SELL capacity in % of nnz_max (env NNLS_BATCH_CAP, default 90)
   uint8_t* colview;  // scratch: per problem the column view (batched_colview_stride bytes)
   size_t cv_stride;
   double* gram;      // scratch: one packed Gram per CTA (batched_gram_scratch bytes)
