@@ -167,10 +167,7 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
     const int64_t e0 = a.nnz_off[prob];
     const int nz = (int)(a.nnz_off[prob + 1] - e0);
     for (int r = tid; r <= m; r += BT) rp[r] = a.rowptr[(size_t)prob * (m + 1) + r];
-    for (int e = tid; e < nz; e += BT) {
-      ci[e] = (uint8_t)a.colind[e0 + e];
-      rv[e] = a.vals[e0 + e];
-    }
+    for (int e = tid; e < nz; e += BT) ci[e] = (uint8_t)a.colind[e0 + e];
     for (int r = tid; r < m; r += BT) bb[r] = a.b[(size_t)prob * m + r];
     for (int q = tid; q < n * W; q += BT) cm[q] = 0u;
     __syncthreads();
@@ -214,6 +211,7 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
         rank += __popc(cm[j * W + wr] & below);
         crow[rank] = (uint8_t)r;
         cpos[rank] = (uint16_t)e;
+        rv[rank] = a.vals[e0 + e];  // values in COLUMN order (the Gram reads them by rank)
       }
     }
     __syncthreads();
@@ -243,8 +241,8 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
           while (both) {
             const int bpos = __ffs(both) - 1;
             const unsigned bl = (1u << bpos) - 1u;
-            const double vi = rv[cpos[ki + __popc(mi & bl)]];
-            const double vj = rv[cpos[kj + __popc(mj & bl)]];
+            const double vi = rv[ki + __popc(mi & bl)];
+            const double vj = rv[kj + __popc(mj & bl)];
             sacc = __dadd_rn(sacc, __dmul_rn(vi, vj));
             both &= both - 1u;
           }
@@ -256,7 +254,7 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
     }
     for (int j = tid; j < n; j += BT) {
       double sacc = 0.0;
-      for (int t = co[j]; t < co[j + 1]; ++t) sacc = __dadd_rn(sacc, __dmul_rn(rv[cpos[t]], bb[crow[t]]));
+      for (int t = co[j]; t < co[j + 1]; ++t) sacc = __dadd_rn(sacc, __dmul_rn(rv[t], bb[crow[t]]));
       c[j] = sacc;
     }
     // the column view goes to kernel B now (phase 2 overwrites it)
