@@ -1,0 +1,7 @@
+set -u
+O=gpurun_out/r2w
+mkdir -p $O
+timeout 600 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
+echo done
