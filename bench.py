@@ -286,14 +286,15 @@ class Ctx:
         return sum(a.elapsed_time(b) for a, b in ev)
 
 
-def measure_single(C, cfg, steps, warmup, shard=False, with_e2e=True, full_fact=True, trace=True, **solver_kw):
+def measure_single(C, cfg, steps, warmup, shard=False, with_e2e=True, full_fact=True, trace=True, raw=False,
+                   **solver_kw):
     """Single problem (configs 0-3).  shard (N > 1, config 2): row-sharded Gram
     + reduce to rank 0, the loop on rank 0."""
     import nnls_gen as g
     import paper_cs_0408029_b200 as P
     torch, args = C.torch, C.args
     world, rank = C.world, C.rank
-    prob = g.make_problem(cfg, seed=args.seed + (0 if shard else rank))
+    prob = g.make_problem(cfg, seed=args.seed + (0 if shard else rank), raw=raw)
     host = dict(rowptr=prob.rowptr, colind=prob.colind, vals=prob.vals, b=prob.b)
     if shard:
         from paper_cs_0408029_b200.dist import reduce_gram, row_block, row_shards
@@ -574,6 +575,15 @@ def run_ours(args):
                                             if k in ("value", "ms_per_step", "phase_ms_per_step", "per_solve")}
             extra["adaptive_lsqr_mode3"]["per_solve"].pop("trace", None)
             extra["adaptive_lsqr_mode3"]["workload"] = workload_desc(cfg, args.batch) + ", lsqr_mode 3"
+            # the unquantized variant: A^T A and A^T b are not exact in FP64, so
+            # the Gram takes the ordered (oracle summation order) path
+            r = measure_single(C, cfg, args.steps, 3, with_e2e=False, full_fact=False, raw=True)
+            extra["raw_inputs"] = {k: v for k, v in round_res(r).items()
+                                   if k in ("value", "ms_per_step", "phase_ms_per_step", "per_solve",
+                                            "kernel_rooflines")}
+            extra["raw_inputs"]["per_solve"].pop("trace", None)
+            extra["raw_inputs"]["workload"] = (workload_desc(cfg, args.batch).replace("(2^-12 grid)", "(raw)")
+                                               + ", unquantized values (ordered Gram path)")
         elif cfg != 4:
             r = measure_batched(C, max(3, args.steps // 4), 3, with_e2e=False)
             extra["config4_sharded"] = {k: v for k, v in round_res(r).items()

@@ -99,6 +99,7 @@ struct nnls_handle {
   Buf Gp;                                 // row-shard partial: packed lower G (n(n+1)/2) then c (n)
   int shard = 0;                          // 0 whole problem, 1 shard root (full A), 2 row block only
   Buf mask, x, y, xF, Fidx, Gidx;         // pivot state
+  Buf inflist;                            // fused dual: the iteration's infeasible indices
   Buf pos, Fs, xs;                        // factor reuse: order positions, F sorted, x_F by index
   Buf Lt, flags;                          // Cholesky tiles + DAG flags
   Buf U, V, W, X, R, partials, xfin;      // LSQR / report
@@ -112,6 +113,7 @@ struct nnls_handle {
   bool no_cluster = false;  // force the full-grid LSQR (tests / env NNLS_NO_CLUSTER)
   bool no_graph = false;    // host-driven pivot loop (env NNLS_NO_GRAPH, or capture failed)
   bool no_reuse = false;    // F in index order, no factor reuse across iterations (env NNLS_NO_REUSE)
+  bool no_fuse = false;     // separate count/exchange pass in decide (env NNLS_NO_FUSED_DUAL)
   bool no_exact_gram = false;  // always the row-ordered Gram kernel (env NNLS_NO_EXACT_GRAM)
   cudaGraphExec_t gexec = nullptr;
   std::vector<double> gkey;
@@ -237,6 +239,7 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->xF, sizeof(double) * (size_t)(n + kTile)));
   CK(ensure(h->Fidx, sizeof(int32_t) * (size_t)n));
   CK(ensure(h->Gidx, sizeof(int32_t) * (size_t)n));
+  CK(ensure(h->inflist, sizeof(int32_t) * (size_t)n));
   CK(ensure(h->pos, sizeof(int32_t) * (size_t)n));
   CK(ensure(h->Fs, sizeof(int32_t) * (size_t)n));
   CK(ensure(h->xs, sizeof(double) * (size_t)n));
@@ -354,6 +357,7 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
   h->no_cluster = env_on("NNLS_NO_CLUSTER");
   h->no_graph = env_on("NNLS_NO_GRAPH");
   h->no_reuse = env_on("NNLS_NO_REUSE");
+  h->no_fuse = env_on("NNLS_NO_FUSED_DUAL");
   h->no_exact_gram = env_on("NNLS_NO_EXACT_GRAM");
   *out = h;
   return NNLS_OK;
@@ -612,6 +616,7 @@ namespace {
 int32_t* pos_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<int32_t>(h->pos); }
 int32_t* fs_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<int32_t>(h->Fs); }
 double* xs_or_null(nnls_handle* h) { return h->no_reuse ? nullptr : P<double>(h->xs); }
+int32_t* inflist_or_null(nnls_handle* h) { return h->no_fuse ? nullptr : P<int32_t>(h->inflist); }
 
 // one pivot iteration: decide -> (gather + Cholesky + forward) -> back solve -> dual
 cudaError_t launch_iteration(nnls_handle* h, cudaStream_t s, const cudaGraphConditionalHandle* loop) {
@@ -632,7 +637,7 @@ cudaError_t launch_iteration(nnls_handle* h, cudaStream_t s, const cudaGraphCond
   if (e == cudaSuccess)
     e = launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
                     P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), h->prm.zero_tol, st, h->sms, s,
-                    fs_or_null(h), xs_or_null(h));
+                    fs_or_null(h), xs_or_null(h), inflist_or_null(h));
   return e;
 }
 
@@ -644,9 +649,9 @@ std::vector<double> graph_key(nnls_handle* h) {
                            (double)h->h->plan[3], p.zero_tol, (double)p.p_max, (double)p.max_iter,
                            (double)p.lsqr_mode, (double)p.lsqr_itn_limit, p.lsqr_atol, p.lsqr_btol,
                            p.lsqr_conlim, (double)p.kkt, (double)h->trace_cap, (double)h->no_cluster,
-                           (double)h->no_reuse, p.adaptive_threshold, (double)p.notpd_fallback};
+                           (double)h->no_reuse, (double)h->no_fuse, p.adaptive_threshold, (double)p.notpd_fallback};
   const Buf* bufs[] = {&h->rowptr, &h->colind, &h->vals, &h->b, &h->colptr, &h->rowind, &h->cvals,
-                       &h->Gc, &h->mask, &h->x, &h->y, &h->xF, &h->Fidx, &h->Gidx, &h->pos, &h->Fs, &h->xs, &h->Lt, &h->flags,
+                       &h->Gc, &h->mask, &h->x, &h->y, &h->xF, &h->Fidx, &h->Gidx, &h->inflist, &h->pos, &h->Fs, &h->xs, &h->Lt, &h->flags,
                        &h->U, &h->V, &h->W, &h->X, &h->R, &h->partials, &h->xfin, &h->st, &h->trace,
                        &h->Fval, &h->Fcol, &h->Fcnt, &h->cwork};
   for (const Buf* b : bufs) k.push_back((double)(uintptr_t)b->p);
@@ -809,7 +814,7 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
       TIMED(NNLS_PH_DUAL, 1,
             launch_dual(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), P<double>(h->xF),
                         P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y), p.zero_tol, st,
-                        h->sms, s, fs_or_null(h), xs_or_null(h)));
+                        h->sms, s, fs_or_null(h), xs_or_null(h), inflist_or_null(h)));
     }
     {
       const int ib = tm_begin(h);

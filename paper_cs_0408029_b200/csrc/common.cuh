@@ -42,6 +42,11 @@ struct DevState {
   double kappa;           // lsqr_mode 3: condition estimate of the final (A^T A)_FF (condest.cu)
   int32_t refined;        // 1: the final x comes from LSQR
   int32_t lsqr_fallbacks; // NOT_PD iterations solved by LSQR instead (notpd_fallback)
+  // fused dual + exchange (pivot.cu dual_kernel with an infeasible list)
+  int32_t decided;        // 1: the dual kernel counted, chose the branch and exchanged; decide only compacts
+  int32_t inf_count;      // infeasible entries appended to the list so far (= k at the end)
+  int32_t inf_last1;      // 1 + the largest infeasible index (0: none)
+  uint32_t dual_ticket;   // CTAs of the dual kernel that finished (the last one decides)
 };
 
 struct TraceRec {

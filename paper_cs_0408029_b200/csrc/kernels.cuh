@@ -80,7 +80,8 @@ cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t*
 cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
                         const int32_t* Gidx, const double* xF, uint8_t* mask, double* x,
                         double* y, double tol, DevState* st, int sm_count, cudaStream_t s,
-                        const int32_t* Fs = nullptr, const double* xs = nullptr);
+                        const int32_t* Fs = nullptr, const double* xs = nullptr,
+                        int32_t* inflist = nullptr);
 
 // ---- a5/a6 Cholesky + solves (cholesky.cu) -------------------------------
 size_t chol_tile_doubles(int n);

@@ -4,7 +4,11 @@
 //   a3 decide    count infeasibles, choose the branch, exchange
 //   a4 compact   Fidx / Gidx by warp ballot + block prefix scan
 //   a7/a8 dual   y_G = (A^T A)_GF x_F - (A^T b)_G (Eq. 5, Gram form), then
-//                |x_F|, |y_G| < tol -> 0 (reading c1)
+//                |x_F|, |y_G| < tol -> 0 (reading c1); inside the
+//                pivot loop the same kernel also counts the infeasibles
+//                (warp/block reductions + one atomic per CTA), and its last
+//                CTA chooses the branch and applies the exchange,
+//                so decide is left with the compaction (a4)
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -48,6 +52,10 @@ __global__ void init_kernel(int n, const double* __restrict__ c, uint8_t* mask, 
     st->kappa = 0.0;
     st->refined = 0;
     st->lsqr_fallbacks = 0;
+    st->decided = 0;
+    st->inf_count = 0;
+    st->inf_last1 = 0;
+    st->dual_ticket = 0u;
   }
 }
 
@@ -298,6 +306,34 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
 }
 
 // ------------------------------------------------- decide + exchange (a3, a4)
+// The branch of P:89-101 from the infeasible count kk of this iteration (one
+// thread): -1 feasible (k = 0, the while-loop ends) or the iteration limit
+// (reading c12); 0 block exchange with progress; 1 block exchange
+// within the p no-progress budget; 2 single exchange.
+__device__ int choose_branch(DevState* st, int kk) {
+  int branch;
+  st->k = kk;
+  if (kk == 0) {
+    st->done = 1;
+    branch = -1;
+  } else if (st->iter >= st->max_iter) {
+    st->status = 8;  // ITERATION_LIMIT
+    branch = -1;
+  } else if (kk < st->N) {
+    st->N = kk;
+    st->p = st->p_max;
+    branch = 0;
+  } else if (st->p > 0) {
+    st->p -= 1;
+    branch = 1;
+  } else {
+    st->singles += 1;
+    branch = 2;
+  }
+  st->branch = branch;
+  return branch;
+}
+
 // One CTA of 1024 threads.  Each thread owns the indices i = tid + 1024 q, so
 // the "snapshot before any flip" of reading c10 is automatic: a thread reads
 // its own (mask, x, y) and flips only its own entries after the block-wide
@@ -327,70 +363,58 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
     return;
   }
 
-  // pass 1: k = #{i in F: x_i < 0} + #{j in G: y_j < 0} (reading c5);
-  // largest infeasible original index (reading c6)
-  int k = 0, last = -1;
-  for (int i = tid; i < n; i += kDecideThreads) {
-    const bool inf = mask[i] ? (x[i] < 0.0) : (y[i] < 0.0);
-    if (inf) {
-      ++k;
-      last = i;
-    }
-  }
-  k = warp_sum_i(k);
-  last = warp_max_i(last);
-  if (lane == 0) {
-    s_cnt[wid] = k;
-    s_max[wid] = last;
-  }
+  // (fused) the dual kernel already counted, chose the branch and exchanged
+  if (tid == 0) s_branch = st->decided ? st->branch : -2;
   __syncthreads();
-  if (wid == 0) {
-    int kk = s_cnt[lane], ll = s_max[lane];
-    kk = warp_sum_i(kk);
-    ll = warp_max_i(ll);
-    if (lane == 0) {
-      int branch;
-      st->k = kk;
-      if (kk == 0) {
-        st->done = 1;  // feasible: the while-loop of P:89 ends
-        branch = -1;
-      } else if (st->iter >= st->max_iter) {
-        st->status = 8;  // ITERATION_LIMIT (reading c12)
-        branch = -1;
-      } else if (kk < st->N) {
-        st->N = kk;
-        st->p = st->p_max;
-        branch = 0;
-      } else if (st->p > 0) {
-        st->p -= 1;
-        branch = 1;
-      } else {
-        st->singles += 1;
-        branch = 2;
+  int branch = s_branch;
+  if (branch == -2) {
+    // pass 1: k = #{i in F: x_i < 0} + #{j in G: y_j < 0} (reading c5);
+    // largest infeasible original index (reading c6)
+    int k = 0, last = -1;
+    for (int i = tid; i < n; i += kDecideThreads) {
+      const bool inf = mask[i] ? (x[i] < 0.0) : (y[i] < 0.0);
+      if (inf) {
+        ++k;
+        last = i;
       }
-      st->branch = branch;
-      s_branch = branch;
-      s_fprev = st->keep_none ? 0 : st->f;  // (keep_none: the previous factor failed, nothing is kept)
-      st->keep_none = 0;
-      s_last = ll;
-      s_carryF = 0;
-      s_carryG = 0;
+    }
+    k = warp_sum_i(k);
+    last = warp_max_i(last);
+    if (lane == 0) {
+      s_cnt[wid] = k;
+      s_max[wid] = last;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int kk = s_cnt[lane], ll = s_max[lane];
+      kk = warp_sum_i(kk);
+      ll = warp_max_i(ll);
+      if (lane == 0) {
+        s_branch = choose_branch(st, kk);
+        s_last = ll;
+      }
+    }
+    __syncthreads();
+    branch = s_branch;
+    if (branch < 0) {
+      if (use_loop && tid == 0) cudaGraphSetConditional(loop, 0);  // feasible / iteration limit
+      return;
+    }
+    const int lastidx = s_last;
+    // pass 2: exchange (from the snapshot: each thread re-reads its own entries)
+    for (int i = tid; i < n; i += kDecideThreads) {
+      const uint8_t mi = mask[i];
+      const bool inf = mi ? (x[i] < 0.0) : (y[i] < 0.0);
+      const bool flip = (branch == 2) ? (i == lastidx) : inf;
+      if (flip) mask[i] = mi ? 0 : 1;
     }
   }
-  __syncthreads();
-  const int branch = s_branch;
-  if (branch < 0) {
-    if (use_loop && tid == 0) cudaGraphSetConditional(loop, 0);  // feasible / iteration limit
-    return;
-  }
-  const int lastidx = s_last;
-
-  // pass 2: exchange (from the snapshot: each thread re-reads its own entries)
-  for (int i = tid; i < n; i += kDecideThreads) {
-    const uint8_t mi = mask[i];
-    const bool inf = mi ? (x[i] < 0.0) : (y[i] < 0.0);
-    const bool flip = (branch == 2) ? (i == lastidx) : inf;
-    if (flip) mask[i] = mi ? 0 : 1;
+  if (tid == 0) {
+    st->decided = 0;
+    s_fprev = st->keep_none ? 0 : st->f;  // (keep_none: the previous factor failed, nothing is kept)
+    st->keep_none = 0;
+    s_carryF = 0;
+    s_carryG = 0;
   }
   __syncthreads();
 
@@ -474,12 +498,41 @@ cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y
 // --------------------------------------------------------- dual (a7, a8)
 // Warps over G: y_j = sum_a G[j, Fidx[a]] x_F[a] - c_j, from the UNCLAMPED
 // x_F (reading c3), then zeroing.  Threads over F: scatter the zeroed x_F.
-__global__ void __launch_bounds__(256) dual_kernel(
+//
+// Fused count + exchange (inflist != nullptr, the pivot loop): every entry
+// found infeasible after the zeroing (x_i < 0 for i in F, y_j < 0 for j in
+// G -- the count of P:90 over the same snapshot as the decide kernel's pass)
+// is appended to inflist through a per-CTA shared-memory list (one global
+// atomic per CTA); the largest such index is a block max, then one atomicMax.
+// The last CTA to finish (a ticket after a release fence) takes the branch of
+// P:89-101 and flips the listed entries (block exchange) or only the
+// largest one (single exchange); decide then only compacts and orders
+// the new F.  (The dual kernel never reads mask, so flipping it in its own
+// last CTA cannot race with the other CTAs.)
+constexpr int kDualThreads = 256;
+constexpr int kDualList = 512;  // per-CTA infeasible list; overflow goes straight to global
+
+__device__ __forceinline__ void dual_note_infeasible(int i, int* s_n, int* s_list, DevState* st,
+                                                     int32_t* inflist) {
+  const int slot = atomicAdd(s_n, 1);
+  if (slot < kDualList) s_list[slot] = i;
+  else inflist[atomicAdd(&st->inf_count, 1)] = i;
+}
+
+__global__ void __launch_bounds__(kDualThreads) dual_kernel(
     int n, const double* __restrict__ G, int ldg, const double* __restrict__ c,
     const int32_t* __restrict__ Fidx, const int32_t* __restrict__ Gidx,
     const double* __restrict__ xF, uint8_t* __restrict__ mask, double* __restrict__ x,
     double* __restrict__ y, double tol, DevState* st, const int32_t* __restrict__ Fs,
-    const double* __restrict__ xs) {
+    const double* __restrict__ xs, int32_t* __restrict__ inflist) {
+  __shared__ int s_n, s_lastinf, s_base, s_islast, s_branch, s_k;
+  __shared__ int s_list[kDualList];
+  const bool fused = inflist != nullptr;
+  if (threadIdx.x == 0) {
+    s_n = 0;
+    s_lastinf = -1;
+  }
+  __syncthreads();
   // Before waiting for the back substitution (PDL: it lets this grid start
   // once it runs): gather this warp's first G row entries G[j, F] into
   // registers -- G, F and the sets come from earlier kernels (decide).
@@ -589,6 +642,10 @@ __global__ void __launch_bounds__(256) dual_kernel(
         y[j] = v;
       }
       x[j] = 0.0;
+      if (fused && v < 0.0 && av >= tol) {  // y_j < 0 after the zeroing
+        dual_note_infeasible(j, &s_n, s_list, st, inflist);
+        atomicMax(&s_lastinf, j);
+      }
     }
   }
   for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < f; a += gridDim.x * blockDim.x) {
@@ -601,6 +658,10 @@ __global__ void __launch_bounds__(256) dual_kernel(
     } else {
       above = fmin(above, av);
       x[i] = v;
+      if (fused && v < 0.0) {  // x_i < 0 after the zeroing
+        dual_note_infeasible(i, &s_n, s_list, st, inflist);
+        atomicMax(&s_lastinf, i);
+      }
     }
     y[i] = 0.0;
   }
@@ -625,19 +686,60 @@ __global__ void __launch_bounds__(256) dual_kernel(
       if (ab < INFINITY) atomicMin(&st->above_bits, dbits(ab));
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->iter += 1;
-  (void)mask;
+  if (!fused) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->iter += 1;
+    return;
+  }
+  // (the __syncthreads above also published s_n / s_list / s_lastinf)
+  const int nloc = min(s_n, kDualList);
+  if (threadIdx.x == 0) {
+    s_base = nloc > 0 ? atomicAdd(&st->inf_count, nloc) : 0;
+    if (s_lastinf >= 0) atomicMax(&st->inf_last1, s_lastinf + 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nloc; e += blockDim.x) inflist[s_base + e] = s_list[e];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // release: this CTA's x, y, list entries before its ticket
+    s_islast = atomicAdd(&st->dual_ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_islast) return;
+  __threadfence();  // acquire: every CTA's entries
+  if (threadIdx.x == 0) {
+    st->iter += 1;  // (the completed solve of this iteration, reading c11)
+    const int kk = atomicAdd(&st->inf_count, 0);
+    const int branch = choose_branch(st, kk);
+    st->decided = 1;
+    s_branch = branch;
+    s_k = kk;
+    s_lastinf = atomicAdd(&st->inf_last1, 0) - 1;
+    st->inf_count = 0;  // (ready for the next iteration: every CTA is done)
+    st->inf_last1 = 0;
+    st->dual_ticket = 0u;
+  }
+  __syncthreads();
+  const int branch = s_branch;
+  if (branch == 0 || branch == 1) {  // block exchange of every infeasible entry
+    for (int e = threadIdx.x; e < s_k; e += blockDim.x) {
+      const int i = __ldcg(&inflist[e]);
+      mask[i] = mask[i] ? 0 : 1;
+    }
+  } else if (branch == 2 && threadIdx.x == 0) {  // single exchange of the largest index
+    const int i = s_lastinf;
+    mask[i] = mask[i] ? 0 : 1;
+  }
 }
 
 cudaError_t launch_dual(int n, const double* G, int ldg, const double* c, const int32_t* Fidx,
                         const int32_t* Gidx, const double* xF, uint8_t* mask, double* x,
                         double* y, double tol, DevState* st, int sm_count, cudaStream_t s,
-                        const int32_t* Fs, const double* xs) {
+                        const int32_t* Fs, const double* xs, int32_t* inflist) {
   int blocks = (n + 7) / 8;  // one warp per G index upper bound
   if (blocks > sm_count * 8) blocks = sm_count * 8;
   if (blocks < 1) blocks = 1;
-  return launch_pdl(dual_kernel, dim3(blocks), dim3(256), 0, s, n, G, ldg, c, Fidx, Gidx, xF, mask, x, y, tol, st,
-                    Fs, xs);
+  return launch_pdl(dual_kernel, dim3(blocks), dim3(kDualThreads), 0, s, n, G, ldg, c, Fidx, Gidx, xF, mask, x, y,
+                    tol, st, Fs, xs, inflist);
 }
 
 // --------------------------------------------- NOT_PD fallback

@@ -527,6 +527,19 @@ def test_index_order_path(P, cfg, seed, monkeypatch):
     assert_parity(P, g.make_problem(cfg, seed))
 
 
+@pytest.mark.parametrize("cfg,seed", [(0, 6), (1, 3), (3, 3)])
+@pytest.mark.parametrize("graph", [True, False])
+def test_unfused_decide_path(P, cfg, seed, graph, monkeypatch):
+    """By default the dual kernel also counts the infeasibles and its last CTA
+    takes the branch and applies the exchange (north_star step 4); the
+    separate count + exchange pass of the decide kernel (NNLS_NO_FUSED_DUAL)
+    must agree, in the graph loop and the host-driven loop."""
+    monkeypatch.setenv("NNLS_NO_FUSED_DUAL", "1")
+    if not graph:
+        monkeypatch.setenv("NNLS_NO_GRAPH", "1")
+    assert_parity(P, g.make_problem(cfg, seed))
+
+
 def test_graph_replay_across_loads(P):
     """One handle, the captured solve graph is reused / rebuilt across loads."""
     S = P.Solver(trace=1)
