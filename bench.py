@@ -214,8 +214,8 @@ def chol_flops(f, q=0):
 
 def phase_work(phase, prob, traces, lsqr_itns, nnzF_list):
     m, n, nnz = prob.m, prob.n, prob.nnz
-    if phase == "gram":       # read CSR+CSC+b, write full G (n*n) and c
-        return "hbm", float(2 * 12 * nnz + 4 * (m + n) + 8 * m + 8 * n * n + 8 * n)
+    if phase == "gram":       # read CSR+CSC+b, write full G (n*n) and c; once per solve
+        return "hbm", float(len(traces) * (2 * 12 * nnz + 4 * (m + n) + 8 * m + 8 * n * n + 8 * n))
     if phase == "chol_factor":
         return "tensor", float(sum(chol_flops(t["f"], t.get("kept", 0)) for tr in traces for t in tr))
     if phase == "chol_solve":

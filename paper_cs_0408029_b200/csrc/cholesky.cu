@@ -35,6 +35,7 @@
 //     - P_J^T x_{J+2}) fed by helper tasks through mailboxes.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -803,7 +804,8 @@ __device__ __forceinline__ void ring_consume_updates(HelperRing& R, const double
 __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
     const double* __restrict__ G, int ldg, const double* __restrict__ cvec,
     const int32_t* __restrict__ Fidx, double* __restrict__ Lt, double* __restrict__ Linv,
-    int* __restrict__ flags, int tri, DevState* st, unsigned long long* __restrict__ box, int boxlen) {
+    int* __restrict__ flags, int tri, DevState* st, unsigned long long* __restrict__ box, int boxlen,
+    int halves_mode) {
   extern __shared__ double smem[];
   pdl_wait();
   // helpers: BUF(0) = S, BUF(1..4) = operand double-buffers.
@@ -989,7 +991,7 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
       // row chain runs by half tiles (Th, kind 6) when all its tasks fit on the
       // helpers at once, else by whole tiles (kind 2): a waiting task holds its CTA
       const int nr = ntr - jq;
-      const bool halves = 2 * nr * (jq - 1) <= (int)gridDim.x - 2;
+      const bool halves = halves_mode >= 0 ? halves_mode != 0 : 2 * nr * (jq - 1) <= (int)gridDim.x - 2;
       const int per = halves ? 2 : 1;
       const int nh = (jq - 1) * nr * per;
       const int u = t - (jq - 1);
@@ -1599,9 +1601,14 @@ cudaError_t launch_chol_factor(int n, const double* G, int ldg, const double* c,
   if (grid < 2) grid = 2;
   double* Linv = Lt + (size_t)tri_tiles(n) * TS;
   const int ntr = (n + 1 + T - 1) / T;
+  // restart row chains by half tiles: -1 when all fit on the helpers (default), 0 never, 1 always
+  static const int halves_mode = [] {
+    const char* v = getenv("NNLS_RESTART_HALVES");
+    return (v != nullptr && v[0] != 0) ? atoi(v) : -1;
+  }();
   unsigned long long* box = reinterpret_cast<unsigned long long*>(Lt + ((size_t)tri_tiles(n) + 3 * (size_t)ntr) * TS);
   return launch_pdl(chol_factor_kernel, dim3(grid), dim3(kHelperThreads), sizeof(double) * kSmemDoubles, s, G, ldg, c,
-                    Fidx, Lt, Linv, flags, tri_tiles(n), st, box, ntr * T);
+                    Fidx, Lt, Linv, flags, tri_tiles(n), st, box, ntr * T, halves_mode);
 }
 
 cudaError_t launch_chol_backsolve(int n, const double* Lt, int* flags, double* xF, DevState* st,

@@ -59,7 +59,7 @@ __device__ void block_partial_minmax(double v, double* partials, int slot, doubl
 }
 // all CTAs: sum partials[*][slot .. slot+nv) (nv <= 3) with every thread of
 // the block (fixed order per thread, then a fixed block reduction: the
-// result is identical in every CTA).  red[] holds 3 x 16 doubles.
+// result is identical in every CTA).  red[] holds 3 x 32 doubles.
 __device__ void grid_sum3(const double* partials, int slot, int nv, double* out, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double sv[3] = {0.0, 0.0, 0.0};
@@ -68,11 +68,11 @@ __device__ void grid_sum3(const double* partials, int slot, int nv, double* out,
   for (int q = 0; q < nv; ++q) sv[q] = warp_sum(sv[q]);
   __syncthreads();
   if (lane == 0)
-    for (int q = 0; q < nv; ++q) red[16 * q + wid] = sv[q];
+    for (int q = 0; q < nv; ++q) red[32 * q + wid] = sv[q];
   __syncthreads();
   for (int q = 0; q < nv; ++q) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[16 * q + w];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[32 * q + w];
     out[q] = t;
   }
 }
@@ -83,11 +83,11 @@ __device__ void block_partial_sum3(const double* v, int nv, double* partials, in
   for (int q = 0; q < nv; ++q) x[q] = warp_sum(v[q]);
   __syncthreads();
   if (lane == 0)
-    for (int q = 0; q < nv; ++q) red[16 * q + wid] = x[q];
+    for (int q = 0; q < nv; ++q) red[32 * q + wid] = x[q];
   __syncthreads();
   if (wid == 0) {
     for (int q = 0; q < nv; ++q) {
-      double y = lane < (int)(blockDim.x >> 5) ? red[16 * q + lane] : 0.0;
+      double y = lane < (int)(blockDim.x >> 5) ? red[32 * q + lane] : 0.0;
       y = warp_sum(y);
       if (lane == 0) partials[blockIdx.x * kSlots + slot + q] = y;
     }
@@ -115,6 +115,14 @@ __device__ double grid_total(const double* partials, int slot, double* bcast, in
 
 // debug hook: per-phase %globaltimer stamps of CTA 0 (nnls_debug_lsqr_profile)
 __device__ unsigned long long* g_lsqr_prof = nullptr;
+#define LG_MARK(slot)                                                                      \
+  do {                                                                                     \
+    if (g_lsqr_prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {                   \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_lsqr_prof[63 * 16 + (slot)] = t_;                                                  \
+    }                                                                                      \
+  } while (0)
 #define LG_STAMP(slot)                                                                     \
   do {                                                                                     \
     if (g_lsqr_prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && itn < 64) {        \
@@ -124,212 +132,218 @@ __device__ unsigned long long* g_lsqr_prof = nullptr;
     }                                                                                      \
   } while (0)
 
-__global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double red[48];
-  __shared__ double bcast;
+// The global-memory LSQR iteration (any cooperative grid): A_F from the
+// compacted rows (Fval/Fcol/Fcnt) and the CSC in global memory / L2.  On
+// return X[j] (j in F) holds the LSQR x.
+__device__ void lsqr_iterate_global(const LsqrArgs& a, cg::grid_group& grid, int mode, int f, double* red,
+                                    double* bcast_p, int& itn, int& istop) {
+  double& bcast = *bcast_p;
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nthr = gridDim.x * blockDim.x;
   const int m = a.m, n = a.n;
-  const int status = a.st->status;
-  const int f = a.st->f;
   const uint8_t* __restrict__ mask = a.mask;
-  const int mode0 = (status == 0 && a.st->done && f > 0) ? a.mode : 0;
-  // mode 3 (adaptive): condest.cu decided -- LSQR as mode 1, or the NE x
-  const int mode = mode0 == 3 ? (a.st->refined ? 1 : 0) : mode0;
-
-  int itn = 0, istop = 0;
-  if (mode != 0) {
-    const int itn_limit = a.itn_limit > 0 ? a.itn_limit : 4 * f;
-    // ---- start: U = rhs (cold: b; warm: b - A_F x_ne); beta = |U|
-    double p = 0.0;
-    for (int r = gwarp; r < m; r += nwarps) {
+  const int itn_limit = a.itn_limit > 0 ? a.itn_limit : 4 * f;
+  // ---- start: U = rhs (cold: b; warm: b - A_F x_ne); beta = |U|
+  double p = 0.0;
+  for (int r = gwarp; r < m; r += nwarps) {
+    double s = 0.0;
+    if (mode == 2) {
+      for (int t = a.rowptr[r] + lane; t < a.rowptr[r + 1]; t += 32) {
+        const int j = a.colind[t];
+        if (mask[j]) s = fma(a.vals[t], a.x_ne[j], s);
+      }
+      s = warp_sum(s);
+    }
+    if (lane == 0) {
+      const double u = a.b[r] - s;
+      a.U[r] = u;
+      p += u * u;
+    }
+  }
+  for (int j = gtid; j < n; j += nthr) {
+    a.V[j] = 0.0;
+    a.W[j] = 0.0;
+    a.X[j] = 0.0;
+  }
+  block_partial_sum(p, a.partials, 0, red);
+  grid.sync();
+  double beta = sqrt(grid_total(a.partials, 0, &bcast, 0));
+  const double bnorm = beta;
+  // V = A_F^T u (u = U / beta); alpha = |V|
+  p = 0.0;
+  if (beta > 0.0) {
+    const double ib = 1.0 / beta;
+    for (int j = gwarp; j < n; j += nwarps) {
+      if (!mask[j]) continue;
       double s = 0.0;
-      if (mode == 2) {
-        for (int t = a.rowptr[r] + lane; t < a.rowptr[r + 1]; t += 32) {
-          const int j = a.colind[t];
-          if (mask[j]) s = fma(a.vals[t], a.x_ne[j], s);
-        }
-        s = warp_sum(s);
-      }
+      for (int t = a.colptr[j] + lane; t < a.colptr[j + 1]; t += 32)
+        s = fma(a.cvals[t], __ldcg(&a.U[a.rowind[t]]), s);
+      s = warp_sum(s) * ib;
       if (lane == 0) {
-        const double u = a.b[r] - s;
-        a.U[r] = u;
-        p += u * u;
-      }
-    }
-    for (int j = gtid; j < n; j += nthr) {
-      a.V[j] = 0.0;
-      a.W[j] = 0.0;
-      a.X[j] = 0.0;
-    }
-    block_partial_sum(p, a.partials, 0, red);
-    grid.sync();
-    double beta = sqrt(grid_total(a.partials, 0, &bcast, 0));
-    const double bnorm = beta;
-    // V = A_F^T u (u = U / beta); alpha = |V|
-    p = 0.0;
-    if (beta > 0.0) {
-      const double ib = 1.0 / beta;
-      for (int j = gwarp; j < n; j += nwarps) {
-        if (!mask[j]) continue;
-        double s = 0.0;
-        for (int t = a.colptr[j] + lane; t < a.colptr[j + 1]; t += 32)
-          s = fma(a.cvals[t], __ldcg(&a.U[a.rowind[t]]), s);
-        s = warp_sum(s) * ib;
-        if (lane == 0) {
-          a.V[j] = s;
-          p += s * s;
-        }
-      }
-    }
-    block_partial_sum(p, a.partials, 1, red);
-    grid.sync();
-    double alpha = beta > 0.0 ? sqrt(grid_total(a.partials, 1, &bcast, 0)) : 0.0;
-    if (alpha > 0.0) {
-      const double ia = 1.0 / alpha;
-      for (int j = gtid; j < n; j += nthr) {
-        if (!mask[j]) continue;
-        const double v = __ldcg(&a.V[j]) * ia;
-        a.V[j] = v;
-        a.W[j] = v;
-      }
-    }
-    grid.sync();
-    double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
-    const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
-    // Two grid barriers per iteration: the |d|^2, |x|^2 partials of
-    // iteration t ride on iteration t+1's first barrier, and t's stopping
-    // test is taken there (x is not touched in between).
-    double pd = 0.0, px = 0.0, last_phi = 0.0, last_sn = 0.0;
-    bool pending = false;
-    const int32_t* __restrict__ Fidx = a.Fidx;
-    // V holds v unnormalised (V = v / vscale) from phase B on, so phase C
-    // never writes it: phase A of the next iteration reads V with no barrier
-    // after phase C
-    double vscale = 1.0;
-    if (alpha * beta != 0.0) {
-      for (;;) {
-        const bool more = itn < itn_limit;
-        LG_STAMP(0);
-        // ---- phase A: U = A v - alpha u, u = U / beta.  Four rows per warp
-        //      pass (8 lanes each), so four rows' gathers are in flight at once
-        const double au = beta > 0.0 ? alpha / beta : 0.0;
-        p = 0.0;
-        if (more) {
-          const int sub = lane >> 3, sl = lane & 7;
-          for (int r0 = gwarp * 4; r0 < m; r0 += nwarps * 4) {
-            const int r = r0 + sub;
-            double s = 0.0;
-            if (r < m) {  // A restricted to F (lsqr_compact_kernel): V is zero off F
-              const int t0 = a.rowptr[r], t1 = t0 + __ldcg(&a.Fcnt[r]);
-#pragma unroll 2
-              for (int t = t0 + sl; t < t1; t += 8) s = fma(__ldcg(&a.Fval[t]), __ldcg(&a.V[__ldcg(&a.Fcol[t])]), s);
-            }
-            s += __shfl_xor_sync(kFull, s, 4);
-            s += __shfl_xor_sync(kFull, s, 2);
-            s += __shfl_xor_sync(kFull, s, 1);
-            if (sl == 0 && r < m) {
-              const double u = s * vscale - au * a.U[r];
-              a.U[r] = u;
-              p += u * u;
-            }
-          }
-        }
-        LG_STAMP(1);
-        {
-          const double v3[3] = {p, pd, px};
-          block_partial_sum3(v3, 3, a.partials, 0, red);
-        }
-        grid.sync();
-        LG_STAMP(2);
-        double gt[3];
-        grid_sum3(a.partials, 0, 3, gt, red);
-        if (pending) {  // stopping test of the previous iteration
-          ddnorm += gt[1];
-          const double xnorm = sqrt(gt[2]);
-          const double acond = anorm * sqrt(ddnorm);
-          const double rnorm = phibar;
-          const double arnorm = alpha * fabs(last_sn * last_phi);
-          const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
-          const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
-          const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
-          const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
-          const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
-          if (itn >= itn_limit) istop = 7;
-          if (1.0 + test3 <= 1.0) istop = 6;
-          if (1.0 + test2 <= 1.0) istop = 5;
-          if (1.0 + tt1 <= 1.0) istop = 4;
-          if (test3 <= ctol) istop = 3;
-          if (test2 <= a.atol) istop = 2;
-          if (test1 <= rtol) istop = 1;
-          if (istop != 0) break;
-        }
-        ++itn;
-        const double beta_new = sqrt(gt[0]);
-        // ---- phase B: V' = A_F^T u - beta v (warp per F column)
-        double alpha_new = alpha;
-        if (beta_new > 0.0) {
-          anorm = sqrt(anorm * anorm + alpha * alpha + beta_new * beta_new);
-          const double ib = 1.0 / beta_new;
-          p = 0.0;
-          for (int k = gwarp; k < f; k += nwarps) {
-            const int j = Fidx[k];
-            double s = 0.0;
-            const int c1 = a.colptr[j + 1];
-#pragma unroll 2
-            for (int t = a.colptr[j] + lane; t < c1; t += 32) s = fma(a.cvals[t], __ldcg(&a.U[a.rowind[t]]), s);
-            s = warp_sum(s) * ib;
-            if (lane == 0) {
-              const double v = s - beta_new * (__ldcg(&a.V[j]) * vscale);
-              a.V[j] = v;  // unnormalised
-              p += v * v;
-            }
-          }
-          LG_STAMP(3);
-          block_partial_sum(p, a.partials, 4, red);
-          grid.sync();
-          LG_STAMP(4);
-          grid_sum3(a.partials, 4, 1, gt, red);
-          alpha_new = sqrt(gt[0]);
-        }
-        beta = beta_new;
-        // ---- rotation (replicated scalars)
-        const double rho = sqrt(rhobar * rhobar + beta * beta);
-        const double irho = 1.0 / rho;
-        const double cs = rhobar * irho, sn = beta * irho;
-        const double theta = sn * alpha_new;
-        rhobar = -cs * alpha_new;
-        const double phi = cs * phibar;
-        phibar = sn * phibar;
-        const double t1 = phi * irho, t2 = -theta * irho;
-        // ---- phase C: v = V'/alpha, x += t1 w, w = v + t2 w (F columns; V not written)
-        if (beta_new > 0.0 && alpha_new > 0.0) vscale = 1.0 / alpha_new;
-        pd = 0.0;
-        px = 0.0;
-        for (int k = gtid; k < f; k += nthr) {
-          const int j = Fidx[k];
-          const double v = __ldcg(&a.V[j]) * vscale;
-          const double w = a.W[j];
-          const double d = w * irho;
-          pd += d * d;
-          const double x = a.X[j] + t1 * w;
-          a.X[j] = x;
-          a.W[j] = v + t2 * w;
-          px += x * x;
-        }
-        alpha = alpha_new;
-        last_phi = phi;
-        last_sn = sn;
-        pending = true;
-        LG_STAMP(5);
+        a.V[j] = s;
+        p += s * s;
       }
     }
   }
+  block_partial_sum(p, a.partials, 1, red);
+  grid.sync();
+  double alpha = beta > 0.0 ? sqrt(grid_total(a.partials, 1, &bcast, 0)) : 0.0;
+  if (alpha > 0.0) {
+    const double ia = 1.0 / alpha;
+    for (int j = gtid; j < n; j += nthr) {
+      if (!mask[j]) continue;
+      const double v = __ldcg(&a.V[j]) * ia;
+      a.V[j] = v;
+      a.W[j] = v;
+    }
+  }
+  grid.sync();
+  double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
+  const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
+  // Two grid barriers per iteration: the |d|^2, |x|^2 partials of
+  // iteration t ride on iteration t+1's first barrier, and t's stopping
+  // test is taken there (x is not touched in between).
+  double pd = 0.0, px = 0.0, last_phi = 0.0, last_sn = 0.0;
+  bool pending = false;
+  const int32_t* __restrict__ Fidx = a.Fidx;
+  // V holds v unnormalised (V = v / vscale) from phase B on, so phase C
+  // never writes it: phase A of the next iteration reads V with no barrier
+  // after phase C
+  double vscale = 1.0;
+  if (alpha * beta != 0.0) {
+    for (;;) {
+      const bool more = itn < itn_limit;
+      LG_STAMP(0);
+      // ---- phase A: U = A v - alpha u, u = U / beta.  Four rows per warp
+      //      pass (8 lanes each), so four rows' gathers are in flight at once
+      const double au = beta > 0.0 ? alpha / beta : 0.0;
+      p = 0.0;
+      if (more) {
+        const int sub = lane >> 3, sl = lane & 7;
+        for (int r0 = gwarp * 4; r0 < m; r0 += nwarps * 4) {
+          const int r = r0 + sub;
+          double s = 0.0;
+          if (r < m) {  // A restricted to F (lsqr_compact_kernel): V is zero off F
+            const int t0 = a.rowptr[r], t1 = t0 + __ldcg(&a.Fcnt[r]);
+#pragma unroll 2
+            for (int t = t0 + sl; t < t1; t += 8) s = fma(__ldcg(&a.Fval[t]), __ldcg(&a.V[__ldcg(&a.Fcol[t])]), s);
+          }
+          s += __shfl_xor_sync(kFull, s, 4);
+          s += __shfl_xor_sync(kFull, s, 2);
+          s += __shfl_xor_sync(kFull, s, 1);
+          if (sl == 0 && r < m) {
+            const double u = s * vscale - au * a.U[r];
+            a.U[r] = u;
+            p += u * u;
+          }
+        }
+      }
+      LG_STAMP(1);
+      {
+        const double v3[3] = {p, pd, px};
+        block_partial_sum3(v3, 3, a.partials, 0, red);
+      }
+      grid.sync();
+      LG_STAMP(2);
+      double gt[3];
+      grid_sum3(a.partials, 0, 3, gt, red);
+      if (pending) {  // stopping test of the previous iteration
+        ddnorm += gt[1];
+        const double xnorm = sqrt(gt[2]);
+        const double acond = anorm * sqrt(ddnorm);
+        const double rnorm = phibar;
+        const double arnorm = alpha * fabs(last_sn * last_phi);
+        const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+        const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
+        const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
+        const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
+        const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
+        if (itn >= itn_limit) istop = 7;
+        if (1.0 + test3 <= 1.0) istop = 6;
+        if (1.0 + test2 <= 1.0) istop = 5;
+        if (1.0 + tt1 <= 1.0) istop = 4;
+        if (test3 <= ctol) istop = 3;
+        if (test2 <= a.atol) istop = 2;
+        if (test1 <= rtol) istop = 1;
+        if (istop != 0) break;
+      }
+      ++itn;
+      const double beta_new = sqrt(gt[0]);
+      // ---- phase B: V' = A_F^T u - beta v (warp per F column)
+      double alpha_new = alpha;
+      if (beta_new > 0.0) {
+        anorm = sqrt(anorm * anorm + alpha * alpha + beta_new * beta_new);
+        const double ib = 1.0 / beta_new;
+        p = 0.0;
+        for (int k = gwarp; k < f; k += nwarps) {
+          const int j = Fidx[k];
+          double s = 0.0;
+          const int c1 = a.colptr[j + 1];
+#pragma unroll 2
+          for (int t = a.colptr[j] + lane; t < c1; t += 32) s = fma(a.cvals[t], __ldcg(&a.U[a.rowind[t]]), s);
+          s = warp_sum(s) * ib;
+          if (lane == 0) {
+            const double v = s - beta_new * (__ldcg(&a.V[j]) * vscale);
+            a.V[j] = v;  // unnormalised
+            p += v * v;
+          }
+        }
+        LG_STAMP(3);
+        block_partial_sum(p, a.partials, 4, red);
+        grid.sync();
+        LG_STAMP(4);
+        grid_sum3(a.partials, 4, 1, gt, red);
+        alpha_new = sqrt(gt[0]);
+      }
+      beta = beta_new;
+      // ---- rotation (replicated scalars)
+      const double rho = sqrt(rhobar * rhobar + beta * beta);
+      const double irho = 1.0 / rho;
+      const double cs = rhobar * irho, sn = beta * irho;
+      const double theta = sn * alpha_new;
+      rhobar = -cs * alpha_new;
+      const double phi = cs * phibar;
+      phibar = sn * phibar;
+      const double t1 = phi * irho, t2 = -theta * irho;
+      // ---- phase C: v = V'/alpha, x += t1 w, w = v + t2 w (F columns; V not written)
+      if (beta_new > 0.0 && alpha_new > 0.0) vscale = 1.0 / alpha_new;
+      pd = 0.0;
+      px = 0.0;
+      for (int k = gtid; k < f; k += nthr) {
+        const int j = Fidx[k];
+        const double v = __ldcg(&a.V[j]) * vscale;
+        const double w = a.W[j];
+        const double d = w * irho;
+        pd += d * d;
+        const double x = a.X[j] + t1 * w;
+        a.X[j] = x;
+        a.W[j] = v + t2 * w;
+        px += x * x;
+      }
+      alpha = alpha_new;
+      last_phi = phi;
+      last_sn = sn;
+      pending = true;
+      LG_STAMP(5);
+    }
+  }
+}
 
+// x (LSQR result on F, correction, or the NE x), zeroing (c16), and the
+// a11 report; every CTA of the cooperative grid
+__device__ void lsqr_finish(const LsqrArgs& a, cg::grid_group& grid, int mode, int f, int itn, int istop,
+                            double* red, double* bcast_p) {
+  double& bcast = *bcast_p;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthr = gridDim.x * blockDim.x;
+  const int m = a.m, n = a.n;
+  const uint8_t* __restrict__ mask = a.mask;
   // ---- x: LSQR result on F (mode 1), correction (mode 2) or NE x; zeroing (c16)
   double pinf = 0.0;
   for (int j = gtid; j < n; j += nthr) {
@@ -354,15 +368,24 @@ __global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
   if (!a.kkt) return;
   // ---- report: R = A x - b, objective; y' = A^T R; KKT residuals (Eq. 3)
   double po = 0.0;
-  for (int r = gwarp; r < m; r += nwarps) {
-    double s = 0.0;
-    for (int t = a.rowptr[r] + lane; t < a.rowptr[r + 1]; t += 32)
-      s = fma(a.vals[t], __ldcg(&a.x_out[a.colind[t]]), s);
-    s = warp_sum(s);
-    if (lane == 0) {
-      const double rr = s - a.b[r];
-      a.R[r] = rr;
-      po += rr * rr;
+  {  // eight lanes per row, four rows per warp pass (latency-bound gathers in flight)
+    const int sub = lane >> 3, sl = lane & 7;
+    for (int r0 = gwarp * 4; r0 < m; r0 += nwarps * 4) {
+      const int r = r0 + sub;
+      double s = 0.0;
+      if (r < m) {
+        const int t1 = a.rowptr[r + 1];
+#pragma unroll 2
+        for (int t = a.rowptr[r] + sl; t < t1; t += 8) s = fma(a.vals[t], __ldcg(&a.x_out[a.colind[t]]), s);
+      }
+      s += __shfl_xor_sync(kFull, s, 4);
+      s += __shfl_xor_sync(kFull, s, 2);
+      s += __shfl_xor_sync(kFull, s, 1);
+      if (sl == 0 && r < m) {
+        const double rr = s - a.b[r];
+        a.R[r] = rr;
+        po += rr * rr;
+      }
     }
   }
   block_partial_sum(po, a.partials, 0, red);
@@ -370,8 +393,9 @@ __global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
   double mx = INFINITY, my = INFINITY, mc = 0.0, dot = 0.0;
   for (int j = gwarp; j < n; j += nwarps) {
     double s = 0.0;
-    for (int t = a.colptr[j] + lane; t < a.colptr[j + 1]; t += 32)
-      s = fma(a.cvals[t], __ldcg(&a.R[a.rowind[t]]), s);
+    const int t1 = a.colptr[j + 1];
+#pragma unroll 4
+    for (int t = a.colptr[j] + lane; t < t1; t += 32) s = fma(a.cvals[t], __ldcg(&a.R[a.rowind[t]]), s);
     s = warp_sum(s);
     if (lane == 0) {
       const double xj = __ldcg(&a.x_out[j]);
@@ -402,15 +426,496 @@ __global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
   }
 }
 
+__device__ __forceinline__ int lsqr_mode_of(const LsqrArgs& a, int f) {
+  const int mode0 = (a.st->status == 0 && a.st->done && f > 0) ? a.mode : 0;
+  // mode 3 (adaptive): condest.cu decided -- LSQR as mode 1, or the NE x
+  return mode0 == 3 ? (a.st->refined ? 1 : 0) : mode0;
+}
+
+__global__ void __launch_bounds__(kThreads) lsqr_final_kernel(LsqrArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[96];
+  __shared__ double bcast;
+  LG_MARK(0);
+  const int f = a.st->f;
+  const int mode = lsqr_mode_of(a, f);
+  int itn = 0, istop = 0;
+  if (mode != 0) lsqr_iterate_global(a, grid, mode, f, red, &bcast, itn, istop);
+  LG_MARK(2);
+  lsqr_finish(a, grid, mode, f, itn, istop, red, &bcast);
+  LG_MARK(3);
+}
+
+// ===========================================================================
+// Grid-resident LSQR (config 2 and other problems too large for one
+// cluster): one CTA per SM (kResThreads) keeps, for the whole solve, a row
+// slice of A_F (rows [r0,r1), columns renumbered to their position in F) in
+// two orders -- by row for A_F v, and the same entries by F column for this
+// slice's share of A_F^T u -- plus its piece of u, the pieces of v, w, x of
+// its F columns [k0,k1), and a replica of all of v, in shared memory.
+// Per iteration:
+//   A  rows:  U = A_F v - alpha u; the slice's partial sums of A_F^T U,
+//             written as part[cta][k] (shared memory only until that store)  |U|^2
+//   -- grid barrier --
+//   B  cols:  V = A_F^T u - beta v for own columns: the G partials of each
+//             column summed in a fixed order (L2 reads, deterministic)  |V|^2
+//   -- grid barrier --
+//   C  cols:  x, w updates; the v replica refreshed from V (f doubles, L2)
+// No u or v element is gathered from global memory.  The scalar recurrence,
+// the vscale bookkeeping, the deterministic norm reductions and the
+// stopping tests are those of lsqr_iterate_global, so both paths compute the
+// same LSQR iterates up to the summation order of the two products.  The
+// slice sizes are planned in the kernel (F is only known on the device); if
+// any CTA's slices exceed kResSmem (or G f > nnz: the partials live in
+// Fval), every CTA takes the global-memory iteration instead (the decision
+// is grid-uniform).
+// ===========================================================================
+#ifndef NNLS_RES_THREADS
+#define NNLS_RES_THREADS 512
+#endif
+constexpr int kResThreads = NNLS_RES_THREADS;
+constexpr int kResSmem = 222 * 1024;
+
+__device__ __forceinline__ size_t res_al(size_t b) { return (b + 15) & ~(size_t)15; }
+
+// block-wide sum returned to every thread
+__device__ double block_sum_all(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+// block-wide exclusive scan of one int per thread; *total = the block sum
+__device__ int block_scan_excl(int v, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) t += y;
+    }
+    wsum[lane] = t;
+  }
+  __syncthreads();
+  *total = wsum[nw - 1];
+  return (wid > 0 ? wsum[wid - 1] : 0) + x - v;
+}
+
+// false (grid-uniform): the slices do not fit, nothing but the map was written
+__device__ bool lsqr_iterate_resident(const LsqrArgs& a, cg::grid_group& grid, int mode, int f, double* red,
+                                      double* bcast, int* wsum, int& itn, int& istop) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  const int tid = threadIdx.x, nb = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nb >> 5;
+  const int G = gridDim.x, bid = blockIdx.x;
+  const int m = a.m;
+  const int32_t* __restrict__ Fidx = a.Fidx;
+  int* map = reinterpret_cast<int*>(a.R);  // j -> position of j in F (R is free until the report)
+  // per-CTA partial sums of A_F^T U, [cta][k] (coalesced stores): in Fval
+  // (its entries are in shared memory after the setup; the plan checks G f <= nnz)
+  double* part = a.Fval;
+  const int r0 = (int)((long long)m * bid / G), r1 = (int)((long long)m * (bid + 1) / G);
+  const int k0 = (int)((long long)f * bid / G), k1 = (int)((long long)f * (bid + 1) / G);
+  const int R = r1 - r0, C = k1 - k0;
+  // ---- plan
+  for (int k = bid * nb + tid; k < f; k += G * nb) map[Fidx[k]] = k;
+  double nzr = 0.0;
+  for (int r = r0 + tid; r < r1; r += nb) nzr += (double)a.Fcnt[r];
+  const size_t NZR = (size_t)block_sum_all(nzr, red);
+  const size_t o_ul = res_al(8 * (size_t)f), o_vo = o_ul + res_al(8 * (size_t)R);
+  const size_t o_wo = o_vo + res_al(8 * (size_t)C), o_xo = o_wo + res_al(8 * (size_t)C);
+  const size_t o_rv = o_xo + res_al(8 * (size_t)C), o_qv = o_rv + res_al(8 * NZR);
+  const size_t o_rp = o_qv + res_al(8 * NZR), o_rc = o_rp + res_al(4 * (size_t)(R + 1));
+  const size_t o_qp = o_rc + res_al(4 * NZR), o_qr = o_qp + res_al(4 * (size_t)(f + 1));
+  // column totals: nch chunks of CTAs per own column, then the chunk sums in order
+  const int nch = C > 0 ? max(1, min(G, nb / C)) : 1;
+  const size_t o_ct = o_qr + res_al(4 * max(NZR, (size_t)R + 1));
+  const size_t need = o_ct + res_al(8 * ((size_t)nch * C + C));
+  if (tid == 0) a.partials[bid * kSlots + 7] = (double)need;
+  grid.sync();
+  const bool fits = (long long)G * f <= (long long)a.rowptr[m] && R < (1 << 30);
+  if (!fits || grid_total(a.partials, 7, bcast, 2) > (double)kResSmem) return false;
+  double* vs = reinterpret_cast<double*>(rsm);
+  double* ul = reinterpret_cast<double*>(rsm + o_ul);
+  double* Vo = reinterpret_cast<double*>(rsm + o_vo);
+  double* Wo = reinterpret_cast<double*>(rsm + o_wo);
+  double* Xo = reinterpret_cast<double*>(rsm + o_xo);
+  double* rv = reinterpret_cast<double*>(rsm + o_rv);  // row slice: values, F positions
+  double* qv = reinterpret_cast<double*>(rsm + o_qv);  // the same entries by F column: values, local rows
+  int* rp = reinterpret_cast<int*>(rsm + o_rp);
+  int* rc = reinterpret_cast<int*>(rsm + o_rc);
+  int* qp = reinterpret_cast<int*>(rsm + o_qp);
+  int* qr = reinterpret_cast<int*>(rsm + o_qr);
+  double* ctot = reinterpret_cast<double*>(rsm + o_ct);  // [C] totals, then [nch][C] chunk sums
+  // ---- slices.  Row pointers by a block scan of the F counts (the global
+  // row starts staged beside them); the entries copied one per thread (row
+  // by a binary search of the pointers); the column view of the same entries
+  // by a counting sort on the F position, each column's few entries then put
+  // in row order (a deterministic summation order for partial_AtU).
+  int* rsrc = qr;  // (staging: the global start of each row; qr is filled last)
+  {
+    int run = 0, tot = 0;
+    for (int base = 0; base < R; base += nb) {
+      const int i = base + tid;
+      const int cnt = i < R ? a.Fcnt[r0 + i] : 0;
+      const int ex = block_scan_excl(cnt, wsum, &tot);
+      if (i < R) {
+        rp[i] = run + ex;
+        rsrc[i] = a.rowptr[r0 + i];
+      }
+      run += tot;
+    }
+    if (tid == 0) rp[R] = run;
+  }
+  int* cur = reinterpret_cast<int*>(vs);  // (column counters; vs is filled after the setup)
+  for (int k = tid; k <= f; k += nb) cur[k] = 0;
+  __syncthreads();
+#pragma unroll 4
+  for (int t = tid; t < (int)NZR; t += nb) {
+    int lo = 0, hi = R;  // row i: rp[i] <= t < rp[i+1]
+    while (hi - lo > 1) {
+      const int md = (lo + hi) >> 1;
+      if (rp[md] <= t) lo = md; else hi = md;
+    }
+    const int src = rsrc[lo] + (t - rp[lo]);
+    rv[t] = a.Fval[src];
+    const int k = __ldcg(&map[a.Fcol[src]]);
+    rc[t] = k;
+    atomicAdd(&cur[k], 1);
+  }
+  __syncthreads();
+  {
+    int run = 0, tot = 0;
+    for (int base = 0; base < f; base += nb) {
+      const int k = base + tid;
+      const int cnt = k < f ? cur[k] : 0;
+      const int ex = block_scan_excl(cnt, wsum, &tot);
+      if (k < f) {
+        qp[k] = run + ex;
+        cur[k] = run + ex;
+      }
+      run += tot;
+    }
+    if (tid == 0) qp[f] = run;
+  }
+  __syncthreads();
+  for (int i = wid; i < R; i += nw)
+    for (int t = rp[i] + lane; t < rp[i + 1]; t += 32) {
+      const int d = atomicAdd(&cur[rc[t]], 1);
+      qv[d] = rv[t];
+      qr[d] = i;
+    }
+  __syncthreads();
+  for (int k = tid; k < f; k += nb) {  // insertion sort of column k's entries by row
+    const int q0 = qp[k], q1 = qp[k + 1];
+    for (int t = q0 + 1; t < q1; ++t) {
+      const int rr = qr[t];
+      const double vv = qv[t];
+      int u = t - 1;
+      while (u >= q0 && qr[u] > rr) {
+        qr[u + 1] = qr[u];
+        qv[u + 1] = qv[u];
+        --u;
+      }
+      qr[u + 1] = rr;
+      qv[u + 1] = vv;
+    }
+  }
+  for (int c = tid; c < C; c += nb) {
+    Vo[c] = 0.0;
+    Wo[c] = 0.0;
+    Xo[c] = 0.0;
+  }
+  if (mode == 2)
+    for (int k = tid; k < f; k += nb) vs[k] = a.x_ne[Fidx[k]];
+  __syncthreads();
+  LG_MARK(1);
+  const int itn_limit = a.itn_limit > 0 ? a.itn_limit : 4 * f;
+  // partial A_F^T U of this CTA's rows, column k -> part[bid * f + k] (fixed order per column)
+  auto partial_AtU = [&]() {
+    double* dst = part + (size_t)bid * f;
+    for (int k = tid; k < f; k += 2 * nb) {  // columns k and k + nb interleaved
+      const int k2 = k + nb;
+      const int a0 = qp[k], a1 = qp[k + 1];
+      const int b0 = k2 < f ? qp[k2] : 0, b1 = k2 < f ? qp[k2 + 1] : 0;
+      double s = 0.0, s2 = 0.0;
+      for (int t = 0; t < max(a1 - a0, b1 - b0); ++t) {
+        if (a0 + t < a1) s = fma(qv[a0 + t], ul[qr[a0 + t]], s);
+        if (b0 + t < b1) s2 = fma(qv[b0 + t], ul[qr[b0 + t]], s2);
+      }
+      dst[k] = s;
+      if (k2 < f) dst[k2] = s2;
+    }
+  };
+  // own columns: ctot[c] = the G partials of column k0 + c, summed over CTAs
+  // [G h / nch, G (h+1) / nch) per chunk h, then over h in order (the same
+  // order in every run); consecutive threads read consecutive columns
+  auto column_totals = [&]() {
+    double* cs = ctot + C;
+    for (int idx = tid; idx < nch * C; idx += nb) {
+      const int c = idx % C, h = idx / C;
+      const int b1 = (int)((long long)G * (h + 1) / nch);
+      double s = 0.0;
+      for (int b = (int)((long long)G * h / nch); b < b1; ++b) s += __ldcg(&part[(size_t)b * f + k0 + c]);
+      cs[idx] = s;
+    }
+    __syncthreads();
+    for (int c = tid; c < C; c += nb) {
+      double s = 0.0;
+      for (int h = 0; h < nch; ++h) s += cs[h * C + c];
+      ctot[c] = s;
+    }
+  };
+  // ---- start: U = rhs (cold: b; warm: b - A_F x_ne); beta = |U|
+  double p = 0.0;
+  for (int i = tid; i < R; i += nb) {
+    double s = 0.0;
+    if (mode == 2)
+      for (int t = rp[i]; t < rp[i + 1]; ++t) s = fma(rv[t], vs[rc[t]], s);
+    const double u = a.b[r0 + i] - s;
+    ul[i] = u;
+    p += u * u;
+  }
+  block_partial_sum(p, a.partials, 0, red);  // (its barriers order ul before the partial products)
+  grid.sync();                               // every CTA's Fval reads done: part may be written
+  partial_AtU();
+  grid.sync();
+  double beta = sqrt(grid_total(a.partials, 0, bcast, 0));
+  const double bnorm = beta;
+  // V = A_F^T u (u = U / beta); alpha = |V|
+  p = 0.0;
+  if (beta > 0.0) {
+    const double ib = 1.0 / beta;
+    column_totals();
+    for (int c = tid; c < C; c += nb) {
+      const double s = ctot[c] * ib;
+      Vo[c] = s;
+      a.V[k0 + c] = s;
+      p += s * s;
+    }
+  }
+  block_partial_sum(p, a.partials, 1, red);
+  grid.sync();
+  double alpha = beta > 0.0 ? sqrt(grid_total(a.partials, 1, bcast, 0)) : 0.0;
+  if (alpha > 0.0) {
+    const double ia = 1.0 / alpha;
+    for (int c = tid; c < C; c += nb) {
+      const double v = Vo[c] * ia;
+      Vo[c] = v;
+      Wo[c] = v;
+    }
+    for (int k = tid; k < f; k += nb) vs[k] = __ldcg(&a.V[k]) * ia;
+  }
+  __syncthreads();
+  double rhobar = alpha, phibar = beta, anorm = 0.0, ddnorm = 0.0;
+  const double ctol = a.conlim > 0.0 ? 1.0 / a.conlim : 0.0;
+  double pd = 0.0, px = 0.0, last_phi = 0.0, last_sn = 0.0;
+  bool pending = false;
+  double vscale = 1.0;  // Vo, vs and V hold v unnormalised (v = V vscale), as in lsqr_iterate_global
+  if (alpha * beta != 0.0) {
+    const int g4 = tid >> 2, s4 = tid & 3, ng4 = nb >> 2;
+    for (;;) {
+      const bool more = itn < itn_limit;
+      LG_STAMP(0);
+      // ---- phase A: U = A_F v - alpha u (four lanes per row), then this
+      //      slice's partial A_F^T U (phase B's products) -- shared memory only
+      const double au = beta > 0.0 ? alpha / beta : 0.0;
+      p = 0.0;
+      if (more) {
+        if (R <= nb) {  // a thread per row, four independent gathers in flight
+          if (tid < R) {
+            const int t0 = rp[tid], t1 = rp[tid + 1];
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int t = t0;
+            for (; t + 4 <= t1; t += 4) {
+              s0 = fma(rv[t], vs[rc[t]], s0);
+              s1 = fma(rv[t + 1], vs[rc[t + 1]], s1);
+              s2 = fma(rv[t + 2], vs[rc[t + 2]], s2);
+              s3 = fma(rv[t + 3], vs[rc[t + 3]], s3);
+            }
+            for (; t < t1; ++t) s0 = fma(rv[t], vs[rc[t]], s0);
+            const double s = (s0 + s1) + (s2 + s3);
+            const double u = s * vscale - au * ul[tid];
+            ul[tid] = u;
+            p += u * u;
+          }
+        } else {
+          for (int base = 0; base < R; base += ng4) {
+            const int i = base + g4;
+            double s = 0.0;
+            if (i < R) {
+              const int t1 = rp[i + 1];
+              for (int t = rp[i] + s4; t < t1; t += 4) s = fma(rv[t], vs[rc[t]], s);
+            }
+            s += __shfl_xor_sync(kFull, s, 2);
+            s += __shfl_xor_sync(kFull, s, 1);
+            if (s4 == 0 && i < R) {
+              const double u = s * vscale - au * ul[i];
+              ul[i] = u;
+              p += u * u;
+            }
+          }
+        }
+        LG_STAMP(6);
+        __syncthreads();
+        partial_AtU();
+      }
+      LG_STAMP(1);
+      {
+        const double v3[3] = {p, pd, px};
+        block_partial_sum3(v3, 3, a.partials, 0, red);
+      }
+      grid.sync();
+      LG_STAMP(2);
+      double gt[3];
+      grid_sum3(a.partials, 0, 3, gt, red);
+      if (pending) {  // stopping test of the previous iteration
+        ddnorm += gt[1];
+        const double xnorm = sqrt(gt[2]);
+        const double acond = anorm * sqrt(ddnorm);
+        const double rnorm = phibar;
+        const double arnorm = alpha * fabs(last_sn * last_phi);
+        const double test1 = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+        const double test2 = (anorm * rnorm) > 0.0 ? arnorm / (anorm * rnorm) : 0.0;
+        const double test3 = acond > 0.0 ? 1.0 / acond : 0.0;
+        const double tt1 = bnorm > 0.0 ? test1 / (1.0 + anorm * xnorm / bnorm) : 0.0;
+        const double rtol = a.btol + (bnorm > 0.0 ? a.atol * anorm * xnorm / bnorm : 0.0);
+        if (itn >= itn_limit) istop = 7;
+        if (1.0 + test3 <= 1.0) istop = 6;
+        if (1.0 + test2 <= 1.0) istop = 5;
+        if (1.0 + tt1 <= 1.0) istop = 4;
+        if (test3 <= ctol) istop = 3;
+        if (test2 <= a.atol) istop = 2;
+        if (test1 <= rtol) istop = 1;
+        if (istop != 0) break;
+      }
+      ++itn;
+      const double beta_new = sqrt(gt[0]);
+      // ---- phase B: V' = A_F^T u - beta v, own columns: the G partials summed (L2, coalesced)
+      double alpha_new = alpha;
+      if (beta_new > 0.0) {
+        anorm = sqrt(anorm * anorm + alpha * alpha + beta_new * beta_new);
+        const double ib = 1.0 / beta_new;
+        p = 0.0;
+        column_totals();
+        for (int c = tid; c < C; c += nb) {
+          const double v = ctot[c] * ib - beta_new * (Vo[c] * vscale);
+          Vo[c] = v;  // unnormalised
+          a.V[k0 + c] = v;
+          p += v * v;
+        }
+        LG_STAMP(3);
+        block_partial_sum(p, a.partials, 4, red);
+        grid.sync();
+        LG_STAMP(4);
+        grid_sum3(a.partials, 4, 1, gt, red);
+        alpha_new = sqrt(gt[0]);
+      }
+      beta = beta_new;
+      // ---- rotation (replicated scalars)
+      const double rho = sqrt(rhobar * rhobar + beta * beta);
+      const double irho = 1.0 / rho;
+      const double cs = rhobar * irho, sn = beta * irho;
+      const double theta = sn * alpha_new;
+      rhobar = -cs * alpha_new;
+      const double phi = cs * phibar;
+      phibar = sn * phibar;
+      const double t1 = phi * irho, t2 = -theta * irho;
+      // ---- phase C: v = V'/alpha, x += t1 w, w = v + t2 w (own columns); v replica
+      if (beta_new > 0.0 && alpha_new > 0.0) vscale = 1.0 / alpha_new;
+      pd = 0.0;
+      px = 0.0;
+      for (int c = tid; c < C; c += nb) {
+        const double v = Vo[c] * vscale;
+        const double w = Wo[c];
+        const double d = w * irho;
+        pd += d * d;
+        const double x = Xo[c] + t1 * w;
+        Xo[c] = x;
+        Wo[c] = v + t2 * w;
+        px += x * x;
+      }
+      if (beta_new > 0.0)
+        for (int k = tid; k < f; k += nb) vs[k] = __ldcg(&a.V[k]);
+      __syncthreads();
+      alpha = alpha_new;
+      last_phi = phi;
+      last_sn = sn;
+      pending = true;
+      LG_STAMP(5);
+    }
+  }
+  for (int c = tid; c < C; c += nb) a.X[Fidx[k0 + c]] = Xo[c];
+  return true;
+}
+
+__global__ void __launch_bounds__(kResThreads, 1) lsqr_resident_kernel(LsqrArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[96];
+  __shared__ double bcast;
+  __shared__ int wsum[32];
+  LG_MARK(0);
+  const int f = a.st->f;
+  const int mode = lsqr_mode_of(a, f);
+  int itn = 0, istop = 0;
+  if (mode != 0) {
+    if (lsqr_iterate_resident(a, grid, mode, f, red, &bcast, wsum, itn, istop)) {
+      grid.sync();  // X of every slice -> the output pass
+    } else {
+      lsqr_iterate_global(a, grid, mode, f, red, &bcast, itn, istop);
+    }
+  }
+  LG_MARK(2);
+  lsqr_finish(a, grid, mode, f, itn, istop, red, &bcast);
+  LG_MARK(3);
+}
+
 cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s) {
+  LsqrArgs args = a;
+  void* params[] = {&args};
+  static const bool no_res = [] {
+    const char* v = getenv("NNLS_NO_RESIDENT_LSQR");
+    return v != nullptr && v[0] != 0 && v[0] != '0';
+  }();
+  if (!no_res) {
+    static DeviceOnce once;
+    const int ok = device_once(once, [] {
+      if (cudaFuncSetAttribute(lsqr_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmem) !=
+          cudaSuccess)
+        return -1;
+      int per = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lsqr_resident_kernel, kResThreads, kResSmem) !=
+              cudaSuccess ||
+          per < 1)
+        return -1;
+      return 1;
+    });
+    if (ok == 1)
+      return cudaLaunchCooperativeKernel((void*)lsqr_resident_kernel, dim3(sm_count), dim3(kResThreads), params,
+                                         (size_t)kResSmem, s);
+    cudaGetLastError();
+  }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsqr_final_kernel, kThreads, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorLaunchOutOfResources;
   if (per_sm > 4) per_sm = 4;  // partials[] holds 4 CTAs per SM
   int grid = sm_count * per_sm;  // every co-resident CTA (latency-bound gathers)
-  LsqrArgs args = a;
-  void* params[] = {&args};
   return cudaLaunchCooperativeKernel((void*)lsqr_final_kernel, dim3(grid), dim3(kThreads), params, 0, s);
 }
 

@@ -1,0 +1,6 @@
+set -u
+O=gpurun_out/r3g
+mkdir -p $O
+timeout 300 python scripts/lsqr_c2_run.py 2 > $O/run.txt 2>&1 || exit 1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:lsqr_resident -s 1 -c 1 -o $O/lsqr_res -f python scripts/lsqr_c2_run.py 2 > $O/ncu.log 2>&1
+echo done

@@ -32,4 +32,12 @@ names = ["A spmv", "A blocksum+sync", "A gridsum+test+B spmv", "B blocksum+sync"
 for k, nm in enumerate(names):
     d = [(st(r, k + 1) - st(r, k)) / 1e3 for r in rows]
     print(f"{nm:22s} {np.mean(d):8.2f} us")
+if p[rows[0], 6] > 0:
+    print("  (A: spmv part %.2f us, partial A^T U %.2f us)" % (np.mean([(p[r, 6] - p[r, 0]) / 1e3 for r in rows]),
+                                                          np.mean([(p[r, 1] - p[r, 6]) / 1e3 for r in rows])))
+m = p[63]
+if m[0] > 0:
+    print("kernel: setup %.1f us, to loop end %.1f us, finish %.1f us, total %.1f us" % (
+        (m[1] - m[0]) / 1e3 if m[1] > 0 else float("nan"), (m[2] - m[0]) / 1e3 if m[2] > 0 else float("nan"),
+        (m[3] - m[2]) / 1e3 if m[2] > 0 else float("nan"), (m[3] - m[0]) / 1e3))
 print("per iteration", np.mean([(p[r + 1, 0] - p[r, 0]) / 1e3 for r in rows]), "us; lsqr_iterations", info["lsqr_iterations"])
