@@ -94,7 +94,7 @@ struct nnls_handle {
   int64_t nnz = 0;
   bool loaded = false, gram_ready = false;
   Buf rowptr, colind, vals, b;           // CSR + rhs
-  Buf colptr, rowind, cvals, cursor, tmp_row, tmp_val;  // CSC
+  Buf colptr, rowind, cvals, cursor, tmp_row, tmp_val, csc_temp;  // CSC (csc_temp: radix-sort scratch)
   Buf Gc;                                 // G (n x ldg) followed by c (n)
   Buf Gp;                                 // row-shard partial: packed lower G (n(n+1)/2) then c (n)
   int shard = 0;                          // 0 whole problem, 1 shard root (full A), 2 row block only
@@ -115,6 +115,7 @@ struct nnls_handle {
   bool no_reuse = false;    // F in index order, no factor reuse across iterations (env NNLS_NO_REUSE)
   bool no_fuse = false;     // separate count/exchange pass in decide (env NNLS_NO_FUSED_DUAL)
   bool no_exact_gram = false;  // always the row-ordered Gram kernel (env NNLS_NO_EXACT_GRAM)
+  bool no_sort_csc = false;    // CSC by scatter + rank instead of the radix sort (env NNLS_NO_SORT_CSC)
   cudaGraphExec_t gexec = nullptr;
   std::vector<double> gkey;
   cudaStream_t gstream = nullptr;
@@ -232,6 +233,8 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   CK(ensure(h->cvals, sizeof(double) * (size_t)nnz));
   CK(ensure(h->tmp_row, sizeof(int32_t) * (size_t)nnz));
   CK(ensure(h->tmp_val, sizeof(double) * (size_t)nnz));
+  const size_t csc_tb = h->no_sort_csc ? 0 : csc_sort_temp_bytes(nnz, n);
+  if (csc_tb > 0) CK(ensure(h->csc_temp, csc_tb));
   CK(ensure(h->Gc, sizeof(double) * ((size_t)n * h->ldg + n)));
   CK(ensure(h->mask, (size_t)n));
   CK(ensure(h->x, sizeof(double) * (size_t)n));
@@ -287,18 +290,35 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   TIMED(NNLS_PH_CSC, nnz > 0 ? 2 : 1,
         launch_csc_count(m, n, nnz, P<int32_t>(h->colind), P<int32_t>(h->colptr),
                          P<int32_t>(h->cursor), s, P<int>(h->err) + 2));
-  CK(launch_lsqr_plan(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colptr), P<int>(h->err) + 4, s));
+  // (the cluster LSQR keeps replicas of u and v in every CTA's shared memory:
+  // no plan when those alone exceed it)
+  const bool cl_possible = 8 * ((size_t)m + n) < 220 * 1024;
+  if (cl_possible)
+    CK(launch_lsqr_plan(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colptr), P<int>(h->err) + 4, s));
   tm_end(h, NNLS_PH_CSC, -1, 1);
   CK(cudaMemcpyAsync(h->h->err, h->err.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int herr = h->h->err[0];
   if (herr) return map_err_bits(herr);
   memcpy(h->h->plan, h->h->err + 4, sizeof(h->h->plan));  // cluster LSQR slice maxima
-  TIMED(NNLS_PH_CSC, 2,
-        launch_csc_fill(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
-                        P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                        P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s,
-                        h->h->err[2]));
+  if (!cl_possible) {  // maxima that no cluster holds: the grid LSQR runs
+    h->h->plan[0] = m;
+    h->h->plan[1] = (int)(nnz < INT32_MAX ? nnz : INT32_MAX);
+    h->h->plan[2] = n;
+    h->h->plan[3] = h->h->plan[1];
+  }
+  if (csc_tb > 0) {
+    TIMED(NNLS_PH_CSC, 3,
+          launch_csc_fill_sorted(m, n, nnz, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                                 P<int32_t>(h->rowind), P<double>(h->cvals), P<int32_t>(h->tmp_row),
+                                 P<double>(h->tmp_val), h->csc_temp.p, h->csc_temp.cap, s));
+  } else {
+    TIMED(NNLS_PH_CSC, 2,
+          launch_csc_fill(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
+                          P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
+                          P<int32_t>(h->cursor), P<int32_t>(h->tmp_row), P<double>(h->tmp_val), s,
+                          h->h->err[2]));
+  }
   double* G = P<double>(h->Gc);
   double* c = G + (size_t)n * h->ldg;
   int ldg = h->ldg;
@@ -359,6 +379,7 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
   h->no_reuse = env_on("NNLS_NO_REUSE");
   h->no_fuse = env_on("NNLS_NO_FUSED_DUAL");
   h->no_exact_gram = env_on("NNLS_NO_EXACT_GRAM");
+  h->no_sort_csc = env_on("NNLS_NO_SORT_CSC");
   *out = h;
   return NNLS_OK;
 }
@@ -955,7 +976,7 @@ nnls_status nnls_destroy(nnls_handle* h) {
   if (!h) return NNLS_OK;
   if (h->stream) cudaStreamSynchronize(h->stream);
   Buf* bufs[] = {&h->rowptr, &h->colind, &h->vals, &h->b, &h->colptr, &h->rowind, &h->cvals,
-                 &h->cursor, &h->tmp_row, &h->tmp_val, &h->Gc, &h->mask, &h->x, &h->y, &h->xF,
+                 &h->cursor, &h->tmp_row, &h->tmp_val, &h->csc_temp, &h->Gc, &h->mask, &h->x, &h->y, &h->xF,
                  &h->Fidx, &h->Gidx, &h->Lt, &h->flags, &h->U, &h->V, &h->W, &h->X, &h->R,
                  &h->partials, &h->xfin, &h->st, &h->err, &h->trace, &h->b_nnz_off, &h->b_info_i,
                  &h->b_info_d, &h->b_x, &h->b_mask, &h->Fval, &h->Fcol, &h->Fcnt, &h->b_colview, &h->b_gram,

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -286,6 +288,64 @@ cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* 
     csc_sort_kernel<<<cb, 256, 0, s>>>(n, colptr, tmp_row, tmp_val, rowind, cvals);
   }
   return cudaGetLastError();
+}
+
+// CSR -> CSC as a stable radix sort of the entries by column: the CSR lists
+// them in increasing row order, so a stable sort on the column index leaves
+// each column's rows sorted (the same CSC as the scatter + rank path, in a
+// few streaming passes instead of atomics and O(len^2) ranking).  The value
+// sorted along is (row << 32 | entry index); one gather then writes rowind
+// and cvals.
+__global__ void csc_expand_kernel(int m, const int32_t* __restrict__ rowptr, unsigned long long* __restrict__ pk) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
+    const int t1 = rowptr[r + 1];
+    for (int t = rowptr[r] + lane; t < t1; t += 32) pk[t] = ((unsigned long long)(unsigned)r << 32) | (unsigned)t;
+  }
+}
+__global__ void csc_gather_kernel(int64_t nnz, const double* __restrict__ vals, int32_t* __restrict__ rowind,
+                                  double* cvals) {
+  pdl_wait();
+  const unsigned long long* pk = reinterpret_cast<const unsigned long long*>(cvals);  // sorted (row, t), in place
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = pk[p];
+    rowind[p] = (int32_t)(v >> 32);
+    cvals[p] = vals[(unsigned)(v & 0xffffffffu)];
+  }
+}
+static int csc_key_bits(int n) {
+  int b = 1;
+  while (b < 31 && (1 << b) < n) ++b;
+  return b;
+}
+size_t csc_sort_temp_bytes(int64_t nnz, int n) {
+  if (nnz <= 0 || nnz >= ((int64_t)1 << 31)) return 0;
+  size_t bytes = 0;
+  if (cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                      (const unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)nnz, 0,
+                                      csc_key_bits(n)) != cudaSuccess)
+    return 0;
+  return bytes;
+}
+cudaError_t launch_csc_fill_sorted(int m, int n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                                   const double* vals, int32_t* rowind, double* cvals, int32_t* tmp_row,
+                                   double* tmp_val, void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (nnz <= 0) return cudaSuccess;
+  unsigned long long* pin = reinterpret_cast<unsigned long long*>(tmp_val);
+  unsigned long long* pout = reinterpret_cast<unsigned long long*>(cvals);
+  int rb = (int)(((int64_t)m * 32 + 255) / 256);
+  if (rb > 4096) rb = 4096;
+  if (rb < 1) rb = 1;
+  cudaError_t e = launch_pdl(csc_expand_kernel, dim3(rb), dim3(256), 0, s, m, rowptr, pin);
+  if (e != cudaSuccess) return e;
+  size_t tb = temp_bytes;
+  e = cub::DeviceRadixSort::SortPairs(temp, tb, colind, tmp_row, pin, pout, (int)nnz, 0, csc_key_bits(n), s);
+  if (e != cudaSuccess) return e;
+  int gb = (int)((nnz + 255) / 256);
+  if (gb > 8192) gb = 8192;
+  return launch_pdl(csc_gather_kernel, dim3(gb), dim3(256), 0, s, nnz, vals, rowind, cvals);
 }
 
 // ---------------------------------------------------------------- Gram

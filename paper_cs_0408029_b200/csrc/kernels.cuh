@@ -24,6 +24,12 @@ cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* 
                             const double* vals, const int32_t* colptr, int32_t* rowind,
                             double* cvals, int32_t* cursor, int32_t* tmp_row, double* tmp_val,
                             cudaStream_t s, int maxcnt = -1);
+// the same CSC by a stable radix sort on the column (CUB): temp_bytes from
+// csc_sort_temp_bytes (0: not available, use launch_csc_fill)
+size_t csc_sort_temp_bytes(int64_t nnz, int n);
+cudaError_t launch_csc_fill_sorted(int m, int n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                                   const double* vals, int32_t* rowind, double* cvals, int32_t* tmp_row,
+                                   double* tmp_val, void* temp, size_t temp_bytes, cudaStream_t s);
 cudaError_t launch_csr_to_csc(int m, int n, int64_t nnz, const int32_t* rowptr,
                               const int32_t* colind, const double* vals, int32_t* colptr,
                               int32_t* rowind, double* cvals, int32_t* cursor, int32_t* tmp_row,
