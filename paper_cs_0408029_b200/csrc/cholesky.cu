@@ -371,17 +371,26 @@ __device__ __forceinline__ void syrk_blocks(double* __restrict__ S, const double
   const double* b1 = X + (8 * J + rq) * LDS + kq;
   const double* a2 = X + (8 * max(I2, 0) + rq) * LDS + kq;
   const double* b2 = X + (8 * max(J2, 0) + rq) * LDS + kq;
-  double c0 = C1[0], c1 = C1[1], d0 = C2[0], d1 = C2[1];
+  // four independent accumulator pairs per block (k steps 4q mod 16): a
+  // 4-deep DMMA dependency chain instead of 16 on the chain's POTRF
+  double c[4][2], d[4][2];
+  c[0][0] = C1[0];
+  c[0][1] = C1[1];
+  d[0][0] = C2[0];
+  d[0][1] = C2[1];
+#pragma unroll
+  for (int q = 1; q < 4; ++q) c[q][0] = c[q][1] = d[q][0] = d[q][1] = 0.0;
 #pragma unroll
   for (int kk = 0; kk < T; kk += 4) {
-    dmma8x8x4(c0, c1, -a1[kk], b1[kk]);
-    dmma8x8x4(d0, d1, -a2[kk], b2[kk]);  // (a dummy copy of block 1 when J2 < 0)
+    const int q = (kk >> 2) & 3;
+    dmma8x8x4(c[q][0], c[q][1], -a1[kk], b1[kk]);
+    dmma8x8x4(d[q][0], d[q][1], -a2[kk], b2[kk]);  // (a dummy copy of block 1 when J2 < 0)
   }
-  C1[0] = c0;
-  C1[1] = c1;
+  C1[0] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+  C1[1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
   if (J2 >= 0) {
-    C2[0] = d0;
-    C2[1] = d1;
+    C2[0] = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
+    C2[1] = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
   }
 }
 
@@ -801,6 +810,89 @@ __device__ __forceinline__ void ring_consume_updates(HelperRing& R, const double
   }
 }
 
+// Split-K consumer layout of the piped helper tasks: warp w (0..7) owns the
+// 32 x 32 quadrant (w & 3) of the tile and the k-half (w >> 2) of every
+// update -- 16 independent 8x8 accumulators per warp and half the fragment
+// loads per DMMA of the 16 x 32 layout; the two k-halves are summed once at
+// the end of the task (q32_reduce).
+__device__ __forceinline__ void q32_origin(int w, int& rb0, int& cb0, int& k0) {
+  rb0 = ((w & 3) >> 1) * 32;
+  cb0 = (w & 1) * 32;
+  k0 = (w >> 2) * 32;
+}
+__device__ __forceinline__ void gather_acc32(double (&acc)[4][4][2], const double* __restrict__ G, int ldg,
+                                             const double* __restrict__ cvec, const int32_t* __restrict__ Fidx,
+                                             int f, int i, int jj, int lane, int rb0, int cb0) {
+  const int rv = min(T, f + 1 - i * T), cv = min(T, f - jj * T);
+  int gr[4], gc[8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = rb0 + 8 * a + (lane >> 2);
+    gr[a] = (r < rv) ? ((i * T + r < f) ? Fidx[i * T + r] : -1) : -2;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int cc = cb0 + 8 * q + 2 * (lane & 3) + v;
+      gc[2 * q + v] = (cc < cv) ? Fidx[jj * T + cc] : -1;
+    }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int r = rb0 + 8 * a + (lane >> 2), cc = cb0 + 8 * q + 2 * (lane & 3) + v;
+        const int gcv = gc[2 * q + v];
+        double x = 0.0;
+        if (gr[a] != -2 && gcv >= 0 && (i != jj || cc <= r))
+          x = (gr[a] >= 0) ? G[(size_t)gr[a] * ldg + gcv] : cvec[gcv];
+        acc[a][q][v] = x;
+      }
+}
+__device__ __forceinline__ void acc32_io(double (&acc)[4][4][2], double* S, int lane, int rb0, int cb0, int mode) {
+  // mode 0: store, 1: load, 2: add
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        double* p = S + (rb0 + 8 * a + (lane >> 2)) * LDS + cb0 + 8 * q + 2 * (lane & 3) + v;
+        if (mode == 0) *p = acc[a][q][v];
+        else if (mode == 1) acc[a][q][v] = *p;
+        else acc[a][q][v] += *p;
+      }
+}
+// acc -= A B^T over k in [k0, k0+32) for the warp's 32 x 32 quadrant
+__device__ __forceinline__ void dmma_q32_sub(double (&acc)[4][4][2], const double* __restrict__ A,
+                                             const double* __restrict__ B, int lane, int rb0, int cb0, int k0) {
+#pragma unroll 2
+  for (int kk = k0; kk < k0 + 32; kk += 4) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) av[a] = -A[(rb0 + 8 * a + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bv[q] = B[(cb0 + 8 * q + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dmma8x8x4(acc[a][q][0], acc[a][q][1], av[a], bv[q]);
+  }
+}
+__device__ __forceinline__ void ring_consume_updates32(HelperRing& R, const double* ring, double (&acc)[4][4][2],
+                                                       int kmax, unsigned& cnt, int lane, int rb0, int cb0, int k0) {
+  for (int k = 0; k < kmax; ++k, ++cnt) {
+    const int sidx = (int)(cnt % kStages);
+    ring_wait(&R.full[sidx], (cnt / kStages) & 1);
+    const double* slot = ring + (size_t)(2 * sidx) * TS;
+    dmma_q32_sub(acc, slot, slot + TS, lane, rb0, cb0, k0);
+    __syncwarp();
+    if (lane == 0) ring_arrive(&R.empty[sidx]);
+  }
+}
+
 __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
     const double* __restrict__ G, int ldg, const double* __restrict__ cvec,
     const int32_t* __restrict__ Fidx, double* __restrict__ Lt, double* __restrict__ Linv,
@@ -991,7 +1083,9 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
       // row chain runs by half tiles (Th, kind 6) when all its tasks fit on the
       // helpers at once, else by whole tiles (kind 2): a waiting task holds its CTA
       const int nr = ntr - jq;
-      const bool halves = halves_mode >= 0 ? halves_mode != 0 : 2 * nr * (jq - 1) <= (int)gridDim.x - 2;
+      // (measured at config 2: with 2 new tile rows the half-tile chains win even
+      // when they cannot all be resident, 340 -> 255 us; with 7 they lose)
+      const bool halves = halves_mode >= 0 ? halves_mode != 0 : (2 * nr * (jq - 1) <= (int)gridDim.x - 2 || nr <= 2);
       const int per = halves ? 2 : 1;
       const int nh = (jq - 1) * nr * per;
       const int u = t - (jq - 1);
@@ -1041,17 +1135,28 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
         else rcnt += kmax + (trsm ? 1 : 0);
         continue;
       }
-      // ---- consumer warps 0..7
-      const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
-      double acc[2][4][2];
-      gather_acc(acc, G, ldg, cvec, Fidx, f, ti, tj, lane, rb0, cb0);
-      ring_consume_updates(R, ring, acc, kmax, rcnt, lane, rb0, cb0);
+      // ---- consumer warps 0..7: split-K 32 x 32 quadrants (q32_origin)
+      int rb0, cb0, k0;
+      q32_origin(w, rb0, cb0, k0);
+      double acc[4][4][2];
+      if (k0 == 0) {
+        gather_acc32(acc, G, ldg, cvec, Fidx, f, ti, tj, lane, rb0, cb0);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[a][q][0] = acc[a][q][1] = 0.0;
+      }
+      ring_consume_updates32(R, ring, acc, kmax, rcnt, lane, rb0, cb0, k0);
       // S: slot B of the next stage (free: the producer waits for the next task)
       double* Sx = ring + (size_t)(2 * (rcnt % kStages) + 1) * TS;
+      csync();  // every warp is past its updates (a fast warp runs up to kStages ahead): Sx is free
+      if (k0 != 0) acc32_io(acc, Sx, lane, rb0, cb0, 0);  // the second k-half's sums
+      csync();
+      if (k0 == 0) acc32_io(acc, Sx, lane, rb0, cb0, 2);
       if (trsm) {
         const int sidx = (int)(rcnt % kStages);
-        csync();  // every warp is past its updates (a fast warp runs up to kStages ahead): Sx is free
-        acc_store(acc, Sx, lane, rb0, cb0);
+        if (k0 == 0) acc32_io(acc, Sx, lane, rb0, cb0, 0);
         ring_wait(&R.full[sidx], (rcnt / kStages) & 1);  // Linv_jj in slot A
         csync();
         double acc8[8][2];
@@ -1072,7 +1177,7 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
       } else {
         // partial tiles go out in the global tile layout straight from the fragments
         double* dst = Lt + (size_t)tidx(ti, tj) * TS;
-        acc_store(acc, dst, lane, rb0, cb0);
+        if (k0 == 0) acc32_io(acc, dst, lane, rb0, cb0, 0);
         publish_flag(&F.part[tidx(ti, tj)], epoch);
         if (kind == 0) PROF_STAMP(1000 + ti, 2);
         else if (kind == 1) PROF_STAMP(1000 + tj, 0);
