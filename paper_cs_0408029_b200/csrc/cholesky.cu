@@ -641,54 +641,6 @@ __device__ __forceinline__ void gather_tile(double* __restrict__ S, const double
   }
 }
 
-// S (smem tile i,jj) -= sum_{k < kmax} L(i,k) L(jj,k)^T, operands double-
-// buffered through BUF(1..4) with cp.async (waits on the "full" flags; tiles
-// in rows < jq are kept from the previous factorization and need none).
-__device__ __forceinline__ void left_update(double* __restrict__ smem, double* __restrict__ S,
-                                            const double* __restrict__ Lt, const int* __restrict__ full,
-                                            int epoch, int i, int jj, int kmax, int jq, int* s_ready) {
-  if (kmax <= 0) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
-  double acc[2][4][2];
-  acc_load(acc, S, lane, rb0, cb0);
-  bool have_next = false;
-  for (int k = 0; k < kmax; ++k) {
-    double* LA = smem + ((k & 1) ? 3 : 1) * (T * LDS);
-    double* LB = smem + ((k & 1) ? 4 : 2) * (T * LDS);
-    if (!have_next) {
-      if (tid == 0) {
-        if (i >= jq) wait_flag(&full[tidx(i, k)], epoch);
-        if (jj >= jq) wait_flag(&full[tidx(jj, k)], epoch);
-      }
-      csync();
-      tile_async(LA, Lt + (size_t)tidx(i, k) * TS);
-      tile_async(LB, Lt + (size_t)tidx(jj, k) * TS);
-      cp_async_commit();
-    }
-    have_next = false;
-    if (k + 1 < kmax) {
-      if (tid == 0)
-        *s_ready = (i < jq || ld_acquire(&full[tidx(i, k + 1)]) == epoch) &&
-                   (jj < jq || ld_acquire(&full[tidx(jj, k + 1)]) == epoch);
-      csync();
-      if (*s_ready) {
-        tile_async(smem + ((k & 1) ? 1 : 3) * (T * LDS), Lt + (size_t)tidx(i, k + 1) * TS);
-        tile_async(smem + ((k & 1) ? 2 : 4) * (T * LDS), Lt + (size_t)tidx(jj, k + 1) * TS);
-        cp_async_commit();
-        have_next = true;
-      }
-    }
-    if (have_next) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    csync();
-    dmma_tile<true>(acc, LA, LB, lane, rb0, cb0);
-    csync();
-  }
-  acc_store(acc, S, lane, rb0, cb0);
-  csync();
-}
-
 // ---------------------------------------------------------------------------
 // Helper operand pipeline (warp-specialized).  A helper CTA is 8 consumer
 // warps (the DMMA updates, 256 threads as everywhere in this file) plus one
@@ -903,7 +855,7 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
   // helpers: BUF(0) = S, BUF(1..4) = operand double-buffers.
   // chain: BUF(0)/BUF(1) = diagonal tile of column j (alternating), BUF(5) = A/L(j+1,j)
   __shared__ double rinv[T];
-  __shared__ int s_task, s_ready, s_bad, s_role;
+  __shared__ int s_task, s_bad, s_role;
   const int f = st->f;
   const int epoch = st->epoch;
   if (f <= 0 || st->done || st->status != 0) return;  // (graph loop: nothing to solve)
@@ -1123,16 +1075,37 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
     }
     if (kind < 0) break;
     // ---- pipelined kinds: P(j+1,j+1), P(j+1,j), T(i,j) outside a restart row chain, D(jq)
-    const bool piped = kind == 0 || kind == 1 || kind == 3 || (kind == 2 && !(j < jq && j > 0));
+    const bool piped = kind == 0 || kind == 1 || kind == 3 || kind == 2;
     if (piped) {
       const int ti = kind == 3 ? jq : (kind == 2 ? i : j + 1);
       const int tj = kind == 3 ? jq : (kind == 0 ? j + 1 : j);
-      const int kmax = kind == 3 ? jq : j;
+      // restart row chain (whole tiles): L(i,j) = B - L(i,j-1) W_j with
+      // B = (A(i,j) - sum_{k<j-1} L(i,k) L(j,k)^T) Linv_jj^T: the ring carries
+      // the j-1 updates, Linv_jj, then {L(i,j-1), W_j} as one more stage
+      const bool rchain = kind == 2 && j < jq && j > 0;
+      const int kmax = kind == 3 ? jq : (rchain ? j - 1 : j);
       const bool trsm = kind == 2;
       double* ring = smem;
       if (w == kThreads / 32) {  // ---- producer warp
-        if (lane == 0) ring_produce(R, ring, Lt, Linv, F, epoch, ti, tj, kmax, jq, trsm ? tj : -1, rcnt);
-        else rcnt += kmax + (trsm ? 1 : 0);
+        if (lane == 0) {
+          ring_produce(R, ring, Lt, Linv, F, epoch, ti, tj, kmax, jq, trsm ? tj : -1, rcnt);
+          if (rchain) {
+            const int sidx = (int)(rcnt % kStages);
+            const unsigned use = rcnt / kStages;
+            if (use > 0) ring_wait(&R.empty[sidx], (use - 1) & 1);
+            double* slot = ring + (size_t)(2 * sidx) * TS;
+            wait_flag(&F.part[tidx(tj, tj - 1)], epoch);  // W_j (task W(j)): in flight first
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            ring_expect(&R.full[sidx], 2u * TS * 8);
+            ring_load_tile(slot + TS, Wbuf + (size_t)tj * TS, &R.full[sidx]);
+            wait_flag(&F.full[tidx(ti, tj - 1)], epoch);  // L(i,j-1): the row chain's previous step
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            ring_load_tile(slot, Lt + (size_t)tidx(ti, tj - 1) * TS, &R.full[sidx]);
+            ++rcnt;
+          }
+        } else {
+          rcnt += kmax + (trsm ? 1 : 0) + (rchain ? 1 : 0);
+        }
         continue;
       }
       // ---- consumer warps 0..7: split-K 32 x 32 quadrants (q32_origin)
@@ -1164,6 +1137,37 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
         csync();
         store_rows8(acc8, Sx, w, lane);
         csync();
+        if (rchain) {  // Sx = B; the last step L(i,j) = B - L(i,j-1) W_j (split-K, the tail stage)
+          __syncwarp();
+          if (lane == 0) ring_arrive(&R.empty[sidx]);
+          ++rcnt;
+          const int s2 = (int)(rcnt % kStages);
+          if (k0 == 0) {
+            acc32_io(acc, Sx, lane, rb0, cb0, 1);
+          } else {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[a][q][0] = acc[a][q][1] = 0.0;
+          }
+          ring_wait(&R.full[s2], (rcnt / kStages) & 1);
+          const double* slot = ring + (size_t)(2 * s2) * TS;
+          dmma_q32_sub(acc, slot, slot + TS, lane, rb0, cb0, k0);
+          __syncwarp();
+          if (lane == 0) ring_arrive(&R.empty[s2]);
+          ++rcnt;
+          csync();  // B read by every warp
+          if (k0 != 0) acc32_io(acc, Sx, lane, rb0, cb0, 0);
+          csync();
+          if (k0 == 0) {
+            acc32_io(acc, Sx, lane, rb0, cb0, 2);
+            acc32_io(acc, Sx, lane, rb0, cb0, 0);
+          }
+          csync();
+          store_tile(Lt + (size_t)tidx(ti, tj) * TS, Sx);
+          publish_flag(&F.full[tidx(ti, tj)], epoch);
+          continue;
+        }
         store_tile(Lt + (size_t)tidx(ti, tj) * TS, Sx);
         __syncwarp();
         if (lane == 0) ring_arrive(&R.empty[sidx]);
@@ -1274,92 +1278,7 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
       publish_flag(&F.part[tidx(j, j - 1)], epoch);  // (a kept tile's part flag: W_j ready)
       continue;
     }
-    if (kind == 3) {                 // D(jq): diagonal tile jq, all updates k < jq
-      PROF_STAMP(1199, 0);
-      gather_tile(S, G, ldg, cvec, Fidx, f, jq, jq);
-      csync();
-      left_update(smem, S, Lt, F.full, epoch, jq, jq, jq, jq, &s_ready);
-      store_tile(Lt + (size_t)tidx(jq, jq) * TS, S);
-      publish_flag(&F.part[tidx(jq, jq)], epoch);
-      PROF_STAMP(1199, 1);
-      continue;
-    }
-    if (kind == 0) {                 // P(j+1, j+1): diagonal tile, updates k < j
-      gather_tile(S, G, ldg, cvec, Fidx, f, j + 1, j + 1);
-      csync();
-      left_update(smem, S, Lt, F.full, epoch, j + 1, j + 1, j, jq, &s_ready);
-      store_tile(Lt + (size_t)tidx(j + 1, j + 1) * TS, S);
-      publish_flag(&F.part[tidx(j + 1, j + 1)], epoch);
-      PROF_STAMP(1000 + j + 1, 2);
-    } else if (kind == 1) {          // P(j+1, j): updates k < j (the chain does the TRSM)
-      gather_tile(S, G, ldg, cvec, Fidx, f, j + 1, j);
-      csync();
-      left_update(smem, S, Lt, F.full, epoch, j + 1, j, j, jq, &s_ready);
-      PROF_STAMP(1000 + j, 4);
-      store_tile(Lt + (size_t)tidx(j + 1, j) * TS, S);
-      publish_flag(&F.part[tidx(j + 1, j)], epoch);
-      PROF_STAMP(1000 + j, 0);
-    } else if (j < jq && j > 0) {    // T(i, j) below a kept prefix: the row chain of the restart
-      // L(i,j) = B - L(i,j-1) W_j with B = (A(i,j) - sum_{k<j-1} L(i,k) L(j,k)^T) Linv_jj^T and
-      // W_j = L(j,j-1)^T Linv_jj^T (task W(j)): B is formed BEFORE L(i,j-1) arrives, so the
-      // per-column step of the chain is one product (no update + TRSM pair)
-      const int rb0 = (w >> 1) * 16, cb0 = (w & 1) * 32;
-      double* Lv = smem + 5 * T * LDS;   // Linv_jj
-      double* Wt = smem + 2 * T * LDS;   // W_j^T
-      double* Xp = smem + 3 * T * LDS;   // L(i, j-1)
-      tile_async(Lv, Linv + (size_t)j * TS);
-      cp_async_commit();
-      gather_tile(S, G, ldg, cvec, Fidx, f, i, j);
-      csync();
-      left_update(smem, S, Lt, F.full, epoch, i, j, j - 1, jq, &s_ready);  // k < j-1
-      cp_async_wait<0>();
-      if (tid == 0) wait_flag(&F.part[tidx(j, j - 1)], epoch);
-      csync();
-      tile_async(Wt, Wbuf + (size_t)j * TS);  // (in flight during B)
-      cp_async_commit();
-      {
-        double acc8[8][2];
-        gemm_linvT(acc8, S, Lv, w, lane);
-        csync();
-        store_rows8(acc8, S, w, lane);  // S = B
-      }
-      if (tid == 0) wait_flag(&F.full[tidx(i, j - 1)], epoch);
-      csync();
-      tile_async(Xp, Lt + (size_t)tidx(i, j - 1) * TS);
-      cp_async_commit();
-      cp_async_wait<0>();
-      csync();
-      {
-        double acc[2][4][2];
-        acc_load(acc, S, lane, rb0, cb0);
-        dmma_tile<true>(acc, Xp, Wt, lane, rb0, cb0);  // S -= L(i,j-1) W_j
-        acc_store(acc, S, lane, rb0, cb0);
-      }
-      csync();
-      store_tile(Lt + (size_t)tidx(i, j) * TS, S);
-      publish_flag(&F.full[tidx(i, j)], epoch);
-    } else {                         // T(i, j): updates k < j, then L(i,j) = A(i,j) Linv_jj^T
-      gather_tile(S, G, ldg, cvec, Fidx, f, i, j);
-      csync();
-      left_update(smem, S, Lt, F.full, epoch, i, j, j, jq, &s_ready);
-      double* LB = smem + T * LDS;
-      if (tid == 0 && j >= jq) wait_flag(&F.inv[j], epoch);  // (a kept column's Linv is in place)
-      csync();
-      load_tile(LB, Linv + (size_t)j * TS);
-      csync();
-      double acc[8][2];
-      gemm_linvT(acc, S, LB, w, lane);
-      csync();
-      store_rows8(acc, S, w, lane);
-      csync();
-      store_tile(Lt + (size_t)tidx(i, j) * TS, S);
-      publish_flag(&F.full[tidx(i, j)], epoch);
-      if (jq > 0 && j == 0 && i >= jq && tid == 0) {  // (the restart's half-tile chain starts here)
-        st_release(&F.part[tidx(i, j)], epoch);
-        st_release(&F.half1[tidx(i, j)], epoch);
-      }
-      if (i == j + 2) PROF_STAMP(1000 + j + 1, 1);
-    }
+    // (every other kind runs on the helper operand pipeline above)
   }
 }
 
