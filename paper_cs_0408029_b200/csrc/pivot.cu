@@ -207,20 +207,31 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
                                int32_t* __restrict__ Fs, int fprev, int* s_wF, int* s_wG, int* s_wS,
                                int* s_cnt, int* s_f, int* s_g, int* s_s, int* s_q, int* s_old,
                                void* sort_smem) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const unsigned lt = (1u << lane) - 1u;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  // Each thread owns kE consecutive indices per sweep (n <= 1024 kE: one
+  // sweep), its (mask, pos) held in registers from (1) to (2): one block
+  // reduction and one block scan per sweep instead of per 1024 indices.
+  constexpr int kE = 8;
+  const int span = kE * (int)blockDim.x;
   // (1) q = first position of the previous order whose member left F
   int qloc = fprev;
-  for (int i = tid; i < n; i += blockDim.x) {
-    const int pi = pos[i];
-    if (pi >= 0 && !mask[i]) qloc = min(qloc, pi);
+  for (int base = 0; base < n; base += span) {
+    const int i0 = base + kE * tid;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+      const int i = i0 + e;
+      if (i < n) {
+        const int pi = pos[i];
+        if (pi >= 0 && !mask[i]) qloc = min(qloc, pi);
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) qloc = min(qloc, __shfl_xor_sync(kFull, qloc, o));
   if (lane == 0) s_cnt[wid] = qloc;
   __syncthreads();
   if (wid == 0) {
-    int v = lane < (int)(blockDim.x >> 5) ? s_cnt[lane] : fprev;
+    int v = lane < nw ? s_cnt[lane] : fprev;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
     if (lane == 0) {
@@ -235,51 +246,79 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
   const int q = *s_q;
   // (2) the tail R = F minus the prefix -> Fidx[q..) in index order; G ->
   // Gidx, F -> Fs (both in index order)
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int i = base + tid;
-    const bool valid = i < n;
-    const bool inF = valid && mask[i];
-    const int pi = valid ? pos[i] : -1;
-    const bool inR = inF && !(pi >= 0 && pi < q);
-    const bool inG = valid && !inF;
-    const unsigned bR = __ballot_sync(kFull, inR), bG = __ballot_sync(kFull, inG),
-                   bS = __ballot_sync(kFull, inF), bO = __ballot_sync(kFull, inR && pi >= 0);
-    if (lane == 0 && bO != 0u) atomicAdd(s_old, __popc(bO));
-    if (lane == 0) {
-      s_wF[wid] = __popc(bR);
-      s_wG[wid] = __popc(bG);
-      s_wS[wid] = __popc(bS);
+  for (int base = 0; base < n; base += span) {
+    const int i0 = base + kE * tid;
+    unsigned fR = 0u, fG = 0u, fS = 0u;
+    int cR = 0, cG = 0, cS = 0, cO = 0;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+      const int i = i0 + e;
+      if (i < n) {
+        const bool inF = mask[i] != 0;
+        const int pi = pos[i];
+        const bool inR = inF && !(pi >= 0 && pi < q);
+        fR |= (inR ? 1u : 0u) << e;
+        fG |= (inF ? 0u : 1u) << e;
+        fS |= (inF ? 1u : 0u) << e;
+        cO += (inR && pi >= 0) ? 1 : 0;
+      }
     }
+    cR = __popc(fR);
+    cG = __popc(fG);
+    cS = __popc(fS);
+    // block exclusive scan of (cR, cG, cS)
+    int ia = cR, ib = cG, ic = cS;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ya = __shfl_up_sync(kFull, ia, o), yb = __shfl_up_sync(kFull, ib, o),
+                yc = __shfl_up_sync(kFull, ic, o);
+      if (lane >= o) {
+        ia += ya;
+        ib += yb;
+        ic += yc;
+      }
+    }
+    cO = warp_sum_i(cO);
+    if (lane == 31) {
+      s_wF[wid] = ia;
+      s_wG[wid] = ib;
+      s_wS[wid] = ic;
+    }
+    if (lane == 0 && cO != 0) atomicAdd(s_old, cO);
     __syncthreads();
     if (wid == 0) {
-      const int nw = blockDim.x >> 5;
       int a = lane < nw ? s_wF[lane] : 0, bb = lane < nw ? s_wG[lane] : 0, cc = lane < nw ? s_wS[lane] : 0;
-      int ia = a, ib = bb, ic = cc;
+      int xa = a, xb = bb, xc = cc;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int ya = __shfl_up_sync(kFull, ia, o), yb = __shfl_up_sync(kFull, ib, o),
-            yc = __shfl_up_sync(kFull, ic, o);
+        const int ya = __shfl_up_sync(kFull, xa, o), yb = __shfl_up_sync(kFull, xb, o),
+                  yc = __shfl_up_sync(kFull, xc, o);
         if (lane >= o) {
-          ia += ya;
-          ib += yb;
-          ic += yc;
+          xa += ya;
+          xb += yb;
+          xc += yc;
         }
       }
-      s_wF[lane] = ia - a;
-      s_wG[lane] = ib - bb;
-      s_wS[lane] = ic - cc;
+      s_wF[lane] = xa - a;
+      s_wG[lane] = xb - bb;
+      s_wS[lane] = xc - cc;
       if (lane == 31) {
-        s_cnt[0] = ia;
-        s_cnt[1] = ib;
-        s_cnt[2] = ic;
+        s_cnt[0] = xa;
+        s_cnt[1] = xb;
+        s_cnt[2] = xc;
       }
     }
     __syncthreads();
-    if (inR) Fidx[*s_f + s_wF[wid] + __popc(bR & lt)] = i;
-    if (inF) Fs[*s_s + s_wS[wid] + __popc(bS & lt)] = i;
-    if (inG) {
-      Gidx[*s_g + s_wG[wid] + __popc(bG & lt)] = i;
-      pos[i] = -1;
+    int oR = *s_f + s_wF[wid] + ia - cR, oG = *s_g + s_wG[wid] + ib - cG, oS = *s_s + s_wS[wid] + ic - cS;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+      const int i = i0 + e;
+      if ((fR >> e) & 1u) Fidx[oR++] = i;
+      if ((fS >> e) & 1u) Fs[oS++] = i;
+      if ((fG >> e) & 1u) {
+        Gidx[oG++] = i;
+        pos[i] = -1;
+      }
     }
     __syncthreads();
     if (tid == 0) {
