@@ -577,6 +577,7 @@ LsqrArgs lsqr_args(nnls_handle* h) {
   a.Fcol = P<int32_t>(h->Fcol);
   a.Fcnt = P<int32_t>(h->Fcnt);
   a.Fidx = h->no_reuse ? P<int32_t>(h->Fidx) : P<int32_t>(h->Fs);  // F (index order when reusing)
+  a.Gidx = P<int32_t>(h->Gidx);  // G in index order (decide)
   a.plan = P<int>(h->err) + 4;
   return a;
 }

@@ -142,6 +142,7 @@ struct LsqrArgs {
   // (row r: Fcnt[r] entries from offset rowptr[r]); built by launch_lsqr_compact
   double* Fval; int32_t* Fcol; int32_t* Fcnt;
   const int32_t* Fidx;  // the final F (f entries; from the last decide)
+  const int32_t* Gidx;  // the final G (n - f entries, index order; the resident report)
   const int* plan;      // cluster slice plan (lsqr_plan_kernel: maxima, row bounds, column bounds)
 };
 cudaError_t launch_lsqr_compact(const LsqrArgs& a, int sm_count, cudaStream_t s);

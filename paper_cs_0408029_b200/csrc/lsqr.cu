@@ -358,6 +358,7 @@ __device__ void lsqr_finish(const LsqrArgs& a, cg::grid_group& grid, int mode, i
   }
   block_partial_minmax(pinf, a.partials, 4, red, false);
   grid.sync();
+  LG_MARK(4);
   const double infeas = grid_total(a.partials, 4, &bcast, 2);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.st->lsqr_iterations = itn;
@@ -390,6 +391,7 @@ __device__ void lsqr_finish(const LsqrArgs& a, cg::grid_group& grid, int mode, i
   }
   block_partial_sum(po, a.partials, 0, red);
   grid.sync();
+  LG_MARK(5);
   double mx = INFINITY, my = INFINITY, mc = 0.0, dot = 0.0;
   for (int j = gwarp; j < n; j += nwarps) {
     double s = 0.0;
@@ -410,6 +412,7 @@ __device__ void lsqr_finish(const LsqrArgs& a, cg::grid_group& grid, int mode, i
   block_partial_minmax(mc, a.partials, 3, red, false);
   block_partial_sum(dot, a.partials, 4, red);
   grid.sync();
+  LG_MARK(6);
   if (blockIdx.x == 0) {
     const double obj = grid_total(a.partials, 0, &bcast, 0);
     const double gmx = grid_total(a.partials, 1, &bcast, 1);
@@ -860,7 +863,101 @@ __device__ bool lsqr_iterate_resident(const LsqrArgs& a, cg::grid_group& grid, i
       LG_STAMP(5);
     }
   }
-  for (int c = tid; c < C; c += nb) a.X[Fidx[k0 + c]] = Xo[c];
+  LG_MARK(2);
+  // ---- x (zeroing, c16) and the a11 report from the resident slices: x is
+  // zero off F, so R = A x - b needs only the row slice (x_F replicated in
+  // shared memory), A^T R on the F columns is the partial-sum pass of
+  // phase B, and only the G columns gather R from global memory (CSC).
+  double pinf = 0.0;
+  for (int c = tid; c < C; c += nb) {
+    const int j = Fidx[k0 + c];
+    double v = mode == 2 ? a.x_ne[j] + Xo[c] : Xo[c];
+    if (fabs(v) < a.tol) v = 0.0;
+    if (v < 0.0) pinf = 1.0;
+    a.x_out[j] = v;
+    a.V[k0 + c] = v;  // (compact copy for the replicas)
+    Wo[c] = v;
+  }
+  const int g = a.n - f;
+  const int32_t* __restrict__ Gidx = a.Gidx;
+  const int q0 = (int)((long long)g * bid / G), q1 = (int)((long long)g * (bid + 1) / G);
+  for (int t = q0 + tid; t < q1; t += nb) a.x_out[Gidx[t]] = 0.0;
+  block_partial_minmax(pinf, a.partials, 4, red, false);
+  grid.sync();
+  LG_MARK(4);
+  const double infeas = grid_total(a.partials, 4, bcast, 2);
+  if (bid == 0 && tid == 0) {
+    a.st->lsqr_iterations = itn;
+    a.st->lsqr_stop = istop;
+    a.st->infeasible_after_lsqr = (infeas > 0.0) ? 1 : 0;
+    a.st->free_count = f;
+  }
+  if (!a.kkt) return true;
+  for (int k = tid; k < f; k += nb) vs[k] = __ldcg(&a.V[k]);
+  __syncthreads();
+  double po = 0.0;
+  for (int i = tid; i < R; i += nb) {  // R = A_F x_F - b on own rows
+    double s0 = 0.0, s1 = 0.0;
+    const int t1 = rp[i + 1];
+    int t = rp[i];
+    for (; t + 2 <= t1; t += 2) {
+      s0 = fma(rv[t], vs[rc[t]], s0);
+      s1 = fma(rv[t + 1], vs[rc[t + 1]], s1);
+    }
+    if (t < t1) s0 = fma(rv[t], vs[rc[t]], s0);
+    const double rr = (s0 + s1) - a.b[r0 + i];
+    ul[i] = rr;
+    a.R[r0 + i] = rr;
+    po += rr * rr;
+  }
+  __syncthreads();
+  partial_AtU();  // this slice's partial A_F^T R
+  block_partial_sum(po, a.partials, 0, red);
+  grid.sync();
+  LG_MARK(5);
+  double mx = INFINITY, my = INFINITY, mc = 0.0, dot = 0.0;
+  column_totals();  // own F columns: y'_j
+  for (int c = tid; c < C; c += nb) {
+    const double xj = Wo[c], yj = ctot[c];
+    mx = fmin(mx, xj);
+    my = fmin(my, yj);
+    mc = fmax(mc, fabs(xj * yj));
+    dot += xj * yj;
+  }
+  for (int t = q0 + wid; t < q1; t += nw) {  // own G columns: y'_j = A_j^T R (x_j = 0)
+    const int j = Gidx[t];
+    double sj = 0.0;
+    const int t1 = a.colptr[j + 1];
+#pragma unroll 4
+    for (int e = a.colptr[j] + lane; e < t1; e += 32) sj = fma(a.cvals[e], __ldcg(&a.R[a.rowind[e]]), sj);
+    sj = warp_sum(sj);
+    if (lane == 0) {
+      mx = fmin(mx, 0.0);
+      my = fmin(my, sj);
+    }
+  }
+  block_partial_minmax(mx, a.partials, 1, red, true);
+  block_partial_minmax(my, a.partials, 2, red, true);
+  block_partial_minmax(mc, a.partials, 3, red, false);
+  block_partial_sum(dot, a.partials, 4, red);
+  grid.sync();
+  LG_MARK(6);
+  if (bid == 0 && wid < 5) {  // five totals at once (a warp each, fixed order)
+    const int kind = wid == 0 || wid == 4 ? 0 : (wid == 3 ? 2 : 1);
+    double v = kind == 0 ? 0.0 : (kind == 1 ? INFINITY : -INFINITY);
+    for (int b = lane; b < G; b += 32) {
+      const double u = __ldcg(&a.partials[b * kSlots + wid]);
+      v = kind == 0 ? v + u : (kind == 1 ? fmin(v, u) : fmax(v, u));
+    }
+    v = kind == 0 ? warp_sum(v) : (kind == 1 ? warp_min(v) : warp_max(v));
+    if (lane == 0) {
+      if (wid == 0) a.st->objective = 0.5 * v;
+      else if (wid == 1) a.st->kkt_min_x = v;
+      else if (wid == 2) a.st->kkt_min_y = v;
+      else if (wid == 3) a.st->kkt_max_comp = v;
+      else a.st->kkt_dot = v;
+    }
+  }
   return true;
 }
 
@@ -875,10 +972,10 @@ __global__ void __launch_bounds__(kResThreads, 1) lsqr_resident_kernel(LsqrArgs 
   int itn = 0, istop = 0;
   if (mode != 0) {
     if (lsqr_iterate_resident(a, grid, mode, f, red, &bcast, wsum, itn, istop)) {
-      grid.sync();  // X of every slice -> the output pass
-    } else {
-      lsqr_iterate_global(a, grid, mode, f, red, &bcast, itn, istop);
+      LG_MARK(3);  // (x and the report done from the slices)
+      return;
     }
+    lsqr_iterate_global(a, grid, mode, f, red, &bcast, itn, istop);
   }
   LG_MARK(2);
   lsqr_finish(a, grid, mode, f, itn, istop, red, &bcast);

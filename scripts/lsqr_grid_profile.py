@@ -40,4 +40,7 @@ if m[0] > 0:
     print("kernel: setup %.1f us, to loop end %.1f us, finish %.1f us, total %.1f us" % (
         (m[1] - m[0]) / 1e3 if m[1] > 0 else float("nan"), (m[2] - m[0]) / 1e3 if m[2] > 0 else float("nan"),
         (m[3] - m[2]) / 1e3 if m[2] > 0 else float("nan"), (m[3] - m[0]) / 1e3))
+if m[4] > 0:
+    print("finish: x out %.1f us, R = Ax-b %.1f us, y' = A^T R %.1f us, reduce %.1f us" % (
+        (m[4] - m[2]) / 1e3, (m[5] - m[4]) / 1e3, (m[6] - m[5]) / 1e3, (m[3] - m[6]) / 1e3))
 print("per iteration", np.mean([(p[r + 1, 0] - p[r, 0]) / 1e3 for r in rows]), "us; lsqr_iterations", info["lsqr_iterations"])
