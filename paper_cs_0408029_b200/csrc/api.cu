@@ -649,7 +649,7 @@ cudaError_t launch_iteration(nnls_handle* h, cudaStream_t s, const cudaGraphCond
   TraceRec* trace = h->trace_cap > 0 ? P<TraceRec>(h->trace) : nullptr;
   cudaError_t e = launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
                                 P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s, loop,
-                                pos_or_null(h), fs_or_null(h));
+                                pos_or_null(h), fs_or_null(h), xs_or_null(h));
   if (e == cudaSuccess)
     e = launch_chol_factor(n, G, h->ldg, c, P<int32_t>(h->Fidx), P<double>(h->Lt), P<int>(h->flags), st,
                            h->sms, s);
@@ -815,7 +815,7 @@ nnls_status nnls_solve(nnls_handle* h, double* x_out, nnls_info* info) {
       TIMED(NNLS_PH_DECIDE, 1,
             launch_decide(n, P<uint8_t>(h->mask), P<double>(h->x), P<double>(h->y),
                           P<int32_t>(h->Fidx), P<int32_t>(h->Gidx), st, trace, h->trace_cap, s, nullptr,
-                          pos_or_null(h), fs_or_null(h)));
+                          pos_or_null(h), fs_or_null(h), xs_or_null(h)));
       nnls_status rs = read_state(h);
       if (rs != NNLS_OK) return rs;
       const DevState& hs = h->h->st;

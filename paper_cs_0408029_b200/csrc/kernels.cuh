@@ -78,7 +78,7 @@ cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double
 cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
                           int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
                           cudaStream_t s, const cudaGraphConditionalHandle* loop = nullptr,
-                          int32_t* pos = nullptr, int32_t* Fs = nullptr);
+                          int32_t* pos = nullptr, int32_t* Fs = nullptr, double* xs = nullptr);
 cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t* Fidx,
                            int32_t* Gidx, double* xF, DevState* st, cudaStream_t s);
 // y_G = G_GF x_F - c_G (Gram form of Eq. 5), zeroing, scatter x_F into x.

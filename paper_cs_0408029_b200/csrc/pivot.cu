@@ -204,7 +204,8 @@ constexpr size_t kTailSortSmem = sizeof(typename TailSort<kOrderMax / kDecideThr
 __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const double* __restrict__ x,
                                const double* __restrict__ y, int32_t* __restrict__ pos,
                                int32_t* __restrict__ Fidx, int32_t* __restrict__ Gidx,
-                               int32_t* __restrict__ Fs, int fprev, int* s_wF, int* s_wG, int* s_wS,
+                               int32_t* __restrict__ Fs, double* __restrict__ xs, int fprev, int* s_wF,
+                               int* s_wG, int* s_wS,
                                int* s_cnt, int* s_f, int* s_g, int* s_s, int* s_q, int* s_old,
                                void* sort_smem) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -318,6 +319,7 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
       if ((fG >> e) & 1u) {
         Gidx[oG++] = i;
         pos[i] = -1;
+        if (xs != nullptr) xs[i] = 0.0;  // (the dual streams whole G rows against xs: zero off F)
       }
     }
     __syncthreads();
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
     int n, uint8_t* __restrict__ mask, const double* __restrict__ x,
     const double* __restrict__ y, int32_t* __restrict__ Fidx, int32_t* __restrict__ Gidx,
     DevState* st, TraceRec* trace, int trace_cap, cudaGraphConditionalHandle loop, int use_loop,
-    int32_t* pos, int32_t* Fs) {
+    int32_t* pos, int32_t* Fs, double* xs) {
   extern __shared__ __align__(16) unsigned char s_sort[];  // (pos != nullptr) the tail sort's storage
   pdl_wait();
   __shared__ int s_cnt[32], s_max[32];
@@ -460,8 +462,8 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(
   if (pos == nullptr) {
     block_compact(n, mask, Fidx, Gidx, s_wF, s_wG, s_cnt, &s_carryF, &s_carryG);
   } else {
-    order_free_set(n, mask, x, y, pos, Fidx, Gidx, Fs, s_fprev, s_wF, s_wG, s_wS, s_cnt, &s_carryF, &s_carryG,
-                   &s_carryS, &s_q, &s_old, s_sort);
+    order_free_set(n, mask, x, y, pos, Fidx, Gidx, Fs, xs, s_fprev, s_wF, s_wG, s_wS, s_cnt, &s_carryF,
+                   &s_carryG, &s_carryS, &s_q, &s_old, s_sort);
   }
   if (tid == 0) {
     const int f = s_carryF;
@@ -523,14 +525,14 @@ cudaError_t launch_compact(int n, const uint8_t* mask, const double* x, int32_t*
 cudaError_t launch_decide(int n, uint8_t* mask, const double* x, const double* y, int32_t* Fidx,
                           int32_t* Gidx, DevState* st, TraceRec* trace, int trace_cap,
                           cudaStream_t s, const cudaGraphConditionalHandle* loop, int32_t* pos,
-                          int32_t* Fs) {
+                          int32_t* Fs, double* xs) {
   const size_t smem = pos != nullptr ? kTailSortSmem : 0;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   return launch_pdl(decide_kernel, dim3(1), dim3(kDecideThreads), smem, s, n, mask, x, y, Fidx, Gidx, st, trace,
-                    trace_cap, loop ? *loop : cudaGraphConditionalHandle{}, loop ? 1 : 0, pos, Fs);
+                    trace_cap, loop ? *loop : cudaGraphConditionalHandle{}, loop ? 1 : 0, pos, Fs, xs);
   return cudaGetLastError();
 }
 
@@ -575,29 +577,26 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
   // Before waiting for the back substitution (PDL: it lets this grid start
   // once it runs): gather this warp's first G row entries G[j, F] into
   // registers -- G, F and the sets come from earlier kernels (decide).
-  constexpr int PF = 16;  // prefetched entries per lane (f <= 512: the whole row)
+  // With the factor-reuse views (Fs, xs: x_F scattered by index, zero on G
+  // -- decide zeroes the G entries, the back substitution writes F), row j
+  // of G is streamed WHOLE with 16-byte loads against xs: the same DRAM
+  // sectors as gathering its F entries (about two of the four doubles of
+  // every sector are in F), read in order; the G terms add exact zeros.
+  constexpr int PF = 8;  // prefetched double2 per lane
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int f = st->f, g = st->g;
+  const int n2 = n >> 1;
   const bool pre = Fs != nullptr && !st->done && gwarp < g;
-  double pg[PF];
-  int pi[PF];
+  double2 pg[PF];
 #pragma unroll
-  for (int k = 0; k < PF; ++k) {
-    pi[k] = 0;
-    pg[k] = 0.0;
-  }
+  for (int k = 0; k < PF; ++k) pg[k] = make_double2(0.0, 0.0);
   if (pre) {
-    const double* Gj = G + (size_t)Gidx[gwarp] * ldg;
+    const double2* G2 = reinterpret_cast<const double2*>(G + (size_t)Gidx[gwarp] * ldg);
 #pragma unroll
-    for (int k = 0; k < PF; ++k) {
-      const int a = lane + 32 * k;
-      if (a < f) {
-        pi[k] = __ldg(&Fs[a]);
-        pg[k] = Gj[pi[k]];
-      }
-    }
+    for (int k = 0; k < PF; ++k)
+      if (lane + 32 * k < n2) pg[k] = __ldcs(&G2[lane + 32 * k]);
   }
   pdl_wait();
   const int status = st->status;
@@ -609,25 +608,18 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
     return;
   }
   if (st->done) return;
-  // the prefetched entries, in the loop's own order (then dead)
-  double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-  int pa = lane;
+  const double2* __restrict__ X2 = reinterpret_cast<const double2*>(xs);
+  // the prefetched entries (then dead)
+  double p0 = 0.0, p1 = 0.0;
   if (pre) {
 #pragma unroll
-    for (int k = 0; k < PF; k += 4) {
-      const int a0 = lane + 32 * k;
-      if (a0 + 96 < f) {
-        p0 = fma(pg[k], xs[pi[k]], p0);
-        p1 = fma(pg[k + 1], xs[pi[k + 1]], p1);
-        p2 = fma(pg[k + 2], xs[pi[k + 2]], p2);
-        p3 = fma(pg[k + 3], xs[pi[k + 3]], p3);
-      } else {  // the tail (p0), then nothing is left
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (a0 + 32 * q < f) p0 = fma(pg[k + q], xs[pi[k + q]], p0);
+    for (int k = 0; k < PF; ++k) {
+      if (lane + 32 * k < n2) {
+        const double2 xv = __ldg(&X2[lane + 32 * k]);
+        p0 = fma(pg[k].x, xv.x, p0);
+        p1 = fma(pg[k].y, xv.y, p1);
       }
     }
-    pa = (lane + 32 * (PF - 4) + 96 < f) ? lane + 32 * PF : f;  // (continue after a full last group)
   }
   double below = 0.0, above = INFINITY;
   for (int jj = gwarp; jj < g; jj += nwarps) {
@@ -640,25 +632,35 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int a = lane;
     if (Fs != nullptr) {
+      const double2* __restrict__ G2 = reinterpret_cast<const double2*>(Gj);
+      int t = lane;
       if (jj == gwarp && pre) {
         s0 = p0;
         s1 = p1;
-        s2 = p2;
-        s3 = p3;
-        a = pa;
+        t = lane + 32 * PF;
       }
-#pragma unroll 4
-      for (; a + 96 < f; a += 128) {
-        const int i0 = __ldg(&Fs[a]), i1 = __ldg(&Fs[a + 32]), i2 = __ldg(&Fs[a + 64]), i3 = __ldg(&Fs[a + 96]);
-        s0 = fma(Gj[i0], xs[i0], s0);
-        s1 = fma(Gj[i1], xs[i1], s1);
-        s2 = fma(Gj[i2], xs[i2], s2);
-        s3 = fma(Gj[i3], xs[i3], s3);
+      // eight 16-byte loads of the row in flight per lane (a warp streams a
+      // whole 64 KB row: its memory-level parallelism sets the pace)
+      for (; t + 32 * 7 < n2; t += 32 * 8) {
+        double2 gv[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) gv[u] = __ldcs(&G2[t + 32 * u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = __ldg(&X2[t + 32 * u]);
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          s0 = fma(gv[u].x, xv[u].x, s0);
+          s1 = fma(gv[u].y, xv[u].y, s1);
+          s2 = fma(gv[u + 1].x, xv[u + 1].x, s2);
+          s3 = fma(gv[u + 1].y, xv[u + 1].y, s3);
+        }
       }
-      for (; a < f; a += 32) {
-        const int i = __ldg(&Fs[a]);
-        s0 = fma(Gj[i], xs[i], s0);
+      for (; t < n2; t += 32) {
+        const double2 g0 = __ldcs(&G2[t]), x0 = __ldg(&X2[t]);
+        s0 = fma(g0.x, x0.x, s0);
+        s1 = fma(g0.y, x0.y, s1);
       }
+      if ((n & 1) && lane == 0) s0 = fma(Gj[n - 1], xs[n - 1], s0);
     } else {
       for (; a + 96 < f; a += 128) {
         const int i0 = __ldg(&Fidx[a]), i1 = __ldg(&Fidx[a + 32]), i2 = __ldg(&Fidx[a + 64]), i3 = __ldg(&Fidx[a + 96]);
