@@ -213,15 +213,16 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
   // sweep), its (mask, pos) held in registers from (1) to (2): one block
   // reduction and one block scan per sweep instead of per 1024 indices.
   constexpr int kE = 8;
-  const int span = kE * (int)blockDim.x;
+  const int E = min(kE, max(1, (n + (int)blockDim.x - 1) / (int)blockDim.x));
+  const int span = E * (int)blockDim.x;
   // (1) q = first position of the previous order whose member left F
   int qloc = fprev;
   for (int base = 0; base < n; base += span) {
-    const int i0 = base + kE * tid;
+    const int i0 = base + E * tid;
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
       const int i = i0 + e;
-      if (i < n) {
+      if (e < E && i < n) {
         const int pi = pos[i];
         if (pi >= 0 && !mask[i]) qloc = min(qloc, pi);
       }
@@ -248,13 +249,13 @@ __device__ void order_free_set(int n, const uint8_t* __restrict__ mask, const do
   // (2) the tail R = F minus the prefix -> Fidx[q..) in index order; G ->
   // Gidx, F -> Fs (both in index order)
   for (int base = 0; base < n; base += span) {
-    const int i0 = base + kE * tid;
+    const int i0 = base + E * tid;
     unsigned fR = 0u, fG = 0u, fS = 0u;
     int cR = 0, cG = 0, cS = 0, cO = 0;
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
       const int i = i0 + e;
-      if (i < n) {
+      if (e < E && i < n) {
         const bool inF = mask[i] != 0;
         const int pi = pos[i];
         const bool inR = inF && !(pi >= 0 && pi < q);
@@ -588,7 +589,10 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int f = st->f, g = st->g;
   const int n2 = n >> 1;
-  const bool pre = Fs != nullptr && !st->done && gwarp < g;
+  // (dense rows only when G streams from DRAM: for a small, L2-resident G the
+  // F-entry gathers read half the bytes -- config 1: 43 vs 61 us)
+  const bool dense = Fs != nullptr && n >= 2048;
+  const bool pre = dense && !st->done && gwarp < g;
   double2 pg[PF];
 #pragma unroll
   for (int k = 0; k < PF; ++k) pg[k] = make_double2(0.0, 0.0);
@@ -597,6 +601,27 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
 #pragma unroll
     for (int k = 0; k < PF; ++k)
       if (lane + 32 * k < n2) pg[k] = __ldcs(&G2[lane + 32 * k]);
+  }
+  // (sparse rows: the first row's F entries G[j, Fs[a]] gathered ahead instead)
+  constexpr int PS = 16;
+  const bool pres = Fs != nullptr && !dense && !st->done && gwarp < g;
+  double ps[PS];
+  int pi[PS];
+#pragma unroll
+  for (int k = 0; k < PS; ++k) {
+    pi[k] = 0;
+    ps[k] = 0.0;
+  }
+  if (pres) {
+    const double* Gj = G + (size_t)Gidx[gwarp] * ldg;
+#pragma unroll
+    for (int k = 0; k < PS; ++k) {
+      const int a = lane + 32 * k;
+      if (a < f) {
+        pi[k] = __ldg(&Fs[a]);
+        ps[k] = Gj[pi[k]];
+      }
+    }
   }
   pdl_wait();
   const int status = st->status;
@@ -610,7 +635,25 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
   if (st->done) return;
   const double2* __restrict__ X2 = reinterpret_cast<const double2*>(xs);
   // the prefetched entries (then dead)
-  double p0 = 0.0, p1 = 0.0;
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+  int pa = lane;
+  if (pres) {
+#pragma unroll
+    for (int k = 0; k < PS; k += 4) {
+      const int a0 = lane + 32 * k;
+      if (a0 + 96 < f) {
+        p0 = fma(ps[k], xs[pi[k]], p0);
+        p1 = fma(ps[k + 1], xs[pi[k + 1]], p1);
+        p2 = fma(ps[k + 2], xs[pi[k + 2]], p2);
+        p3 = fma(ps[k + 3], xs[pi[k + 3]], p3);
+      } else {  // the tail (p0), then nothing is left
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (a0 + 32 * q < f) p0 = fma(ps[k + q], xs[pi[k + q]], p0);
+      }
+    }
+    pa = (lane + 32 * (PS - 4) + 96 < f) ? lane + 32 * PS : f;  // (continue after a full last group)
+  }
   if (pre) {
 #pragma unroll
     for (int k = 0; k < PF; ++k) {
@@ -631,7 +674,7 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
     // index order (Fs) with x_F scattered to xs, so G_j is read in order.
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int a = lane;
-    if (Fs != nullptr) {
+    if (dense) {
       const double2* __restrict__ G2 = reinterpret_cast<const double2*>(Gj);
       int t = lane;
       if (jj == gwarp && pre) {
@@ -661,6 +704,26 @@ __global__ void __launch_bounds__(kDualThreads) dual_kernel(
         s1 = fma(g0.y, x0.y, s1);
       }
       if ((n & 1) && lane == 0) s0 = fma(Gj[n - 1], xs[n - 1], s0);
+    } else if (Fs != nullptr) {  // F in index order (Fs) against x scattered to xs: G_j read in order
+      if (jj == gwarp && pres) {
+        s0 = p0;
+        s1 = p1;
+        s2 = p2;
+        s3 = p3;
+        a = pa;
+      }
+#pragma unroll 4
+      for (; a + 96 < f; a += 128) {
+        const int i0 = __ldg(&Fs[a]), i1 = __ldg(&Fs[a + 32]), i2 = __ldg(&Fs[a + 64]), i3 = __ldg(&Fs[a + 96]);
+        s0 = fma(Gj[i0], xs[i0], s0);
+        s1 = fma(Gj[i1], xs[i1], s1);
+        s2 = fma(Gj[i2], xs[i2], s2);
+        s3 = fma(Gj[i3], xs[i3], s3);
+      }
+      for (; a < f; a += 32) {
+        const int i = __ldg(&Fs[a]);
+        s0 = fma(Gj[i], xs[i], s0);
+      }
     } else {
       for (; a + 96 < f; a += 128) {
         const int i0 = __ldg(&Fidx[a]), i1 = __ldg(&Fidx[a + 32]), i2 = __ldg(&Fidx[a + 64]), i3 = __ldg(&Fidx[a + 96]);
