@@ -144,6 +144,7 @@ struct LsqrArgs {
   const int32_t* Fidx;  // the final F (f entries; from the last decide)
   const int32_t* Gidx;  // the final G (n - f entries, index order; the resident report)
   const int* plan;      // cluster slice plan (lsqr_plan_kernel: maxima, row bounds, column bounds)
+  int res_cap;          // resident LSQR: slice budget override in bytes (0: the kernel's maximum)
 };
 cudaError_t launch_lsqr_compact(const LsqrArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s);

@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -552,7 +553,8 @@ __device__ bool lsqr_iterate_resident(const LsqrArgs& a, cg::grid_group& grid, i
   if (tid == 0) a.partials[bid * kSlots + 7] = (double)need;
   grid.sync();
   const bool fits = (long long)G * f <= (long long)a.rowptr[m] && R < (1 << 30);
-  if (!fits || grid_total(a.partials, 7, bcast, 2) > (double)kResSmem) return false;
+  const double cap = (a.res_cap > 0 && a.res_cap < kResSmem) ? (double)a.res_cap : (double)kResSmem;
+  if (!fits || grid_total(a.partials, 7, bcast, 2) > cap) return false;
   double* vs = reinterpret_cast<double*>(rsm);
   double* ul = reinterpret_cast<double*>(rsm + o_ul);
   double* Vo = reinterpret_cast<double*>(rsm + o_vo);
@@ -985,10 +987,12 @@ __global__ void __launch_bounds__(kResThreads, 1) lsqr_resident_kernel(LsqrArgs 
 cudaError_t launch_lsqr_final(const LsqrArgs& a, int sm_count, cudaStream_t s) {
   LsqrArgs args = a;
   void* params[] = {&args};
-  static const bool no_res = [] {
-    const char* v = getenv("NNLS_NO_RESIDENT_LSQR");
-    return v != nullptr && v[0] != 0 && v[0] != '0';
-  }();
+  // (read per launch: a handle captures its solve graph once, so a test can
+  // select the path per handle)
+  const char* ev = getenv("NNLS_NO_RESIDENT_LSQR");
+  const bool no_res = ev != nullptr && ev[0] != 0 && ev[0] != '0';
+  const char* cv = getenv("NNLS_RESIDENT_CAP");  // shared-memory budget of the slices (bytes; test hook)
+  args.res_cap = (cv != nullptr && cv[0] != 0) ? atoi(cv) : 0;
   if (!no_res) {
     static DeviceOnce once;
     const int ok = device_once(once, [] {

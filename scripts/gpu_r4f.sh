@@ -1,0 +1,10 @@
+set -u
+O=gpurun_out/r4f
+mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+for c in 1 3 2 2; do
+timeout 300 python bench.py --config $c --no-extra --no-cpu-baseline --no-e2e --steps 20 > $O/bench_c$c.json 2> $O/bench_c$c.err
+python -c "
+import json; d=json.load(open('$O/bench_c$c.json')); print('c$c', d['value'], d['ms_per_step'], d['phase_ms_per_step']['dual'], d['phase_ms_per_step']['chol_solve'], d['phase_ms_per_step']['decide'], d['phase_ms_per_step']['csc'])" >> $O/summary.txt
+done
+echo done

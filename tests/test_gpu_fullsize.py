@@ -129,3 +129,50 @@ def test_config2_oracle_parity(P, seed):
     assert np.abs(np.asarray(x) - xo).max() <= 1e-9 * np.abs(xo).max()
     assert np.abs(S.x_ne() - xne).max() <= 1e-9 * np.abs(xne).max()
     assert abs(info["objective"] - float(gold["objective"])) <= 1e-9 * float(gold["objective"])
+
+
+# ------------------------------------- config 2: the alternative device paths
+def _golden_check(S, x, info, seed=0):
+    gold = np.load(os.path.join(GOLDEN, f"config2_seed{seed}.npz"))
+    mask_or = np.unpackbits(gold["mask_bits"])[: S.n]
+    assert info["status"] == 0
+    assert np.array_equal(S.free_set().astype(np.uint8), mask_or)
+    assert info["iterations"] == int(gold["iterations"])
+    xo = gold["x"]
+    assert np.abs(np.asarray(x) - xo).max() <= 1e-9 * np.abs(xo).max()
+    assert abs(info["objective"] - float(gold["objective"])) <= 1e-9 * float(gold["objective"])
+    assert info["kkt_min_x"] >= 0.0
+
+
+@pytest.mark.parametrize("path", ["resident", "resident_fallback", "global"])
+def test_config2_lsqr_paths(P, path, monkeypatch):
+    """Config 2's final LSQR runs on the grid-resident kernel (row slices of
+    A_F in shared memory); the same kernel's in-kernel fallback when the
+    slices exceed the budget (forced by NNLS_RESIDENT_CAP) and the
+    global-memory kernel (NNLS_NO_RESIDENT_LSQR) must reach the same x
+    within the north_star bar, with the same report."""
+    if path == "resident_fallback":
+        monkeypatch.setenv("NNLS_RESIDENT_CAP", "1024")
+    elif path == "global":
+        monkeypatch.setenv("NNLS_NO_RESIDENT_LSQR", "1")
+    prob = g.make_problem(2, 0)
+    S = P.setup(prob)
+    x, info = S.solve()
+    _golden_check(S, x, info)
+    assert 20 <= info["lsqr_iterations"] <= 60
+
+
+def test_config2_csc_scatter_path(P, monkeypatch):
+    """From 1M entries the CSC is built by a stable radix sort on the column;
+    the atomic scatter + rank path (NNLS_NO_SORT_CSC) must give the same CSC:
+    the exact Gram bitwise on sampled rows, and the same solve."""
+    prob = g.make_problem(2, 0)
+    S1 = P.setup(prob)
+    monkeypatch.setenv("NNLS_NO_SORT_CSC", "1")
+    S2 = P.setup(prob)
+    G1, c1 = S1.gram()
+    G2, c2 = S2.gram()
+    rows = np.random.default_rng(0).choice(prob.n, 64, replace=False)
+    assert np.array_equal(G1[rows], G2[rows]) and np.array_equal(c1, c2)
+    x, info = S2.solve()
+    _golden_check(S2, x, info)
