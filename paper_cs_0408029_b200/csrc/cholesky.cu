@@ -899,6 +899,7 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
     double* Tm = smem + 3 * (T * LDS);    // trtri scratch
     int first_bad = -1;
     int* pending = nullptr;  // (tid 224) flag of the last stored sub tile, not yet released
+    int* pending2 = nullptr; // (tid 224) the last L_jj's flag, not yet released
     for (int e = tid; e < T * T; e += kThreads)  // Linv's strict upper part, never written
       if ((e % T) > (e / T)) Xinv[(e / T) * LDS + (e % T)] = 0.0;
     for (int j = jq; j < ntc; ++j) {
@@ -926,8 +927,9 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
       if ((tid >> 5) == 7) {
         // ---- warp 7: release the pending flag, then prefetch both partials
         const int lane = tid & 31;
-        if (pending != nullptr && lane == 0) bulk_store_release(pending, epoch);
+        if (pending != nullptr && lane == 0) bulk_store_release(pending, epoch, pending2);
         pending = nullptr;
+        pending2 = nullptr;
         int want = (has_sub ? 1 : 0) | (has_next ? 2 : 0);
         while (want) {
           int ok = 0;
@@ -968,24 +970,28 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
         // Linv_jj: the sub-diagonal TRSMs become products, and the back
         // substitution uses it (trtri64 fences Xinv for its bulk store)
         trtri64<7>(Xinv, Sd, rinv, cv, Tm, j);
+        // Linv_jj out with plain stores (the helpers' T(i,j) tasks wait for it:
+        // released right after the barrier below, no bulk-store drain on the path)
+        for (int e = tid; e < T * T / 2; e += kThreads - 32) {
+          const int o = ((2 * e) / T) * LDS + (2 * e) % T;
+          *reinterpret_cast<double2*>(Linv + (size_t)j * TS + o) = *reinterpret_cast<const double2*>(Xinv + o);
+        }
         PROF_STAMP(j, 3);
       }
-      csync();  // L_jj, Linv_jj done; partials in smem
+      csync();  // L_jj, Linv_jj done (Linv_jj stored); partials in smem
       const int lane = tid & 31, w = tid >> 5;
       PROF_STAMP(j, 2);
       if (tid == kThreads - 32) {
-        bulk_store_tile(Lt + (size_t)tidx(j, j) * TS, Sd);
-        bulk_store_tile(Linv + (size_t)j * TS, Xinv);
+        st_release(&F.inv[j], epoch);
+        bulk_store_tile(Lt + (size_t)tidx(j, j) * TS, Sd);  // (released late: only the back substitution reads L_jj)
       }
       if (!has_sub) {  // last column without a sub-diagonal tile
-        if (tid == kThreads - 32) bulk_store_release(&F.inv[j], epoch, &F.full[tidx(j, j)]);
+        if (tid == kThreads - 32) bulk_store_release(&F.full[tidx(j, j)], epoch);
         break;
       }
-      {  // L(j+1,j) = A(j+1,j) L_jj^-T = A(j+1,j) Linv_jj^T; then warp 7
-         // releases L_jj and Linv_jj (their bulk stores drained meanwhile)
+      {  // L(j+1,j) = A(j+1,j) L_jj^-T = A(j+1,j) Linv_jj^T
         double acc[8][2];
         gemm_linvT(acc, Lnext, Xinv, w, lane);
-        if (tid == kThreads - 32) bulk_store_release(&F.inv[j], epoch, &F.full[tidx(j, j)]);
         csync();
         store_rows8(acc, Lnext, w, lane);
       }
@@ -995,9 +1001,10 @@ __global__ void __launch_bounds__(kHelperThreads, 1) chol_factor_kernel(
       if (tid == kThreads - 32) bulk_store_tile(Lt + (size_t)tidx(j + 1, j) * TS, Lnext);
       // (A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T is applied inside the next POTRF)
       pending = &F.full[tidx(j + 1, j)];  // released by warp 7 in the next POTRF (or below)
+      pending2 = &F.full[tidx(j, j)];     // (L_jj: its bulk store drains meanwhile)
       PROF_STAMP(j, 5);
     }
-    if (pending != nullptr && tid == kThreads - 32) bulk_store_release(pending, epoch);  // last sub tile
+    if (pending != nullptr && tid == kThreads - 32) bulk_store_release(pending, epoch, pending2);  // last sub tile
     // NOT_PD is raised only after the whole chain ran: helpers read the status
     // at entry, and a helper that left early must not strand the chain
     if (tid == 0 && first_bad >= 0) {
