@@ -676,7 +676,14 @@ __device__ bool lsqr_iterate_resident(const LsqrArgs& a, cg::grid_group& grid, i
       const int c = idx % C, h = idx / C;
       const int b1 = (int)((long long)G * (h + 1) / nch);
       double s = 0.0;
-      for (int b = (int)((long long)G * h / nch); b < b1; ++b) s += __ldcg(&part[(size_t)b * f + k0 + c]);
+      for (int b = (int)((long long)G * h / nch); b < b1; b += 8) {  // eight loads in flight, summed in order
+        double pv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pv[u] = b + u < b1 ? __ldcg(&part[(size_t)(b + u) * f + k0 + c]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (b + u < b1) s += pv[u];
+      }
       cs[idx] = s;
     }
     __syncthreads();
