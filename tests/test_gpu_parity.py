@@ -697,3 +697,13 @@ def test_dense_gram_row_shard_packed(P):
         buf = gram_tensor(S).cpu().numpy()
         Gb, cb = O.gram(g.Problem(r1 - r0, n, rp, ci, v, b, prob.x_gen, prob.kind, prob.seed))
         assert np.array_equal(buf[:n * (n + 1) // 2], Gb[tril]) and np.array_equal(buf[n * (n + 1) // 2:], cb)
+
+
+@pytest.mark.parametrize("shape", [dict(m=30000, n=3001, density=0.003), dict(m=12000, n=2049, density=0.01)])
+def test_large_odd_shapes(P, shape):
+    """Shapes beyond one cluster's shared memory with an odd n >= 2048: the
+    grid-resident LSQR (row slices of A_F in every SM), the dual streaming
+    whole G rows (16-byte loads plus the odd last column), ragged Cholesky
+    tiles and factor reuse -- F, the iteration count and the trace identical
+    to the oracle, x within the north_star bar."""
+    assert_parity(P, g.make_problem(shape, seed=7))
