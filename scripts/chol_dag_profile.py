@@ -83,14 +83,14 @@ for j in [jj for jj in (1, 2, 3, 30, 50) if jj < len(p)]:
                                      str(pp[j][2][k] - pp[j][0][k]) if pp[j][2][k] > 0 else "-"))
     print("  j=%d total %d  " % (j, pp[j][1][7] - pp[j][3][0]) + "  ".join(row))
 # back substitution chain (rows 900+J, slot 0): x_J computed on the chain CTA
-bs = allp[900:900 + 200, 0]
+bs = allp[900:900 + 100, 0]
 idx = np.flatnonzero(bs > 0)
 if idx.size:
     t = bs[idx]
     order = np.argsort(t)
     print("backsolve chain: x_J done at (us from the first):",
           " ".join("J%d:%.2f" % (idx[k], (t[k] - t.min()) / 1e3) for k in order))
-    full = allp[900:900 + 200]
+    full = allp[900:900 + 100]
     t0 = t.min()
     print("  J   N armed   a_J in   x_J done   x_J published (us)")
     for k in order:
