@@ -275,12 +275,28 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
   if (cap > 0) CK(ensure(h->trace, sizeof(TraceRec) * (size_t)cap));
 
   int ib = tm_begin(h);
-  CK(cudaMemcpyAsync(h->rowptr.p, rowptr, sizeof(int32_t) * (size_t)(m + 1), cudaMemcpyDefault, s));
-  if (nnz > 0) {
-    CK(cudaMemcpyAsync(h->colind.p, colind, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDefault, s));
-    CK(cudaMemcpyAsync(h->vals.p, vals, sizeof(double) * (size_t)nnz, cudaMemcpyDefault, s));
+  // device-resident inputs: one copy kernel; otherwise (host memory) the copy engines
+  bool all_dev = true;
+  for (const void* ptr : {(const void*)rowptr, (const void*)colind, (const void*)vals, (const void*)b}) {
+    cudaPointerAttributes pa;
+    if (ptr == nullptr) continue;
+    if (cudaPointerGetAttributes(&pa, ptr) != cudaSuccess || pa.type != cudaMemoryTypeDevice) all_dev = false;
+    cudaGetLastError();
   }
-  CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)m, cudaMemcpyDefault, s));
+  if (all_dev) {
+    const void* src[4] = {rowptr, colind, vals, b};
+    void* dst[4] = {h->rowptr.p, h->colind.p, h->vals.p, h->b.p};
+    const size_t by[4] = {sizeof(int32_t) * (size_t)(m + 1), nnz > 0 ? sizeof(int32_t) * (size_t)nnz : 0,
+                          nnz > 0 ? sizeof(double) * (size_t)nnz : 0, sizeof(double) * (size_t)m};
+    CK(launch_upload_copy(src, dst, by, h->sms, s));
+  } else {
+    CK(cudaMemcpyAsync(h->rowptr.p, rowptr, sizeof(int32_t) * (size_t)(m + 1), cudaMemcpyDefault, s));
+    if (nnz > 0) {
+      CK(cudaMemcpyAsync(h->colind.p, colind, sizeof(int32_t) * (size_t)nnz, cudaMemcpyDefault, s));
+      CK(cudaMemcpyAsync(h->vals.p, vals, sizeof(double) * (size_t)nnz, cudaMemcpyDefault, s));
+    }
+    CK(cudaMemcpyAsync(h->b.p, b, sizeof(double) * (size_t)m, cudaMemcpyDefault, s));
+  }
   CK(cudaMemsetAsync(h->err.p, 0, sizeof(int) * 64, s));
   tm_end(h, NNLS_PH_UPLOAD, ib, 0);
   TIMED(NNLS_PH_VALIDATE, 1,

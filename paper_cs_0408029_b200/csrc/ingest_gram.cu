@@ -290,6 +290,50 @@ cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* 
   return cudaGetLastError();
 }
 
+// Device-to-device input upload in ONE launch (rowptr, colind, vals, b as
+// four segments of a grid-stride copy, 16-byte moves where both sides are
+// aligned) instead of four cudaMemcpyAsync calls.
+struct CopySeg {
+  const char* src;
+  char* dst;
+  size_t bytes;
+};
+__global__ void __launch_bounds__(256) upload_copy_kernel(CopySeg s0, CopySeg s1, CopySeg s2, CopySeg s3) {
+  const CopySeg sg[4] = {s0, s1, s2, s3};
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const CopySeg c = sg[q];
+    if (c.bytes == 0) continue;
+    const bool al = ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst)) & 15) == 0;
+    size_t done = 0;
+    if (al) {
+      const size_t n16 = c.bytes / 16;
+      const uint4* sv = reinterpret_cast<const uint4*>(c.src);
+      uint4* dv = reinterpret_cast<uint4*>(c.dst);
+      for (size_t i = tid; i < n16; i += nth) dv[i] = __ldcs(&sv[i]);
+      done = n16 * 16;
+    }
+    for (size_t i = done + tid; i < c.bytes; i += nth) c.dst[i] = c.src[i];
+  }
+}
+cudaError_t launch_upload_copy(const void* const* src, void* const* dst, const size_t* bytes, int sm_count,
+                               cudaStream_t s) {
+  CopySeg g[4];
+  size_t tot = 0;
+  for (int q = 0; q < 4; ++q) {
+    g[q].src = static_cast<const char*>(src[q]);
+    g[q].dst = static_cast<char*>(dst[q]);
+    g[q].bytes = bytes[q];
+    tot += bytes[q];
+  }
+  long long blocks = (long long)((tot / 16 + 255) / 256);
+  if (blocks > (long long)sm_count * 8) blocks = (long long)sm_count * 8;
+  if (blocks < 1) blocks = 1;
+  upload_copy_kernel<<<(int)blocks, 256, 0, s>>>(g[0], g[1], g[2], g[3]);
+  return cudaGetLastError();
+}
+
 // CSR -> CSC as a stable radix sort of the entries by column: the CSR lists
 // them in increasing row order, so a stable sort on the column index leaves
 // each column's rows sorted (the same CSC as the scatter + rank path, in a

@@ -24,6 +24,9 @@ cudaError_t launch_csc_fill(int m, int n, const int32_t* rowptr, const int32_t* 
                             const double* vals, const int32_t* colptr, int32_t* rowind,
                             double* cvals, int32_t* cursor, int32_t* tmp_row, double* tmp_val,
                             cudaStream_t s, int maxcnt = -1);
+// four device-to-device copies (src[q] -> dst[q], bytes[q]) in one launch
+cudaError_t launch_upload_copy(const void* const* src, void* const* dst, const size_t* bytes, int sm_count,
+                               cudaStream_t s);
 // the same CSC by a stable radix sort on the column (CUB): temp_bytes from
 // csc_sort_temp_bytes (0: not available, use launch_csc_fill)
 size_t csc_sort_temp_bytes(int64_t nnz, int n);
