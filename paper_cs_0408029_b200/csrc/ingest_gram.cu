@@ -90,8 +90,96 @@ __global__ void validate_kernel(int m, int n, int64_t nnz, const int32_t* __rest
   if (threadIdx.x < 4 && s_st[threadIdx.x]) atomicMax(err + kErrExp + threadIdx.x, s_st[threadIdx.x]);
 }
 
+// Flat variant for large inputs: the entries are checked by a coalesced
+// pass (range, finiteness, exponent statistics) that also counts every
+// descent colind[t] <= colind[t-1]; the rows are checked by a thread each,
+// which counts the descents that sit at the first entry of a non-empty row
+// (allowed: a new row starts).  Any other descent is an out-of-order or
+// repeated column: the last CTA to finish compares the two counts (err[60],
+// err[61], zeroed with the rest of err) and raises bit 2.
+__global__ void __launch_bounds__(256) validate_flat_kernel(int m, int n, int64_t nnz,
+                                                             const int32_t* __restrict__ rowptr,
+                                                             const int32_t* __restrict__ colind,
+                                                             const double* __restrict__ vals,
+                                                             const double* __restrict__ b, int* err) {
+  __shared__ int s_st[4];
+  __shared__ unsigned long long s_d[2];
+  __shared__ bool s_last;
+  if (threadIdx.x < 4) s_st[threadIdx.x] = 0;
+  if (threadIdx.x < 2) s_d[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  int e_local = 0, maxlen = 0;
+  int hA = 0, lA = 0, hb = 0, lb = 0;
+  unsigned long long dall = 0, dstart = 0;
+  for (int64_t t = tid; t < nnz; t += nth) {  // entries: coalesced
+    const int cidx = colind[t];
+    const double v = vals[t];
+    if (cidx < 0 || cidx >= n) e_local |= 2;
+    if (!isfinite(v)) e_local |= 4;
+    exact_bits(v, hA, lA);
+    if (t > 0 && colind[t - 1] >= cidx) ++dall;
+  }
+  for (int64_t r = tid; r < m; r += nth) {  // rows: a thread each
+    const int64_t lo = rowptr[r], hi = rowptr[r + 1];
+    if (r == 0 && lo != 0) e_local |= 1;
+    if (r == m - 1 && hi != nnz) e_local |= 1;
+    if (hi < lo || lo < 0 || hi > nnz) e_local |= 1;
+    else {
+      if (hi - lo > maxlen) maxlen = (int)min((int64_t)0x7fffffff, hi - lo);
+      if (hi > lo && lo > 0 && colind[lo - 1] >= colind[lo]) ++dstart;
+    }
+    const double bv = b[r];
+    if (!isfinite(bv)) e_local |= 4;
+    exact_bits(bv, hb, lb);
+  }
+  if (e_local) atomicOr(err, e_local);
+  maxlen = warp_max_i(maxlen);
+  if (lane == 0 && maxlen > 0) atomicMax(err + 1, maxlen);  // longest row (LSQR planning)
+  hA = warp_max_i(hA);
+  lA = warp_max_i(lA);
+  hb = warp_max_i(hb);
+  lb = warp_max_i(lb);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dall += __shfl_xor_sync(kFull, dall, o);
+    dstart += __shfl_xor_sync(kFull, dstart, o);
+  }
+  if (lane == 0) {
+    if (hA) atomicMax(&s_st[0], hA);
+    if (lA) atomicMax(&s_st[1], lA);
+    if (hb) atomicMax(&s_st[2], hb);
+    if (lb) atomicMax(&s_st[3], lb);
+    if (dall) atomicAdd(&s_d[0], dall);
+    if (dstart) atomicAdd(&s_d[1], dstart);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && s_st[threadIdx.x]) atomicMax(err + kErrExp + threadIdx.x, s_st[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(err + 60);  // err[60..63]
+    if (s_d[0]) atomicAdd(&d[0], s_d[0]);
+    if (s_d[1]) atomicAdd(&d[1], s_d[1]);
+    __threadfence();
+    s_last = atomicAdd(reinterpret_cast<unsigned*>(err + 59), 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long* d = reinterpret_cast<const unsigned long long*>(err + 60);
+    if (atomicAdd(const_cast<unsigned long long*>(&d[0]), 0ull) != atomicAdd(const_cast<unsigned long long*>(&d[1]), 0ull))
+      atomicOr(err, 2);
+  }
+}
+
 cudaError_t launch_validate(int m, int n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
                             const double* vals, const double* b, int* err, cudaStream_t s) {
+  if (nnz >= (1 << 20)) {  // (large inputs: the flat, coalesced variant)
+    int blocks = (int)((nnz + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    validate_flat_kernel<<<blocks, 256, 0, s>>>(m, n, nnz, rowptr, colind, vals, b, err);
+    return cudaGetLastError();
+  }
   int blocks = (int)((((int64_t)m * 32) + 255) / 256);
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) blocks = 1;

@@ -707,3 +707,30 @@ def test_large_odd_shapes(P, shape):
     tiles and factor reuse -- F, the iteration count and the trace identical
     to the oracle, x within the north_star bar."""
     assert_parity(P, g.make_problem(shape, seed=7))
+
+
+def test_invalid_inputs_large(P):
+    """From 1M entries the CSR is validated by the flat two-count kernel: an
+    out-of-range, a repeated and an out-of-order column inside a row, a
+    descending pair across a row boundary (valid), a non-finite value or b,
+    and a bad rowptr must give the same status codes as the small-input path."""
+    p = g.make_problem(dict(m=40000, n=8000, density=0.004), seed=3)
+    assert p.nnz >= (1 << 20)
+    S = P.Solver()
+    r = int(p.rowptr[20000])  # a row in the middle
+    lo, hi = int(p.rowptr[20000]), int(p.rowptr[20001])
+    assert hi - lo >= 3
+    cases = []
+    bad = p.colind.copy(); bad[lo + 1] = p.n; cases.append((p.rowptr, bad, p.vals, p.b, P.ERR_INDEX))
+    bad = p.colind.copy(); bad[lo + 1] = bad[lo]; cases.append((p.rowptr, bad, p.vals, p.b, P.ERR_INDEX))
+    bad = p.colind.copy(); bad[lo], bad[lo + 1] = bad[lo + 1], bad[lo]; cases.append((p.rowptr, bad, p.vals, p.b, P.ERR_INDEX))
+    v = p.vals.copy(); v[r + 2] = np.inf; cases.append((p.rowptr, p.colind, v, p.b, P.ERR_NONFINITE))
+    bb = p.b.copy(); bb[7] = np.nan; cases.append((p.rowptr, p.colind, p.vals, bb, P.ERR_NONFINITE))
+    rp = p.rowptr.copy(); rp[-1] -= 1; cases.append((rp, p.colind, p.vals, p.b, P.ERR_DIMENSION))
+    for rowptr, colind, vals, b, code in cases:
+        with pytest.raises(P.NNLSError) as e:
+            S.load(p.m, p.n, rowptr, colind, vals, b)
+        assert e.value.status == code
+    S.load_problem(p)  # valid afterwards (descents at row starts are allowed)
+    x, info = S.solve()
+    assert info["status"] == 0 and info["kkt_min_x"] >= 0.0
