@@ -214,8 +214,13 @@ __global__ void colcount_kernel(int64_t nnz, int n, const int32_t* __restrict__ 
   }
 }
 static void launch_colcount(int64_t nnz, int n, const int32_t* colind, int32_t* colptr, cudaStream_t s) {
-  long long b = nnz / (8LL * (n > 0 ? n : 1));  // ~8 entries per bin per CTA
-  if (b > 296) b = 296;
+  // ~8 entries per bin per CTA, but at least ~16K entries per CTA up to one
+  // CTA per SM (config 2: 25 -> 98 CTAs; the flush adds one atomic per
+  // non-empty bin per CTA)
+  long long b = nnz / (8LL * (n > 0 ? n : 1));
+  const long long bmin = nnz / 16384;
+  if (b < bmin) b = bmin;
+  if (b > 148) b = 148;
   if (b < 1) b = 1;
   const size_t smem = n <= kHistMax ? sizeof(int) * (size_t)n : 0;
   colcount_kernel<<<(int)b, 1024, smem, s>>>(nnz, n, colind, colptr);
