@@ -699,6 +699,14 @@ def test_dense_gram_row_shard_packed(P):
         assert np.array_equal(buf[:n * (n + 1) // 2], Gb[tril]) and np.array_equal(buf[n * (n + 1) // 2:], cb)
 
 
+@pytest.mark.parametrize("lsqr_mode", [1, 2, 0])
+def test_large_shape_lsqr_modes(P, lsqr_mode):
+    """The grid-resident LSQR's warm start (mode 2: the correction from the NE
+    x, U = b - A_F x_NE from the row slices) and mode 0 (the NE x, no LSQR:
+    the global report path) at a shape beyond one cluster."""
+    assert_parity(P, g.make_problem(dict(m=30000, n=3001, density=0.003), seed=8), lsqr_mode=lsqr_mode)
+
+
 @pytest.mark.parametrize("shape", [dict(m=30000, n=3001, density=0.003), dict(m=12000, n=2049, density=0.01)])
 def test_large_odd_shapes(P, shape):
     """Shapes beyond one cluster's shared memory with an odd n >= 2048: the
