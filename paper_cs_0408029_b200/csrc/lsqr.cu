@@ -704,7 +704,9 @@ __device__ bool lsqr_iterate_resident(const LsqrArgs& a, cg::grid_group& grid, i
     p += u * u;
   }
   block_partial_sum(p, a.partials, 0, red);  // (its barriers order ul before the partial products)
+  LG_MARK(8);
   grid.sync();                               // every CTA's Fval reads done: part may be written
+  LG_MARK(9);
   partial_AtU();
   grid.sync();
   double beta = sqrt(grid_total(a.partials, 0, bcast, 0));
@@ -741,6 +743,7 @@ __device__ bool lsqr_iterate_resident(const LsqrArgs& a, cg::grid_group& grid, i
   double vscale = 1.0;  // Vo, vs and V hold v unnormalised (v = V vscale), as in lsqr_iterate_global
   if (alpha * beta != 0.0) {
     const int g4 = tid >> 2, s4 = tid & 3, ng4 = nb >> 2;
+    LG_MARK(7);
     for (;;) {
       const bool more = itn < itn_limit;
       LG_STAMP(0);

@@ -43,4 +43,7 @@ if m[0] > 0:
 if m[4] > 0:
     print("finish: x out %.1f us, R = Ax-b %.1f us, y' = A^T R %.1f us, reduce %.1f us" % (
         (m[4] - m[2]) / 1e3, (m[5] - m[4]) / 1e3, (m[6] - m[5]) / 1e3, (m[3] - m[6]) / 1e3))
+if m[7] > 0:
+    print("start: setup end -> first sync arrive %.1f, first sync %.1f, -> loop %.1f us" % (
+        (m[8] - m[1]) / 1e3, (m[9] - m[8]) / 1e3, (m[7] - m[9]) / 1e3))
 print("per iteration", np.mean([(p[r + 1, 0] - p[r, 0]) / 1e3 for r in rows]), "us; lsqr_iterations", info["lsqr_iterations"])
