@@ -176,3 +176,25 @@ def test_config2_csc_scatter_path(P, monkeypatch):
     assert np.array_equal(G1[rows], G2[rows]) and np.array_equal(c1, c2)
     x, info = S2.solve()
     _golden_check(S2, x, info)
+
+
+def test_config2_bitwise_repeatable(P):
+    """Every reduction on the device path has a fixed order (exact integer
+    Gram atomics, per-tile Cholesky tasks with fixed split-K sums, warp sums in
+    the dual, CTA-ordered LSQR partials), so repeated solves -- on one handle
+    and on a fresh one -- must give bitwise identical x, F, trace and report.
+    A race in the flag / mailbox protocols of the factorization, the back
+    substitution or the LSQR would show up here as run-to-run differences."""
+    prob = g.make_problem(2, 1)
+    S = P.setup(prob, trace=1)
+    x0, i0 = S.solve()
+    x0 = np.array(x0)
+    m0, t0 = S.free_set().copy(), [(t["k"], t["branch"], t["f"], t["kept"]) for t in S.trace()]
+    for rep in range(6):
+        Sx = S if rep % 2 == 0 else P.setup(prob, trace=1)
+        x, info = Sx.solve()
+        assert np.array_equal(np.array(x), x0), f"run {rep}: x differs"
+        assert np.array_equal(Sx.free_set(), m0)
+        assert [(t["k"], t["branch"], t["f"], t["kept"]) for t in Sx.trace()] == t0
+        for key in ("iterations", "lsqr_iterations", "objective", "kkt_min_y", "kkt_dot"):
+            assert info[key] == i0[key], key

@@ -742,3 +742,29 @@ def test_invalid_inputs_large(P):
     S.load_problem(p)  # valid afterwards (descents at row starts are allowed)
     x, info = S.solve()
     assert info["status"] == 0 and info["kkt_min_x"] >= 0.0
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_bitwise_repeatable(P, cfg):
+    """Configs 1 and 3 (cluster LSQR, restart chains by half tiles and whole
+    tiles): repeated solves bitwise identical (fixed-order reductions)."""
+    prob = g.make_problem(cfg, 2)
+    x0, i0 = P.setup(prob).solve()
+    x0 = np.array(x0)
+    for _ in range(4):
+        x, info = P.setup(prob).solve()
+        assert np.array_equal(np.array(x), x0)
+        assert info["iterations"] == i0["iterations"] and info["lsqr_iterations"] == i0["lsqr_iterations"]
+
+
+def test_batched_bitwise_repeatable(P):
+    """The batched kernels (per-CTA problems, fixed-order sums): two solves of
+    the same 2048-problem slice, and the pipelined run, bitwise identical."""
+    B = g.make_batch(seed=5, start=0, count=2048)
+    o1 = P.BatchedSolver().load_batch(B).solve()
+    o2 = P.BatchedSolver().load_batch(B).solve()
+    o3 = P.BatchedSolver().run_batch(B)
+    for o in (o2, o3):
+        assert np.array_equal(np.asarray(o["x"]), np.asarray(o1["x"]))
+        assert np.array_equal(np.asarray(o["mask"]), np.asarray(o1["mask"]))
+        assert np.array_equal(o["info"]["iterations"], o1["info"]["iterations"])
