@@ -132,7 +132,7 @@ __device__ long long* g_batch_prof = nullptr;
 
 __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max) {
   long long bp_t = clock64();
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   unsigned char* smb = reinterpret_cast<unsigned char*>(sm);
   const int m = a.m, n = a.n, W = (m + 31) / 32;
   const Lay Ly = layout(m, n, nnz_max);
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
     BP_MARK(0);  // load
     // column view: row bitmasks, counts (block scan), row lists in row order
     for (int r = tid; r < m; r += BT)
-      for (int e = rp[r]; e < rp[r + 1]; ++e) atomicOr(&cm[ci[e] * W + (r >> 5)], 1u << (r & 31));
+      for (int e = rp[r]; e < rp[r + 1]; ++e) atomicOr(&cm[(r >> 5) * n + ci[e]], 1u << (r & 31));
     __syncthreads();
     {
       // each thread owns a contiguous run of columns; block-wide exclusive scan
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
       const int j0 = tid * per, j1 = min(n, j0 + per);
       int run = 0;
       for (int j = j0; j < j1; ++j)
-        for (int q = 0; q < W; ++q) run += __popc(cm[j * W + q]);
+        for (int q = 0; q < W; ++q) run += __popc(cm[q * n + j]);
       int incl = run;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
       int acc = base + incl - run;
       for (int j = j0; j < j1; ++j) {
         co[j] = acc;
-        for (int q = 0; q < W; ++q) acc += __popc(cm[j * W + q]);
+        for (int q = 0; q < W; ++q) acc += __popc(cm[q * n + j]);
       }
       if (tid == BT - 1) co[n] = base + incl;
     }
@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
       for (int e = rp[r]; e < rp[r + 1]; ++e) {
         const int j = ci[e];
         int rank = co[j];
-        for (int q = 0; q < wr; ++q) rank += __popc(cm[j * W + q]);
-        rank += __popc(cm[j * W + wr] & below);
+        for (int q = 0; q < wr; ++q) rank += __popc(cm[q * n + j]);
+        rank += __popc(cm[wr * n + j] & below);
         crow[rank] = (uint8_t)r;
         cpos[rank] = (uint16_t)e;
         rv[rank] = a.vals[e0 + e];  // values in COLUMN order (the Gram reads them by rank)
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
         double sacc = 0.0;
         int ki = co[i], kj = co[j];
         for (int wq = 0; wq < W; ++wq) {
-          const unsigned mi = cm[i * W + wq], mj = cm[j * W + wq];
+          const unsigned mi = cm[wq * n + i], mj = cm[wq * n + j];
           unsigned both = mi & mj;
           while (both) {
             const int bpos = __ffs(both) - 1;
@@ -351,9 +351,12 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
       // left-looking by columns (the oracle's jki order per entry, so the
       // factor is bit-identical) on warp 0 alone (f <= n <= 64: lane owns rows
       // jj+1+lane and jj+33+lane of step jj): in step jj the owner of row
-      // i > jj finishes L(i, jj) with a sequential dot in increasing k; the
-      // owner of row jj+1 then also finishes the next pivot L(jj+1, jj+1) ->
-      // one warp barrier per column, the other warps wait once
+      // i > jj finishes L(i, jj) with a sequential dot in increasing k and
+      // subtracts L(i, jj)^2 from its diagonal entry (the pivot's sum, kept
+      // running in place: the same terms in the same order as the oracle's
+      // dot); the owner of row jj+1 then takes the square root of the now
+      // complete next pivot -> one warp barrier per column, the other warps
+      // wait once
       __syncthreads();  // the gathered L
       if (wid == 0) {
         if (lane == 0) {
@@ -376,11 +379,14 @@ __global__ void __launch_bounds__(BT, 9) batched_kernel(BatchArgs a, int nnz_max
               for (int k = 0; k < jj; ++k) sacc = __dsub_rn(sacc, __dmul_rn(L[ri + k], L[rj + k]));
               sacc = sacc / L[rj + jj];
               L[ri + jj] = sacc;
-              if (i == jj + 1 && i < f) {  // the next pivot
-                double d = L[ri + i];
-                for (int k = 0; k <= jj; ++k) d = __dsub_rn(d, __dmul_rn(L[ri + k], L[ri + k]));
-                if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) atomicMin(&s_bad, i);
-                L[ri + i] = sqrt(d);
+              if (i < f) {  // the pivot's running sum: d_i -= L(i,jj)^2 (increasing k, as the oracle)
+                const double d = __dsub_rn(L[ri + i], __dmul_rn(sacc, sacc));
+                if (i == jj + 1) {  // the next pivot, complete
+                  if (!(d > 0.0) || d < 1e-300 || !isfinite(d)) atomicMin(&s_bad, i);
+                  L[ri + i] = sqrt(d);
+                } else {
+                  L[ri + i] = d;
+                }
               }
             }
           }
