@@ -115,6 +115,7 @@ struct nnls_handle {
   bool no_reuse = false;    // F in index order, no factor reuse across iterations (env NNLS_NO_REUSE)
   bool no_fuse = false;     // separate count/exchange pass in decide (env NNLS_NO_FUSED_DUAL)
   bool no_exact_gram = false;  // always the row-ordered Gram kernel (env NNLS_NO_EXACT_GRAM)
+  int claim_min_n = 2048;  // general values: the CTA-per-row claim-ordered Gram kernel from this n (env NNLS_CLAIM_MIN_N)
   bool no_sort_csc = false;    // CSC by scatter + rank instead of the radix sort (env NNLS_NO_SORT_CSC)
   cudaGraphExec_t gexec = nullptr;
   std::vector<double> gkey;
@@ -363,7 +364,8 @@ nnls_status load_impl(nnls_handle* h, int32_t m, int32_t n, int64_t nnz, const i
     TIMED(NNLS_PH_GRAM, 1,
           launch_gram(m, n, P<int32_t>(h->rowptr), P<int32_t>(h->colind), P<double>(h->vals),
                       P<int32_t>(h->colptr), P<int32_t>(h->rowind), P<double>(h->cvals),
-                      P<double>(h->b), r0, r1, G, ldg, c, h->sms, s, exact, gram_exact_lmin(h->h->err)));
+                      P<double>(h->b), r0, r1, G, ldg, c, h->sms, s, exact, gram_exact_lmin(h->h->err),
+                      n >= h->claim_min_n ? h->h->err[1] : 0, h->h->err[2]));
     h->gram_dense = false;
   }
   h->loaded = true;
@@ -397,6 +399,7 @@ nnls_status create_impl(nnls_handle** out, const nnls_params* p, void* stream) {
   h->no_reuse = env_on("NNLS_NO_REUSE");
   h->no_fuse = env_on("NNLS_NO_FUSED_DUAL");
   h->no_exact_gram = env_on("NNLS_NO_EXACT_GRAM");
+  if (const char* v = getenv("NNLS_CLAIM_MIN_N")) h->claim_min_n = atoi(v);
   h->no_sort_csc = env_on("NNLS_NO_SORT_CSC");
   *out = h;
   return NNLS_OK;

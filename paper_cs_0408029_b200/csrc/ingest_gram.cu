@@ -700,6 +700,161 @@ __global__ void __launch_bounds__(512) gram_exact_kernel(
   }
 }
 
+// Row-ordered Gram for general (inexact) values with the whole CTA on one G
+// row: the ordered kernel above keeps ONE warp per G row (its accumulator row
+// is n doubles of shared memory), so at n = 8000 three warps per SM wait on
+// the A-row gathers.  Here a CTA owns G row i; its 16 warps take 16
+// consecutive contributing A rows r (a batch, in increasing r), one row per
+// warp, all gathers in flight together and the next batch's issued before
+// this one is applied.  The oracle's order only matters between products
+// that land on the SAME j, so the batch's (j, a_ri a_rj) tuples -- tuple
+// index = (row slot, entry), the oracle's order -- are applied in passes:
+// every pending tuple claims tag[j] with a 32-bit shared-memory atomicMax of
+// (epoch, -index); after a barrier the claim's winner (the earliest pending
+// tuple of that j) adds its product, the others stay pending for the next
+// pass.  Distinct j's proceed in parallel, equal j's in increasing row order:
+// every G_ij sees the oracle's terms, order and roundings (separate multiply
+// and add), bit for bit.  At config 2 a batch holds ~640 tuples over 8000
+// accumulators: ~4 % of them wait a pass (the diagonal j = i, present in
+// every contributing row, is summed apart by one thread).  Host-selected when the longest row
+// fits a warp's two to four entries per lane (128) and the longest column the tuple
+// stage (kExactTuples); c_i is summed in increasing r by the last thread,
+// 16 terms per batch.
+constexpr int kClaimRowMax = 128;
+template <int H>  // entries per lane: rows of up to 32 H entries
+__global__ void __launch_bounds__(512) gram_claim_kernel(
+    int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+    const double* __restrict__ vals, const int32_t* __restrict__ colptr,
+    const int32_t* __restrict__ rowind, const double* __restrict__ cvals,
+    const double* __restrict__ b, int row_begin, int row_end, double* __restrict__ G, int ldg,
+    double* __restrict__ c) {
+  pdl_wait();
+  extern __shared__ double acc[];  // [n] accumulators, then [n] int tags
+  int* tag = reinterpret_cast<int*>(acc + n);
+  __shared__ double s_a[kExactTuples], s_cp[kExactTuples];
+  __shared__ int s_lo[kExactTuples], s_len[kExactTuples];
+  __shared__ double s_dg[16];  // the batch's diagonal products a_ri^2, by row slot
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+  for (int j = tid; j < n; j += nt) tag[j] = 0;
+  int epoch = 0;
+  auto load_tuple = [&](int i, double& a, int& lo, int& len, double& cp) {
+    a = 0.0;
+    lo = 0;
+    len = 0;
+    cp = 0.0;
+    if (i >= n) return;
+    const int e0 = colptr[i], cnt = colptr[i + 1] - e0;  // cnt <= kExactTuples (host-checked)
+    if (tid < cnt) {
+      const int r = rowind[e0 + tid];
+      a = cvals[e0 + tid];
+      if (r >= row_begin && r < row_end) {
+        lo = rowptr[r];
+        len = rowptr[r + 1] - lo;  // <= 32 H (host-checked)
+        cp = __dmul_rn(a, b[r]);
+      }
+    }
+  };
+  double ta, tcp;
+  int tlo, tlen;
+  load_tuple(blockIdx.x, ta, tlo, tlen, tcp);
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int j = tid; j < n; j += nt) acc[j] = 0.0;
+    if (tid < kExactTuples) {
+      s_a[tid] = ta;
+      s_lo[tid] = tlo;
+      s_len[tid] = tlen;
+      s_cp[tid] = tcp;
+    }
+    const int cnt = colptr[i + 1] - colptr[i];
+    __syncthreads();
+    load_tuple(i + gridDim.x, ta, tlo, tlen, tcp);  // next G row's tuples, in flight meanwhile
+    // the warp's row of a batch: entries lane + 32 h -> (j, a_ri a_rj)
+    auto load_row = [&](int q, int (&j)[H], double (&p)[H], double& a) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        j[h] = -1;
+        p[h] = 0.0;
+      }
+      a = 0.0;
+      if (q >= cnt) return;
+      a = s_a[q];
+      const int lo = s_lo[q], len = s_len[q];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int t = lane + 32 * h;
+        if (t < len) {
+          j[h] = colind[lo + t];
+          p[h] = vals[lo + t];  // (multiplied by a_ri at use: the gathers stay in flight over a batch)
+        }
+      }
+    };
+    int jn[H];
+    double pn[H];
+    double an;
+    load_row(wid, jn, pn, an);
+    double ci = 0.0, di = 0.0;
+    for (int q0 = 0; q0 < cnt; q0 += nw) {
+      int jc[H];
+      double pc[H];
+      bool pend[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        jc[h] = jn[h];
+        pc[h] = __dmul_rn(an, pn[h]);
+        pend[h] = jc[h] >= 0;
+        // j = i: EVERY contributing row has it (G_ii = sum a_ri^2), so the
+        // claims would serialise the whole batch; summed by one thread instead
+        if (jc[h] == i) {
+          s_dg[wid] = pc[h];
+          pend[h] = false;
+        }
+      }
+      load_row(q0 + nw + wid, jn, pn, an);
+      if (tid == nt - 1) {  // c_i = sum_r a_ri b_r in increasing r (rows outside the shard: none)
+        const int qe = min(cnt, q0 + nw);
+        for (int q = q0; q < qe; ++q)
+          if (s_len[q] > 0) ci = __dadd_rn(ci, s_cp[q]);
+      }
+      // tuple index (row slot, entry) = wid * 32 H + 32 h + lane; earlier tuple -> larger key
+      const int low = (16 * 32 * H - 1) - (wid * 32 * H + lane);
+      constexpr int kShift = H <= 2 ? 10 : 11;  // 16 * 32 * H keys
+      int any;
+      bool first = true;
+      do {
+        ++epoch;
+        const int kb = (epoch << kShift) | low;
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+          if (pend[h]) atomicMax(&tag[jc[h]], kb - 32 * h);
+        __syncthreads();
+        if (first && tid == nt - 33) {  // G_ii in increasing r (a row in the shard holds column i)
+          const int qe = min(cnt, q0 + nw);
+          for (int q = q0; q < qe; ++q)
+            if (s_len[q] > 0) di = __dadd_rn(di, s_dg[q - q0]);
+        }
+        first = false;
+        bool left = false;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          if (pend[h] && tag[jc[h]] == kb - 32 * h) {
+            acc[jc[h]] = __dadd_rn(acc[jc[h]], pc[h]);
+            pend[h] = false;
+          }
+          left |= pend[h];
+        }
+        any = __syncthreads_or(left);
+      } while (any);
+    }
+    if (tid == nt - 1) c[i] = ci;
+    double* Gi = ldg > 0 ? G + (size_t)i * ldg : G + (size_t)i * (i + 1) / 2;  // (packed: j <= i)
+    const int jn_ = ldg > 0 ? n : i + 1;
+    for (int j = tid; j < jn_; j += nt)
+      if (j != i) Gi[j] = acc[j];
+    if (tid == nt - 33) Gi[i] = di;
+    __syncthreads();
+  }
+}
+
 // Packed lower triangle (row i at offset i(i+1)/2, j <= i) -> full symmetric
 // n x ldg matrix.  32 x 32 blocks (bi >= bj) through shared memory so both the
 // lower block (row copy) and its mirror (transposed) are written coalesced.
@@ -777,7 +932,7 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
                         const double* vals, const int32_t* colptr, const int32_t* rowind,
                         const double* cvals, const double* b, int row_begin, int row_end,
                         double* G, int ldg, double* c, int sm_count, cudaStream_t s, bool exact,
-                        int exact_lmin) {
+                        int exact_lmin, int max_row, int max_col) {
   (void)m;
   if (exact && (size_t)n * sizeof(double) <= 160 * 1024) {
     static DeviceOnce attr_x;
@@ -796,6 +951,28 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
     const double sc = ldexp(1.0, -2 * exact_lmin);
     return launch_pdl(gram_exact_kernel, dim3((int)blocks), dim3(512), smem, s, n, rowptr, colind, vals, colptr,
                       rowind, cvals, b, row_begin, row_end, G, ldg, c, sc, 1.0 / sc);
+  }
+  // general values: a CTA per G row with claim-ordered batches when the rows
+  // and columns fit its stages (max_row / max_col = 0: unknown -> not taken)
+  if (!exact && max_row > 0 && max_row <= kClaimRowMax && max_col > 0 && max_col <= kExactTuples &&
+      (size_t)n * 12 <= 200 * 1024) {
+    const int H = max_row <= 64 ? 2 : (max_row <= 96 ? 3 : 4);
+    auto kern = H == 2 ? gram_claim_kernel<2> : (H == 3 ? gram_claim_kernel<3> : gram_claim_kernel<4>);
+    static DeviceOnce attr_c[3];
+    cudaError_t ea = cudaSuccess;
+    if (!device_once(attr_c[H - 2], [&]() {
+          ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024));
+          return ea == cudaSuccess ? 1 : 0;
+        }))
+      return ea;
+    const size_t smem = 12 * (size_t)n;
+    int per_sm = (int)((224 * 1024) / (smem + 13 * 1024));  // (12.3 KB static per CTA)
+    if (per_sm > 4) per_sm = 4;
+    if (per_sm < 1) per_sm = 1;
+    long long blocks = (long long)sm_count * per_sm;
+    if (blocks > n) blocks = n;
+    return launch_pdl(kern, dim3((int)blocks), dim3(512), smem, s, n, rowptr, colind, vals, colptr, rowind, cvals,
+                      b, row_begin, row_end, G, ldg, c);
   }
   // One chunk = the whole row when it fits (measured: splitting a row into
   // column chunks multiplies the A-row gathers and is slower at config 2).

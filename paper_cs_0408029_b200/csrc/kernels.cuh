@@ -65,7 +65,8 @@ cudaError_t launch_gram_dense(int n, const int32_t* rowptr, const int32_t* colin
 cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* colind,
                         const double* vals, const int32_t* colptr, const int32_t* rowind,
                         const double* cvals, const double* b, int row_begin, int row_end,
-                        double* G, int ldg, double* c, int sm_count, cudaStream_t s, bool exact = false, int exact_lmin = 0);
+                        double* G, int ldg, double* c, int sm_count, cudaStream_t s, bool exact = false, int exact_lmin = 0,
+                        int max_row = 0, int max_col = 0);
 
 // ---- a2/a3/a4/a7/a8 pivot steps (pivot.cu) -----------------------------
 cudaError_t launch_init(int n, const double* c, uint8_t* mask, double* x, double* y, double tol,

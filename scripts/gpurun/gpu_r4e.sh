@@ -1,10 +1,13 @@
+# claim-ordered Gram kernel: bitwise tests, config-2 raw timing against the warp-per-row kernel
 set -u
 O=gpurun_out/r4e
 mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
-for c in 1 3 2 2; do
-timeout 300 python bench.py --config $c --no-extra --no-cpu-baseline --no-e2e --steps 20 > $O/bench_c$c.json 2> $O/bench_c$c.err
-python -c "
-import json; d=json.load(open('$O/bench_c$c.json')); print('c$c', d['value'], d['ms_per_step'], d['phase_ms_per_step']['dual'], d['phase_ms_per_step']['chol_solve'], d['phase_ms_per_step']['decide'], d['phase_ms_per_step']['csc'])" >> $O/summary.txt
-done
+timeout 900 python -m pytest tests -m gpu -q -x -k "gram" > $O/pytest_gram.log 2>&1; echo "rc=$?" >> $O/pytest_gram.log
+tail -5 $O/pytest_gram.log
+timeout 600 python scripts/gram_raw_run.py 5 > $O/claim.log 2>&1; cat $O/claim.log
+NNLS_CLAIM_MIN_N=1000000 timeout 600 python scripts/gram_raw_run.py 5 > $O/warp.log 2>&1; cat $O/warp.log
+CFG=3 timeout 600 python scripts/gram_raw_run.py 5 > $O/claim_c3.log 2>&1; cat $O/claim_c3.log
+CFG=3 NNLS_CLAIM_MIN_N=1 timeout 600 python scripts/gram_raw_run.py 5 > $O/claim_c3f.log 2>&1; cat $O/claim_c3f.log
+CFG=1 timeout 600 python scripts/gram_raw_run.py 5 > $O/claim_c1.log 2>&1; cat $O/claim_c1.log
+CFG=1 NNLS_CLAIM_MIN_N=1 timeout 600 python scripts/gram_raw_run.py 5 > $O/claim_c1f.log 2>&1; cat $O/claim_c1f.log
 echo done

@@ -1,10 +1,8 @@
+# claim-ordered Gram kernel at config 2 raw: timing and one ncu --set full capture
 set -u
 O=gpurun_out/r4f
 mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
-for c in 1 3 2 2; do
-timeout 300 python bench.py --config $c --no-extra --no-cpu-baseline --no-e2e --steps 20 > $O/bench_c$c.json 2> $O/bench_c$c.err
-python -c "
-import json; d=json.load(open('$O/bench_c$c.json')); print('c$c', d['value'], d['ms_per_step'], d['phase_ms_per_step']['dual'], d['phase_ms_per_step']['chol_solve'], d['phase_ms_per_step']['decide'], d['phase_ms_per_step']['csc'])" >> $O/summary.txt
-done
+timeout 600 python scripts/gram_raw_run.py 5 > $O/claim.log 2>&1; cat $O/claim.log
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gram_claim" --launch-skip 1 -c 1 \
+  -o $O/full_c2raw_gram_claim -f python scripts/gram_raw_run.py 2 > $O/ncu.log 2>&1
 echo done

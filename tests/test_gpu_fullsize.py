@@ -9,7 +9,7 @@ solve everything within a test's time budget:
   free-set solution against an independent least-squares solve on A_F.
 * config 4 (all 65536 problems, one launch): 256 problems drawn across the
   batch solved by the oracle one by one (F, iteration counts, x), and the KKT
-  report of every problem.
+  conditions of every problem recomputed from the inputs with numpy.
 """
 import os
 
@@ -56,6 +56,30 @@ def test_config2_sampled_gram_exact(config2):
     assert np.array_equal(c[cols], ref_c)
 
 
+def test_config2_raw_claim_gram_matches_warp_ordered(P, monkeypatch):
+    """Config 2 with unquantized values: the claim-ordered Gram (CTA per G row,
+    the default from n = 2048) and the warp-per-row ordered kernel give the
+    same bits, and sampled entries equal the oracle-order sum written out here
+    (products in increasing row order, separate multiply and add: P:126)."""
+    prob = g.make_problem(2, 0, raw=True)
+    S = P.setup(prob)
+    G, c = S.gram()
+    monkeypatch.setenv("NNLS_CLAIM_MIN_N", "1000000")
+    Gw, cw = P.setup(prob).gram()
+    assert np.array_equal(G, Gw) and np.array_equal(c, cw)
+    A = sp.csr_matrix((prob.vals, prob.colind, prob.rowptr), shape=(prob.m, prob.n)).tocsc()
+    A.sort_indices()
+    rng = np.random.default_rng(3)
+    for i, j in zip(rng.integers(0, prob.n, 300), rng.integers(0, prob.n, 300)):
+        ri, vi = A.indices[A.indptr[i]:A.indptr[i + 1]], A.data[A.indptr[i]:A.indptr[i + 1]]
+        rj, vj = A.indices[A.indptr[j]:A.indptr[j + 1]], A.data[A.indptr[j]:A.indptr[j + 1]]
+        common, ia, ja = np.intersect1d(ri, rj, return_indices=True)
+        acc = 0.0
+        for a, bb in zip(vi[ia], vj[ja]):                  # increasing r
+            acc = acc + a * bb
+        assert G[i, j] == acc and G[j, i] == acc, (i, j)
+
+
 def test_config2_kkt(config2):
     """x >= 0; y = A^T (A x - b) >= 0 on G and ~0 on F; x_i y_i ~ 0."""
     prob, x, A, mask, info = config2["prob"], config2["x"], config2["A"], config2["mask"], config2["info"]
@@ -96,6 +120,46 @@ def test_config4_full_batch_sampled_parity(P):
         assert info["iterations"][p] == r["iterations"], p
         scale = max(np.abs(r["x"]).max(), 1e-300)
         assert np.abs(xs[p] - r["x"]).max() <= 1e-9 * scale, p
+
+
+def _batch_kkt(B, xs, lo, hi):
+    """y = A^T (A x - b) of problems [lo, hi) with numpy alone (flat CSR):
+    returns (y, scale) per problem, scale = max |A^T b| (Eq. 3)."""
+    m, n, cnt = B.m, B.n, hi - lo
+    e0, e1 = int(B.nnz_off[lo]), int(B.nnz_off[hi])
+    rp = np.asarray(B.rowptr).reshape(B.count, m + 1)[lo:hi]
+    counts = np.diff(rp, axis=1).reshape(-1)
+    rows = np.repeat(np.arange(cnt * m, dtype=np.int64), counts)
+    pid = np.repeat(np.arange(cnt, dtype=np.int64), np.diff(np.asarray(B.nnz_off[lo:hi + 1])))
+    cols = np.asarray(B.colind[e0:e1], dtype=np.int64) + pid * n
+    vals = np.asarray(B.vals[e0:e1])
+    b = np.asarray(B.b).reshape(B.count, m)[lo:hi].reshape(-1)
+    x = xs[lo:hi].reshape(-1)
+    r = np.bincount(rows, weights=vals * x[cols], minlength=cnt * m) - b
+    y = np.bincount(cols, weights=vals * r[rows], minlength=cnt * n).reshape(cnt, n)
+    c = np.bincount(cols, weights=vals * b[rows], minlength=cnt * n).reshape(cnt, n)
+    return y, np.abs(c).max(axis=1)
+
+
+def test_config4_full_batch_kkt_every_problem(P):
+    """Every one of the 65536 solutions satisfies Eq. 3: x >= 0 and
+    zero off F, y = A^T (A x - b) ~ 0 on F and >= 0 on G, x_i y_i ~ 0 -- y
+    recomputed here from the inputs with numpy (a property that holds at any
+    size; the kernels' own KKT report is not used)."""
+    B = g.make_batch(seed=0, start=0, count=65536)
+    out = P.BatchedSolver().load_batch(B).solve()
+    xs = np.ascontiguousarray(out["x"].reshape(B.count, B.n))
+    masks = out["mask"].reshape(B.count, B.n).astype(bool)
+    assert np.all(out["info"]["status"] == 0)
+    assert xs.min() >= 0.0 and np.all(xs[~masks] == 0.0)
+    for lo in range(0, B.count, 8192):
+        hi = min(B.count, lo + 8192)
+        y, scale = _batch_kkt(B, xs, lo, hi)
+        mk, x = masks[lo:hi], xs[lo:hi]
+        tol = 1e-9 * scale[:, None]
+        assert np.all(np.abs(y) * mk <= tol), lo
+        assert np.all(np.where(mk, 0.0, y) >= -tol), lo
+        assert np.all(np.abs(x * y) <= tol * np.maximum(1.0, x.max(axis=1))[:, None]), lo
 
 
 # ------------------------------------------------ config 2 against the oracle

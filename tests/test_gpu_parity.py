@@ -82,6 +82,43 @@ def test_gram_bitwise_raw_inputs(P):
     assert np.array_equal(G, Go) and np.array_equal(c, co)
 
 
+@pytest.mark.parametrize("shape", [dict(m=400, n=150, density=0.05), dict(m=900, n=40, density=0.3),
+                                   dict(m=2500, n=1100, density=0.02), dict(m=320, n=300, density=0.15), dict(m=320, n=300, density=0.25),
+                                   dict(m=400, n=300, density=0.38), dict(m=5, n=5, density=1.0)])
+def test_gram_claim_ordered_path_bitwise(P, shape, monkeypatch):
+    """General (unquantized) values on the CTA-per-G-row kernel that applies
+    each batch of rows by claims (equal j's in increasing row order): the
+    oracle's bits (rows <= 128 entries in 2-4 per lane, columns <= 512).  The second
+    shape packs ~270 entries into each of 40 columns, so most tuples of a batch
+    collide and wait several passes; NNLS_CLAIM_MIN_N forces the path at small n."""
+    monkeypatch.setenv("NNLS_CLAIM_MIN_N", "1")
+    prob = g.make_problem(shape, seed=6, raw=True)
+    G, c = P.setup(prob).gram()
+    Go, co = O.gram(prob)
+    assert np.array_equal(G, Go) and np.array_equal(c, co)
+    monkeypatch.setenv("NNLS_CLAIM_MIN_N", "1000000")      # the warp-per-row kernel: same bits
+    Gw, cw = P.setup(prob).gram()
+    assert np.array_equal(Gw, Go) and np.array_equal(cw, co)
+
+
+def test_gram_claim_ordered_row_shard_packed(P, monkeypatch):
+    """The claim-ordered kernel over a row block, packed-triangle output (the
+    row-shard partial): equal to the oracle's Gram of that block."""
+    from paper_cs_0408029_b200.dist import gram_tensor, row_shards
+    monkeypatch.setenv("NNLS_CLAIM_MIN_N", "1")
+    prob = g.make_problem(dict(m=1200, n=260, density=0.04), seed=8, raw=True)
+    (r0, r1) = row_shards(prob.m, 3)[1]
+    S = P.ShardSolver(prob.m, prob.n, prob.rowptr, prob.colind, prob.vals, prob.b, r0, r1)
+    buf = gram_tensor(S).cpu().numpy()
+    lo, hi = prob.rowptr[r0], prob.rowptr[r1]
+    blk = g.Problem(r1 - r0, prob.n, prob.rowptr[r0:r1 + 1] - lo, prob.colind[lo:hi], prob.vals[lo:hi],
+                    prob.b[r0:r1], prob.x_gen, prob.kind, prob.seed)
+    Gb, cb = O.gram(blk)
+    n = prob.n
+    assert np.array_equal(buf[:n * (n + 1) // 2], Gb[np.tril_indices(n)])
+    assert np.array_equal(buf[n * (n + 1) // 2:], cb)
+
+
 @pytest.mark.parametrize("cfg", [1, dict(m=3000, n=12, density=0.5)])
 def test_gram_exact_and_ordered_paths_agree(P, cfg, monkeypatch):
     """Quantized inputs take the exact-arithmetic Gram (any summation order,
