@@ -809,11 +809,18 @@ __global__ void __launch_bounds__(512) gram_claim_kernel(
           pend[h] = false;
         }
       }
+      if (lane == 0 && jc[0] < 0) s_dg[wid] = 0.0;  // no row in this slot (or outside the shard)
       load_row(q0 + nw + wid, jn, pn, an);
-      if (tid == nt - 1) {  // c_i = sum_r a_ri b_r in increasing r (rows outside the shard: none)
-        const int qe = min(cnt, q0 + nw);
-        for (int q = q0; q < qe; ++q)
-          if (s_len[q] > 0) ci = __dadd_rn(ci, s_cp[q]);
+      // c_i = sum_r a_ri b_r in increasing r: the batch's 16 terms loaded together,
+      // then the dependent adds (slots past the column's end and rows outside
+      // the shard hold +0.0: x + 0.0 = x, a running sum from +0.0 is never -0.0)
+      if (tid == nt - 1) {
+        double t[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) t[u] = s_cp[min(q0 + u, kExactTuples - 1)];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (q0 + u < kExactTuples) ci = __dadd_rn(ci, t[u]);
       }
       // tuple index (row slot, entry) = wid * 32 H + 32 h + lane; earlier tuple -> larger key
       const int low = (16 * 32 * H - 1) - (wid * 32 * H + lane);
@@ -827,10 +834,12 @@ __global__ void __launch_bounds__(512) gram_claim_kernel(
         for (int h = 0; h < H; ++h)
           if (pend[h]) atomicMax(&tag[jc[h]], kb - 32 * h);
         __syncthreads();
-        if (first && tid == nt - 33) {  // G_ii in increasing r (a row in the shard holds column i)
-          const int qe = min(cnt, q0 + nw);
-          for (int q = q0; q < qe; ++q)
-            if (s_len[q] > 0) di = __dadd_rn(di, s_dg[q - q0]);
+        if (first && tid == nt - 33) {  // G_ii in increasing r (row slots without the column: +0.0)
+          double t[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) t[u] = s_dg[u];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) di = __dadd_rn(di, t[u]);
         }
         first = false;
         bool left = false;
