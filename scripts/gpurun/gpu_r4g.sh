@@ -1,10 +1,12 @@
+# claim-ordered vs warp-per-row Gram (unquantized values): crossover in n (m = 5 n, ~40 entries per row)
 set -u
 O=gpurun_out/r4g
 mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
-for c in 2 1; do
-timeout 300 python bench.py --config $c --no-extra --no-cpu-baseline --no-e2e --steps 20 > $O/bench_c$c.json 2> $O/bench_c$c.err
-python -c "
-import json; d=json.load(open('$O/bench_c$c.json')); print('c$c', d['value'], d['ms_per_step'], d['phase_ms_per_step'])" >> $O/summary.txt
+for N in 2048 3000 4000 6000 12000 16000; do
+  D=$(python -c "print(40.0/$N)")
+  for MIN in 1 1000000; do
+    echo "n=$N min_n=$MIN" >> $O/sweep.log
+    M=$((5*N)) N=$N D=$D NNLS_CLAIM_MIN_N=$MIN timeout 600 python scripts/gram_raw_run.py 5 >> $O/sweep.log 2>&1
+  done
 done
-echo done
+cat $O/sweep.log

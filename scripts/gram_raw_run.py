@@ -11,7 +11,8 @@ import paper_cs_0408029_b200 as P  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 cfg = int(os.environ.get("CFG", "2"))
-prob = g.make_problem(cfg, seed=0, raw=True)
+shape = dict(m=int(os.environ["M"]), n=int(os.environ["N"]), density=float(os.environ["D"])) if "M" in os.environ else cfg
+prob = g.make_problem(shape, seed=0, raw=True)
 S = P.setup(prob)
 P.timing_enable(S.h)
 for _ in range(reps):
