@@ -1,13 +1,16 @@
+# claim-ordered Gram: one barrier per pass (parity tags, 1024 threads) vs two barriers (512 threads): tests + timing
 set -u
 O=gpurun_out/r4h
 mkdir -p $O
-for c in 2 1 3; do
-timeout 300 python bench.py --config $c --no-extra --no-cpu-baseline --no-e2e --steps 20 > $O/bench_c$c.json 2> $O/bench_c$c.err
-python -c "
-import json; d=json.load(open('$O/bench_c$c.json')); ps=d.get('per_solve',{}); print('c$c', d['value'], d['ms_per_step'], d['phase_ms_per_step']['chol_factor'], [ (t['f'], t['kept']) for t in ps.get('trace',[])])" >> $O/summary.txt
-NNLS_ORDER_MODE=1 timeout 300 python bench.py --config $c --no-extra --no-cpu-baseline --no-e2e --steps 20 > $O/bench_c${c}_m1.json 2> $O/bench_c${c}_m1.err
-python -c "
-import json; d=json.load(open('$O/bench_c${c}_m1.json')); ps=d.get('per_solve',{}); print('c$c m1', d['value'], d['ms_per_step'], d['phase_ms_per_step']['chol_factor'], [ (t['f'], t['kept']) for t in ps.get('trace',[])])" >> $O/summary.txt
+timeout 900 python -m pytest tests -m gpu -q -x -k "gram" > $O/pytest_gram.log 2>&1; echo "rc=$?" >> $O/pytest_gram.log
+tail -3 $O/pytest_gram.log
+NNLS_CLAIM_TWO_BARRIERS=1 timeout 900 python -m pytest tests -m gpu -q -x -k "gram" > $O/pytest_gram2.log 2>&1; echo "rc=$?" >> $O/pytest_gram2.log
+tail -3 $O/pytest_gram2.log
+for TB in 0 1; do
+  echo "two_barriers=$TB config 2 raw"; NNLS_CLAIM_TWO_BARRIERS=$TB timeout 600 python scripts/gram_raw_run.py 5 2>&1 | grep -v checksum
+  for N in 4000 6000 12000; do
+    D=$(python -c "print(40.0/$N)")
+    echo "two_barriers=$TB n=$N"; M=$((5*N)) N=$N D=$D NNLS_CLAIM_TWO_BARRIERS=$TB timeout 600 python scripts/gram_raw_run.py 5 2>&1 | grep -v checksum
+  done
 done
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 echo done
