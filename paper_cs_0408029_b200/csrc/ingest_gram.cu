@@ -717,8 +717,8 @@ __global__ void __launch_bounds__(512) gram_exact_kernel(
 // and add), bit for bit.  At config 2 a batch holds ~640 tuples over 8000
 // accumulators: ~4 % of them wait a pass (the diagonal j = i, present in
 // every contributing row, is summed apart by one thread).  Host-selected when the longest row
-// fits a warp's two to four entries per lane (128) and the longest column the tuple
-// stage (kExactTuples); c_i is summed in increasing r by the last thread,
+// fits a warp's two to four entries per lane (128); a column longer than the
+// tuple stage (kExactTuples) is taken in segments; c_i is summed in increasing r by the last thread,
 // 16 terms per batch.
 constexpr int kClaimRowMax = 128;
 template <int H>  // entries per lane: rows of up to 32 H entries
@@ -737,14 +737,16 @@ __global__ void __launch_bounds__(512) gram_claim_kernel(
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x, nw = nt >> 5;
   for (int j = tid; j < n; j += nt) tag[j] = 0;
   int epoch = 0;
-  auto load_tuple = [&](int i, double& a, int& lo, int& len, double& cp) {
+  // tuple of entry sb + tid of column i (a column longer than the stage is
+  // taken in segments of kExactTuples entries: sb = the segment's start)
+  auto load_tuple = [&](int i, int sb, double& a, int& lo, int& len, double& cp) {
     a = 0.0;
     lo = 0;
     len = 0;
     cp = 0.0;
     if (i >= n) return;
-    const int e0 = colptr[i], cnt = colptr[i + 1] - e0;  // cnt <= kExactTuples (host-checked)
-    if (tid < cnt) {
+    const int e0 = colptr[i] + sb, cnt = colptr[i + 1] - e0;
+    if (tid < cnt && tid < kExactTuples) {
       const int r = rowind[e0 + tid];
       a = cvals[e0 + tid];
       if (r >= row_begin && r < row_end) {
@@ -756,18 +758,26 @@ __global__ void __launch_bounds__(512) gram_claim_kernel(
   };
   double ta, tcp;
   int tlo, tlen;
-  load_tuple(blockIdx.x, ta, tlo, tlen, tcp);
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    for (int j = tid; j < n; j += nt) acc[j] = 0.0;
+  load_tuple(blockIdx.x, 0, ta, tlo, tlen, tcp);
+  double ci = 0.0, di = 0.0;
+  for (int i = blockIdx.x, sb = 0; i < n;) {
+    if (sb == 0) {
+      for (int j = tid; j < n; j += nt) acc[j] = 0.0;
+      ci = 0.0;
+      di = 0.0;
+    }
     if (tid < kExactTuples) {
       s_a[tid] = ta;
       s_lo[tid] = tlo;
       s_len[tid] = tlen;
       s_cp[tid] = tcp;
     }
-    const int cnt = colptr[i + 1] - colptr[i];
+    const int cnt_all = colptr[i + 1] - colptr[i];
+    const int cnt = min(kExactTuples, cnt_all - sb);
+    const bool last_seg = sb + kExactTuples >= cnt_all;
+    const int i_next = last_seg ? i + (int)gridDim.x : i, sb_next = last_seg ? 0 : sb + kExactTuples;
     __syncthreads();
-    load_tuple(i + gridDim.x, ta, tlo, tlen, tcp);  // next G row's tuples, in flight meanwhile
+    load_tuple(i_next, sb_next, ta, tlo, tlen, tcp);  // the next stage's tuples, in flight meanwhile
     // the warp's row of a batch: entries lane + 32 h -> (j, a_ri a_rj)
     auto load_row = [&](int q, int (&j)[H], double (&p)[H], double& a) {
 #pragma unroll
@@ -792,7 +802,6 @@ __global__ void __launch_bounds__(512) gram_claim_kernel(
     double pn[H];
     double an;
     load_row(wid, jn, pn, an);
-    double ci = 0.0, di = 0.0;
     for (int q0 = 0; q0 < cnt; q0 += nw) {
       int jc[H];
       double pc[H];
@@ -854,13 +863,17 @@ __global__ void __launch_bounds__(512) gram_claim_kernel(
         any = __syncthreads_or(left);
       } while (any);
     }
-    if (tid == nt - 1) c[i] = ci;
-    double* Gi = ldg > 0 ? G + (size_t)i * ldg : G + (size_t)i * (i + 1) / 2;  // (packed: j <= i)
-    const int jn_ = ldg > 0 ? n : i + 1;
-    for (int j = tid; j < jn_; j += nt)
-      if (j != i) Gi[j] = acc[j];
-    if (tid == nt - 33) Gi[i] = di;
+    if (last_seg) {
+      if (tid == nt - 1) c[i] = ci;
+      double* Gi = ldg > 0 ? G + (size_t)i * ldg : G + (size_t)i * (i + 1) / 2;  // (packed: j <= i)
+      const int jn_ = ldg > 0 ? n : i + 1;
+      for (int j = tid; j < jn_; j += nt)
+        if (j != i) Gi[j] = acc[j];
+      if (tid == nt - 33) Gi[i] = di;
+    }
     __syncthreads();
+    i = i_next;
+    sb = sb_next;
   }
 }
 
@@ -963,7 +976,7 @@ cudaError_t launch_gram(int m, int n, const int32_t* rowptr, const int32_t* coli
   }
   // general values: a CTA per G row with claim-ordered batches when the rows
   // and columns fit its stages (max_row / max_col = 0: unknown -> not taken)
-  if (!exact && max_row > 0 && max_row <= kClaimRowMax && max_col > 0 && max_col <= kExactTuples &&
+  if (!exact && max_row > 0 && max_row <= kClaimRowMax && max_col > 0 &&
       (size_t)n * 12 <= 200 * 1024) {
     const int H = max_row <= 64 ? 2 : (max_row <= 96 ? 3 : 4);
     auto kern = H == 2 ? gram_claim_kernel<2> : (H == 3 ? gram_claim_kernel<3> : gram_claim_kernel<4>);

@@ -84,11 +84,13 @@ def test_gram_bitwise_raw_inputs(P):
 
 @pytest.mark.parametrize("shape", [dict(m=400, n=150, density=0.05), dict(m=900, n=40, density=0.3),
                                    dict(m=2500, n=1100, density=0.02), dict(m=320, n=300, density=0.15), dict(m=320, n=300, density=0.25),
-                                   dict(m=400, n=300, density=0.38), dict(m=5, n=5, density=1.0)])
+                                   dict(m=400, n=300, density=0.38), dict(m=5, n=5, density=1.0),
+                                   dict(m=6000, n=100, density=0.3), dict(m=1100, n=90, density=0.5)])
 def test_gram_claim_ordered_path_bitwise(P, shape, monkeypatch):
     """General (unquantized) values on the CTA-per-G-row kernel that applies
     each batch of rows by claims (equal j's in increasing row order): the
-    oracle's bits (rows <= 128 entries in 2-4 per lane, columns <= 512).  The second
+    oracle's bits (rows <= 128 entries in 2-4 per lane; columns longer
+    than the 512-tuple stage -- the last two shapes: ~1800 and ~550 entries -- in segments).  The second
     shape packs ~270 entries into each of 40 columns, so most tuples of a batch
     collide and wait several passes; NNLS_CLAIM_MIN_N forces the path at small n."""
     monkeypatch.setenv("NNLS_CLAIM_MIN_N", "1")
