@@ -1,6 +1,12 @@
+# claim-ordered Gram with long columns (segments): tall problems, unquantized values
 set -u
 O=gpurun_out/r4j
 mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
-timeout 300 python bench.py --no-extra --no-cpu-baseline --no-e2e --steps 10 > $O/bench.json 2> $O/bench.err
-echo done
+for SH in "200000 8000 0.005" "100000 4000 0.01" "400000 12000 0.003"; do
+  set -- $SH
+  for MIN in 1 1000000; do
+    echo "m=$1 n=$2 d=$3 min_n=$MIN" >> $O/sweep.log
+    M=$1 N=$2 D=$3 NNLS_CLAIM_MIN_N=$MIN timeout 900 python scripts/gram_raw_run.py 3 2>&1 | grep -v checksum >> $O/sweep.log
+  done
+done
+cat $O/sweep.log
