@@ -721,6 +721,10 @@ __global__ void __launch_bounds__(512) gram_exact_kernel(
 // tuple stage (kExactTuples) is taken in segments; c_i is summed in increasing r by the last thread,
 // 16 terms per batch.
 constexpr int kClaimRowMax = 128;
+#ifndef NNLS_CLAIM_EPOCH_MAX  // (a small value exercises the restart in tests: NNLS_EXTRA_NVCC_FLAGS)
+#define NNLS_CLAIM_EPOCH_MAX ((1 << 20) - 1024)
+#endif
+constexpr int kClaimEpochMax = NNLS_CLAIM_EPOCH_MAX;
 template <int H>  // entries per lane: rows of up to 32 H entries
 __global__ void __launch_bounds__(512) gram_claim_kernel(
     int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
@@ -765,6 +769,13 @@ __global__ void __launch_bounds__(512) gram_claim_kernel(
       for (int j = tid; j < n; j += nt) acc[j] = 0.0;
       ci = 0.0;
       di = 0.0;
+    }
+    // a stage takes at most 32 batches x 16 passes = 512 epochs: restart them
+    // (uniform; the staging barrier below orders it) before the keys' epoch
+    // field (20 bits at H >= 3) could overflow on very long columns
+    if (epoch > kClaimEpochMax) {
+      for (int j = tid; j < n; j += nt) tag[j] = 0;
+      epoch = 0;
     }
     if (tid < kExactTuples) {
       s_a[tid] = ta;
